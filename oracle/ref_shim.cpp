@@ -1,0 +1,375 @@
+// TEST INFRASTRUCTURE ONLY (oracle). C shim over the UNMODIFIED reference library
+// (/root/reference/proj/src, compiled in place by oracle/Makefile into oracle/_ref/).
+// It lets pytest (ctypes) call the reference's own code: RNG (rng.hpp), fold schemes
+// (folds.cpp), simulators, Model evaluations (model.hpp:24-78), leapfrog / hmc_step
+// (hmc.cpp), adapt_full_data (adapt.cpp) and run_pcv (engine.cpp). It is the checker
+// the C restatement (oracle/pcv_oracle.c) is pinned against, and the `--impl reference`
+// CPU arm of bench.py. Never linked into the product.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../include/pcvg.h"
+#include "pcv/adapt.hpp"
+#include "pcv/engine.hpp"
+#include "pcv/errors.hpp"
+#include "pcv/folds.hpp"
+#include "pcv/hmc.hpp"
+#include "pcv/models/grouped_regression.hpp"
+#include "pcv/models/radon.hpp"
+#include "pcv/models/seasonal_ar.hpp"
+#include "pcv/rng.hpp"
+#include "ref_plugins.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PCVG_OK;
+  } catch (const pcv::invalid_input& e) {
+    return fail(PCVG_INVALID_INPUT, e.what());
+  } catch (const pcv::numeric_fault& e) {
+    return fail(PCVG_NUMERIC_FAULT, e.what());
+  } catch (const pcv::adaptation_failure& e) {
+    return fail(PCVG_ADAPTATION_FAILURE, e.what());
+  } catch (const pcv::undefined_diagnostic& e) {
+    return fail(PCVG_UNDEFINED_DIAGNOSTIC, e.what());
+  } catch (const pcv::unsupported_score& e) {
+    return fail(PCVG_UNSUPPORTED_SCORE, e.what());
+  } catch (const std::exception& e) {
+    return fail(PCVG_INVALID_INPUT, e.what());
+  }
+}
+
+pcv::Dataset to_dataset(const pcvg_dataset* d) {
+  pcv::Dataset out;
+  const long n = static_cast<long>(d->n_obs);
+  out.n_cov = d->n_cov;
+  out.y.assign(d->y, d->y + n);
+  if (d->n_cov > 0) out.x.assign(d->x, d->x + n * d->n_cov);
+  if (d->group_id) out.group_id.assign(d->group_id, d->group_id + n);
+  if (d->time_index) out.time_index.assign(d->time_index, d->time_index + n);
+  return out;
+}
+
+struct RefModel {
+  std::unique_ptr<pcv::Model> model;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* pcvref_last_error() { return g_err.c_str(); }
+
+uint64_t pcvref_stream_key(uint64_t kind, uint64_t a, uint64_t b, uint64_t c) {
+  return pcv::stream_key(static_cast<pcv::StreamKind>(kind), a, b, c);
+}
+
+int pcvref_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
+                        const uint64_t* arg, int64_t n, double* out) {
+  return guarded([&] {
+    pcv::CounterRng rng(seed, stream);
+    if (skip_block >= 0) rng.skip_to(static_cast<uint64_t>(skip_block));
+    for (int64_t i = 0; i < n; ++i) {
+      switch (ops[i]) {
+        case 'u': out[i] = rng.uniform(); break;
+        case 'n': out[i] = rng.normal(); break;
+        case '4': out[i] = static_cast<double>(rng.next_u32()); break;
+        case 'b': out[i] = static_cast<double>(rng.below(arg[i])); break;
+        default: throw pcv::invalid_input("bad rng op");
+      }
+    }
+  });
+}
+
+int pcvref_make_kfold(int64_t n, int32_t K, uint64_t seed, int32_t* out) {
+  return guarded([&] {
+    pcv::Dataset d;
+    d.y.assign(n, 0.0);
+    const auto f = pcv::make_kfold_scheme(d, K, seed);
+    std::memcpy(out, f.test_index.data(), sizeof(int32_t) * n);
+  });
+}
+
+int pcvref_make_time_blocks(const pcvg_dataset* ds, int32_t K, int32_t* out) {
+  return guarded([&] {
+    const auto f = pcv::make_time_block_scheme(to_dataset(ds), K);
+    std::memcpy(out, f.test_index.data(), sizeof(int32_t) * ds->n_obs);
+  });
+}
+
+int pcvref_make_logo(const pcvg_dataset* ds, int32_t* out, int32_t* K) {
+  return guarded([&] {
+    const auto f = pcv::make_logo_scheme(to_dataset(ds));
+    std::memcpy(out, f.test_index.data(), sizeof(int32_t) * ds->n_obs);
+    *K = f.K;
+  });
+}
+
+int pcvref_simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_beta, uint64_t seed,
+                            double* y, double* x, int32_t* g) {
+  return guarded([&] {
+    pcv::GroupedSimOptions o;
+    o.groups = J;
+    o.per_group = Nj;
+    o.covariates = P;
+    o.min_omitted_beta = min_beta;
+    const auto r = pcv::simulate_grouped_regression(o, seed);
+    std::memcpy(y, r.data.y.data(), sizeof(double) * r.data.y.size());
+    std::memcpy(x, r.data.x.data(), sizeof(double) * r.data.x.size());
+    std::memcpy(g, r.data.group_id.data(), sizeof(int32_t) * r.data.group_id.size());
+  });
+}
+
+int pcvref_simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y, double* x,
+                          int32_t* g) {
+  return guarded([&] {
+    const auto r = pcv::simulate_radon_style(houses, counties, seed);
+    std::memcpy(y, r.data.y.data(), sizeof(double) * r.data.y.size());
+    std::memcpy(x, r.data.x.data(), sizeof(double) * r.data.x.size());
+    std::memcpy(g, r.data.group_id.data(), sizeof(int32_t) * r.data.group_id.size());
+  });
+}
+
+int pcvref_simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho, double amp,
+                             double sigma, uint64_t seed, double* y, double* x, int64_t* t) {
+  return guarded([&] {
+    pcv::SeasonalSimOptions o;
+    o.months = months;
+    o.ar_order = p;
+    o.dummies = q;
+    o.rho = rho;
+    o.seasonal_amp = amp;
+    o.sigma = sigma;
+    const auto r = pcv::simulate_seasonal_ar(o, seed);
+    std::memcpy(y, r.data.y.data(), sizeof(double) * r.data.y.size());
+    std::memcpy(x, r.data.x.data(), sizeof(double) * r.data.x.size());
+    for (size_t i = 0; i < r.data.time_index.size(); ++i) t[i] = r.data.time_index[i];
+  });
+}
+
+// Builds a reference Model (or an oracle plugin on the reference API) from a descriptor.
+void* pcvref_model_create(const pcvg_dataset* ds, const pcvg_folds* fs,
+                          const pcvg_model_spec* spec, const char* name) {
+  RefModel* out = nullptr;
+  const int rc = guarded([&] {
+    pcv::Dataset d = to_dataset(ds);
+    auto rm = std::make_unique<RefModel>();
+    const std::string nm = name ? name : "M";
+    if (fs->intervals) {
+      if (spec->family != PCVG_FAMILY_SEASONAL_AR)
+        throw pcv::invalid_input("hv-block folds are only wired for seasonal-ar");
+      std::vector<pcvoracle::HvFold> hv(fs->K);
+      for (int k = 0; k < fs->K; ++k)
+        hv[k] = {fs->intervals[4 * k], fs->intervals[4 * k + 1], fs->intervals[4 * k + 2],
+                 fs->intervals[4 * k + 3]};
+      rm->model = std::make_unique<pcvoracle::HvSeasonalARModel>(
+          nm, d, std::move(hv), spec->ar_order, spec->dummies,
+          spec->rho_transform == PCVG_RHO_SYMMETRIC ? pcv::RhoTransform::Symmetric
+                                                    : pcv::RhoTransform::HalfOpen);
+    } else {
+      pcv::FoldAssignment f;
+      f.K = fs->K;
+      f.test_index.assign(fs->test_index, fs->test_index + ds->n_obs);
+      switch (spec->family) {
+        case PCVG_FAMILY_GROUPED: {
+          std::vector<int> mask;
+          if (spec->covariate_mask) mask.assign(spec->covariate_mask, spec->covariate_mask + ds->n_cov);
+          rm->model = std::make_unique<pcv::GroupedRegressionModel>(nm, std::move(d), std::move(f), mask);
+          break;
+        }
+        case PCVG_FAMILY_RADON:
+          rm->model = std::make_unique<pcv::RadonStyleModel>(nm, std::move(d), std::move(f),
+                                                             spec->include_floor != 0);
+          break;
+        case PCVG_FAMILY_SEASONAL_AR:
+          rm->model = std::make_unique<pcv::SeasonalARModel>(
+              nm, std::move(d), std::move(f), spec->ar_order, spec->dummies,
+              spec->rho_transform == PCVG_RHO_SYMMETRIC ? pcv::RhoTransform::Symmetric
+                                                        : pcv::RhoTransform::HalfOpen);
+          break;
+        case PCVG_FAMILY_LOGISTIC:
+          rm->model = std::make_unique<pcvoracle::LogisticModel>(nm, std::move(d), std::move(f));
+          break;
+        default:
+          throw pcv::invalid_input("family not wired in the reference shim");
+      }
+    }
+    out = rm.release();
+  });
+  return rc == PCVG_OK ? out : nullptr;
+}
+
+void pcvref_model_destroy(void* h) { delete static_cast<RefModel*>(h); }
+
+static const pcv::Model& M(void* h) { return *static_cast<RefModel*>(h)->model; }
+
+int32_t pcvref_model_dim(void* h) { return M(h).dim(); }
+int64_t pcvref_test_size(void* h, int32_t fold) { return M(h).test_size(fold); }
+
+double pcvref_log_joint(void* h, const double* theta, int32_t fold) {
+  return M(h).log_joint({theta, static_cast<size_t>(M(h).dim())}, fold);
+}
+void pcvref_grad(void* h, const double* theta, int32_t fold, double* grad) {
+  const size_t d = M(h).dim();
+  M(h).grad_log_joint({theta, d}, fold, {grad, d});
+}
+double pcvref_log_pred(void* h, const double* theta, int32_t fold) {
+  return M(h).log_pred({theta, static_cast<size_t>(M(h).dim())}, fold);
+}
+double pcvref_log_lik_test(void* h, const double* theta, int32_t fold) {
+  return M(h).log_lik_test({theta, static_cast<size_t>(M(h).dim())}, fold);
+}
+void pcvref_initial_draw(void* h, uint64_t seed, uint64_t stream, double* out) {
+  pcv::CounterRng rng(seed, stream);
+  const auto v = M(h).initial_draw(rng);
+  std::memcpy(out, v.data(), sizeof(double) * v.size());
+}
+
+int32_t pcvref_leapfrog(void* h, int32_t fold, double step, int32_t n_lf, const double* inv_mass,
+                        double* q, double* p) {
+  const size_t d = M(h).dim();
+  std::vector<double> grad(d);
+  return pcv::leapfrog({q, d}, {p, d}, M(h), fold, step, n_lf, {inv_mass, d}, grad) ? 1 : 0;
+}
+
+// n consecutive reference hmc_step calls on stream CounterRng(seed, stream).
+int pcvref_hmc_chain(void* h, int32_t fold, double step, int32_t n_lf, const double* inv_mass,
+                     uint64_t seed, uint64_t stream, const double* theta0, int64_t n_steps,
+                     double* traj, int32_t* divergent, int32_t* accepted, double* delta_h) {
+  return guarded([&] {
+    const size_t d = M(h).dim();
+    pcv::KernelParams kp{step, n_lf, std::vector<double>(inv_mass, inv_mass + d)};
+    pcv::ChainState st{std::vector<double>(theta0, theta0 + d), pcv::CounterRng(seed, stream), 0};
+    pcv::HmcWorkspace ws;
+    for (int64_t s = 0; s < n_steps; ++s) {
+      const auto info = pcv::hmc_step(st, M(h), fold, kp, ws);
+      std::memcpy(traj + s * d, st.position.data(), sizeof(double) * d);
+      if (divergent) divergent[s] = info.divergent;
+      if (accepted) accepted[s] = info.accepted;
+      if (delta_h) delta_h[s] = info.delta_h;
+    }
+  });
+}
+
+int pcvref_adapt(void* h, int32_t chains, int64_t warmup, int64_t draws, int32_t n_lf,
+                 double target, double init_step, uint64_t seed, int32_t model_id,
+                 double* step_out, double* inv_mass_out, double* bank_out, double* mean_accept,
+                 int64_t* divergences) {
+  return guarded([&] {
+    pcv::AdaptConfig ac;
+    ac.chains = chains;
+    ac.warmup = warmup;
+    ac.draws = draws;
+    ac.n_leapfrog = n_lf;
+    ac.target_accept = target;
+    ac.init_step_size = init_step;
+    const auto fit = pcv::adapt_full_data(M(h), ac, seed, model_id);
+    *step_out = fit.kparams.step_size;
+    const size_t d = M(h).dim();
+    std::memcpy(inv_mass_out, fit.kparams.inv_mass_diag.data(), sizeof(double) * d);
+    for (size_t r = 0; r < fit.draws.size(); ++r)
+      std::memcpy(bank_out + r * d, fit.draws[r].data(), sizeof(double) * d);
+    if (mean_accept) *mean_accept = fit.mean_accept;
+    if (divergences) *divergences = fit.divergences;
+  });
+}
+
+int pcvref_run_pcv(int32_t n_models, void** models, const int32_t* model_ids,
+                   const pcvg_kernel* kernels, const double* const* banks,
+                   const int64_t* bank_rows, const pcvg_run_config* c, int32_t threads,
+                   pcvg_report* rep) {
+  return guarded([&] {
+    pcv::RunConfig cfg;
+    cfg.chains = c->chains;
+    cfg.iters = c->iters;
+    cfg.warmup = c->warmup;
+    cfg.batch_size = c->batch_size;
+    cfg.blocks = c->blocks;
+    cfg.bench_draws = c->bench_draws;
+    cfg.bench_quantile = c->bench_quantile;
+    cfg.seed = c->seed;
+    cfg.score = static_cast<pcv::ScoreKind>(c->score);
+    cfg.checkpoint_every = c->checkpoint_every;
+    cfg.thread_budget = threads;
+    cfg.shared_streams = c->shared_streams != 0;
+    std::vector<pcv::FullDataFit> fits(n_models);
+    std::vector<pcv::ModelInput> inputs;
+    for (int m = 0; m < n_models; ++m) {
+      const size_t d = M(models[m]).dim();
+      fits[m].kparams.step_size = kernels[m].step_size;
+      fits[m].kparams.n_leapfrog = kernels[m].n_leapfrog;
+      fits[m].kparams.inv_mass_diag.assign(kernels[m].inv_mass_diag,
+                                           kernels[m].inv_mass_diag + d);
+      for (int64_t r = 0; r < bank_rows[m]; ++r)
+        fits[m].draws.emplace_back(banks[m] + r * d, banks[m] + (r + 1) * d);
+      inputs.push_back({&M(models[m]), &fits[m], model_ids[m]});
+    }
+    const pcv::PcvReport r = pcv::run_pcv(inputs, cfg);
+    const int K = r.folds, L = r.chains;
+    for (int m = 0; m < n_models; ++m) {
+      const auto& mr = r.models[m];
+      for (int k = 0; k < K; ++k) {
+        const auto& fs = mr.folds[k];
+        const size_t i = static_cast<size_t>(m) * K + k;
+        rep->folds.estimate[i] = fs.estimate;
+        rep->folds.log_f_hat[i] = fs.log_f_hat;
+        rep->folds.mc_contribution[i] = fs.mc_contribution;
+        if (rep->folds.naive_contribution) rep->folds.naive_contribution[i] = NAN;
+        rep->folds.ess[i] = fs.ess;
+        rep->folds.rhat[i] = fs.rhat;
+        rep->folds.batches[i] = fs.batches;
+        rep->folds.fault[i] = fs.fault;
+        rep->folds.failed[i] = fs.failed;
+        for (int ch = 0; ch < L; ++ch)
+          rep->divergences[(i)*L + ch] = mr.divergences[k][ch];
+      }
+      rep->score_total[m] = mr.score_total;
+      rep->numeric_faults[m] = mr.numeric_faults;
+      rep->rhat_excluded[m] = mr.rhat_excluded;
+    }
+    for (int k = 0; k < K; ++k) rep->delta_k[k] = r.delta_k[k];
+    rep->n_checkpoints = static_cast<int32_t>(r.snapshots.size());
+    for (size_t s = 0; s < r.snapshots.size(); ++s) {
+      const auto& sn = r.snapshots[s];
+      double* o = rep->snapshots + 7 * s;
+      o[0] = static_cast<double>(sn.iteration);
+      o[1] = sn.delta_hat;
+      o[2] = sn.mcse;
+      o[3] = sn.epistemic_se;
+      o[4] = sn.prob_a_better;
+      o[5] = sn.ess;
+      o[6] = sn.rhat_max;
+    }
+    rep->benchmark_count = static_cast<int32_t>(r.benchmark.values.size());
+    for (size_t b = 0; b < r.benchmark.values.size(); ++b) rep->benchmark[b] = r.benchmark.values[b];
+    rep->delta_hat = r.delta_hat;
+    rep->mcse = r.mcse;
+    rep->sigma2_delta = r.sigma2_delta;
+    rep->epistemic_se = r.epistemic_se;
+    rep->prob_a_better = r.prob_a_better;
+    rep->ess_overall = r.ess_overall;
+    rep->rhat_max = r.rhat_max;
+    rep->dropped_batch_draws = r.dropped_batch_draws;
+    rep->verdict_pass = r.verdict.pass;
+    rep->verdict_quantile = r.verdict.quantile;
+    rep->verdict_quantile_value = r.verdict.quantile_value;
+    rep->verdict_observed = r.verdict.observed;
+    rep->iters_run = r.iters;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,1082 @@
+// libpcvg.so: the C ABI (include/pcvg.h) over the B200 kernels.
+//
+// Host driver for Steps 2-4 of the reference engine (engine.cpp:257-483): model upload in the
+// device layout, chain-state allocation, the warm-up / sampling launches, per-fold reductions and
+// the Step-4 merge (compute_stats, failed folds, shuffle benchmark, verdict). Every preconditions
+// check of the reference is repeated here and returned as a status code (errors.hpp taxonomy).
+// There is no CPU fallback: without a working CUDA device every device entry point returns
+// PCVG_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/pcvg.h"
+#include "host_common.hpp"
+#include "types.cuh"
+
+namespace pcvg {
+
+// kernels (gauss_kernel.cu, logistic_kernel.cu, chain_kernels.cu)
+int gauss_lanes_per_chain(const ModelDev& M, int nch);
+cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st);
+cudaError_t launch_logistic(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const double* bank,
+                               int64_t bank_rows, cudaStream_t st);
+cudaError_t launch_centers(const ChainsDev& S, int nfold, int64_t warmup, double* centers, int D,
+                           cudaStream_t st);
+cudaError_t launch_fold_stats(const ChainsDev& S, int nfold, int64_t n, int b, int D,
+                              double* estimate, double* log_f_hat, double* mc, double* naive,
+                              double* ess, double* rhat, int64_t* batches, int32_t* fault,
+                              cudaStream_t st);
+// host_folds.cpp
+void rng_sequence(uint64_t, uint64_t, int64_t, const char*, const uint64_t*, int64_t, double*);
+void make_loo(int64_t, int32_t*, int32_t*);
+void make_logo(const pcvg_dataset*, int32_t*, int32_t*);
+void make_kfold(int64_t, int32_t, uint64_t, int32_t*);
+void make_time_blocks(const pcvg_dataset*, int32_t, int32_t*);
+void make_hv_block(const pcvg_dataset*, int32_t, int64_t, int64_t*);
+void make_hv_racine(const pcvg_dataset*, int64_t, int64_t, int64_t*);
+void simulate_grouped(int32_t, int32_t, int32_t, double, uint64_t, double*, double*, int32_t*);
+void simulate_radon(int32_t, int32_t, uint64_t, double*, double*, int32_t*);
+void simulate_seasonal(int64_t, int32_t, int32_t, double, double, double, uint64_t, double*, double*, int64_t*);
+void simulate_linreg(int64_t, int32_t, uint64_t, double*, double*, int32_t*);
+void simulate_logistic(int64_t, int32_t, uint64_t, double*, double*);
+// stats.cpp
+void merge_stats(int32_t n_models, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
+                 int32_t final_checkpoint, const pcvg_fold_table* folds, const double* y_x,
+                 const double* y_x2, int D_used, pcvg_report* rep);
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(PCVG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(v.size());
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
+  }
+  std::vector<T> download(cudaStream_t st) const {
+    std::vector<T> v(n);
+    if (n) {
+      ck(cudaMemcpyAsync(v.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost, st), "download");
+      ck(cudaStreamSynchronize(st), "sync");
+    }
+    return v;
+  }
+};
+
+struct HostModel {
+  int family = 0;
+  int64_t n = 0;
+  int K = 0;
+  int J = 0, ng = 0, dim = 0, nc = 0;
+  int model_id = 0;
+  bool hv = false;
+  std::vector<int> perm;  // device row -> original row
+  std::vector<int> fold_seg, seg_row;
+  DevBuf<double> y, x, xr, inv_mass, bank;
+  DevBuf<int> key, grp_ptr, lo, hi, ntrain, fseg, sgroup, sunseen, srow, srows;
+  int64_t bank_rows = 0;
+  ModelDev md{};
+};
+
+struct ChainSet {
+  int nch = 0, dim = 0, D = 0;
+  DevBuf<double> pos, grad, wp, lp0, warm, cached;
+  DevBuf<int8_t> cur, has;
+  DevBuf<uint64_t> stream, rpos;
+  DevBuf<int64_t> div;
+  DevBuf<int> fold_override;
+  // accumulators
+  DevBuf<double> u_x, u_x2, z_x, v_x, v_x2, center, y_x, y_x2;
+  DevBuf<int64_t> committed, count, faults;
+  DevBuf<int32_t> pending;
+
+  void alloc(int n, int d, int blocks) {
+    nch = n;
+    dim = d;
+    D = blocks;
+    pos.alloc(2 * static_cast<size_t>(d) * n);
+    grad.alloc(2 * static_cast<size_t>(d) * n);
+    wp.alloc(static_cast<size_t>(d) * n);
+    lp0.alloc(n);
+    warm.alloc(n);
+    cached.alloc(n);
+    cur.alloc(n);
+    has.alloc(n);
+    stream.alloc(n);
+    rpos.alloc(n);
+    div.alloc(n);
+    u_x.alloc(n);
+    u_x2.alloc(n);
+    z_x.alloc(n);
+    v_x.alloc(n);
+    v_x2.alloc(n);
+    center.alloc(n);
+    y_x.alloc(static_cast<size_t>(std::max(blocks, 1)) * n);
+    y_x2.alloc(static_cast<size_t>(std::max(blocks, 1)) * n);
+    committed.alloc(n);
+    count.alloc(n);
+    faults.alloc(n);
+    pending.alloc(n);
+  }
+  ChainsDev view(int L, int fold0, uint64_t seed, uint64_t stream_model) const {
+    ChainsDev s{};
+    s.nch = nch;
+    s.L = L;
+    s.fold0 = fold0;
+    s.fold_override = fold_override.p;
+    s.seed = seed;
+    s.stream_model = stream_model;
+    s.pos = pos.p;
+    s.grad = grad.p;
+    s.wp = wp.p;
+    s.lp0 = lp0.p;
+    s.cur = cur.p;
+    s.rng_stream = stream.p;
+    s.rng_pos = rpos.p;
+    s.rng_cached = cached.p;
+    s.rng_has = has.p;
+    s.divergences = div.p;
+    s.warm_sum = warm.p;
+    s.acc = AccumDev{u_x.p, u_x2.p, z_x.p, v_x.p, v_x2.p, committed.p, pending.p, count.p, faults.p, center.p, y_x.p, y_x2.p};
+    return s;
+  }
+};
+
+}  // namespace
+}  // namespace pcvg
+
+using namespace pcvg;
+
+struct pcvg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<std::unique_ptr<HostModel>> models;
+  std::string err;
+  // run state
+  bool begun = false;
+  pcvg_run_config cfg{};
+  int b = 0, fb = 0, fe = 0;
+  std::vector<std::unique_ptr<ChainSet>> chains;
+  std::vector<std::unique_ptr<DevBuf<double>>> centers;
+  std::vector<std::vector<int64_t>> div_base;
+  int64_t iters_done = 0;
+  double last_ms = 0.0, warm_ms = 0.0, sample_ms = 0.0;
+  int64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int32_t guarded(pcvg_ctx* ctx, F&& f) {
+  try {
+    f();
+    return PCVG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    if (ctx) ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    if (ctx) ctx->err = e.what();
+    return PCVG_INVALID_INPUT;
+  }
+}
+
+int n_groups(const pcvg_dataset* d) {
+  int j = 0;
+  for (int64_t i = 0; i < d->n_obs; ++i) j = std::max(j, d->group_id[i] + 1);
+  return j;
+}
+
+// Device layout of one model.
+std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* f,
+                                       const pcvg_model_spec* s, const pcvg_kernel* kp,
+                                       const double* bank, int64_t bank_rows, int model_id) {
+  if (!d || !f || !s || !kp) throw Error(PCVG_INVALID_INPUT, "null descriptor");
+  if (d->n_obs < 1) throw Error(PCVG_INVALID_INPUT, "dataset is empty");
+  if (d->n_obs > (1LL << 30)) throw Error(PCVG_INVALID_INPUT, "dataset too large for int32 row ids");
+  auto hm = std::make_unique<HostModel>();
+  HostModel& m = *hm;
+  const int64_t n = d->n_obs;
+  m.family = s->family;
+  m.n = n;
+  m.K = f->K;
+  m.model_id = model_id;
+  m.hv = f->intervals != nullptr;
+  if (!f->test_index && !f->intervals) throw Error(PCVG_INVALID_INPUT, "folds need test_index or intervals");
+  if (f->K < 1) throw Error(PCVG_INVALID_INPUT, "fold count must be at least 1");
+  const bool hier = s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON;
+  if (d->group_id) {  // Dataset::validate (dataset.cpp:19-39)
+    std::vector<char> seen(n_groups(d), 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (d->group_id[i] < 0) throw Error(PCVG_INVALID_INPUT, "group ids must be 0-based");
+      seen[d->group_id[i]] = 1;
+    }
+    for (char c : seen)
+      if (!c) throw Error(PCVG_INVALID_INPUT, "group ids must form a contiguous 0..J-1 range");
+  }
+  switch (s->family) {
+    case PCVG_FAMILY_GROUPED:
+      if (!d->group_id) throw Error(PCVG_INVALID_INPUT, "grouped regression needs a group column");
+      if (d->n_cov > 8) throw Error(PCVG_INVALID_INPUT, "grouped family supports at most 8 covariates on device");
+      m.J = n_groups(d);
+      m.nc = d->n_cov;
+      m.ng = d->n_cov + 3;
+      break;
+    case PCVG_FAMILY_RADON:
+      if (!d->group_id || d->n_cov < 1)
+        throw Error(PCVG_INVALID_INPUT, "radon-style model needs a group column and a floor covariate");
+      m.J = n_groups(d);
+      m.nc = 1;
+      m.ng = 4;
+      break;
+    case PCVG_FAMILY_SEASONAL_AR:
+      if (s->ar_order < 1) throw Error(PCVG_INVALID_INPUT, "AR order must be at least 1");
+      if (s->dummies < 0) throw Error(PCVG_INVALID_INPUT, "dummy count must be non-negative");
+      if (d->n_cov < s->ar_order + s->dummies)
+        throw Error(PCVG_INVALID_INPUT, "dataset must carry lag and dummy covariates");
+      if (s->ar_order + s->dummies > 13) throw Error(PCVG_INVALID_INPUT, "seasonal family supports p + q <= 13 on device");
+      m.J = 0;
+      m.nc = s->ar_order + s->dummies;
+      m.ng = m.nc + 2;
+      break;
+    case PCVG_FAMILY_LOGISTIC:
+      if (d->n_cov > 51) throw Error(PCVG_INVALID_INPUT, "logistic family supports at most 51 covariates on device");
+      m.J = 0;
+      m.nc = d->n_cov;
+      m.ng = d->n_cov + 1;
+      break;
+    default:
+      throw Error(PCVG_INVALID_INPUT, "model family not available on device (rat-growth is a next-round item)");
+  }
+  m.dim = m.J + m.ng;
+  if (!kp->inv_mass_diag) throw Error(PCVG_INVALID_INPUT, "inverse mass diagonal missing");
+  if (kp->n_leapfrog < 1) throw Error(PCVG_INVALID_INPUT, "n_leapfrog must be >= 1");
+  for (int i = 0; i < m.dim; ++i)
+    if (!(kp->inv_mass_diag[i] > 0.0)) throw Error(PCVG_INVALID_INPUT, "inverse mass diagonal must be positive");
+  if (!bank || bank_rows < 1) throw Error(PCVG_INVALID_INPUT, "empty full-data draw bank");
+
+  // time rank (hv folds)
+  std::vector<int64_t> rank;
+  if (m.hv) {
+    if (!d->time_index) throw Error(PCVG_INVALID_INPUT, "hv-block folds need a time column");
+    const auto order = time_order(d->time_index, n);
+    rank.assign(n, 0);
+    for (int64_t r = 0; r < n; ++r) rank[order[r]] = r;
+  }
+  // fold validation (folds.cpp:25-41 / hv analogue)
+  std::vector<int64_t> test_count(m.K, 0);
+  if (!m.hv) {
+    for (int64_t i = 0; i < n; ++i) {
+      const int t = f->test_index[i];
+      if (t < 0 || t >= m.K) throw Error(PCVG_INVALID_INPUT, "test_index out of range");
+      ++test_count[t];
+    }
+    for (int k = 0; k < m.K; ++k) {
+      if (test_count[k] == 0) throw Error(PCVG_INVALID_INPUT, "fold " + std::to_string(k) + " has empty test set");
+      if (test_count[k] == n) throw Error(PCVG_INVALID_INPUT, "fold " + std::to_string(k) + " has empty training set");
+    }
+  } else {
+    for (int k = 0; k < m.K; ++k) {
+      const int64_t* iv = f->intervals + 4 * k;
+      if (!(0 <= iv[2] && iv[2] <= iv[0] && iv[0] < iv[1] && iv[1] <= iv[3] && iv[3] <= n))
+        throw Error(PCVG_INVALID_INPUT, "hv-block fold " + std::to_string(k) + " has a malformed interval");
+      if (iv[3] - iv[2] >= n) throw Error(PCVG_INVALID_INPUT, "fold " + std::to_string(k) + " has empty training set");
+    }
+  }
+
+  // device row order: group-major for hierarchical families (stable)
+  m.perm.resize(n);
+  std::iota(m.perm.begin(), m.perm.end(), 0);
+  std::vector<int> grp_ptr;
+  if (hier) {
+    std::stable_sort(m.perm.begin(), m.perm.end(),
+                     [&](int a, int b) { return d->group_id[a] < d->group_id[b]; });
+    grp_ptr.assign(m.J + 1, 0);
+    for (int64_t i = 0; i < n; ++i) ++grp_ptr[d->group_id[i] + 1];
+    for (int g = 0; g < m.J; ++g) grp_ptr[g + 1] += grp_ptr[g];
+  }
+  std::vector<int> inv(n);
+  for (int64_t r = 0; r < n; ++r) inv[m.perm[r]] = static_cast<int>(r);
+
+  const bool logistic = s->family == PCVG_FAMILY_LOGISTIC;
+  const int64_t n_pad = logistic ? ((n + 63) / 64) * 64 : n;
+  std::vector<double> y(n_pad, 0.0);
+  std::vector<int> key(n_pad, -1);
+  std::vector<double> xc(static_cast<size_t>(std::max(m.nc, 1)) * n, 0.0);
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t i = m.perm[r];
+    y[r] = d->y[i];
+    key[r] = m.hv ? static_cast<int>(rank[i]) : f->test_index[i];
+    for (int c = 0; c < m.nc; ++c) xc[static_cast<size_t>(c) * n + r] = d->x[i * d->n_cov + c];
+  }
+  m.y.upload(y);
+  m.key.upload(key);
+  m.x.upload(xc);
+  int nc_pad = 0;
+  if (logistic) {
+    nc_pad = 52;
+    std::vector<double> xr(static_cast<size_t>(n_pad) * nc_pad, 0.0);
+    for (int64_t r = 0; r < n; ++r) {
+      xr[r * nc_pad] = 1.0;
+      for (int c = 0; c < m.nc; ++c) xr[r * nc_pad + 1 + c] = d->x[m.perm[r] * d->n_cov + c];
+    }
+    m.xr.upload(xr);
+  }
+  m.grp_ptr.upload(hier ? grp_ptr : std::vector<int>{0});
+
+  // fold tables (index K = sentinel: nothing held out)
+  std::vector<int> lo(m.K + 1, 0), hi(m.K + 1, 0), ntr(m.K + 1, static_cast<int>(n));
+  for (int k = 0; k < m.K; ++k) {
+    if (m.hv) {
+      lo[k] = static_cast<int>(f->intervals[4 * k + 2]);
+      hi[k] = static_cast<int>(f->intervals[4 * k + 3]);
+      ntr[k] = static_cast<int>(n - (hi[k] - lo[k]));
+    } else {
+      lo[k] = k;
+      hi[k] = k + 1;
+      ntr[k] = static_cast<int>(n - test_count[k]);
+    }
+  }
+  m.lo.upload(lo);
+  m.hi.upload(hi);
+  m.ntrain.upload(ntr);
+
+  // test segments (fold_meta_, grouped_regression.cpp:27-47): test rows grouped by group in
+  // increasing group order, rows increasing within a group; unseen = no training row in group.
+  const int Jg = hier ? m.J : 1;
+  std::vector<int64_t> gsize(Jg, 0);
+  for (int64_t i = 0; i < n; ++i) gsize[hier ? d->group_id[i] : 0]++;
+  std::vector<int> bucket_ptr, bucket_rows;
+  if (!m.hv) {
+    bucket_ptr.assign(m.K + 1, 0);
+    bucket_rows.resize(n);
+    for (int64_t i = 0; i < n; ++i) ++bucket_ptr[f->test_index[i] + 1];
+    for (int k = 0; k < m.K; ++k) bucket_ptr[k + 1] += bucket_ptr[k];
+    std::vector<int> fill(bucket_ptr.begin(), bucket_ptr.end() - 1);
+    for (int64_t i = 0; i < n; ++i) bucket_rows[fill[f->test_index[i]]++] = static_cast<int>(i);
+  }
+  std::vector<int> seg_group, seg_unseen, seg_rows;
+  m.fold_seg.assign(m.K + 2, 0);
+  m.seg_row.assign(1, 0);
+  std::vector<int64_t> excl(Jg, 0), cnt(Jg, 0), start(Jg, 0);
+  std::vector<int> tmp, order_rows;
+  for (int k = 0; k < m.K; ++k) {
+    m.fold_seg[k] = static_cast<int>(seg_group.size());
+    tmp.clear();
+    if (!m.hv) {
+      for (int t = bucket_ptr[k]; t < bucket_ptr[k + 1]; ++t) tmp.push_back(bucket_rows[t]);
+    } else {
+      for (int64_t i = 0; i < n; ++i)
+        if (rank[i] >= f->intervals[4 * k] && rank[i] < f->intervals[4 * k + 1]) tmp.push_back(static_cast<int>(i));
+    }
+    std::fill(excl.begin(), excl.end(), 0);
+    std::fill(cnt.begin(), cnt.end(), 0);
+    if (!m.hv) {
+      for (int i : tmp) excl[hier ? d->group_id[i] : 0]++;
+    } else if (hier) {
+      for (int64_t i = 0; i < n; ++i)
+        if (rank[i] >= f->intervals[4 * k + 2] && rank[i] < f->intervals[4 * k + 3]) excl[d->group_id[i]]++;
+    }
+    for (int i : tmp) cnt[hier ? d->group_id[i] : 0]++;
+    int64_t acc = 0;
+    for (int g = 0; g < Jg; ++g) {
+      start[g] = acc;
+      acc += cnt[g];
+    }
+    order_rows.assign(tmp.size(), 0);
+    for (int i : tmp) order_rows[start[hier ? d->group_id[i] : 0]++] = i;
+    size_t off = 0;
+    for (int g = 0; g < Jg; ++g) {
+      if (cnt[g] == 0) continue;
+      seg_group.push_back(hier ? g : -1);
+      seg_unseen.push_back(hier ? (gsize[g] - excl[g] == 0 ? 1 : 0) : 0);
+      for (int64_t t = 0; t < cnt[g]; ++t) seg_rows.push_back(inv[order_rows[off + t]]);
+      off += cnt[g];
+      m.seg_row.push_back(static_cast<int>(seg_rows.size()));
+    }
+  }
+  m.fold_seg[m.K] = static_cast<int>(seg_group.size());
+  m.fold_seg[m.K + 1] = static_cast<int>(seg_group.size());
+  m.fseg.upload(m.fold_seg);
+  m.sgroup.upload(seg_group.empty() ? std::vector<int>{0} : seg_group);
+  m.sunseen.upload(seg_unseen.empty() ? std::vector<int>{0} : seg_unseen);
+  m.srow.upload(m.seg_row);
+  m.srows.upload(seg_rows.empty() ? std::vector<int>{0} : seg_rows);
+
+  m.inv_mass.upload(std::vector<double>(kp->inv_mass_diag, kp->inv_mass_diag + m.dim));
+  m.bank.upload(std::vector<double>(bank, bank + bank_rows * m.dim));
+  m.bank_rows = bank_rows;
+
+  ModelDev& md = m.md;
+  md.family = s->family;
+  md.n = static_cast<int>(n);
+  md.nc = m.nc;
+  md.J = m.J;
+  md.ng = m.ng;
+  md.dim = m.dim;
+  md.K = m.K;
+  md.y = m.y.p;
+  md.x = m.x.p;
+  md.xr = m.xr.p;
+  md.nc_pad = nc_pad;
+  md.key = m.key.p;
+  md.grp_ptr = m.grp_ptr.p;
+  md.fold_lo = m.lo.p;
+  md.fold_hi = m.hi.p;
+  md.n_train = m.ntrain.p;
+  md.fold_seg = m.fseg.p;
+  md.seg_group = m.sgroup.p;
+  md.seg_unseen = m.sunseen.p;
+  md.seg_row = m.srow.p;
+  md.seg_rows = m.srows.p;
+  md.inv_mass = m.inv_mass.p;
+  md.step = kp->step_size;
+  md.n_lf = kp->n_leapfrog;
+  for (int c = 0; c < kMaxCov; ++c)
+    md.cmask[c] = (s->family == PCVG_FAMILY_GROUPED && c < m.nc)
+                      ? ((s->covariate_mask == nullptr || s->covariate_mask[c]) ? 1.0 : 0.0)
+                      : 0.0;
+  md.include_floor = s->include_floor != 0;
+  md.p = s->ar_order;
+  md.q = s->dummies;
+  md.rho_sym = s->rho_transform == PCVG_RHO_SYMMETRIC;
+  // prior normalising constants with glibc (priors.hpp:13-26)
+  md.c_lhn10 = 0.5 * std::log(2.0 / (3.141592653589793238462643383279 * 10.0));
+  md.c_lhn1 = 0.5 * std::log(2.0 / (3.141592653589793238462643383279 * 1.0));
+  md.c_lgamma6_9 = 6.0 * std::log(9.0) - std::lgamma(6.0);
+  md.c_lgamma10_10 = 10.0 * std::log(10.0) - std::lgamma(10.0);
+  md.c_lbeta55 = std::lgamma(10.0) - std::lgamma(5.0) - std::lgamma(5.0);
+  md.c_log4 = std::log(4.0);
+  return hm;
+}
+
+void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const RunArgs& A) {
+  cudaError_t e;
+  if (m.family == PCVG_FAMILY_LOGISTIC) {
+    e = launch_logistic(m.md, S, A, ctx->stream);
+  } else {
+    const int T = gauss_lanes_per_chain(m.md, S.nch);
+    e = launch_gauss(m.md, S, A, T, ctx->stream);
+  }
+  ++ctx->launches;
+  ck(e, "kernel launch");
+}
+
+RunArgs make_args(int mode, int64_t n_iters) {
+  RunArgs a{};
+  a.mode = mode;
+  a.n_iters = n_iters;
+  return a;
+}
+
+int effective_batch(const pcvg_run_config* c) {  // engine.cpp:5-9
+  if (c->batch_size > 0) return c->batch_size;
+  return std::max(1, static_cast<int>(std::sqrt(static_cast<double>(c->iters) * c->chains)));
+}
+
+void validate_run(const pcvg_ctx* ctx, const pcvg_run_config* c) {
+  if (!c) throw Error(PCVG_INVALID_INPUT, "null run config");
+  // RunConfig::validate, engine.cpp:21-30
+  if (c->chains < 2) throw Error(PCVG_INVALID_INPUT, "need at least 2 chains per fold (Rhat)");
+  if (c->iters < 1) throw Error(PCVG_INVALID_INPUT, "need at least 1 sampling iteration");
+  if (c->warmup < 0) throw Error(PCVG_INVALID_INPUT, "warmup must be non-negative");
+  if (c->iters < effective_batch(c)) throw Error(PCVG_INVALID_INPUT, "chain length must cover at least one batch");
+  if (c->blocks < 1) throw Error(PCVG_INVALID_INPUT, "need at least 1 shuffle block");
+  if (c->bench_draws < 1) throw Error(PCVG_INVALID_INPUT, "need at least 1 benchmark draw");
+  if (c->checkpoint_every < 0) throw Error(PCVG_INVALID_INPUT, "checkpoint_every must be >= 0");
+  if (c->chains > 64) throw Error(PCVG_INVALID_INPUT, "at most 64 chains per fold on device");
+  // run_pcv preconditions, engine.cpp:258-271
+  if (ctx->models.empty() || ctx->models.size() > 2)
+    throw Error(PCVG_INVALID_INPUT, "run_pcv takes one or two models");
+  const int K = ctx->models[0]->K;
+  for (const auto& m : ctx->models)
+    if (m->K != K) throw Error(PCVG_INVALID_INPUT, "models must share one fold assignment");
+  if (c->score == PCVG_SCORE_HS || c->score == PCVG_SCORE_DSS)
+    throw Error(PCVG_UNSUPPORTED_SCORE, "score hs/dss is not yet implemented on device (LogS only)");
+  if (c->score != PCVG_SCORE_LOGS) throw Error(PCVG_INVALID_INPUT, "unknown score");
+  if (K < 2) throw Error(PCVG_INVALID_INPUT, "uncertainty estimates need at least 2 folds");
+  if (c->fold_begin < 0 || c->fold_end < c->fold_begin || c->fold_end > K)
+    throw Error(PCVG_INVALID_INPUT, "bad fold shard");
+  if (c->early_stop) {
+    if (c->checkpoint_every <= 0 || c->iters % c->checkpoint_every != 0)
+      throw Error(PCVG_INVALID_INPUT, "early_stop needs checkpoint_every dividing iters");
+  }
+}
+
+void require_device(pcvg_ctx* ctx) {
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pcvg_abi_version(void) { return PCVG_ABI_VERSION; }
+
+const char* pcvg_last_error(const pcvg_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+const char* pcvg_status_name(int32_t s) {
+  switch (s) {
+    case PCVG_OK: return "ok";
+    case PCVG_INVALID_INPUT: return "invalid_input";
+    case PCVG_NUMERIC_FAULT: return "numeric_fault";
+    case PCVG_ADAPTATION_FAILURE: return "adaptation_failure";
+    case PCVG_UNDEFINED_DIAGNOSTIC: return "undefined_diagnostic";
+    case PCVG_UNSUPPORTED_SCORE: return "unsupported_score";
+    case PCVG_CUDA_ERROR: return "cuda_error";
+    case PCVG_COMM_ERROR: return "comm_error";
+  }
+  return "unknown";
+}
+
+pcvg_status pcvg_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
+                              const uint64_t* arg, int64_t n, double* out) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { rng_sequence(seed, stream, skip_block, ops, arg, n, out); }));
+}
+pcvg_status pcvg_make_loo(int64_t n, int32_t* ti, int32_t* K) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { make_loo(n, ti, K); }));
+}
+pcvg_status pcvg_make_logo(const pcvg_dataset* d, int32_t* ti, int32_t* K) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { make_logo(d, ti, K); }));
+}
+pcvg_status pcvg_make_kfold(int64_t n, int32_t K, uint64_t seed, int32_t* ti) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { make_kfold(n, K, seed, ti); }));
+}
+pcvg_status pcvg_make_time_blocks(const pcvg_dataset* d, int32_t K, int32_t* ti) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { make_time_blocks(d, K, ti); }));
+}
+pcvg_status pcvg_make_hv_block(const pcvg_dataset* d, int32_t K, int64_t h, int64_t* iv) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { make_hv_block(d, K, h, iv); }));
+}
+pcvg_status pcvg_make_hv_racine(const pcvg_dataset* d, int64_t v, int64_t h, int64_t* iv) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { make_hv_racine(d, v, h, iv); }));
+}
+pcvg_status pcvg_simulate_grouped(int32_t J, int32_t Nj, int32_t P, double mb, uint64_t seed,
+                                  double* y, double* x, int32_t* g) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_grouped(J, Nj, P, mb, seed, y, x, g); }));
+}
+pcvg_status pcvg_simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y,
+                                double* x, int32_t* g) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_radon(houses, counties, seed, y, x, g); }));
+}
+pcvg_status pcvg_simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho, double amp,
+                                   double sigma, uint64_t seed, double* y, double* x, int64_t* t) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_seasonal(months, p, q, rho, amp, sigma, seed, y, x, t); }));
+}
+pcvg_status pcvg_simulate_linreg(int64_t n, int32_t P, uint64_t seed, double* y, double* x, int32_t* g) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_linreg(n, P, seed, y, x, g); }));
+}
+pcvg_status pcvg_simulate_logistic(int64_t n, int32_t P, uint64_t seed, double* y, double* x) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_logistic(n, P, seed, y, x); }));
+}
+
+pcvg_status pcvg_create(int32_t device, pcvg_ctx** out) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] {
+    if (!out) throw Error(PCVG_INVALID_INPUT, "null output");
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "no CUDA device (the PCV sampler has no CPU fallback)");
+    if (device < 0 || device >= count) throw Error(PCVG_CUDA_ERROR, "device index out of range");
+    auto ctx = std::make_unique<pcvg_ctx>();
+    ctx->device = device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreate(&ctx->ev0), "cudaEventCreate");
+    ck(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
+    *out = ctx.release();
+  }));
+}
+
+pcvg_status pcvg_destroy(pcvg_ctx* ctx) {
+  if (!ctx) return PCVG_OK;
+  cudaSetDevice(ctx->device);
+  ctx->chains.clear();
+  ctx->centers.clear();
+  ctx->models.clear();
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PCVG_OK;
+}
+
+pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_folds* folds,
+                           const pcvg_model_spec* spec, const pcvg_kernel* kernel,
+                           const double* bank, int64_t bank_rows, int32_t model_id, int32_t* slot) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx) throw Error(PCVG_INVALID_INPUT, "null context");
+    if (ctx->models.size() >= 2) throw Error(PCVG_INVALID_INPUT, "run_pcv takes one or two models");
+    require_device(ctx);
+    ctx->models.push_back(build_model(data, folds, spec, kernel, bank, bank_rows, model_id));
+    ctx->begun = false;
+    if (slot) *slot = static_cast<int32_t>(ctx->models.size() - 1);
+  }));
+}
+
+pcvg_status pcvg_model_dim(const pcvg_ctx* ctx, int32_t slot, int32_t* dim) {
+  if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size()) || !dim) return PCVG_INVALID_INPUT;
+  *dim = ctx->models[slot]->dim;
+  return PCVG_OK;
+}
+
+pcvg_status pcvg_model_test_size(const pcvg_ctx* ctx, int32_t slot, int32_t fold, int64_t* n) {
+  if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size()) || !n) return PCVG_INVALID_INPUT;
+  const HostModel& m = *ctx->models[slot];
+  if (fold < 0 || fold > m.K) return PCVG_INVALID_INPUT;
+  *n = fold == m.K ? 0 : m.seg_row[m.fold_seg[fold + 1]] - m.seg_row[m.fold_seg[fold]];
+  return PCVG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Temporary chain set for the parity probes: n chains at explicit (fold, theta).
+std::unique_ptr<ChainSet> probe_chains(pcvg_ctx* ctx, const HostModel& m, int64_t n,
+                                       const int32_t* fold, const double* theta) {
+  for (int64_t i = 0; i < n; ++i)
+    if (fold[i] < 0 || fold[i] > m.K) throw Error(PCVG_INVALID_INPUT, "fold id out of range (0..K)");
+  auto cs = std::make_unique<ChainSet>();
+  cs->alloc(static_cast<int>(n), m.dim, 1);
+  std::vector<double> pos(2 * static_cast<size_t>(m.dim) * n, 0.0);
+  for (int64_t c = 0; c < n; ++c)
+    for (int d = 0; d < m.dim; ++d) pos[static_cast<size_t>(d) * n + c] = theta[c * m.dim + d];
+  ck(cudaMemcpy(cs->pos.p, pos.data(), sizeof(double) * pos.size(), cudaMemcpyHostToDevice), "upload");
+  ck(cudaMemset(cs->grad.p, 0, sizeof(double) * cs->grad.n), "memset");
+  ck(cudaMemset(cs->cur.p, 0, n), "memset");
+  ck(cudaMemset(cs->rpos.p, 0, sizeof(uint64_t) * n), "memset");
+  ck(cudaMemset(cs->has.p, 0, n), "memset");
+  ck(cudaMemset(cs->cached.p, 0, sizeof(double) * n), "memset");
+  ck(cudaMemset(cs->div.p, 0, sizeof(int64_t) * n), "memset");
+  ck(cudaMemset(cs->warm.p, 0, sizeof(double) * n), "memset");
+  ck(cudaMemset(cs->stream.p, 0, sizeof(uint64_t) * n), "memset");
+  cs->fold_override.upload(std::vector<int>(fold, fold + n));
+  (void)ctx;
+  return cs;
+}
+
+}  // namespace
+
+extern "C" {
+
+pcvg_status pcvg_eval(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t* fold,
+                      const double* theta, double* log_joint, double* grad) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size())) throw Error(PCVG_INVALID_INPUT, "bad slot");
+    require_device(ctx);
+    const HostModel& m = *ctx->models[slot];
+    if (n < 1) return;
+    auto cs = probe_chains(ctx, m, n, fold, theta);
+    DevBuf<double> out;
+    out.alloc(n);
+    RunArgs a = make_args(kModeEval, 0);
+    a.out_a = out.p;
+    launch_family(ctx, m, cs->view(1, 0, 0, 0), a);
+    ck(cudaStreamSynchronize(ctx->stream), "eval");
+    const auto lj = out.download(ctx->stream);
+    const auto g = cs->grad.download(ctx->stream);
+    for (int64_t c = 0; c < n; ++c) {
+      if (log_joint) log_joint[c] = lj[c];
+      if (grad)
+        for (int d = 0; d < m.dim; ++d) grad[c * m.dim + d] = g[static_cast<size_t>(d) * n + c];
+    }
+  }));
+}
+
+pcvg_status pcvg_eval_pred(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t* fold,
+                           const double* theta, double* log_pred) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size())) throw Error(PCVG_INVALID_INPUT, "bad slot");
+    require_device(ctx);
+    const HostModel& m = *ctx->models[slot];
+    if (n < 1) return;
+    auto cs = probe_chains(ctx, m, n, fold, theta);
+    DevBuf<double> out;
+    out.alloc(n);
+    RunArgs a = make_args(kModePred, 1);
+    a.out_a = out.p;
+    launch_family(ctx, m, cs->view(1, 0, 0, 0), a);
+    ck(cudaStreamSynchronize(ctx->stream), "eval_pred");
+    const auto lp = out.download(ctx->stream);
+    std::copy(lp.begin(), lp.end(), log_pred);
+  }));
+}
+
+pcvg_status pcvg_hmc_probe(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t* fold,
+                           const double* theta, const double* momentum, const double* u,
+                           double* theta_out, double* h0, double* h1, int32_t* accepted,
+                           int32_t* divergent) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size())) throw Error(PCVG_INVALID_INPUT, "bad slot");
+    require_device(ctx);
+    const HostModel& m = *ctx->models[slot];
+    if (n < 1) return;
+    auto cs = probe_chains(ctx, m, n, fold, theta);
+    const ChainsDev S = cs->view(1, 0, 0, 0);
+    launch_family(ctx, m, S, make_args(kModeEval, 0));
+    DevBuf<double> mom, uu, oa, ob;
+    DevBuf<int32_t> fl;
+    mom.upload(std::vector<double>(momentum, momentum + n * m.dim));
+    uu.upload(std::vector<double>(u, u + n));
+    oa.alloc(n);
+    ob.alloc(n);
+    fl.alloc(n);
+    RunArgs a = make_args(kModeProbe, 1);
+    a.probe_momentum = mom.p;
+    a.probe_u = uu.p;
+    a.out_a = oa.p;
+    a.out_b = ob.p;
+    a.out_flags = fl.p;
+    launch_family(ctx, m, S, a);
+    ck(cudaStreamSynchronize(ctx->stream), "hmc_probe");
+    const auto a0 = oa.download(ctx->stream), b0 = ob.download(ctx->stream);
+    const auto f0 = fl.download(ctx->stream);
+    const auto pos = cs->pos.download(ctx->stream);
+    const auto cur = cs->cur.download(ctx->stream);
+    const size_t plane = static_cast<size_t>(m.dim) * n;
+    for (int64_t c = 0; c < n; ++c) {
+      if (h0) h0[c] = a0[c];
+      if (h1) h1[c] = b0[c];
+      if (accepted) accepted[c] = f0[c] & 1;
+      if (divergent) divergent[c] = (f0[c] >> 1) & 1;
+      for (int d = 0; d < m.dim; ++d) theta_out[c * m.dim + d] = pos[cur[c] * plane + static_cast<size_t>(d) * n + c];
+    }
+  }));
+}
+
+pcvg_status pcvg_hmc_chain(pcvg_ctx* ctx, int32_t slot, int32_t fold, int32_t chain, uint64_t seed,
+                           const double* theta0, int64_t n_steps, double* trajectory,
+                           int32_t* divergent) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size())) throw Error(PCVG_INVALID_INPUT, "bad slot");
+    require_device(ctx);
+    const HostModel& m = *ctx->models[slot];
+    if (n_steps < 1) return;
+    auto cs = probe_chains(ctx, m, 1, &fold, theta0);
+    const uint64_t st = stream_key(PCVG_STREAM_CHAIN_SAMPLING, static_cast<uint64_t>(m.model_id),
+                                   static_cast<uint64_t>(fold), static_cast<uint64_t>(chain));
+    ck(cudaMemcpy(cs->stream.p, &st, sizeof st, cudaMemcpyHostToDevice), "upload");
+    ChainsDev S = cs->view(1, 0, seed, static_cast<uint64_t>(m.model_id));
+    launch_family(ctx, m, S, make_args(kModeEval, 0));
+    DevBuf<double> tr;
+    DevBuf<int32_t> dv;
+    tr.alloc(static_cast<size_t>(n_steps) * m.dim);
+    dv.alloc(n_steps);
+    RunArgs a = make_args(kModeChain, n_steps);
+    a.traj = tr.p;
+    a.traj_div = dv.p;
+    launch_family(ctx, m, S, a);
+    ck(cudaStreamSynchronize(ctx->stream), "hmc_chain");
+    const auto t = tr.download(ctx->stream);
+    const auto d = dv.download(ctx->stream);
+    std::copy(t.begin(), t.end(), trajectory);
+    if (divergent) std::copy(d.begin(), d.end(), divergent);
+  }));
+}
+
+int32_t pcvg_checkpoint_count(const pcvg_run_config* cfg) {  // engine.cpp:279-283
+  if (!cfg || cfg->iters < 1) return 0;
+  int32_t n = 0;
+  if (cfg->checkpoint_every > 0)
+    for (int64_t t = cfg->checkpoint_every; t < cfg->iters; t += cfg->checkpoint_every) ++n;
+  return n + 1;
+}
+
+pcvg_status pcvg_begin(pcvg_ctx* ctx, const pcvg_run_config* cfg) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx) throw Error(PCVG_INVALID_INPUT, "null context");
+    validate_run(ctx, cfg);
+    require_device(ctx);
+    ctx->cfg = *cfg;
+    ctx->b = effective_batch(cfg);
+    const int K = ctx->models[0]->K;
+    ctx->fb = cfg->fold_begin;
+    ctx->fe = (cfg->fold_begin == 0 && cfg->fold_end == 0) ? K : cfg->fold_end;
+    const int nfold = ctx->fe - ctx->fb;
+    const int L = cfg->chains;
+    const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
+    ctx->chains.clear();
+    ctx->centers.clear();
+    ctx->div_base.clear();
+    ctx->iters_done = 0;
+    ctx->sample_ms = 0.0;
+    ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
+    for (const auto& mp : ctx->models) {
+      const HostModel& m = *mp;
+      auto cs = std::make_unique<ChainSet>();
+      cs->alloc(nfold * L, m.dim, D);
+      const uint64_t sm = cfg->shared_streams ? 0u : static_cast<uint64_t>(m.model_id);
+      const ChainsDev S = cs->view(L, ctx->fb, cfg->seed, sm);
+      ck(launch_init_chains(m.md, S, m.bank.p, m.bank_rows, ctx->stream), "init_chains");
+      ++ctx->launches;
+      launch_family(ctx, m, S, make_args(kModeEval, 0));
+      if (cfg->warmup > 0) {
+        RunArgs a = make_args(kModeWarmup, cfg->warmup);
+        launch_family(ctx, m, S, a);
+      }
+      auto centers = std::make_unique<DevBuf<double>>();
+      centers->alloc(std::max(nfold, 1));
+      ck(launch_centers(S, nfold, cfg->warmup, centers->p, D, ctx->stream), "centers");
+      ctx->launches += 2;
+      ctx->chains.push_back(std::move(cs));
+      ctx->centers.push_back(std::move(centers));
+    }
+    ck(cudaEventRecord(ctx->ev1, ctx->stream), "event");
+    ck(cudaEventSynchronize(ctx->ev1), "warmup");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->warm_ms = ms;
+    for (const auto& cs : ctx->chains) ctx->div_base.push_back(cs->div.download(ctx->stream));
+    ctx->begun = true;
+  }));
+}
+
+pcvg_status pcvg_advance(pcvg_ctx* ctx, int64_t n_iters) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !ctx->begun) throw Error(PCVG_INVALID_INPUT, "pcvg_begin first");
+    if (n_iters < 0 || ctx->iters_done + n_iters > ctx->cfg.iters)
+      throw Error(PCVG_INVALID_INPUT, "advance past the planned chain length");
+    require_device(ctx);
+    const pcvg_run_config& cfg = ctx->cfg;
+    ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
+    for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+      const HostModel& m = *ctx->models[mi];
+      const uint64_t sm = cfg.shared_streams ? 0u : static_cast<uint64_t>(m.model_id);
+      const ChainsDev S = ctx->chains[mi]->view(cfg.chains, ctx->fb, cfg.seed, sm);
+      RunArgs a = make_args(kModeSample, n_iters);
+      a.iter0 = ctx->iters_done;
+      a.planned_n = cfg.iters;
+      a.D = ctx->chains[mi]->D;
+      a.b = ctx->b;
+      if (n_iters > 0) launch_family(ctx, m, S, a);
+    }
+    ck(cudaEventRecord(ctx->ev1, ctx->stream), "event");
+    ck(cudaEventSynchronize(ctx->ev1), "advance");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->last_ms = ms;
+    ctx->sample_ms += ms;
+    ctx->iters_done += n_iters;
+  }));
+}
+
+pcvg_status pcvg_fold_stats(pcvg_ctx* ctx, pcvg_fold_table* out, int64_t* divergences,
+                            int64_t* dropped, int64_t* iters_done) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !ctx->begun) throw Error(PCVG_INVALID_INPUT, "pcvg_begin first");
+    if (ctx->iters_done < 1) throw Error(PCVG_INVALID_INPUT, "no sampling iterations yet");
+    require_device(ctx);
+    const pcvg_run_config& cfg = ctx->cfg;
+    const int nfold = ctx->fe - ctx->fb, L = cfg.chains;
+    const int nm = static_cast<int>(ctx->models.size());
+    std::vector<std::vector<int64_t>> sdiv(nm);
+    int64_t drop = 0;
+    for (int mi = 0; mi < nm; ++mi) {
+      const ChainSet& cs = *ctx->chains[mi];
+      const ChainsDev S = cs.view(L, ctx->fb, cfg.seed, 0);
+      DevBuf<double> est, lf, mc, nv, ess, rh;
+      DevBuf<int64_t> bt;
+      DevBuf<int32_t> ft;
+      est.alloc(nfold); lf.alloc(nfold); mc.alloc(nfold); nv.alloc(nfold); ess.alloc(nfold); rh.alloc(nfold);
+      bt.alloc(nfold); ft.alloc(nfold);
+      ck(launch_fold_stats(S, nfold, ctx->iters_done, ctx->b, cs.D, est.p, lf.p, mc.p, nv.p, ess.p, rh.p, bt.p, ft.p, ctx->stream), "fold_stats");
+      ++ctx->launches;
+      const auto e = est.download(ctx->stream), l = lf.download(ctx->stream), c = mc.download(ctx->stream),
+                 v = nv.download(ctx->stream), s = ess.download(ctx->stream), r = rh.download(ctx->stream);
+      const auto b = bt.download(ctx->stream);
+      const auto f = ft.download(ctx->stream);
+      const size_t off = static_cast<size_t>(mi) * nfold;
+      for (int k = 0; k < nfold; ++k) {
+        if (out->estimate) out->estimate[off + k] = e[k];
+        if (out->log_f_hat) out->log_f_hat[off + k] = l[k];
+        if (out->mc_contribution) out->mc_contribution[off + k] = c[k];
+        if (out->naive_contribution) out->naive_contribution[off + k] = v[k];
+        if (out->ess) out->ess[off + k] = s[k];
+        if (out->rhat) out->rhat[off + k] = r[k];
+        if (out->batches) out->batches[off + k] = b[k];
+        if (out->fault) out->fault[off + k] = f[k];
+      }
+      const auto dv = cs.div.download(ctx->stream);
+      sdiv[mi].resize(dv.size());
+      for (size_t i = 0; i < dv.size(); ++i) sdiv[mi][i] = dv[i] - ctx->div_base[mi][i];
+      if (divergences)
+        for (size_t i = 0; i < dv.size(); ++i) divergences[off * L + i] = sdiv[mi][i];
+      const auto pend = cs.pending.download(ctx->stream);
+      for (int32_t p : pend) drop += p;
+    }
+    // failed folds (engine.cpp:385-397): every chain of some model divergent on > N/2 iterations
+    if (out->failed) {
+      for (int k = 0; k < nfold; ++k) {
+        bool failed = false;
+        for (int mi = 0; mi < nm && !failed; ++mi) {
+          bool all_bad = true;
+          for (int c = 0; c < L; ++c)
+            if (sdiv[mi][k * L + c] * 2 <= cfg.iters) { all_bad = false; break; }
+          failed = all_bad;
+        }
+        for (int mi = 0; mi < nm; ++mi) out->failed[static_cast<size_t>(mi) * nfold + k] = failed ? 1 : 0;
+      }
+    }
+    if (dropped) *dropped = drop;
+    if (iters_done) *iters_done = ctx->iters_done;
+  }));
+}
+
+pcvg_status pcvg_block_sums(pcvg_ctx* ctx, double* y_x, double* y_x2) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !ctx->begun) throw Error(PCVG_INVALID_INPUT, "pcvg_begin first");
+    require_device(ctx);
+    size_t off = 0;
+    for (const auto& cs : ctx->chains) {
+      const auto a = cs->y_x.download(ctx->stream), b = cs->y_x2.download(ctx->stream);
+      const int D = cs->D, n = cs->nch;
+      for (int c = 0; c < n; ++c)
+        for (int d = 0; d < D; ++d) {
+          y_x[off + static_cast<size_t>(c) * D + d] = a[static_cast<size_t>(d) * n + c];
+          y_x2[off + static_cast<size_t>(c) * D + d] = b[static_cast<size_t>(d) * n + c];
+        }
+      off += static_cast<size_t>(n) * D;
+    }
+  }));
+}
+
+pcvg_status pcvg_timing(const pcvg_ctx* ctx, double* last_ms, int64_t* launches) {
+  if (!ctx) return PCVG_INVALID_INPUT;
+  if (last_ms) *last_ms = ctx->last_ms;
+  if (launches) *launches = ctx->launches;
+  return PCVG_OK;
+}
+
+pcvg_status pcvg_merge(int32_t n_models, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
+                       int32_t final_checkpoint, const pcvg_fold_table* folds, const double* y_x,
+                       const double* y_x2, pcvg_report* report) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] {
+    if (!cfg || !folds || !report || n_models < 1 || n_models > 2 || K < 2)
+      throw Error(PCVG_INVALID_INPUT, "bad merge arguments");
+    const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
+    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, y_x, y_x2, D, report);
+  }));
+}
+
+pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !rep) throw Error(PCVG_INVALID_INPUT, "null argument");
+    if (cfg && (cfg->fold_begin != 0 || cfg->fold_end != 0) &&
+        !(cfg->fold_begin == 0 && cfg->fold_end == (ctx->models.empty() ? 0 : ctx->models[0]->K)))
+      throw Error(PCVG_INVALID_INPUT, "pcvg_run runs every fold; shard with the stepwise API");
+    int32_t st = pcvg_begin(ctx, cfg);
+    if (st != PCVG_OK) throw Error(st, ctx->err);
+    const int K = ctx->models[0]->K, L = cfg->chains;
+    const int nm = static_cast<int>(ctx->models.size());
+    const int D = ctx->chains[0]->D;
+    std::vector<int64_t> cks;
+    if (cfg->checkpoint_every > 0)
+      for (int64_t t = cfg->checkpoint_every; t < cfg->iters; t += cfg->checkpoint_every) cks.push_back(t);
+    cks.push_back(cfg->iters);
+    // per-fold scratch table
+    const size_t rows = static_cast<size_t>(nm) * K;
+    std::vector<double> est(rows), lf(rows), mc(rows), nv(rows), ess(rows), rh(rows);
+    std::vector<int64_t> bt(rows);
+    std::vector<int32_t> ft(rows), fl(rows);
+    pcvg_fold_table tab{est.data(), lf.data(), mc.data(), nv.data(), ess.data(), rh.data(), bt.data(), ft.data(), fl.data()};
+    std::vector<double> yx(rows * L * D), yx2(rows * L * D);
+    int64_t dropped = 0, done = 0;
+    std::vector<int64_t> divs(rows * L);
+    rep->n_checkpoints = 0;
+    bool stopped = false;
+    for (size_t ci = 0; ci < cks.size() && !stopped; ++ci) {
+      st = pcvg_advance(ctx, cks[ci] - ctx->iters_done);
+      if (st != PCVG_OK) throw Error(st, ctx->err);
+      st = pcvg_fold_stats(ctx, &tab, divs.data(), &dropped, &done);
+      if (st != PCVG_OK) throw Error(st, ctx->err);
+      const bool last = ci + 1 == cks.size();
+      bool final_ck = last;
+      if (cfg->early_stop && !last) {
+        // Early-stop rule: blocks are the completed check intervals.
+        st = pcvg_block_sums(ctx, yx.data(), yx2.data());
+        if (st != PCVG_OK) throw Error(st, ctx->err);
+        pcvg_report probe = *rep;
+        std::vector<double> bench(cfg->bench_draws);
+        probe.benchmark = bench.data();
+        probe.snapshots = nullptr;
+        probe.delta_k = nullptr;
+        pcvg_fold_table t2 = tab;
+        t2.failed = nullptr;
+        merge_stats(nm, K, cfg, done, 2, &t2, yx.data(), yx2.data(), static_cast<int>(ci + 1), &probe);
+        if (probe.verdict_pass && std::isfinite(probe.rhat_max) && probe.mcse < probe.epistemic_se) final_ck = true;
+      }
+      if (final_ck) {
+        st = pcvg_block_sums(ctx, yx.data(), yx2.data());
+        if (st != PCVG_OK) throw Error(st, ctx->err);
+        merge_stats(nm, K, cfg, done, 1, &tab, yx.data(), yx2.data(), last ? D : static_cast<int>(ci + 1), rep);
+        stopped = true;
+      } else {
+        pcvg_fold_table t2 = tab;
+        t2.failed = nullptr;
+        merge_stats(nm, K, cfg, done, 0, &t2, nullptr, nullptr, D, rep);
+      }
+      if (rep->snapshots) {
+        double* o = rep->snapshots + 7 * ci;
+        o[0] = static_cast<double>(done);
+        o[1] = rep->delta_hat;
+        o[2] = rep->mcse;
+        o[3] = rep->epistemic_se;
+        o[4] = rep->prob_a_better;
+        o[5] = rep->ess_overall;
+        o[6] = rep->rhat_max;
+      }
+      rep->n_checkpoints = static_cast<int32_t>(ci + 1);
+    }
+    // final tables
+    for (size_t i = 0; i < rows; ++i) {
+      rep->folds.estimate[i] = est[i];
+      rep->folds.log_f_hat[i] = lf[i];
+      rep->folds.mc_contribution[i] = mc[i];
+      if (rep->folds.naive_contribution) rep->folds.naive_contribution[i] = nv[i];
+      rep->folds.ess[i] = ess[i];
+      rep->folds.rhat[i] = rh[i];
+      rep->folds.batches[i] = bt[i];
+      rep->folds.fault[i] = ft[i];
+    }
+    // failed flags after exclusions are written by merge_stats into rep->folds.failed
+    std::copy(divs.begin(), divs.end(), rep->divergences);
+    rep->dropped_batch_draws = dropped;
+    rep->iters_run = done;
+    rep->warmup_ms = ctx->warm_ms;
+    rep->sampling_ms = ctx->sample_ms;
+    rep->gpu_launches = ctx->launches;
+  }));
+}
+
+}  // extern "C"

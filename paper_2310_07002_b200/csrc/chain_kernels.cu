@@ -1,0 +1,192 @@
+// Per-chain setup and per-fold reduction kernels (sm_100a):
+//  * init_chains   - Step 2 warm start (engine.cpp:296-309): stream keys, bank row drawn by
+//                    CounterRng(seed, stream_key(ChainInit, m, k, c)).below(rows), fresh
+//                    ChainSampling stream; one thread per chain.
+//  * set_centers   - centering constants C_k = sum_c warm_c / (L N_wu) in chain order
+//                    (engine.cpp:316-339); one thread per fold.
+//  * fold_stats    - LogS fold score + R-hat of each fold from its L chain accumulators
+//                    (scoring.cpp:10-62, diagnostics.cpp:11-44), same operation order as the
+//                    reference; one thread per fold.
+#include <math_constants.h>
+
+#include "device_common.cuh"
+#include "types.cuh"
+
+namespace pcvg {
+
+namespace {
+
+__global__ void init_chains_kernel(ModelDev M, ChainsDev S, const double* bank, int64_t bank_rows) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= S.nch) return;
+  const int fold = S.fold0 + c / S.L, chain = c % S.L;
+  ChainRng init;
+  init.init(S.seed, stream_key(2 /*ChainInit*/, S.stream_model, fold, chain), 0, 0.0, false);
+  const uint64_t row = init.below(static_cast<uint64_t>(bank_rows));
+  const size_t plane = static_cast<size_t>(M.dim) * S.nch;
+  for (int d = 0; d < M.dim; ++d) {
+    S.pos[static_cast<size_t>(d) * S.nch + c] = bank[row * M.dim + d];
+    S.pos[plane + static_cast<size_t>(d) * S.nch + c] = 0.0;
+  }
+  S.cur[c] = 0;
+  S.rng_stream[c] = stream_key(1 /*ChainSampling*/, S.stream_model, fold, chain);
+  S.rng_pos[c] = 0;
+  S.rng_cached[c] = 0.0;
+  S.rng_has[c] = 0;
+  S.divergences[c] = 0;
+  S.warm_sum[c] = 0.0;
+}
+
+__global__ void reset_accum_kernel(ChainsDev S, int D, double* centers_per_fold) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= S.nch) return;
+  const AccumDev& A = S.acc;
+  A.u_x[c] = -CUDART_INF;
+  A.u_x2[c] = -CUDART_INF;
+  A.z_x[c] = -CUDART_INF;
+  A.v_x[c] = -CUDART_INF;
+  A.v_x2[c] = -CUDART_INF;
+  A.committed[c] = 0;
+  A.pending[c] = 0;
+  A.count[c] = 0;
+  A.faults[c] = 0;
+  A.center[c] = centers_per_fold[c / S.L];
+  for (int d = 0; d < D; ++d) {
+    A.y_x[static_cast<size_t>(d) * S.nch + c] = 0.0;
+    A.y_x2[static_cast<size_t>(d) * S.nch + c] = 0.0;
+  }
+}
+
+__global__ void centers_kernel(ChainsDev S, int nfold, int64_t warmup, double* centers) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nfold) return;
+  double c = 0.0;
+  if (warmup > 0) {
+    const double denom = static_cast<double>(S.L) * static_cast<double>(warmup);
+    for (int ch = 0; ch < S.L; ++ch) c += S.warm_sum[k * S.L + ch] / denom;
+  }
+  centers[k] = c;
+}
+
+__device__ double logsumexp_dev(const double* v, int n) {  // math.hpp:24-32
+  double m = -CUDART_INF;
+  for (int i = 0; i < n; ++i)
+    if (v[i] > m) m = v[i];
+  if (m == -CUDART_INF) return -CUDART_INF;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += exp(v[i] - m);
+  return m + log(s);
+}
+
+struct FoldOut {
+  double *estimate, *log_f_hat, *mc, *naive, *ess, *rhat;
+  int64_t* batches;
+  int32_t* fault;
+};
+
+__global__ void fold_stats_kernel(ChainsDev S, int nfold, int64_t n, int b, int D, FoldOut out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nfold) return;
+  const int l = S.L;
+  const AccumDev& A = S.acc;
+  const int c0 = k * l;
+  const double ln = static_cast<double>(l) * static_cast<double>(n);
+  double ux[64];
+  bool fault = false;
+  int64_t batches = 0;
+  for (int c = 0; c < l; ++c) {
+    ux[c] = A.u_x[c0 + c];
+    fault = fault || A.faults[c0 + c] > 0;
+    batches += A.committed[c0 + c];
+  }
+  const double lf = logsumexp_dev(ux, l) - log(ln);  // scoring.cpp:10-62
+  double mc, naive, ess;
+  if (lf == -CUDART_INF) {
+    fault = true;
+    mc = CUDART_INF;
+    naive = CUDART_INF;
+    ess = CUDART_NAN;
+  } else {
+    double sum_u2 = 0.0;
+    for (int c = 0; c < l; ++c) sum_u2 += exp(A.u_x2[c0 + c] - 2.0 * lf);
+    naive = ln > 1 ? (sum_u2 - ln) / (ln - 1.0) : 0.0;
+    if (naive < 0.0) naive = 0.0;
+    const int64_t a = A.committed[c0];
+    if (batches >= 2 && a >= 1) {
+      double ss = 0.0;
+      for (int c = 0; c < l; ++c) {
+        const double s2 = exp(A.v_x2[c0 + c] - 2.0 * lf);
+        const double s1 = exp(A.v_x[c0 + c] - lf);
+        ss += s2 - 2.0 * s1 + static_cast<double>(A.committed[c0 + c]);
+      }
+      mc = b * ss / (static_cast<double>(batches) - 1.0);
+      if (mc < 0.0) mc = 0.0;
+      ess = mc > 0.0 ? ln * naive / mc : CUDART_NAN;
+    } else {
+      mc = CUDART_NAN;
+      ess = CUDART_NAN;
+    }
+  }
+  // rhat_from_blocks (diagnostics.cpp:11-44)
+  double rhat = CUDART_NAN;
+  if (l >= 2 && n >= 2) {
+    double sx[64], sxx[64];
+    for (int c = 0; c < l; ++c) {
+      double s = 0.0, s2 = 0.0;
+      for (int d = 0; d < D; ++d) s += A.y_x[static_cast<size_t>(d) * S.nch + c0 + c];
+      for (int d = 0; d < D; ++d) s2 += A.y_x2[static_cast<size_t>(d) * S.nch + c0 + c];
+      sx[c] = s;
+      sxx[c] = s2;
+    }
+    double w = 0.0, grand = 0.0;
+    for (int c = 0; c < l; ++c) {
+      w += (sxx[c] - sx[c] * sx[c] / n) / (n - 1.0) / l;
+      grand += sx[c] / n / l;
+    }
+    double bb = 0.0;
+    for (int c = 0; c < l; ++c) {
+      const double dev = sx[c] / n - grand;
+      bb += dev * dev;
+    }
+    bb *= static_cast<double>(n) / (l - 1.0);
+    if (isfinite(w) && isfinite(bb) && w > 0.0) rhat = sqrt(((n - 1.0) / n * w + bb / n) / w);
+  }
+  out.estimate[k] = lf;
+  out.log_f_hat[k] = lf;
+  out.mc[k] = mc;
+  out.naive[k] = naive;
+  out.ess[k] = ess;
+  out.rhat[k] = rhat;
+  out.batches[k] = batches;
+  out.fault[k] = fault ? 1 : 0;
+}
+
+}  // namespace
+
+cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const double* bank,
+                               int64_t bank_rows, cudaStream_t st) {
+  if (S.nch == 0) return cudaSuccess;
+  init_chains_kernel<<<(S.nch + 255) / 256, 256, 0, st>>>(M, S, bank, bank_rows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_centers(const ChainsDev& S, int nfold, int64_t warmup, double* centers,
+                           int D, cudaStream_t st) {
+  if (nfold == 0) return cudaSuccess;
+  centers_kernel<<<(nfold + 127) / 128, 128, 0, st>>>(S, nfold, warmup, centers);
+  reset_accum_kernel<<<(S.nch + 255) / 256, 256, 0, st>>>(S, D, centers);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_stats(const ChainsDev& S, int nfold, int64_t n, int b, int D,
+                              double* estimate, double* log_f_hat, double* mc, double* naive,
+                              double* ess, double* rhat, int64_t* batches, int32_t* fault,
+                              cudaStream_t st) {
+  if (nfold == 0) return cudaSuccess;
+  if (S.L > 64) return cudaErrorInvalidValue;
+  FoldOut o{estimate, log_f_hat, mc, naive, ess, rhat, batches, fault};
+  fold_stats_kernel<<<(nfold + 127) / 128, 128, 0, st>>>(S, nfold, n, b, D, o);
+  return cudaGetLastError();
+}
+
+}  // namespace pcvg

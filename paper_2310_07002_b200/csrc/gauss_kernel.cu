@@ -1,0 +1,612 @@
+// Fused HMC kernel for the Gaussian linear families (sm_100a, FP64):
+//   grouped regression  (grouped_regression.cpp:56-163)  - cfg1 (J=1), paper Ex-1
+//   radon-style         (radon.cpp:50-138)                - cfg3
+//   seasonal AR         (seasonal_ar.cpp:37-115)          - cfg4 (time-block / hv-block folds)
+//
+// All three share one per-observation form: m_i = off(g_i) + sum_c w_c x_ic, r_i = y_i - m_i,
+// and a gradient built from the masked sums S_r[g], S_xr[c], S_rr. One chain is owned by T
+// consecutive lanes (T | 32); the lanes split the observations of every group segment and
+// butterfly-reduce the sums, so each lane ends with identical gradient bits and advances an
+// identical copy of the chain's global parameters (kept in registers). Group parameters live in
+// HBM as [dim][chain] arrays (coalesced across the chains of a warp) and are updated group by
+// group inside the gradient pass. Per HMC transition (hmc.cpp:53-99) the kernel runs n_lf
+// gradient passes (the gradient and log joint at the current position are cached - the reference
+// recomputes the identical bits, hmc.cpp:37,69-70 - and the proposal's log joint is fused into
+// the last pass), the Metropolis test, log_pred and the online accumulator update
+// (accum.cpp:164-182). Chains are independent; a CTA holds 128/T chains.
+#include <math_constants.h>
+
+#include "device_common.cuh"
+#include "types.cuh"
+
+namespace pcvg {
+
+namespace {
+
+constexpr int kBlock = 128;
+
+template <int T>
+__device__ __forceinline__ double lane_sum(double v, unsigned mask) {
+#pragma unroll
+  for (int off = T / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off, T);
+  return v;
+}
+
+__device__ __forceinline__ double logistic_fn(double u) { return 1.0 / (1.0 + exp(-u)); }
+
+// Normals of one HMC momentum refresh read from a snapshot of the chain stream by dimension
+// index: normal i of this transition, honouring a Box-Muller variate cached by the previous
+// transition (rng.hpp:75-87). Lets the group momenta be generated inside the first gradient pass.
+struct NormalCursor {
+  uint64_t pos0;
+  bool hc0;
+  double c0;
+  int64_t pair;
+  double ncos, nsin;
+
+  __device__ void start(const ChainRng& R) {
+    pos0 = R.pos;
+    hc0 = R.has_cached;
+    c0 = R.cached;
+    pair = -1;
+  }
+  __device__ double at(ChainRng& R, int i) {
+    if (hc0) {
+      if (i == 0) return c0;
+      i -= 1;
+    }
+    const int64_t pr = i >> 1;
+    if (pr != pair) {
+      R.pos = pos0 + 4 * static_cast<uint64_t>(pr);
+      const double u1 = R.uniform();
+      const double u2 = R.uniform();
+      const double r = sqrt(-2.0 * log(u1));
+      double s, c;
+      sincos(kTwoPi * u2, &s, &c);
+      ncos = r * c;
+      nsin = r * s;
+      pair = pr;
+    }
+    return (i & 1) ? nsin : ncos;
+  }
+  // Leaves R exactly where the reference stream is after d normal() calls.
+  __device__ void finish(ChainRng& R, int d) {
+    if (d == 0) return;
+    const int m = hc0 ? d - 1 : d;  // normals drawn from fresh pairs
+    const int64_t pairs = (m + 1) / 2;
+    if (m & 1) {
+      R.cached = at(R, d);  // the sin half of the last pair
+      R.has_cached = true;
+    } else {
+      R.has_cached = false;
+    }
+    R.pos = pos0 + 4 * static_cast<uint64_t>(pairs);
+  }
+};
+
+// Per-pass quantities derived from the global parameters.
+template <int NCM>
+struct Prep {
+  double w[NCM];  // covariate weights
+  double off0;    // offset without the group term
+  double v, inv_v, logv;
+  double va, sa;  // group scale (grouped: va = sig_a^2; radon: va, sa = sqrt(va))
+};
+
+// Register slot -> global parameter index. Slots put the parameters whose position depends
+// on runtime sizes (P, p, q) at fixed registers so no register array is indexed dynamically:
+//   grouped  [mu_alpha, log sigma_alpha, log sigma_y, beta_0..beta_{P-1}]
+//   radon    [beta, mu_alpha, log sigma_alpha^2, log sigma_y^2]           (reference order)
+//   seasonal [beta_0, log sigma, cov 0..p+q-1 -> u_1..u_p, beta_1..beta_q]
+template <int FAM>
+__device__ __forceinline__ int gidx(const ModelDev& M, int r) {
+  if constexpr (FAM == kGrouped) return r < 3 ? M.nc + r : r - 3;
+  else if constexpr (FAM == kRadon) return r;
+  else return r == 0 ? M.p : (r == 1 ? M.p + M.q + 1 : (r - 2 < M.p ? r - 2 : r - 1));
+}
+
+template <int FAM, int NCM, int NGM>
+__device__ __forceinline__ void prepare(const ModelDev& M, const double* qG, Prep<NCM>& P) {
+  if constexpr (FAM == kGrouped) {
+#pragma unroll
+    for (int c = 0; c < NCM; ++c) P.w[c] = (c < M.nc) ? M.cmask[c] * qG[3 + c] : 0.0;
+    const double sig_a = exp(qG[1]);
+    const double sig_y = exp(qG[2]);
+    P.va = sig_a * sig_a;
+    P.v = sig_y * sig_y;
+    P.off0 = 0.0;
+  } else if constexpr (FAM == kRadon) {
+    P.w[0] = M.include_floor ? qG[0] : 0.0;
+    P.off0 = qG[1];
+    P.va = exp(qG[2]);
+    P.sa = sqrt(P.va);
+    P.v = exp(qG[3]);
+  } else {  // seasonal
+#pragma unroll
+    for (int c = 0; c < NCM; ++c) {
+      if (c < M.p) {
+        const double w = logistic_fn(qG[2 + c]);
+        P.w[c] = M.rho_sym ? 2.0 * w - 1.0 : 0.5 * (1.0 + w);
+      } else {
+        P.w[c] = c < M.p + M.q ? qG[2 + c] : 0.0;
+      }
+    }
+    P.off0 = qG[0];
+    const double sigma = exp(qG[1]);
+    P.v = sigma * sigma;
+  }
+  P.inv_v = 1.0 / P.v;
+  P.logv = log(P.v);
+}
+
+template <int FAM, int NCM>
+__device__ __forceinline__ double group_offset(const Prep<NCM>& P, double qg) {
+  if constexpr (FAM == kGrouped) return qg;
+  else if constexpr (FAM == kRadon) return P.off0 + P.sa * qg;
+  else return P.off0;
+}
+
+// Replicated (not lane-reduced) per-group accumulators.
+struct GroupAcc {
+  double a0, a1, a2;
+};
+
+// d log p / d q_g given the lane-reduced residual sum of group g; updates replicated sums.
+template <int FAM, int NCM, int NGM>
+__device__ __forceinline__ double group_grad(const Prep<NCM>& P, const double* qG,
+                                            const ModelDev& M, double qg, double srg,
+                                            GroupAcc& G) {
+  if constexpr (FAM == kGrouped) {  // grouped_regression.cpp:100-116
+    const double dev = qg - qG[0];
+    G.a0 += dev / P.va;  // -> d/d mu_alpha
+    G.a1 += dev * dev;   // -> d/d log sigma_alpha, prior
+    return srg / P.v - dev / P.va;
+  } else {  // radon.cpp:93-105
+    G.a0 += srg;       // sum r (-> d/d mu_alpha)
+    G.a1 += srg * qg;  // sum r z (-> d/d log va)
+    G.a2 += qg * qg;   // prior on z
+    return P.sa * srg / P.v - qg;
+  }
+}
+
+// Global gradient and (optionally) log joint from the reduced sums.
+template <int FAM, int NCM, int NGM>
+__device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& P,
+                                            const double* qG, const double* sxr, double sr,
+                                            double srr, const GroupAcc& G, int n_train,
+                                            double* gG, bool value, double& lp) {
+  const double ntr = static_cast<double>(n_train);
+  if constexpr (FAM == kGrouped) {  // grouped_regression.cpp:109-121, 65-85
+#pragma unroll
+    for (int c = 0; c < NCM; ++c)
+      if (c < M.nc) gG[3 + c] = M.cmask[c] * (sxr[c] / P.v) - qG[3 + c];
+    gG[0] = G.a0 - qG[0];
+    gG[1] = G.a1 / P.va - M.J - P.va / 10.0 + 1.0;
+    gG[2] = srr / P.v - ntr - P.v / 10.0 + 1.0;
+    if (value) {
+      double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
+      l += -0.5 * (M.J * (kLog2Pi + log(P.va)) + G.a1 / P.va);
+      l += -0.5 * (kLog2Pi + qG[0] * qG[0]);
+#pragma unroll
+      for (int c = 0; c < NCM; ++c)
+        if (c < M.nc) l += -0.5 * (kLog2Pi + qG[3 + c] * qG[3 + c]);
+      const double sig_a = exp(qG[1]), sig_y = exp(qG[2]);
+      l += M.c_lhn10 - sig_a * sig_a / 20.0 + qG[1];
+      l += M.c_lhn10 - sig_y * sig_y / 20.0 + qG[2];
+      lp = l;
+    }
+  } else if constexpr (FAM == kRadon) {  // radon.cpp:102-106, 50-74
+    gG[0] = (M.include_floor ? sxr[0] / P.v : 0.0) - qG[0];
+    gG[1] = G.a0 / P.v - qG[1] / 4.0;
+    gG[2] = 0.5 * P.sa * G.a1 / P.v + 6.0 - 9.0 * P.va;
+    gG[3] = 0.5 * (srr / P.v - ntr) + 10.0 - 10.0 * P.v;
+    if (value) {
+      double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
+      l += -0.5 * (M.J * kLog2Pi + G.a2);
+      l += -0.5 * (kLog2Pi + qG[0] * qG[0]);
+      l += -0.5 * (kLog2Pi + M.c_log4 + qG[1] * qG[1] / 4.0);
+      l += M.c_lgamma6_9 + 5.0 * qG[2] - 9.0 * P.va + qG[2];
+      l += M.c_lgamma10_10 + 9.0 * qG[3] - 10.0 * P.v + qG[3];
+      lp = l;
+    }
+  } else {  // seasonal_ar.cpp:79-105, 59-77
+    double l = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCM; ++c) {
+      if (c < M.p) {
+        const double w = logistic_fn(qG[2 + c]);
+        const double dw = w * (1.0 - w);
+        const double drho = M.rho_sym ? 2.0 * dw : 0.5 * dw;
+        gG[2 + c] = sxr[c] * drho / P.v + (4.0 * (1.0 - w) - 4.0 * w + 1.0 - 2.0 * w);
+        if (value) l += 4.0 * log(w) + 4.0 * log1p(-w) + M.c_lbeta55 + log(w) + log1p(-w);
+      } else if (c < M.p + M.q) {
+        gG[2 + c] = sxr[c] / P.v - qG[2 + c];
+        if (value) l += -0.5 * (kLog2Pi + qG[2 + c] * qG[2 + c]);
+      }
+    }
+    gG[0] = sr / P.v - qG[0];
+    gG[1] = srr / P.v - ntr - P.v + 1.0;
+    if (value) {
+      l += -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
+      l += -0.5 * (kLog2Pi + qG[0] * qG[0]);
+      const double sigma = exp(qG[1]);
+      l += M.c_lhn1 - sigma * sigma / 2.0 + qG[1];
+      lp = l;
+    }
+  }
+}
+
+// One gradient evaluation at (qG, group params) for chain c. kind: 0 = evaluate at the stored
+// position (no dynamics), 1 = first leapfrog step (fuses momentum draw + half kick + drift of
+// the group dims), 2 = later steps. On leapfrog kinds the group momenta get the kick `scale`.
+template <int FAM, int T, int NCM, int NGM, bool VALUE>
+__device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S, int c, int t,
+                                          unsigned mask, int lo, int hi, int n_train,
+                                          const double* qG, int kind, bool last, double scale,
+                                          int cur, NormalCursor& nc, ChainRng& R,
+                                          const double* probe_p, double* gG, double& lp,
+                                          double& k0g, double& k1g, bool& bad) {
+  Prep<NCM> P;
+  prepare<FAM, NCM, NGM>(M, qG, P);
+  const int n = M.n;
+  const int nch = S.nch;
+  const double eps = M.step, half = 0.5 * M.step;
+  const size_t plane = static_cast<size_t>(M.dim) * nch;
+  double sxr[NCM];
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) sxr[k] = 0.0;
+  double sr_tot = 0.0, srr = 0.0;
+  bool poison = false;
+  GroupAcc G{0.0, 0.0, 0.0};
+  const int ngroups = M.J > 0 ? M.J : 1;
+  for (int g = 0; g < ngroups; ++g) {
+    double qg = 0.0, pg = 0.0;
+    const int r0 = M.J > 0 ? __ldg(M.grp_ptr + g) : 0;
+    const int r1 = M.J > 0 ? __ldg(M.grp_ptr + g + 1) : n;
+    const size_t gi = static_cast<size_t>(g) * nch + c;
+    if constexpr (FAM != kSeasonal) {
+      const double mg = __ldg(M.inv_mass + g);
+      if (kind == 0) {
+        qg = S.pos[cur * plane + gi];
+      } else if (kind == 1) {
+        const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + g]
+                                  : nc.at(R, g) / sqrt(mg);
+        k0g += mg * p0 * p0;
+        pg = p0 + half * S.grad[cur * plane + gi];
+        qg = S.pos[cur * plane + gi] + eps * mg * pg;
+      } else {
+        pg = S.wp[gi];
+        qg = S.pos[(cur ^ 1) * plane + gi] + eps * mg * pg;
+      }
+      bad |= !isfinite(qg);
+    }
+    const double off = group_offset<FAM, NCM>(P, qg);
+    double srg = 0.0;
+    for (int i = r0 + t; i < r1; i += T) {
+      const double yi = __ldg(M.y + i);
+      const int ki = __ldg(M.key + i);
+      double m = off;
+      double xs[NCM];
+#pragma unroll
+      for (int k = 0; k < NCM; ++k) {
+        if (k < M.nc) {
+          xs[k] = __ldg(M.x + static_cast<size_t>(k) * n + i);
+          m = fma(P.w[k], xs[k], m);
+        } else {
+          xs[k] = 0.0;
+        }
+      }
+      const double r = yi - m;
+      const bool train = static_cast<unsigned>(ki - lo) >= static_cast<unsigned>(hi - lo);
+      const double wr = train ? r : 0.0;
+      srg += wr;
+#pragma unroll
+      for (int k = 0; k < NCM; ++k) sxr[k] = fma(xs[k], wr, sxr[k]);
+      srr = fma(wr, r, srr);
+      if (VALUE && !train) poison |= !isfinite(P.logv + r * r * P.inv_v);
+    }
+    if constexpr (FAM != kSeasonal) {
+      srg = lane_sum<T>(srg, mask);
+      const double gg = group_grad<FAM, NCM, NGM>(P, qG, M, qg, srg, G);
+      if (kind == 0) {
+        if (t == 0) S.grad[cur * plane + gi] = gg;
+        bad |= !isfinite(gg);
+      } else {
+        bad |= !isfinite(gg);
+        pg += scale * gg;
+        bad |= !isfinite(pg);
+        if (t == 0) {
+          S.pos[(cur ^ 1) * plane + gi] = qg;
+          S.wp[gi] = pg;
+          if (last) S.grad[(cur ^ 1) * plane + gi] = gg;
+        }
+        if (last) k1g += __ldg(M.inv_mass + g) * pg * pg;
+      }
+    } else {
+      sr_tot += srg;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) sxr[k] = lane_sum<T>(sxr[k], mask);
+  srr = lane_sum<T>(srr, mask);
+  if constexpr (FAM == kSeasonal) sr_tot = lane_sum<T>(sr_tot, mask);
+  if (VALUE) {
+    // any lane's poisoned test row poisons the chain (0 * non-finite = NaN, grouped_regression.cpp:74-76)
+    const unsigned any = __ballot_sync(mask, poison);
+    poison = any != 0;
+  }
+  global_grad<FAM, NCM, NGM>(M, P, qG, sxr, sr_tot, srr, G, n_train, gG, VALUE, lp);
+  if (VALUE && poison) lp = CUDART_NAN;
+  __syncwarp(mask);  // group-dim stores of lane 0 become visible to the chain's lanes
+}
+
+// Model::log_pred at the stored position (grouped_regression.cpp:124-163, radon.cpp:109-138,
+// seasonal_ar.cpp:107-115), observations split across the chain's lanes.
+template <int FAM, int T, int NCM, int NGM>
+__device__ double log_pred(const ModelDev& M, const ChainsDev& S, int c, int t, unsigned mask,
+                           int fold, int cur, const double* qG) {
+  if (fold >= M.K) return 0.0;
+  Prep<NCM> P;
+  prepare<FAM, NCM, NGM>(M, qG, P);
+  const size_t plane = static_cast<size_t>(M.dim) * S.nch;
+  const int s0 = __ldg(M.fold_seg + fold), s1 = __ldg(M.fold_seg + fold + 1);
+  double v_pred = P.v;
+  if constexpr (FAM == kSeasonal) v_pred = exp(2.0 * qG[1]);
+  double lp = 0.0;
+  for (int s = s0; s < s1; ++s) {
+    const int r0 = __ldg(M.seg_row + s), r1 = __ldg(M.seg_row + s + 1);
+    const int g = __ldg(M.seg_group + s);
+    const bool unseen = __ldg(M.seg_unseen + s) != 0;
+    double qg = 0.0;
+    if (FAM != kSeasonal && !unseen) qg = S.pos[cur * plane + static_cast<size_t>(g) * S.nch + c];
+    double a = 0.0, b = 0.0;
+    for (int tt = r0 + t; tt < r1; tt += T) {
+      const int i = __ldg(M.seg_rows + tt);
+      double m;
+      if constexpr (FAM == kGrouped) m = unseen ? qG[0] : qg;
+      else if constexpr (FAM == kRadon) m = unseen ? P.off0 : P.off0 + sqrt(P.va) * qg;
+      else m = P.off0;
+#pragma unroll
+      for (int k = 0; k < NCM; ++k)
+        if (k < M.nc) m = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), m);
+      const double r = __ldg(M.y + i) - m;
+      if (unseen) {
+        a += r * r;
+        b += r;
+      } else {
+        a += -0.5 * (kLog2Pi + log(v_pred) + r * r / v_pred);
+      }
+    }
+    a = lane_sum<T>(a, mask);
+    if (unseen) {  // mvn_logpdf_compound, math.hpp:94-109, sigma2 = vy, tau2 = va
+      b = lane_sum<T>(b, mask);
+      const double sigma2 = P.v, tau2 = P.va;
+      const int nn = r1 - r0;
+      if (!(sigma2 > 0.0) || tau2 < 0.0) return CUDART_NAN;  // numeric_fault in the reference
+      const double denom = sigma2 + nn * tau2;
+      const double quad = (a - tau2 * b * b / denom) / sigma2;
+      const double logdet = (nn - 1) * log(sigma2) + log(denom);
+      lp += -0.5 * (nn * kLog2Pi + logdet + quad);
+    } else {
+      lp += a;
+    }
+  }
+  return lp;
+}
+
+template <int FAM, int T, int NCM, int NGM>
+__global__ void __launch_bounds__(kBlock) gauss_kernel(ModelDev M, ChainsDev S, RunArgs A) {
+  constexpr int kChains = kBlock / T;
+  const int t = threadIdx.x % T;
+  const int local = threadIdx.x / T;
+  const int c = blockIdx.x * kChains + local;
+  if (c >= S.nch) return;
+  const unsigned mask =
+      T == 32 ? 0xffffffffu : (((1u << T) - 1u) << ((threadIdx.x & 31) & ~(T - 1)));
+  const int nch = S.nch;
+  const int fold = S.fold_override ? S.fold_override[c] : S.fold0 + c / S.L;
+  const int lo = __ldg(M.fold_lo + fold), hi = __ldg(M.fold_hi + fold);
+  const int n_train = __ldg(M.n_train + fold);
+  const int J = M.J, ng = M.ng;
+  const size_t plane = static_cast<size_t>(M.dim) * nch;
+  // address of global parameter slot i of chain c in plane b
+  auto gaddr = [&](int b, int i) { return b * plane + static_cast<size_t>(J + gidx<FAM>(M, i)) * nch + c; };
+  int cur = S.cur[c];
+
+  double qG[NGM], pG[NGM], gG[NGM];
+#pragma unroll
+  for (int i = 0; i < NGM; ++i) {
+    qG[i] = i < ng ? S.pos[gaddr(cur, i)] : 0.0;
+    gG[i] = 0.0;
+  }
+  double lp0 = S.lp0[c];
+  ChainRng R;
+  R.init(S.seed, S.rng_stream[c], S.rng_pos[c], S.rng_cached[c], S.rng_has[c] != 0);
+  NormalCursor nc;
+
+  if (A.mode == kModeEval || A.mode == kModePred) {
+    if (A.mode == kModeEval) {
+      double lp = 0.0, k0 = 0.0, k1 = 0.0;
+      bool bad = false;
+      grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, 0, false, 0.0,
+                                        cur, nc, R, nullptr, gG, lp, k0, k1, bad);
+      if (t == 0) {
+#pragma unroll
+        for (int i = 0; i < NGM; ++i)
+          if (i < ng) S.grad[gaddr(cur, i)] = gG[i];
+        S.lp0[c] = lp;
+        if (A.out_a) A.out_a[c] = lp;
+      }
+    } else {
+      const double s = log_pred<FAM, T, NCM, NGM>(M, S, c, t, mask, fold, cur, qG);
+      if (t == 0 && A.out_a) A.out_a[c] = s;
+    }
+    return;
+  }
+
+  const double eps = M.step, half = 0.5 * M.step;
+  const int n_lf = M.n_lf;
+  int64_t div_count = 0;
+  double warm = 0.0;
+  for (int64_t it = 0; it < A.n_iters; ++it) {
+    const double* probe_p = A.mode == kModeProbe ? A.probe_momentum : nullptr;
+    nc.start(R);
+    // Momentum refresh of the global dims (normals J..dim-1 of this transition) + half kick.
+    double k0G = 0.0;
+#pragma unroll
+    for (int i = 0; i < NGM; ++i) {
+      if (i < ng) {
+        const int gi = J + gidx<FAM>(M, i);
+        const double mi = __ldg(M.inv_mass + gi);
+        const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + gi]
+                                  : nc.at(R, gi) / sqrt(mi);
+        k0G += mi * p0 * p0;
+        pG[i] = p0 + half * S.grad[gaddr(cur, i)];
+      }
+    }
+    bool bad = false;
+    double lp1 = 0.0, k0g = 0.0, k1g = 0.0;
+    for (int s = 0; s < n_lf; ++s) {
+      const bool first = s == 0, last = s == n_lf - 1;
+#pragma unroll
+      for (int i = 0; i < NGM; ++i) {
+        if (i < ng) {
+          const double base = first ? S.pos[gaddr(cur, i)] : qG[i];
+          qG[i] = base + eps * __ldg(M.inv_mass + J + gidx<FAM>(M, i)) * pG[i];
+          bad |= !isfinite(qG[i]);
+        } else {
+          qG[i] = 0.0;
+        }
+      }
+      const double scale = last ? half : eps;
+      if (last)
+        grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, first ? 1 : 2,
+                                          true, scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad);
+      else
+        grad_pass<FAM, T, NCM, NGM, false>(M, S, c, t, mask, lo, hi, n_train, qG, first ? 1 : 2,
+                                           false, scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad);
+#pragma unroll
+      for (int i = 0; i < NGM; ++i) {
+        if (i < ng) {
+          bad |= !isfinite(gG[i]);
+          pG[i] += scale * gG[i];
+          bad |= !isfinite(pG[i]);
+        }
+      }
+    }
+    if (!probe_p) nc.finish(R, M.dim);
+    double k1G = 0.0;
+#pragma unroll
+    for (int i = 0; i < NGM; ++i)
+      if (i < ng) k1G += __ldg(M.inv_mass + J + gidx<FAM>(M, i)) * pG[i] * pG[i];
+    // proposal (q', grad(q')) of the global dims into the working plane; accept flips `cur`
+    if (t == 0) {
+#pragma unroll
+      for (int i = 0; i < NGM; ++i) {
+        if (i < ng) {
+          S.pos[gaddr(cur ^ 1, i)] = qG[i];
+          S.grad[gaddr(cur ^ 1, i)] = gG[i];
+        }
+      }
+    }
+    const double h0 = -lp0 + 0.5 * (k0g + k0G);
+    const double h1 = bad ? CUDART_NAN : -lp1 + 0.5 * (k1g + k1G);
+    const double dh = h1 - h0;
+    const bool divergent = bad || isnan(dh) || (isfinite(dh) && fabs(dh) > 1000.0);
+    bool accepted = false;
+    if (divergent) {
+      ++div_count;
+    } else {
+      const double u = probe_p ? A.probe_u[c] : R.uniform();
+      if (log(u) < -dh) {
+        accepted = true;
+        cur ^= 1;
+        lp0 = lp1;
+      }
+    }
+    __syncwarp(mask);  // lane 0's stores are read by the chain's lanes below / next pass
+    if (A.mode == kModeProbe) {
+      if (t == 0) {
+        A.out_a[c] = h0;
+        A.out_b[c] = h1;
+        A.out_flags[c] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
+      }
+      continue;
+    }
+    if (A.mode == kModeChain) {
+      if (t == 0) {
+        for (int d = 0; d < M.dim; ++d)
+          A.traj[it * M.dim + d] = S.pos[cur * plane + static_cast<size_t>(d) * nch + c];
+        A.traj_div[it] = divergent ? 1 : 0;
+      }
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < NGM; ++i) qG[i] = i < ng ? S.pos[gaddr(cur, i)] : 0.0;
+    const double sp = log_pred<FAM, T, NCM, NGM>(M, S, c, t, mask, fold, cur, qG);
+    if (A.mode == kModeWarmup) {
+      warm += sp;
+    } else if (t == 0) {
+      accum_observe(S.acc, c, nch, sp, A.iter0 + it, A.planned_n, A.D, A.b);
+    }
+  }
+  if (t == 0) {
+    S.cur[c] = static_cast<int8_t>(cur);
+    S.lp0[c] = lp0;
+    S.rng_pos[c] = R.pos;
+    S.rng_cached[c] = R.cached;
+    S.rng_has[c] = R.has_cached ? 1 : 0;
+    S.divergences[c] += div_count;
+    if (A.mode == kModeWarmup) S.warm_sum[c] += warm;
+  }
+}
+
+template <int FAM, int NCM, int NGM>
+cudaError_t launch_family(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T,
+                          cudaStream_t st) {
+  const int chains_per_block = kBlock / T;
+  const int grid = (S.nch + chains_per_block - 1) / chains_per_block;
+  if (grid == 0) return cudaSuccess;
+  switch (T) {
+    case 1: gauss_kernel<FAM, 1, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 4: gauss_kernel<FAM, 4, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 8: gauss_kernel<FAM, 8, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 32: gauss_kernel<FAM, 32, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Lanes per chain: enough threads to fill the GPU (>= ~64 resident warps worth of work per SM
+// is not reachable with few chains, so few chains get whole warps), capped by the rows a lane
+// would own in the smallest segment.
+int gauss_lanes_per_chain(const ModelDev& M, int nch) {
+  const long target_threads = 148L * 512;
+  int T = 1;
+  while (T < 32 && static_cast<long>(nch) * T < target_threads) T *= 2;
+  if (T == 2) T = 4;
+  if (T == 16) T = 32;
+  const int rows_per_group = M.J > 0 ? M.n / M.J : M.n;
+  while (T > 1 && rows_per_group < 2 * T) T = T == 32 ? 8 : (T == 8 ? 4 : 1);
+  return T;
+}
+
+cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T,
+                         cudaStream_t st) {
+  switch (M.family) {
+    case kGrouped:
+      if (M.nc > 8) return cudaErrorInvalidValue;
+      return launch_family<kGrouped, 8, 11>(M, S, A, T, st);
+    case kRadon:
+      return launch_family<kRadon, 1, 4>(M, S, A, T, st);
+    case kSeasonal:
+      if (M.nc > 13) return cudaErrorInvalidValue;
+      return launch_family<kSeasonal, 13, 15>(M, S, A, T, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pcvg

@@ -1,0 +1,163 @@
+// Step 4 on the host: merge the per-fold tables (produced on device, gathered across GPUs in
+// fold order) into the global statistics exactly as compute_stats (engine.cpp:117-253), the
+// report assembly (engine.cpp:410-459) and the shuffle benchmark / verdict
+// (engine.cpp:464-480, diagnostics.cpp:76-119). Fold-order sums keep the result bit-identical for
+// any number of GPUs.
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "../../include/pcvg.h"
+#include "host_common.hpp"
+
+namespace pcvg {
+
+namespace {
+
+const double kNaN = std::numeric_limits<double>::quiet_NaN();
+const double kInf = std::numeric_limits<double>::infinity();
+
+bool rhat_from_sums(const double* sx, const double* sxx, int l, int64_t n, double* rhat) {
+  if (l < 2 || n < 2) return false;  // diagnostics.cpp:11-33
+  double w = 0.0, grand = 0.0;
+  for (int c = 0; c < l; ++c) {
+    w += (sxx[c] - sx[c] * sx[c] / n) / (n - 1.0) / l;
+    grand += sx[c] / n / l;
+  }
+  double b = 0.0;
+  for (int c = 0; c < l; ++c) {
+    const double dev = sx[c] / n - grand;
+    b += dev * dev;
+  }
+  b *= static_cast<double>(n) / (l - 1.0);
+  if (!std::isfinite(w) || !std::isfinite(b) || !(w > 0.0)) return false;
+  *rhat = std::sqrt(((n - 1.0) / n * w + b / n) / w);
+  return true;
+}
+
+}  // namespace
+
+// final_checkpoint: 0 = intermediate snapshot (no exclusions), 1 = final (exclusions, per-model
+// report, benchmark + verdict), 2 = early-stop probe (no exclusions, benchmark + verdict on the
+// first D_used blocks).
+void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
+                 int32_t final_checkpoint, const pcvg_fold_table* ft, const double* y_x,
+                 const double* y_x2, int D_used, pcvg_report* rep) {
+  const int l = cfg->chains;
+  const bool final = final_checkpoint == 1;
+  const int D_stride = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
+  std::vector<char> failed(K, 0), excluded(K, 0);
+  if (final && ft->failed)
+    for (int k = 0; k < K; ++k) failed[k] = ft->failed[k] != 0;
+  for (int k = 0; k < K; ++k) {  // engine.cpp:145-155
+    if (final && failed[k]) excluded[k] = 1;
+    if (final)
+      for (int m = 0; m < nm; ++m)
+        if (std::isnan(ft->estimate[static_cast<size_t>(m) * K + k])) excluded[k] = 1;
+  }
+  double naive_sum = 0.0, mc_sum = 0.0, best = -1.0;
+  bool mc_inf = false;
+  for (int m = 0; m < nm; ++m)
+    for (int k = 0; k < K; ++k) {
+      if (excluded[k]) continue;
+      const size_t i = static_cast<size_t>(m) * K + k;
+      if (std::isfinite(ft->mc_contribution[i])) {
+        mc_sum += ft->mc_contribution[i];
+        naive_sum += ft->naive_contribution[i];
+      } else {
+        mc_inf = true;
+      }
+      if (std::isfinite(ft->rhat[i])) best = std::max(best, ft->rhat[i]);  // rhat_max
+    }
+  std::vector<double> included;
+  included.reserve(K);
+  double delta_hat = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double dk = nm == 2 ? ft->estimate[k] - ft->estimate[K + k] : ft->estimate[k];
+    if (final && rep->delta_k) rep->delta_k[k] = dk;
+    if (!excluded[k]) included.push_back(dk);
+  }
+  for (double dk : included) delta_hat += dk;
+  rep->delta_hat = delta_hat;
+  if (included.size() >= 2) {  // selection_probability, scoring.cpp:141-158
+    const double kk = static_cast<double>(included.size());
+    const double mean = delta_hat / kk;
+    double ss = 0.0;
+    for (double dk : included) ss += (dk - mean) * (dk - mean);
+    const double s2 = ss / (kk - 1.0);
+    const double denom = std::sqrt(kk * s2);
+    double prob;
+    if (denom == 0.0) prob = delta_hat > 0.0 ? 1.0 : (delta_hat < 0.0 ? 0.0 : 0.5);
+    else prob = 0.5 * std::erfc(-(delta_hat / denom) * 0.70710678118654752440084436210485);
+    rep->sigma2_delta = s2;
+    rep->epistemic_se = std::sqrt(kk * s2);
+    rep->prob_a_better = nm == 2 ? prob : kNaN;
+  } else {
+    rep->sigma2_delta = rep->epistemic_se = rep->prob_a_better = kNaN;
+  }
+  const double ln = static_cast<double>(l) * iter_count;
+  rep->mcse = mc_inf ? kInf : std::sqrt(mc_sum / ln);
+  rep->ess_overall = mc_sum > 0.0 ? static_cast<double>(l) * iter_count * naive_sum / mc_sum : kNaN;
+  rep->rhat_max = best < 0.0 ? kNaN : best;
+
+  if (final) {
+    for (int m = 0; m < nm; ++m) {
+      rep->score_total[m] = 0.0;
+      rep->numeric_faults[m] = 0;
+      rep->rhat_excluded[m] = 0;
+      for (int k = 0; k < K; ++k) {
+        const size_t i = static_cast<size_t>(m) * K + k;
+        if (rep->folds.failed) rep->folds.failed[i] = excluded[k];
+        if (!excluded[k]) rep->score_total[m] += ft->estimate[i];
+        if (ft->fault[i]) ++rep->numeric_faults[m];
+        if (!std::isfinite(ft->rhat[i]) && !excluded[k]) ++rep->rhat_excluded[m];
+      }
+    }
+  }
+  if (final_checkpoint == 0) return;
+  // shuffle benchmark (diagnostics.cpp:76-101) over non-failed folds, model-major
+  rep->benchmark_count = 0;
+  const int64_t nbench = final ? cfg->iters : iter_count;
+  if (y_x && y_x2 && rep->benchmark) {
+    std::vector<double> sx(l), sxx(l);
+    for (int r = 0; r < cfg->bench_draws; ++r) {
+      HostRng rng(cfg->seed, stream_key(PCVG_STREAM_BENCHMARK, static_cast<uint64_t>(r), 0, 0));
+      double rb = -1.0;
+      for (int m = 0; m < nm; ++m)
+        for (int k = 0; k < K; ++k) {
+          if (failed[k]) continue;
+          const size_t base = (static_cast<size_t>(m) * K + k) * l * D_stride;
+          for (int c = 0; c < l; ++c) {
+            sx[c] = 0.0;
+            sxx[c] = 0.0;
+            for (int blk = 0; blk < D_used; ++blk) {
+              const int src = static_cast<int>(rng.below(static_cast<uint64_t>(l)));
+              sx[c] += y_x[base + static_cast<size_t>(src) * D_stride + blk];
+              sxx[c] += y_x2[base + static_cast<size_t>(src) * D_stride + blk];
+            }
+          }
+          double rr;
+          if (rhat_from_sums(sx.data(), sxx.data(), l, nbench, &rr)) rb = std::max(rb, rr);
+        }
+      if (rb >= 0.0) rep->benchmark[rep->benchmark_count++] = rb;
+    }
+  }
+  rep->verdict_quantile = cfg->bench_quantile;
+  if (std::isfinite(rep->rhat_max) && rep->benchmark_count > 0) {  // diagnostics.cpp:103-119
+    std::vector<double> s(rep->benchmark, rep->benchmark + rep->benchmark_count);
+    std::sort(s.begin(), s.end());
+    const int64_t n = static_cast<int64_t>(s.size());
+    int64_t rank = static_cast<int64_t>(std::ceil(cfg->bench_quantile * n));
+    rank = std::clamp<int64_t>(rank, 1, n);
+    rep->verdict_quantile_value = s[rank - 1];
+    rep->verdict_observed = rep->rhat_max;
+    rep->verdict_pass = rep->rhat_max <= rep->verdict_quantile_value;
+  } else {
+    rep->verdict_pass = 1;
+    rep->verdict_quantile_value = kNaN;
+    rep->verdict_observed = rep->rhat_max;
+  }
+}
+
+}  // namespace pcvg

@@ -1,0 +1,96 @@
+// Device-side descriptors of one uploaded model and of its chains.
+#pragma once
+#include <cstdint>
+
+#include "device_common.cuh"
+
+namespace pcvg {
+
+enum Family : int { kGrouped = 0, kRadon = 1, kSeasonal = 2, kLogistic = 3 };
+
+// Kernel modes.
+enum Mode : int {
+  kModeEval = 0,    // gradient + log joint at the stored position (init, pcvg_eval)
+  kModeWarmup = 1,  // Step 2: hmc steps, Sigma log_pred into warm_sum (hmc.cpp:121-149)
+  kModeSample = 2,  // Step 3: hmc steps, ScoreAccum::observe (engine.cpp:342-381)
+  kModeProbe = 3,   // one hmc step with injected momentum / uniform (parity probe)
+  kModeChain = 4,   // hmc steps writing the trajectory (parity probe)
+  kModePred = 5     // log_pred at the stored position (parity probe)
+};
+
+constexpr int kMaxCov = 16;
+
+struct ModelDev {
+  int family;
+  int n;     // observations (device row order: group-major for hierarchical families)
+  int nc;    // covariate columns read by the kernel
+  int J;     // group parameters (first J dims); 0 if none
+  int ng;    // global parameters (dims J..dim-1)
+  int dim;
+  int K;     // folds; index K is the full-data sentinel
+  const double* y;    // [n]
+  const double* x;    // [nc][n] column-major (coalesced per covariate)
+  const double* xr;   // [n][nc_pad] row-major copy (logistic tiles), may be null
+  int nc_pad;
+  const int* key;     // [n] partition fold id, or time rank (hv-block)
+  const int* grp_ptr; // [J+1]
+  const int* fold_lo; // [K+1] row i is held out of training iff lo <= key[i] < hi
+  const int* fold_hi;
+  const int* n_train; // [K+1]
+  const int* fold_seg;  // [K+2] test segments of fold k: [fold_seg[k], fold_seg[k+1])
+  const int* seg_group;
+  const int* seg_unseen;
+  const int* seg_row;   // [nseg+1]
+  const int* seg_rows;  // device row ids of the test rows
+  const double* inv_mass;  // [dim]
+  double step;
+  int n_lf;
+  // family options and host-computed prior constants (glibc lgamma/log, priors.hpp:13-26)
+  double cmask[kMaxCov];  // grouped covariate mask as 0/1
+  int include_floor;
+  int p, q, rho_sym;
+  double c_lhn10, c_lhn1;  // 0.5 log(2/(pi v)) for v = 10, 1
+  double c_lgamma6_9;      // 6 log 9 - lgamma(6)
+  double c_lgamma10_10;    // 10 log 10 - lgamma(10)
+  double c_lbeta55;        // lgamma(10) - 2 lgamma(5)
+  double c_log4;           // log(4)
+};
+
+struct ChainsDev {
+  int nch;        // chains on this device (task order restricted to the shard)
+  int L;          // chains per fold
+  int fold0;      // first global fold of the shard
+  const int* fold_override;  // probes: explicit fold per chain, or null
+  uint64_t seed;
+  uint64_t stream_model;  // model id used in stream keys (0 under shared_streams)
+  double* pos;    // [2][dim][nch] position (double buffered, `cur` selects)
+  double* grad;   // [2][dim][nch] cached gradient at pos
+  double* wp;     // [dim][nch] working momentum (group dims) / probe scratch
+  double* lp0;    // [nch] cached log joint at pos
+  int8_t* cur;    // [nch]
+  uint64_t* rng_stream;  // [nch] stream_key(ChainSampling, model, fold, chain)
+  uint64_t* rng_pos;
+  double* rng_cached;
+  int8_t* rng_has;
+  int64_t* divergences;  // cumulative (warm-up + sampling), hmc.hpp:20-24
+  double* warm_sum;      // WarmupStats::logpred_sum
+  AccumDev acc;
+};
+
+struct RunArgs {
+  int mode;
+  int64_t n_iters;
+  int64_t iter0;      // sampling iteration index of the first step (block_for)
+  int64_t planned_n;  // N (accum.hpp:96-111)
+  int D;
+  int b;
+  const double* probe_momentum;  // [nch][dim]
+  const double* probe_u;         // [nch]
+  double* out_a;  // probe: h0 / eval: log joint / pred: log_pred   [nch]
+  double* out_b;  // probe: h1                                      [nch]
+  int32_t* out_flags;  // probe: accepted | divergent << 1           [nch]
+  double* traj;        // chain mode: [n_iters][dim]
+  int32_t* traj_div;   // chain mode: [n_iters]
+};
+
+}  // namespace pcvg

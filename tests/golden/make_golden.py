@@ -1,0 +1,169 @@
+"""Generates the committed golden fixtures under tests/golden/ from the REFERENCE itself.
+
+Run here (needs /root/reference compiled into oracle/_ref/libpcvref.so by `make -C oracle ref`):
+    python tests/golden/make_golden.py [name ...]
+
+For every parity configuration it stores (npz): the dataset (from the product simulators, whose
+bit-exactness against the reference simulators is a separate test), the fold assignment, the
+reference's adapt_full_data kernel (step size + inverse mass) and draw bank per model
+(adapt.cpp:96-221, the `_bank.f64` content), and the reference run_pcv report on that input
+(engine.cpp:257-483). The GPU box has no /root/reference: GPU tests and bench.py read these files.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from paper_2310_07002_b200 import abi, pcv  # noqa: E402
+import _oracle as O  # noqa: E402
+
+# name -> (builder, models[(family spec kwargs)], adapt settings, run settings)
+
+
+def _cfg1():
+    d = pcv.simulate_linreg(100, 5, seed=11)
+    f = pcv.make_loo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_GROUPED)]
+
+
+def _ex1():
+    d = pcv.simulate_grouped_regression(50, 5, 4, 1.0, seed=1)
+    f = pcv.make_logo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_GROUPED, covariate_mask=[1, 1, 1, 1]),
+                  dict(family=abi.FAMILY_GROUPED, covariate_mask=[1, 1, 1, 0])]
+
+
+def _radon():
+    d = pcv.simulate_radon_style(1200, 40, 5)
+    f = pcv.make_logo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_RADON, include_floor=1),
+                  dict(family=abi.FAMILY_RADON, include_floor=0)]
+
+
+def _seasonal_tb():
+    d = pcv.simulate_seasonal_ar(600, 2, 11, 0.6, seed=7)
+    f = pcv.make_time_block_scheme(d, 20)
+    return d, f, [dict(family=abi.FAMILY_SEASONAL_AR, ar_order=2, dummies=11),
+                  dict(family=abi.FAMILY_SEASONAL_AR, ar_order=2, dummies=0)]
+
+
+def _seasonal_hv():
+    d = pcv.simulate_seasonal_ar(600, 2, 11, 0.6, seed=7)
+    f = pcv.make_hv_block_scheme(d, 20, 6)
+    return d, f, [dict(family=abi.FAMILY_SEASONAL_AR, ar_order=2, dummies=11)]
+
+
+def _logistic():
+    d = pcv.simulate_logistic(500, 10, seed=1)
+    f = pcv.make_loo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_LOGISTIC)]
+
+
+def _logistic_kfold():
+    d = pcv.simulate_logistic(500, 10, seed=1)
+    f = pcv.make_kfold_scheme(d, 10, 1)
+    return d, f, [dict(family=abi.FAMILY_LOGISTIC)]
+
+
+def _cfg2_bench():
+    d = pcv.simulate_logistic(10000, 50, seed=1)
+    f = pcv.make_loo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_LOGISTIC)]
+
+
+CONFIGS = {
+    # name: (builder, adapt kwargs, run kwargs or None)
+    "cfg1_linreg_loo": (_cfg1, dict(chains=4, warmup=1000, draws=500), dict(chains=4, iters=200, warmup=50, batch_size=20, bench_draws=50, checkpoint_every=100)),
+    "ex1_grouped_logo": (_ex1, dict(chains=4, warmup=1000, draws=250), dict(chains=4, iters=200, warmup=50, batch_size=20, bench_draws=50, checkpoint_every=100)),
+    "radon_logo": (_radon, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
+    "seasonal_timeblocks": (_seasonal_tb, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
+    "seasonal_hvblock": (_seasonal_hv, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
+    "logistic_loo": (_logistic, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
+    "logistic_kfold": (_logistic_kfold, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
+    # bench input only (no reference run: 80k chains is the GPU workload)
+    "cfg2_logistic_bench": (_cfg2_bench, dict(chains=4, warmup=300, draws=250), None),
+}
+
+
+def make(name):
+    builder, akw, rkw = CONFIGS[name]
+    d, f, specs = builder()
+    out = {"y": d.y, "x": d.x, "K": np.int64(f.K)}
+    if name == "cfg2_logistic_bench":  # regenerated bit-exactly by pcv.simulate_logistic
+        out = {"K": np.int64(f.K), "sim_logistic": np.array([d.n_obs, d.x.shape[1], 1], dtype=np.int64)}
+    if d.group_id is not None:
+        out["group_id"] = d.group_id
+    if d.time_index is not None:
+        out["time_index"] = d.time_index
+    if f.test_index is not None and "sim_logistic" not in out:
+        out["test_index"] = f.test_index
+    if f.intervals is not None:
+        out["intervals"] = f.intervals
+    fa = f.arrays()
+    rmodels, kernels, banks = [], [], []
+    for m, s in enumerate(specs):
+        sa = abi.SpecArrays(**s)
+        rm = O.RModel(d, fa, sa)
+        fit = rm.adapt(seed=1, model_id=m, **akw)
+        out[f"spec{m}"] = np.array([s.get("family"), s.get("include_floor", 1), s.get("ar_order", 1),
+                                    s.get("dummies", 0), s.get("rho_transform", 0)], dtype=np.int64)
+        if s.get("covariate_mask") is not None:
+            out[f"mask{m}"] = np.array(s["covariate_mask"], dtype=np.int32)
+        out[f"step{m}"] = np.float64(fit["step_size"])
+        out[f"inv_mass{m}"] = fit["inv_mass_diag"]
+        out[f"bank{m}"] = fit["bank"]
+        out[f"mean_accept{m}"] = np.float64(fit["mean_accept"])
+        rmodels.append(rm)
+        kernels.append(abi.KernelArrays(fit["step_size"], 32, fit["inv_mass_diag"]))
+        banks.append(fit["bank"])
+        print(f"  {name} model {m}: step {fit['step_size']:.4g} accept {fit['mean_accept']:.3f} "
+              f"divergences {fit['divergences']}", flush=True)
+    out["n_models"] = np.int64(len(specs))
+    if rkw is not None:
+        cfg = abi.run_config(seed=1, **rkw)
+        rep = O.run_pcv_ref(rmodels, list(range(len(specs))), kernels, banks, cfg, threads=0)
+        for k in ("delta_hat", "mcse", "sigma2_delta", "epistemic_se", "prob_a_better", "ess_overall",
+                  "rhat_max", "dropped_batch_draws", "verdict_pass", "verdict_quantile_value"):
+            out[f"ref_{k}"] = np.float64(rep[k])
+        for k in ("estimate", "log_f_hat", "mc_contribution", "ess", "rhat", "batches", "fault",
+                  "failed", "divergences", "delta_k", "snapshots", "benchmark"):
+            out[f"ref_{k}"] = rep[k]
+        out["ref_score_total"] = np.array(rep["score_total"])
+        out["run_cfg"] = np.array([rkw["chains"], rkw["iters"], rkw["warmup"], rkw["batch_size"], 5,
+                                   rkw["bench_draws"], rkw.get("checkpoint_every", 0)], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
+def load(name):
+    """Loads a fixture into product descriptors: (data, folds, [(spec kwargs, KernelParams, bank)], npz)."""
+    z = np.load(os.path.join(HERE, f"{name}.npz"))
+    if "sim_logistic" in z:
+        n, p, seed = (int(v) for v in z["sim_logistic"])
+        d = pcv.simulate_logistic(n, p, seed=seed)
+        f = pcv.make_loo_scheme(d)
+    else:
+        d = pcv.Dataset(z["y"], z["x"], z["group_id"] if "group_id" in z else None,
+                        z["time_index"] if "time_index" in z else None)
+        f = pcv.FoldAssignment(int(z["K"]), z["test_index"] if "test_index" in z else None,
+                               z["intervals"] if "intervals" in z else None)
+    models = []
+    for m in range(int(z["n_models"])):
+        fam, floor, p, q, rho = (int(v) for v in z[f"spec{m}"])
+        kw = dict(family=fam, include_floor=floor, ar_order=p, dummies=q, rho_transform=rho)
+        if f"mask{m}" in z:
+            kw["covariate_mask"] = z[f"mask{m}"]
+        kp = pcv.KernelParams(float(z[f"step{m}"]), 32, z[f"inv_mass{m}"])
+        models.append((kw, kp, z[f"bank{m}"]))
+    return d, f, models, z
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CONFIGS)
+    for nm in names:
+        print(nm, flush=True)
+        make(nm)

@@ -1,0 +1,108 @@
+"""Shared helpers for the parity tests: fixture loading into product + oracle models, and the
+condition-aware tolerance of SURVEY.md 8(c): |device - oracle| <= rtol * sum_i |term_i|."""
+import numpy as np
+
+from paper_2310_07002_b200 import abi, pcv
+import _oracle as O
+from make_golden import load
+
+LOG2PI = 1.8378770664093454835606594728112
+
+GAUSS_FIXTURES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks",
+                  "seasonal_hvblock"]
+ALL_FIXTURES = GAUSS_FIXTURES + ["logistic_loo", "logistic_kfold"]
+
+_MODEL_CLS = {
+    abi.FAMILY_GROUPED: lambda nm, d, f, kw: pcv.GroupedRegressionModel(nm, d, f, kw.get("covariate_mask")),
+    abi.FAMILY_RADON: lambda nm, d, f, kw: pcv.RadonStyleModel(nm, d, f, kw["include_floor"]),
+    abi.FAMILY_SEASONAL_AR: lambda nm, d, f, kw: pcv.SeasonalARModel(nm, d, f, kw["ar_order"], kw["dummies"], kw["rho_transform"]),
+    abi.FAMILY_LOGISTIC: lambda nm, d, f, kw: pcv.LogisticModel(nm, d, f),
+}
+
+
+class Case:
+    """One fixture: the dataset/folds, per model the product descriptor, the oracle model,
+    kernel params and bank."""
+
+    def __init__(self, name):
+        self.name = name
+        self.data, self.folds, specs, self.z = load(name)
+        self.fa = self.folds.arrays()
+        self.models, self.omodels, self.kparams, self.banks, self.kws = [], [], [], [], []
+        for m, (kw, kp, bank) in enumerate(specs):
+            self.kws.append(kw)
+            self.models.append(_MODEL_CLS[kw["family"]](f"M{m}", self.data, self.folds, kw))
+            sa = abi.SpecArrays(**kw)
+            self.omodels.append(O.OModel(self.data, self.fa, sa))
+            self.kparams.append(kp)
+            self.banks.append(bank)
+
+    @property
+    def K(self):
+        return self.folds.K
+
+    def excluded(self, fold):
+        n = self.data.n_obs
+        if fold >= self.K:
+            return np.zeros(n, bool)
+        if self.folds.test_index is not None:
+            return self.folds.test_index == fold
+        order = np.argsort(self.data.time_index, kind="stable")
+        rank = np.empty(n, np.int64)
+        rank[order] = np.arange(n)
+        iv = self.folds.intervals.reshape(-1, 4)[fold]
+        return (rank >= iv[2]) & (rank < iv[3])
+
+
+def term_scales(case, m, theta, fold):
+    """(S_lp, S_grad): sums of absolute per-observation terms of log_joint and of a gradient
+    component (an upper bound shared by all components)."""
+    kw = case.kws[m]
+    d = case.data
+    x, y = d.x, d.y
+    train = ~case.excluded(fold)
+    fam = kw["family"]
+    th = np.asarray(theta)
+    big = 10.0 + d.n_obs * 0 + np.abs(th).max() * th.size * 4
+    if fam == abi.FAMILY_LOGISTIC:
+        eta = th[0] + x @ th[1:]
+        r = y - 1 / (1 + np.exp(-eta))
+        s_lp = np.sum(np.abs(y * eta - np.logaddexp(0, eta))[train]) + np.sum(0.5 * (LOG2PI + th ** 2))
+        s_g = np.sum((np.abs(r) * (1 + np.abs(x).sum(1)))[train]) + big
+        return s_lp + 1, s_g
+    if fam == abi.FAMILY_GROUPED:
+        J, P = d.n_groups, x.shape[1]
+        mask = np.ones(P) if kw.get("covariate_mask") is None else np.asarray(kw["covariate_mask"], float)
+        mean = th[d.group_id] + x @ (th[J:J + P] * mask)
+        v = np.exp(th[J + P + 2]) ** 2
+        va = np.exp(th[J + P + 1]) ** 2
+        extra = np.sum(np.abs(th[:J] - th[J + P]) / va + (th[:J] - th[J + P]) ** 2 / va) + J + va
+    elif fam == abi.FAMILY_RADON:
+        J = d.n_groups
+        va, v = np.exp(th[J + 2]), np.exp(th[J + 3])
+        mean = th[J + 1] + np.sqrt(va) * th[d.group_id] + (th[J] if kw["include_floor"] else 0) * x[:, 0]
+        extra = np.sum(th[:J] ** 2) + J + 10 * (va + v)
+    else:
+        p, q = kw["ar_order"], kw["dummies"]
+        w = 1 / (1 + np.exp(-th[:p]))
+        rho = 0.5 * (1 + w) if kw["rho_transform"] == 0 else 2 * w - 1
+        mean = th[p] + x[:, :p] @ rho + x[:, p:p + q] @ th[p + 1:p + 1 + q]
+        v = np.exp(th[p + q + 1]) ** 2
+        extra = v + 10
+    r = y - mean
+    s_lp = np.sum((0.5 * np.abs(LOG2PI + np.log(v) + r * r / v))[train]) + extra + big
+    s_g = np.sum((np.abs(r) / v * (1 + np.abs(x).sum(1) + np.abs(th).max()) + r * r / v + 1)[train]) + extra + big
+    return s_lp, s_g
+
+
+def sample_thetas(case, m, n, seed=0):
+    """Points near the posterior: bank rows plus small perturbations."""
+    rng = np.random.default_rng(seed)
+    bank = case.banks[m]
+    rows = bank[rng.integers(0, bank.shape[0], n)]
+    return rows + 0.05 * rng.standard_normal(rows.shape)
+
+
+def probe_folds(case):
+    K = case.K
+    return sorted({0, 1, K // 2, K - 1, K})
