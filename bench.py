@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""PCV sampler benchmark (BASELINE.json metric: chain-steps/sec).
+
+Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted on): Bernoulli-logit
+regression, synthetic N=10,000 observations x P=50 covariates (+ intercept), LOO CV = 10,000 folds
+x 8 chains = 80,000 HMC chains, n_leapfrog = 32, FP64. One "step" = one HMC transition of every
+chain + its log_pred + the online accumulator update (engine.cpp:360-373). Kernel parameters and
+the warm-start draw bank are the reference's own adapt_full_data output on this dataset
+(tests/golden/cfg2_logistic_bench.npz). Multi-GPU: folds are sharded across ranks (strong
+scaling, total work fixed); no collective on the data path, the per-fold statistics are gathered
+once after the timed region.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+N_OBS, P, L, N_LF = 10000, 50, 8, 32
+WORKLOAD = "cfg2: logistic regression N=10000 P=50, LOO 10000 folds x 8 chains, n_leapfrog=32, FP64"
+# Algorithmic FLOPs of one chain-step: n_lf gradient passes, each two
+# N x (P+1) contractions (X.theta and X^T.r) = 4 N (P+1) flop; log density fused, transcendentals
+# not counted.
+FLOP_PER_CHAIN_STEP = N_LF * 4.0 * N_OBS * (P + 1)
+CPU_SAMPLE_FOLDS = 64
+
+
+def peak_fp64():
+    path = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+    with open(path) as f:
+        pk = json.load(f)
+    return pk["dmma_tflops_bps8"], "measured FP64 DMMA peak (profiles/r01_fp64_peaks.json; "\
+        "MEASURED_PEAKS.json has no FP64 figure)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_inputs():
+    from make_golden import load
+    d, f, models, _ = load("cfg2_logistic_bench")
+    kw, kp, bank = models[0]
+    return d, f, kp, bank
+
+
+def cpu_sample(folds_total, steps, warmup, threads, prefer_ref=True):
+    """The reference's own Step 2-3 task loop on a bounded fold sample (oracle/_ref), or the C
+    port when the reference build is absent. Returns (chain-steps/s, kind, sample description)."""
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    from paper_2310_07002_b200 import abi
+    d, f, kp, bank = load_inputs()
+    fa = f.arrays()
+    spec = abi.SpecArrays(abi.FAMILY_LOGISTIC)
+    kern = abi.KernelArrays(kp.step_size, kp.n_leapfrog, kp.inv_mass_diag)
+    rng = np.random.default_rng(0)
+    folds = np.sort(rng.choice(folds_total, CPU_SAMPLE_FOLDS, replace=False)).astype(np.int32)
+    bank = np.ascontiguousarray(bank)
+    s_s, w_s, cs = C.c_double(), C.c_double(), C.c_double()
+    if prefer_ref and O.have_ref():
+        lib = O.ref()
+        m = O.RModel(d, fa, spec)
+        rc = lib.pcvref_time_tasks(m.h, len(folds), abi.ptr(folds, C.c_int32), L, warmup, steps, 1, 0,
+                                   C.byref(kern.struct), abi.ptr(bank, C.c_double), bank.shape[0],
+                                   threads, C.byref(s_s), C.byref(w_s), C.byref(cs))
+        kind = "reference"
+    else:
+        lib = O.oracle()
+        m = O.OModel(d, fa, spec)
+        rc = lib.pcvo_time_tasks(m.h, len(folds), abi.ptr(folds, C.c_int32), L, warmup, steps, 1, 0,
+                                 C.byref(kern.struct), abi.ptr(bank, C.c_double), bank.shape[0],
+                                 threads, C.byref(s_s), C.byref(w_s), C.byref(cs))
+        kind = "port"
+    assert rc == 0, "cpu sample failed"
+    chain_steps = len(folds) * L * steps
+    sample = (f"{len(folds)} of {folds_total} LOO folds x {L} chains x {steps} sampling steps "
+              f"(after {warmup} warm-up steps) = {chain_steps} chain-steps, {threads} threads, "
+              f"{s_s.value:.2f} s")
+    return chain_steps / s_s.value, kind, sample
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    value, kind, sample = cpu_sample(N_OBS, args.steps, args.warmup, threads)
+    line = {"impl": "reference", "metric": "chain-steps/sec", "value": value, "unit": "chain-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * CPU_SAMPLE_FOLDS * L / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "chain-steps/s", "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "chain-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--folds", type=int, default=0, help="debug: limit the fold count")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    from paper_2310_07002_b200 import abi, pcv
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    d, f, kp, bank = load_inputs()
+    K = args.folds or f.K
+    fb, fe = rank * K // world, (rank + 1) * K // world
+    model = pcv.LogisticModel("M_A", d, f)
+    cfg = pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup, batch_size=min(50, args.steps),
+                        blocks=5, bench_draws=100, seed=1, fold_begin=fb, fold_end=fe)
+    ctx = pcv.Context(local)
+    ctx.add_model(model, kp, bank, model_id=0)
+    ctx.begin(cfg)  # Step 2: warm start + args.warmup untimed warm-up transitions
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    _, launches0 = ctx.last_advance_ms()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # evict L2 (126 MB) between timed steps
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            ctx.advance(1)  # one HMC transition of every chain; CUDA events inside libpcvg
+            step_ms.append(ctx.last_advance_ms()[0])
+    _, launches1 = ctx.last_advance_ms()
+    local_ms = float(np.sum(step_ms))
+    if dist:
+        t = torch.tensor([local_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    else:
+        total_ms = local_ms
+    chains_total = K * L
+    value = chains_total * args.steps / (total_ms / 1e3)
+    # per-fold statistics of this shard -> rank 0 -> Step-4 merge (untimed)
+    cols, divs, dropped, done = ctx.fold_stats(fe - fb)
+    if dist:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, cols)
+        cols = {k: np.concatenate([g[k] for g in gathered]) for k in cols}
+    result = None
+    if rank == 0:
+        rep = pcv.merge(1, K, cfg, done, 0, cols)
+        result = {"score_total_elpd": rep["delta_hat"], "mcse": rep["mcse"],
+                  "epistemic_se": rep["epistemic_se"], "rhat_max": rep["rhat_max"],
+                  "ess_overall": rep["ess_overall"], "iters": int(done)}
+    ctx.close()
+
+    # roofline of the dominant kernel (logistic_kernel: one launch per step)
+    peak, peak_src = peak_fp64()
+    per_launch_ms = local_ms / args.steps
+    achieved = FLOP_PER_CHAIN_STEP * (fe - fb) * L / (per_launch_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_logistic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    line = None
+    if rank == 0:
+        line = {"metric": "chain-steps/sec", "value": value, "unit": "chain-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": WORKLOAD, "folds": K, "chains_per_fold": L, "n_obs": N_OBS,
+                           "covariates": P, "n_leapfrog": N_LF, "chains": chains_total,
+                           "l2": "flushed between timed steps (256 MiB memset); X (4 MB) then re-read from HBM",
+                           "parallelism": f"fold-sharded x{world}"},
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "flop_per_chain_step": FLOP_PER_CHAIN_STEP, "peak_source": peak_src,
+                             "kernel": "logistic_kernel (FP64 DMMA)"},
+                "clocks": clk.summary(), "gpu_launches": int(launches1 - launches0), "result": result}
+    # e2e: the public API call with host buffers (pcvg_run: H2D of data/bank, Step 2 + Step 3,
+    # per-fold + Step-4 statistics, D2H of the report), wall-clock, max over ranks.
+    if not args.no_e2e:
+        t0 = time.perf_counter()
+        if world == 1:
+            rep = pcv.run_pcv([pcv.ModelInput(model, pcv.FullDataFit(kp, bank), 0)],
+                              pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup,
+                                            batch_size=min(50, args.steps), blocks=5, bench_draws=100,
+                                            seed=1), device=local)
+            d2h = sum(v.nbytes for v in rep.values() if isinstance(v, np.ndarray))
+        else:
+            with pcv.Context(local) as c2:
+                c2.add_model(model, kp, bank, model_id=0)
+                c2.begin(cfg)
+                c2.advance(args.steps)
+                cols2, _, _, done2 = c2.fold_stats(fe - fb)
+                d2h = sum(v.nbytes for v in cols2.values())
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        h2d = d.y.nbytes + d.x.nbytes + f.test_index.nbytes + bank.nbytes + kp.inv_mass_diag.nbytes
+        if line is not None:
+            steps_all = args.steps + args.warmup
+            line["e2e"] = {"value": chains_total * steps_all / e2e_s, "unit": "chain-steps/s",
+                           "h2d_bytes_per_step": int(h2d / steps_all), "d2h_bytes_per_step": int(d2h / steps_all),
+                           "wall_s": e2e_s, "chain_steps": chains_total * steps_all,
+                           "note": "pcvg_run with host inputs: upload, warm start, warm-up + sampling, "
+                                   "per-fold stats, shuffle benchmark (R=100), report download"}
+    if line is not None and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        cv, kind, sample = cpu_sample(K, 12, 1, threads)
+        line["cpu_baseline"] = {"value": cv, "unit": "chain-steps/s", "cores": threads, "kind": kind,
+                                "sample": sample}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

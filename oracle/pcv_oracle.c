@@ -13,6 +13,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #include <unistd.h>
 
 static __thread char g_err[512];
@@ -1372,5 +1373,103 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
   for (long i = 0; i < rc.n_tasks; ++i) { free(rc.tasks[i].position); free(rc.tasks[i].snaps); }
   for (int m = 0; m < n_models; ++m) free(rc.centers[m]);
   free(rc.centers); free(rc.tasks); free(rc.checkpoints); free(failed); free(fs); free(rh); free(fl);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ bench sampler timing
+ * Steps 2-3 task loop (engine.cpp:296-381) on a fold sample, `threads` pthreads; the C-port CPU
+ * baseline when the reference build is absent. */
+typedef struct {
+  const pcvo_model* m;
+  const int32_t* folds;
+  int32_t L;
+  int64_t warmup, iters;
+  uint64_t seed;
+  int32_t model_id;
+  const pcvg_kernel* k;
+  const double* bank;
+  int64_t bank_rows;
+  long ntask;
+  atomic_long next;
+  double* pos;  /* [ntask*dim] */
+  pcvo_rng* rng;
+  double* warm;
+  score_accum* acc;
+  int phase;
+} time_ctx;
+
+static void* time_worker(void* arg) {
+  time_ctx* tc = arg;
+  const int d = tc->m->dim;
+  double* mom = malloc(sizeof(double) * d);
+  double* wq = malloc(sizeof(double) * d);
+  double* wp = malloc(sizeof(double) * d);
+  for (;;) {
+    const long i = atomic_fetch_add(&tc->next, 1);
+    if (i >= tc->ntask) break;
+    const int fold = tc->folds[i / tc->L], chain = (int)(i % tc->L);
+    double* pos = tc->pos + i * d;
+    int32_t acc;
+    if (tc->phase == 2) {
+      pcvo_rng init;
+      pcvo_rng_init(&init, tc->seed, pcvo_stream_key(PCVG_STREAM_CHAIN_INIT, (uint64_t)tc->model_id, (uint64_t)fold, (uint64_t)chain));
+      const uint64_t row = pcvo_below(&init, (uint64_t)tc->bank_rows);
+      memcpy(pos, tc->bank + row * d, sizeof(double) * d);
+      pcvo_rng_init(&tc->rng[i], tc->seed, pcvo_stream_key(PCVG_STREAM_CHAIN_SAMPLING, (uint64_t)tc->model_id, (uint64_t)fold, (uint64_t)chain));
+      tc->warm[i] = 0.0;
+      for (int64_t s = 0; s < tc->warmup; ++s) {
+        hmc_step_rng(tc->m, fold, tc->k->step_size, tc->k->n_leapfrog, tc->k->inv_mass_diag, pos, &tc->rng[i], mom, wq, wp, &acc);
+        tc->warm[i] += pcvo_log_pred(tc->m, pos, fold);
+      }
+    } else {
+      const double c = tc->warmup > 0 ? tc->warm[i] / ((double)tc->L * tc->warmup) : 0.0;
+      accum_init(&tc->acc[i], tc->iters < 50 ? (int)tc->iters : 50, 5, tc->iters, c);
+      for (int64_t s = 0; s < tc->iters; ++s) {
+        hmc_step_rng(tc->m, fold, tc->k->step_size, tc->k->n_leapfrog, tc->k->inv_mass_diag, pos, &tc->rng[i], mom, wq, wp, &acc);
+        accum_observe(&tc->acc[i], pcvo_log_pred(tc->m, pos, fold), s);
+      }
+    }
+  }
+  free(mom); free(wq); free(wp);
+  return NULL;
+}
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+int pcvo_time_tasks(const pcvo_model* m, int32_t n_folds, const int32_t* folds, int32_t L,
+                    int64_t warmup, int64_t iters, uint64_t seed, int32_t model_id,
+                    const pcvg_kernel* k, const double* bank, int64_t bank_rows, int32_t threads,
+                    double* sampling_s, double* warmup_s, double* checksum) {
+  time_ctx tc;
+  memset(&tc, 0, sizeof tc);
+  tc.m = m; tc.folds = folds; tc.L = L; tc.warmup = warmup; tc.iters = iters; tc.seed = seed;
+  tc.model_id = model_id; tc.k = k; tc.bank = bank; tc.bank_rows = bank_rows;
+  tc.ntask = (long)n_folds * L;
+  tc.pos = malloc(sizeof(double) * tc.ntask * m->dim);
+  tc.rng = malloc(sizeof(pcvo_rng) * tc.ntask);
+  tc.warm = malloc(sizeof(double) * tc.ntask);
+  tc.acc = malloc(sizeof(score_accum) * tc.ntask);
+  if (threads <= 0) threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+  double t[3];
+  t[0] = now_s();
+  for (int phase = 2; phase <= 3; ++phase) {
+    tc.phase = phase;
+    atomic_store(&tc.next, 0);
+    pthread_t* th = malloc(sizeof(pthread_t) * threads);
+    for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, time_worker, &tc);
+    for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+    free(th);
+    t[phase - 1] = now_s();
+  }
+  *warmup_s = t[1] - t[0];
+  *sampling_s = t[2] - t[1];
+  double cs = 0.0;
+  for (long i = 0; i < tc.ntask; ++i) cs += tc.acc[i].u_x;
+  *checksum = cs;
+  free(tc.pos); free(tc.rng); free(tc.warm); free(tc.acc);
   return 0;
 }

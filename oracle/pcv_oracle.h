@@ -95,6 +95,12 @@ double pcvo_selection_probability(double delta_hat, const double* deltas, int64_
                                   double* sigma2);
 double pcvo_benchmark_quantile(const double* values, int64_t n, double q);
 
+/* Steps 2-3 task loop on a fold sample (bench CPU baseline, kind "port"). */
+int pcvo_time_tasks(const pcvo_model* m, int32_t n_folds, const int32_t* folds, int32_t L,
+                    int64_t warmup, int64_t iters, uint64_t seed, int32_t model_id,
+                    const pcvg_kernel* k, const double* bank, int64_t bank_rows, int32_t threads,
+                    double* sampling_s, double* warmup_s, double* checksum);
+
 const char* pcvo_last_error(void);
 
 #ifdef __cplusplus

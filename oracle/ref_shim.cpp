@@ -5,6 +5,8 @@
 // (hmc.cpp), adapt_full_data (adapt.cpp) and run_pcv (engine.cpp). It is the checker
 // the C restatement (oracle/pcv_oracle.c) is pinned against, and the `--impl reference`
 // CPU arm of bench.py. Never linked into the product.
+#include <chrono>
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -369,6 +371,65 @@ int pcvref_run_pcv(int32_t n_models, void** models, const int32_t* model_ids,
     rep->verdict_quantile_value = r.verdict.quantile_value;
     rep->verdict_observed = r.verdict.observed;
     rep->iters_run = r.iters;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Times the reference's own Step 2-3 task loop (engine.cpp:296-381: warm start, warmup_discard,
+// then hmc_step + log_pred + ScoreAccum::observe per iteration) on a bounded sample of folds with
+// the reference thread pool (parallel_for, engine.cpp:32-61). Used by bench.py's CPU arms.
+int pcvref_time_tasks(void* h, int32_t n_folds, const int32_t* folds, int32_t L, int64_t warmup,
+                      int64_t iters, uint64_t seed, int32_t model_id, const pcvg_kernel* kern,
+                      const double* bank, int64_t bank_rows, int32_t threads, double* sampling_s,
+                      double* warmup_s, double* checksum) {
+  return guarded([&] {
+    const pcv::Model& model = M(h);
+    const size_t d = model.dim();
+    pcv::KernelParams kp{kern->step_size, kern->n_leapfrog,
+                         std::vector<double>(kern->inv_mass_diag, kern->inv_mass_diag + d)};
+    struct Task {
+      pcv::ChainState st{{}, pcv::CounterRng(), 0};
+      pcv::WarmupStats warm;
+      pcv::ScoreAccum acc;
+      int fold = 0, chain = 0;
+    };
+    const long ntask = static_cast<long>(n_folds) * L;
+    std::vector<Task> tasks(ntask);
+    for (long i = 0; i < ntask; ++i) {
+      tasks[i].fold = folds[i / L];
+      tasks[i].chain = static_cast<int>(i % L);
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    pcv::parallel_for(ntask, threads, [&](long i) {
+      Task& t = tasks[i];
+      pcv::CounterRng init(seed, pcv::stream_key(pcv::StreamKind::ChainInit, model_id, t.fold, t.chain));
+      const uint64_t row = init.below(static_cast<uint64_t>(bank_rows));
+      t.st.position.assign(bank + row * d, bank + (row + 1) * d);
+      t.st.rng = pcv::CounterRng(seed, pcv::stream_key(pcv::StreamKind::ChainSampling, model_id, t.fold, t.chain));
+      pcv::HmcWorkspace ws;
+      t.warm = pcv::warmup_discard(t.st, model, t.fold, kp, warmup, pcv::ScoreKind::LogS, ws);
+    });
+    auto t1 = std::chrono::steady_clock::now();
+    const int b = static_cast<int>(std::min<int64_t>(50, iters));
+    pcv::parallel_for(ntask, threads, [&](long i) {
+      Task& t = tasks[i];
+      const double c = warmup > 0 ? t.warm.logpred_sum / (static_cast<double>(L) * warmup) : 0.0;
+      t.acc = pcv::ScoreAccum(b, 5, iters, c);
+      pcv::HmcWorkspace ws;
+      for (int64_t it = 0; it < iters; ++it) {
+        pcv::hmc_step(t.st, model, t.fold, kp, ws);
+        t.acc.observe(model.log_pred(t.st.position, t.fold), it);
+      }
+    });
+    auto t2 = std::chrono::steady_clock::now();
+    *warmup_s = std::chrono::duration<double>(t1 - t0).count();
+    *sampling_s = std::chrono::duration<double>(t2 - t1).count();
+    double cs = 0.0;
+    for (const auto& t : tasks) cs += t.acc.raw.u_x;
+    *checksum = cs;
   });
 }
 

@@ -57,6 +57,8 @@ def oracle():
         _sig(lib, "pcvo_rhat_from_sums", C.c_int, [pf64, pf64, i32, i64, pf64, pf64, pf64])
         _sig(lib, "pcvo_selection_probability", f64, [f64, pf64, i64, pf64])
         _sig(lib, "pcvo_benchmark_quantile", f64, [pf64, i64, f64])
+        _sig(lib, "pcvo_time_tasks", C.c_int, [vp, i32, pi32, i32, i64, i64, u64, i32, P(abi.Kernel), pf64,
+                                                i64, i32, pf64, pf64, pf64])
         _sig(lib, "pcvo_last_error", C.c_char_p, [])
         _oracle = lib
     return _oracle
@@ -94,6 +96,8 @@ def ref():
                                                  pi32, pi32, pf64])
         _sig(lib, "pcvref_adapt", C.c_int, [vp, i32, i64, i64, i32, f64, f64, u64, i32, pf64, pf64,
                                              pf64, pf64, pi64])
+        _sig(lib, "pcvref_time_tasks", C.c_int, [vp, i32, pi32, i32, i64, i64, u64, i32, P(abi.Kernel), pf64,
+                                                  i64, i32, pf64, pf64, pf64])
         _sig(lib, "pcvref_run_pcv", C.c_int, [i32, P(vp), pi32, P(abi.Kernel), P(pf64), pi64,
                                                P(abi.RunConfig), i32, P(abi.Report)])
         _ref = lib
