@@ -42,6 +42,38 @@ __global__ void dmma_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Warps 0..3 of each block run DMMA, warps 4..7 run DFMA: if the two share the FP64 datapath the
+// combined rate stays at the single-pipe peak.
+__global__ void mixed_kernel(double* out, int iters, int dfma_warps) {
+  const int w = threadIdx.x >> 5;
+  if (w < 8 - dfma_warps) {
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+    double c[8][2] = {};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[t][0]), "+d"(c[t][1]) : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+    if (s == 12345.678) out[0] = s;
+  } else {
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-9 + i;
+    for (int it = 0; it < iters * 8; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], 1.0000001, 1e-9);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 12345.678) out[0] = s;
+  }
+}
+
 __global__ void dexp_kernel(double* out, int iters) {
   double x[8];
 #pragma unroll
@@ -110,6 +142,21 @@ int main() {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     printf(", \"dexp_gops\": %.3f", 8.0 * iters * threads * (double)blocks / (ms * 1e-3) / 1e9);
+  }
+  for (int dw : {0, 2, 4, 8}) {
+    const int iters = 4000, threads = 256, blocks = sms * 2;
+    mixed_kernel<<<blocks, threads>>>(out, 10, dw);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    mixed_kernel<<<blocks, threads>>>(out, iters, dw);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    // DMMA warp: 8*iters DMMA x 256 FMA; DFMA warp: 64*iters DFMA x 32 FMA (equal FMA count)
+    const double fma_per_warp = 8.0 * iters * 256;
+    printf(", \"mixed_dfma_warps%d_ms\": %.3f, \"mixed_dfma_warps%d_tflops\": %.3f", dw, ms, dw,
+           2.0 * fma_per_warp * 8 * blocks / (ms * 1e-3) / 1e12);
   }
   printf("}\n");
   return 0;
