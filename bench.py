@@ -178,7 +178,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     d, f, kp, bank = load_inputs()
     K = args.folds or f.K
-    fb, fe = rank * K // world, (rank + 1) * K // world
+    from paper_2310_07002_b200.dist import shard_range
+    fb, fe = shard_range(K, rank, world)
     model = pcv.LogisticModel("M_A", d, f)
     cfg = pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup, batch_size=min(50, args.steps),
                         blocks=5, bench_draws=100, seed=1, fold_begin=fb, fold_end=fe)
@@ -209,9 +210,8 @@ def main():
     # per-fold statistics of this shard -> rank 0 -> Step-4 merge (untimed)
     cols, divs, dropped, done = ctx.fold_stats(fe - fb)
     if dist:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, cols)
-        cols = {k: np.concatenate([g[k] for g in gathered]) for k in cols}
+        from paper_2310_07002_b200 import dist as pdist
+        cols = pdist.gather_fold_tables(cols, 1)
     result = None
     if rank == 0:
         rep = pcv.merge(1, K, cfg, done, 0, cols)

@@ -164,9 +164,9 @@ const char* pcvg_status_name(int32_t status);
 /* ---------------------------------------------------------------- host: RNG + folds
  * Bit-exact restatements of the reference's deterministic host pieces. */
 uint64_t pcvg_stream_key(uint64_t kind, uint64_t a, uint64_t b, uint64_t c); /* rng.hpp:35-43 */
-/* Draws from CounterRng(seed, stream) (rng.hpp:45-143). ops[i] in {'u','n','4' (next_u32),
+/* Draws from CounterRng(seed, stream), after skip_to(skip_block) when do_skip (rng.hpp:45-143). ops[i] in {'u','n','4' (next_u32),
  * 'b' (below(arg[i]))}; out[i] gets the draw as a double (u32/below as exact integers). */
-pcvg_status pcvg_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block,
+pcvg_status pcvg_rng_sequence(uint64_t seed, uint64_t stream, int32_t do_skip, uint64_t skip_block,
                               const char* ops, const uint64_t* arg, int64_t n, double* out);
 pcvg_status pcvg_make_loo(int64_t n_obs, int32_t* test_index, int32_t* K);          /* folds.cpp:43-52 */
 pcvg_status pcvg_make_logo(const pcvg_dataset* d, int32_t* test_index, int32_t* K); /* folds.cpp:54-63 */
@@ -232,6 +232,13 @@ pcvg_status pcvg_hmc_probe(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t
 pcvg_status pcvg_hmc_chain(pcvg_ctx* ctx, int32_t slot, int32_t fold, int32_t chain,
                            uint64_t seed, const double* theta0, int64_t n_steps,
                            double* trajectory, int32_t* divergent);
+
+/* Online accumulators + fold reduction on explicit score streams: chain c feeds
+ * s[c*n .. c*n+n) through ScoreAccum::observe (accum.cpp:164-182) with centre `center`, then the
+ * fold is reduced by logs_fold_score + rhat_from_blocks (scoring.cpp:10-62, diagnostics.cpp:35-44).
+ * out[8] = estimate, log_f_hat, mc_contribution, naive_contribution, ess, rhat, batches, fault. */
+pcvg_status pcvg_score_streams(pcvg_ctx* ctx, int32_t L, int64_t n, const double* s, double center,
+                               int32_t b, int32_t D, double* out);
 
 /* ---------------------------------------------------------------- run (Steps 2-4) */
 int32_t pcvg_checkpoint_count(const pcvg_run_config* cfg);

@@ -154,11 +154,11 @@ uint64_t pcvo_below(pcvo_rng* r, uint64_t n) { /* rng.hpp:99-105 */
     if (v < bound) return v % n;
   }
 }
-int pcvo_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
-                      const uint64_t* arg, int64_t n, double* out) {
+int pcvo_rng_sequence(uint64_t seed, uint64_t stream, int32_t do_skip, uint64_t skip_block,
+                      const char* ops, const uint64_t* arg, int64_t n, double* out) {
   pcvo_rng r;
   pcvo_rng_init(&r, seed, stream);
-  if (skip_block >= 0) pcvo_skip_to(&r, (uint64_t)skip_block);
+  if (do_skip) pcvo_skip_to(&r, skip_block);
   for (int64_t i = 0; i < n; ++i) {
     switch (ops[i]) {
       case 'u': out[i] = pcvo_uniform(&r); break;
@@ -1471,5 +1471,29 @@ int pcvo_time_tasks(const pcvo_model* m, int32_t n_folds, const int32_t* folds, 
   for (long i = 0; i < tc.ntask; ++i) cs += tc.acc[i].u_x;
   *checksum = cs;
   free(tc.pos); free(tc.rng); free(tc.warm); free(tc.acc);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ accumulator probe
+ * Feeds L chains' score streams (stream c = s[c*n .. c*n+n)) through ScoreAccum::observe
+ * (accum.cpp:164-182) and reduces them with logs_fold_score + rhat_from_blocks
+ * (scoring.cpp:10-62, diagnostics.cpp:35-44). out: estimate, log_f_hat, mc, naive, ess, rhat,
+ * batches, fault. */
+int pcvo_score_streams(int32_t L, int64_t n, const double* s, double center, int32_t b, int32_t D,
+                       double* out) {
+  if (L < 1 || L > 256 || n < 1 || D < 1 || D > 16 || b < 1) return set_err(PCVG_INVALID_INPUT, "bad stream probe");
+  score_accum* a = malloc(sizeof(score_accum) * L);
+  const score_accum* ch[256];
+  for (int c = 0; c < L; ++c) {
+    accum_init(&a[c], b, D, n, center);
+    for (int64_t i = 0; i < n; ++i) accum_observe(&a[c], s[c * n + i], i);
+    ch[c] = &a[c];
+  }
+  const fold_score fs = logs_fold_score(ch, L, n);
+  double rh;
+  const int ok = rhat_from_blocks(ch, L, n, &rh);
+  out[0] = fs.estimate; out[1] = fs.log_f_hat; out[2] = fs.mc; out[3] = fs.naive; out[4] = fs.ess;
+  out[5] = ok ? rh : NAN; out[6] = (double)fs.batches; out[7] = fs.fault;
+  free(a);
   return 0;
 }

@@ -39,8 +39,8 @@ double pcvo_normal(pcvo_rng* r);
 uint64_t pcvo_below(pcvo_rng* r, uint64_t n);
 void pcvo_skip_to(pcvo_rng* r, uint64_t block);
 uint64_t pcvo_stream_key(uint64_t kind, uint64_t a, uint64_t b, uint64_t c);
-int pcvo_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
-                      const uint64_t* arg, int64_t n, double* out);
+int pcvo_rng_sequence(uint64_t seed, uint64_t stream, int32_t do_skip, uint64_t skip_block,
+                      const char* ops, const uint64_t* arg, int64_t n, double* out);
 
 /* Fold schemes, folds.cpp:43-108, plus hv-block (new). Return 0 on success. */
 int pcvo_make_kfold(int64_t n, int32_t K, uint64_t seed, int32_t* out);
@@ -100,6 +100,10 @@ int pcvo_time_tasks(const pcvo_model* m, int32_t n_folds, const int32_t* folds, 
                     int64_t warmup, int64_t iters, uint64_t seed, int32_t model_id,
                     const pcvg_kernel* k, const double* bank, int64_t bank_rows, int32_t threads,
                     double* sampling_s, double* warmup_s, double* checksum);
+
+/* Online accumulators + fold reduction on explicit score streams (accum/scoring/diagnostics). */
+int pcvo_score_streams(int32_t L, int64_t n, const double* s, double center, int32_t b, int32_t D,
+                       double* out);
 
 const char* pcvo_last_error(void);
 

@@ -80,11 +80,11 @@ uint64_t pcvref_stream_key(uint64_t kind, uint64_t a, uint64_t b, uint64_t c) {
   return pcv::stream_key(static_cast<pcv::StreamKind>(kind), a, b, c);
 }
 
-int pcvref_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
-                        const uint64_t* arg, int64_t n, double* out) {
+int pcvref_rng_sequence(uint64_t seed, uint64_t stream, int32_t do_skip, uint64_t skip_block,
+                        const char* ops, const uint64_t* arg, int64_t n, double* out) {
   return guarded([&] {
     pcv::CounterRng rng(seed, stream);
-    if (skip_block >= 0) rng.skip_to(static_cast<uint64_t>(skip_block));
+    if (do_skip) rng.skip_to(skip_block);
     for (int64_t i = 0; i < n; ++i) {
       switch (ops[i]) {
         case 'u': out[i] = rng.uniform(); break;

@@ -34,8 +34,10 @@ cudaError_t launch_fold_stats(const ChainsDev& S, int nfold, int64_t n, int b, i
                               double* estimate, double* log_f_hat, double* mc, double* naive,
                               double* ess, double* rhat, int64_t* batches, int32_t* fault,
                               cudaStream_t st);
+cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, int D, int b,
+                                cudaStream_t st);
 // host_folds.cpp
-void rng_sequence(uint64_t, uint64_t, int64_t, const char*, const uint64_t*, int64_t, double*);
+void rng_sequence(uint64_t, uint64_t, int32_t, uint64_t, const char*, const uint64_t*, int64_t, double*);
 void make_loo(int64_t, int32_t*, int32_t*);
 void make_logo(const pcvg_dataset*, int32_t*, int32_t*);
 void make_kfold(int64_t, int32_t, uint64_t, int32_t*);
@@ -561,9 +563,9 @@ const char* pcvg_status_name(int32_t s) {
   return "unknown";
 }
 
-pcvg_status pcvg_rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
-                              const uint64_t* arg, int64_t n, double* out) {
-  return static_cast<pcvg_status>(guarded(nullptr, [&] { rng_sequence(seed, stream, skip_block, ops, arg, n, out); }));
+pcvg_status pcvg_rng_sequence(uint64_t seed, uint64_t stream, int32_t do_skip, uint64_t skip_block,
+                              const char* ops, const uint64_t* arg, int64_t n, double* out) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { rng_sequence(seed, stream, do_skip, skip_block, ops, arg, n, out); }));
 }
 pcvg_status pcvg_make_loo(int64_t n, int32_t* ti, int32_t* K) {
   return static_cast<pcvg_status>(guarded(nullptr, [&] { make_loo(n, ti, K); }));
@@ -805,6 +807,39 @@ pcvg_status pcvg_hmc_chain(pcvg_ctx* ctx, int32_t slot, int32_t fold, int32_t ch
   }));
 }
 
+pcvg_status pcvg_score_streams(pcvg_ctx* ctx, int32_t L, int64_t n, const double* s, double center,
+                               int32_t b, int32_t D, double* out) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || L < 1 || L > 64 || n < 1 || D < 1 || b < 1 || !s || !out)
+      throw Error(PCVG_INVALID_INPUT, "bad stream probe");
+    require_device(ctx);
+    ChainSet cs;
+    cs.alloc(L, 1, D);
+    DevBuf<double> centers, streams;
+    centers.upload(std::vector<double>{center});
+    streams.upload(std::vector<double>(s, s + static_cast<size_t>(L) * n));
+    ChainsDev S = cs.view(L, 0, 0, 0);
+    ck(cudaMemset(cs.warm.p, 0, sizeof(double) * L), "memset");
+    ck(launch_centers(S, 0, 0, centers.p, D, ctx->stream), "reset");  // nfold 0: no centre recompute
+    ck(launch_feed_streams(S, streams.p, n, D, b, ctx->stream), "feed");
+    DevBuf<double> o;
+    o.alloc(6);
+    DevBuf<int64_t> bt;
+    bt.alloc(1);
+    DevBuf<int32_t> ft;
+    ft.alloc(1);
+    ck(launch_fold_stats(S, 1, n, b, D, o.p, o.p + 1, o.p + 2, o.p + 3, o.p + 4, o.p + 5, bt.p, ft.p,
+                         ctx->stream), "fold_stats");
+    ctx->launches += 3;
+    const auto v = o.download(ctx->stream);
+    const auto bb = bt.download(ctx->stream);
+    const auto ff = ft.download(ctx->stream);
+    for (int i = 0; i < 6; ++i) out[i] = v[i];
+    out[6] = static_cast<double>(bb[0]);
+    out[7] = ff[0];
+  }));
+}
+
 int32_t pcvg_checkpoint_count(const pcvg_run_config* cfg) {  // engine.cpp:279-283
   if (!cfg || cfg->iters < 1) return 0;
   int32_t n = 0;
@@ -942,7 +977,7 @@ pcvg_status pcvg_fold_stats(pcvg_ctx* ctx, pcvg_fold_table* out, int64_t* diverg
         for (int mi = 0; mi < nm && !failed; ++mi) {
           bool all_bad = true;
           for (int c = 0; c < L; ++c)
-            if (sdiv[mi][k * L + c] * 2 <= cfg.iters) { all_bad = false; break; }
+            if (sdiv[mi][k * L + c] * 2 <= ctx->iters_done) { all_bad = false; break; }
           failed = all_bad;
         }
         for (int mi = 0; mi < nm; ++mi) out->failed[static_cast<size_t>(mi) * nfold + k] = failed ? 1 : 0;

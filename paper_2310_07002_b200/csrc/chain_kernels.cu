@@ -161,7 +161,20 @@ __global__ void fold_stats_kernel(ChainsDev S, int nfold, int64_t n, int b, int 
   out.fault[k] = fault ? 1 : 0;
 }
 
+// Probe: chain c feeds its explicit score stream through accum_observe (accum.cpp:164-182).
+__global__ void feed_streams_kernel(ChainsDev S, const double* s, int64_t n, int D, int b) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= S.nch) return;
+  for (int64_t i = 0; i < n; ++i) accum_observe(S.acc, c, S.nch, s[c * n + i], i, n, D, b);
+}
+
 }  // namespace
+
+cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, int D, int b,
+                                cudaStream_t st) {
+  feed_streams_kernel<<<(S.nch + 127) / 128, 128, 0, st>>>(S, s, n, D, b);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const double* bank,
                                int64_t bank_rows, cudaStream_t st) {
@@ -172,9 +185,8 @@ cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const doub
 
 cudaError_t launch_centers(const ChainsDev& S, int nfold, int64_t warmup, double* centers,
                            int D, cudaStream_t st) {
-  if (nfold == 0) return cudaSuccess;
-  centers_kernel<<<(nfold + 127) / 128, 128, 0, st>>>(S, nfold, warmup, centers);
-  reset_accum_kernel<<<(S.nch + 255) / 256, 256, 0, st>>>(S, D, centers);
+  if (nfold > 0) centers_kernel<<<(nfold + 127) / 128, 128, 0, st>>>(S, nfold, warmup, centers);
+  if (S.nch > 0) reset_accum_kernel<<<(S.nch + 255) / 256, 256, 0, st>>>(S, D, centers);
   return cudaGetLastError();
 }
 

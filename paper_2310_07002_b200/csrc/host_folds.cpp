@@ -51,10 +51,10 @@ uint64_t pcvg_stream_key(uint64_t kind, uint64_t a, uint64_t b, uint64_t c) {
 // Exported through api.cpp's error-mapping wrapper.
 namespace pcvg {
 
-void rng_sequence(uint64_t seed, uint64_t stream, int64_t skip_block, const char* ops,
-                  const uint64_t* arg, int64_t n, double* out) {
+void rng_sequence(uint64_t seed, uint64_t stream, int32_t do_skip, uint64_t skip_block,
+                  const char* ops, const uint64_t* arg, int64_t n, double* out) {
   HostRng r(seed, stream);
-  if (skip_block >= 0) r.skip_to(static_cast<uint64_t>(skip_block));
+  if (do_skip) r.skip_to(skip_block);
   for (int64_t i = 0; i < n; ++i) {
     switch (ops[i]) {
       case 'u': out[i] = r.uniform(); break;

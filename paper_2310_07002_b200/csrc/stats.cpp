@@ -118,7 +118,7 @@ void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter
   if (final_checkpoint == 0) return;
   // shuffle benchmark (diagnostics.cpp:76-101) over non-failed folds, model-major
   rep->benchmark_count = 0;
-  const int64_t nbench = final ? cfg->iters : iter_count;
+  const int64_t nbench = iter_count;  // = N for a full run (gather_block_sums(chains, n), engine.cpp:471)
   if (y_x && y_x2 && rep->benchmark) {
     std::vector<double> sx(l), sxx(l);
     for (int r = 0; r < cfg->bench_draws; ++r) {

@@ -76,7 +76,7 @@ def load():
     _sig(lib, "pcvg_last_error", C.c_char_p, [vp])
     _sig(lib, "pcvg_status_name", C.c_char_p, [i32])
     _sig(lib, "pcvg_stream_key", u64, [u64, u64, u64, u64])
-    _sig(lib, "pcvg_rng_sequence", i32, [u64, u64, i64, C.c_char_p, abi.P_u64, i64, pf])
+    _sig(lib, "pcvg_rng_sequence", i32, [u64, u64, i32, u64, C.c_char_p, abi.P_u64, i64, pf])
     _sig(lib, "pcvg_make_loo", i32, [i64, pi32, pi32])
     _sig(lib, "pcvg_make_logo", i32, [P(abi.Dataset), pi32, pi32])
     _sig(lib, "pcvg_make_kfold", i32, [i64, i32, u64, pi32])
@@ -98,6 +98,7 @@ def load():
     _sig(lib, "pcvg_eval_pred", i32, [vp, i32, i64, pi32, pf, pf])
     _sig(lib, "pcvg_hmc_probe", i32, [vp, i32, i64, pi32, pf, pf, pf, pf, pf, pf, pi32, pi32])
     _sig(lib, "pcvg_hmc_chain", i32, [vp, i32, i32, i32, u64, pf, i64, pf, pi32])
+    _sig(lib, "pcvg_score_streams", i32, [vp, i32, i64, pf, f64, i32, i32, pf])
     _sig(lib, "pcvg_checkpoint_count", i32, [P(abi.RunConfig)])
     _sig(lib, "pcvg_run", i32, [vp, P(abi.RunConfig), P(abi.Report)])
     _sig(lib, "pcvg_begin", i32, [vp, P(abi.RunConfig)])
@@ -182,12 +183,13 @@ def stream_key(kind, a=0, b=0, c=0):
     return load().pcvg_stream_key(kind, a, b, c)
 
 
-def rng_sequence(seed, stream, ops, args=None, skip_block=-1):
+def rng_sequence(seed, stream, ops, args=None, skip_block=None):
     ops_b = ops.encode() if isinstance(ops, str) else ops
     n = len(ops_b)
     arg = np.zeros(n, dtype=np.uint64) if args is None else np.ascontiguousarray(args, dtype=np.uint64)
     out = np.zeros(n)
-    _check(load().pcvg_rng_sequence(seed, stream, skip_block, ops_b, _p(arg, C.c_uint64), n, _p(out)))
+    _check(load().pcvg_rng_sequence(seed, stream, int(skip_block is not None), skip_block or 0, ops_b,
+                                    _p(arg, C.c_uint64), n, _p(out)))
     return out
 
 
@@ -398,6 +400,15 @@ class Context:
         self._chk(self.lib.pcvg_hmc_chain(self.h, slot, fold, chain, seed, _p(th), n_steps, _p(traj),
                                           _p(div, C.c_int32)))
         return traj, div
+
+    def score_streams(self, streams, center=0.0, batch=10, blocks=5):
+        """Feeds explicit per-chain log-score streams through the device accumulators and the fold
+        reduction; returns dict(estimate, log_f_hat, mc, naive, ess, rhat, batches, fault)."""
+        s = np.ascontiguousarray(np.atleast_2d(streams), dtype=np.float64)
+        out = np.zeros(8)
+        self._chk(self.lib.pcvg_score_streams(self.h, s.shape[0], s.shape[1], _p(s), center, batch,
+                                              blocks, _p(out)))
+        return dict(zip(["estimate", "log_f_hat", "mc", "naive", "ess", "rhat", "batches", "fault"], out))
 
     def run(self, cfg):
         K, L = self.models[0].K, cfg.chains

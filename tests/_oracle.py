@@ -36,7 +36,7 @@ def oracle():
         lib = C.CDLL(ORACLE_SO)
         P = C.POINTER
         _sig(lib, "pcvo_stream_key", u64, [u64, u64, u64, u64])
-        _sig(lib, "pcvo_rng_sequence", C.c_int, [u64, u64, i64, C.c_char_p, pu64, i64, pf64])
+        _sig(lib, "pcvo_rng_sequence", C.c_int, [u64, u64, i32, u64, C.c_char_p, pu64, i64, pf64])
         _sig(lib, "pcvo_make_kfold", C.c_int, [i64, i32, u64, pi32])
         _sig(lib, "pcvo_make_time_blocks", C.c_int, [P(abi.Dataset), i32, pi32])
         _sig(lib, "pcvo_make_hv_block", C.c_int, [P(abi.Dataset), i32, i64, pi64])
@@ -59,6 +59,7 @@ def oracle():
         _sig(lib, "pcvo_benchmark_quantile", f64, [pf64, i64, f64])
         _sig(lib, "pcvo_time_tasks", C.c_int, [vp, i32, pi32, i32, i64, i64, u64, i32, P(abi.Kernel), pf64,
                                                 i64, i32, pf64, pf64, pf64])
+        _sig(lib, "pcvo_score_streams", C.c_int, [i32, i64, pf64, f64, i32, i32, pf64])
         _sig(lib, "pcvo_last_error", C.c_char_p, [])
         _oracle = lib
     return _oracle
@@ -75,7 +76,7 @@ def ref():
         P = C.POINTER
         _sig(lib, "pcvref_last_error", C.c_char_p, [])
         _sig(lib, "pcvref_stream_key", u64, [u64, u64, u64, u64])
-        _sig(lib, "pcvref_rng_sequence", C.c_int, [u64, u64, i64, C.c_char_p, pu64, i64, pf64])
+        _sig(lib, "pcvref_rng_sequence", C.c_int, [u64, u64, i32, u64, C.c_char_p, pu64, i64, pf64])
         _sig(lib, "pcvref_make_kfold", C.c_int, [i64, i32, u64, pi32])
         _sig(lib, "pcvref_make_time_blocks", C.c_int, [P(abi.Dataset), i32, pi32])
         _sig(lib, "pcvref_make_logo", C.c_int, [P(abi.Dataset), pi32, pi32])
