@@ -76,6 +76,49 @@ def _cfg2_bench():
     return d, f, [dict(family=abi.FAMILY_LOGISTIC)]
 
 
+def _cfg3_bench():
+    d = pcv.simulate_radon_style(12000, 400, 5)
+    f = pcv.make_logo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_RADON, include_floor=1),
+                  dict(family=abi.FAMILY_RADON, include_floor=0)]
+
+
+def _cfg4_bench():
+    d = pcv.simulate_seasonal_ar(5000, 2, 11, 0.6, seed=7)
+    f = pcv.make_hv_block_scheme(d, 100, 12)
+    return d, f, [dict(family=abi.FAMILY_SEASONAL_AR, ar_order=2, dummies=11),
+                  dict(family=abi.FAMILY_SEASONAL_AR, ar_order=2, dummies=0)]
+
+
+def _cfg5_bench():
+    d = pcv.simulate_linreg(100000, 5, seed=11)
+    f = pcv.make_loo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_GROUPED)]
+
+
+# Bench fixtures store the simulator call instead of the data (regenerated bit-exactly).
+SIM = {
+    "cfg2_logistic_bench": ("logistic", [10000, 50, 1]),
+    "cfg3_radon_bench": ("radon", [12000, 400, 5]),
+    "cfg4_seasonal_bench": ("seasonal", [5000, 2, 11, 7]),
+    "cfg5_linreg_bench": ("linreg", [100000, 5, 11]),
+}
+
+
+def _regenerate(kind, a):
+    if kind == "logistic":
+        d = pcv.simulate_logistic(a[0], a[1], seed=a[2])
+        return d, pcv.make_loo_scheme(d)
+    if kind == "radon":
+        d = pcv.simulate_radon_style(a[0], a[1], a[2])
+        return d, pcv.make_logo_scheme(d)
+    if kind == "seasonal":
+        d = pcv.simulate_seasonal_ar(a[0], a[1], a[2], 0.6, seed=a[3])
+        return d, pcv.make_hv_block_scheme(d, 100, 12)
+    d = pcv.simulate_linreg(a[0], a[1], seed=a[2])
+    return d, pcv.make_loo_scheme(d)
+
+
 CONFIGS = {
     # name: (builder, adapt kwargs, run kwargs or None)
     "cfg1_linreg_loo": (_cfg1, dict(chains=4, warmup=1000, draws=500), dict(chains=4, iters=200, warmup=50, batch_size=20, bench_draws=50, checkpoint_every=100)),
@@ -87,23 +130,28 @@ CONFIGS = {
     "logistic_kfold": (_logistic_kfold, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
     # bench input only (no reference run: 80k chains is the GPU workload)
     "cfg2_logistic_bench": (_cfg2_bench, dict(chains=4, warmup=300, draws=250), None),
+    "cfg3_radon_bench": (_cfg3_bench, dict(chains=4, warmup=400, draws=25), None),
+    "cfg4_seasonal_bench": (_cfg4_bench, dict(chains=4, warmup=400, draws=25), None),
+    "cfg5_linreg_bench": (_cfg5_bench, dict(chains=4, warmup=300, draws=25), None),
 }
 
 
 def make(name):
     builder, akw, rkw = CONFIGS[name]
     d, f, specs = builder()
-    out = {"y": d.y, "x": d.x, "K": np.int64(f.K)}
-    if name == "cfg2_logistic_bench":  # regenerated bit-exactly by pcv.simulate_logistic
-        out = {"K": np.int64(f.K), "sim_logistic": np.array([d.n_obs, d.x.shape[1], 1], dtype=np.int64)}
-    if d.group_id is not None:
-        out["group_id"] = d.group_id
-    if d.time_index is not None:
-        out["time_index"] = d.time_index
-    if f.test_index is not None and "sim_logistic" not in out:
-        out["test_index"] = f.test_index
-    if f.intervals is not None:
-        out["intervals"] = f.intervals
+    if name in SIM:
+        kind, args = SIM[name]
+        out = {"K": np.int64(f.K), "sim_kind": np.array(kind), "sim_args": np.array(args, dtype=np.int64)}
+    else:
+        out = {"y": d.y, "x": d.x, "K": np.int64(f.K)}
+        if d.group_id is not None:
+            out["group_id"] = d.group_id
+        if d.time_index is not None:
+            out["time_index"] = d.time_index
+        if f.test_index is not None:
+            out["test_index"] = f.test_index
+        if f.intervals is not None:
+            out["intervals"] = f.intervals
     fa = f.arrays()
     rmodels, kernels, banks = [], [], []
     for m, s in enumerate(specs):
@@ -146,6 +194,8 @@ def load(name):
         n, p, seed = (int(v) for v in z["sim_logistic"])
         d = pcv.simulate_logistic(n, p, seed=seed)
         f = pcv.make_loo_scheme(d)
+    elif "sim_kind" in z:
+        d, f = _regenerate(str(z["sim_kind"]), [int(v) for v in z["sim_args"]])
     else:
         d = pcv.Dataset(z["y"], z["x"], z["group_id"] if "group_id" in z else None,
                         z["time_index"] if "time_index" in z else None)
