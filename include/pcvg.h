@@ -211,6 +211,13 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
                            const double* bank, int64_t bank_rows, int32_t model_id,
                            int32_t* slot);
 pcvg_status pcvg_model_dim(const pcvg_ctx* ctx, int32_t slot, int32_t* dim);
+
+/* Kernel selection. AUTO picks the FP64 tensor-core GLM kernel for predictors without group
+ * effects when enough chains (or a row-split cluster) fill the GPU, else the generic lane-split
+ * kernel; GENERIC / TENSOR force one (tests run both). Logistic always uses the tensor kernel,
+ * hierarchical families (J > 1) always the generic one. */
+enum { PCVG_KERNEL_AUTO = 0, PCVG_KERNEL_GENERIC = 1, PCVG_KERNEL_TENSOR = 2 };
+pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy);
 pcvg_status pcvg_model_test_size(const pcvg_ctx* ctx, int32_t slot, int32_t fold, int64_t* n);
 
 /* Parity probes (device). n evaluation points: fold[n], theta[n*dim]. */

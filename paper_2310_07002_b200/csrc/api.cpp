@@ -22,10 +22,12 @@
 
 namespace pcvg {
 
-// kernels (gauss_kernel.cu, logistic_kernel.cu, chain_kernels.cu)
+// kernels (gauss_kernel.cu, glm_kernel.cu, chain_kernels.cu)
 int gauss_lanes_per_chain(const ModelDev& M, int nch);
 cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st);
-cudaError_t launch_logistic(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+int glm_width(int family, int J, int nc);
+int glm_cluster_size(int n, int kp, int nch);
+cudaError_t launch_glm(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
 cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const double* bank,
                                int64_t bank_rows, cudaStream_t st);
 cudaError_t launch_centers(const ChainsDev& S, int nfold, int64_t warmup, double* centers, int D,
@@ -178,7 +180,8 @@ using namespace pcvg;
 struct pcvg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t stream2 = nullptr;  // second candidate model runs concurrently (engine.cpp:342)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evj = nullptr;
   std::vector<std::unique_ptr<HostModel>> models;
   std::string err;
   // run state
@@ -191,6 +194,7 @@ struct pcvg_ctx {
   int64_t iters_done = 0;
   double last_ms = 0.0, warm_ms = 0.0, sample_ms = 0.0;
   int64_t launches = 0;
+  int policy = PCVG_KERNEL_AUTO;
 };
 
 namespace {
@@ -330,8 +334,9 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   std::vector<int> inv(n);
   for (int64_t r = 0; r < n; ++r) inv[m.perm[r]] = static_cast<int>(r);
 
-  const bool logistic = s->family == PCVG_FAMILY_LOGISTIC;
-  const int64_t n_pad = logistic ? ((n + 63) / 64) * 64 : n;
+  // Tensor-core (GLM) path: no group effects beyond one intercept (glm_kernel.cu).
+  const int glm_kp = glm_width(s->family, m.J, m.nc);
+  const int64_t n_pad = glm_kp > 0 ? ((n + 255) / 256) * 256 : n;
   std::vector<double> y(n_pad, 0.0);
   std::vector<int> key(n_pad, -1);
   std::vector<double> xc(static_cast<size_t>(std::max(m.nc, 1)) * n, 0.0);
@@ -345,8 +350,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   m.key.upload(key);
   m.x.upload(xc);
   int nc_pad = 0;
-  if (logistic) {
-    nc_pad = 52;
+  if (glm_kp > 0) {
+    nc_pad = glm_kp;
     std::vector<double> xr(static_cast<size_t>(n_pad) * nc_pad, 0.0);
     for (int64_t r = 0; r < n; ++r) {
       xr[r * nc_pad] = 1.0;
@@ -482,13 +487,26 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   return hm;
 }
 
-void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const RunArgs& A) {
+// Tensor-core GLM kernel or the generic lane-split kernel: the GLM path needs a
+// predictor without group effects; for few chains it only pays once a cluster split fills the GPU.
+bool use_glm(const pcvg_ctx* ctx, const HostModel& m, int nch) {
+  if (m.md.nc_pad == 0) return false;
+  if (m.family == PCVG_FAMILY_LOGISTIC) return true;  // no generic kernel for the logit link
+  if (ctx->policy == PCVG_KERNEL_GENERIC) return false;
+  if (ctx->policy == PCVG_KERNEL_TENSOR) return true;
+  const int tiles = (nch + 63) / 64;
+  return tiles * glm_cluster_size(m.md.n, m.md.nc_pad, nch) >= 24;
+}
+
+void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const RunArgs& A,
+                   cudaStream_t st = nullptr) {
+  if (!st) st = ctx->stream;
   cudaError_t e;
-  if (m.family == PCVG_FAMILY_LOGISTIC) {
-    e = launch_logistic(m.md, S, A, ctx->stream);
+  if (use_glm(ctx, m, S.nch)) {
+    e = launch_glm(m.md, S, A, st);
   } else {
     const int T = gauss_lanes_per_chain(m.md, S.nch);
-    e = launch_gauss(m.md, S, A, T, ctx->stream);
+    e = launch_gauss(m.md, S, A, T, st);
   }
   ++ctx->launches;
   ck(e, "kernel launch");
@@ -614,6 +632,8 @@ pcvg_status pcvg_create(int32_t device, pcvg_ctx** out) {
     ctx->device = device;
     ck(cudaSetDevice(device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&ctx->evj, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreate(&ctx->ev0), "cudaEventCreate");
     ck(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
     *out = ctx.release();
@@ -628,6 +648,8 @@ pcvg_status pcvg_destroy(pcvg_ctx* ctx) {
   ctx->models.clear();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evj) cudaEventDestroy(ctx->evj);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PCVG_OK;
@@ -644,6 +666,12 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
     ctx->begun = false;
     if (slot) *slot = static_cast<int32_t>(ctx->models.size() - 1);
   }));
+}
+
+pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy) {
+  if (!ctx || policy < PCVG_KERNEL_AUTO || policy > PCVG_KERNEL_TENSOR) return PCVG_INVALID_INPUT;
+  ctx->policy = policy;
+  return PCVG_OK;
 }
 
 pcvg_status pcvg_model_dim(const pcvg_ctx* ctx, int32_t slot, int32_t* dim) {
@@ -867,26 +895,30 @@ pcvg_status pcvg_begin(pcvg_ctx* ctx, const pcvg_run_config* cfg) {
     ctx->iters_done = 0;
     ctx->sample_ms = 0.0;
     ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
-    for (const auto& mp : ctx->models) {
-      const HostModel& m = *mp;
+    ck(cudaStreamWaitEvent(ctx->stream2, ctx->ev0, 0), "wait");
+    for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+      const HostModel& m = *ctx->models[mi];
+      cudaStream_t st = mi == 0 ? ctx->stream : ctx->stream2;
       auto cs = std::make_unique<ChainSet>();
       cs->alloc(nfold * L, m.dim, D);
       const uint64_t sm = cfg->shared_streams ? 0u : static_cast<uint64_t>(m.model_id);
       const ChainsDev S = cs->view(L, ctx->fb, cfg->seed, sm);
-      ck(launch_init_chains(m.md, S, m.bank.p, m.bank_rows, ctx->stream), "init_chains");
+      ck(launch_init_chains(m.md, S, m.bank.p, m.bank_rows, st), "init_chains");
       ++ctx->launches;
-      launch_family(ctx, m, S, make_args(kModeEval, 0));
+      launch_family(ctx, m, S, make_args(kModeEval, 0), st);
       if (cfg->warmup > 0) {
         RunArgs a = make_args(kModeWarmup, cfg->warmup);
-        launch_family(ctx, m, S, a);
+        launch_family(ctx, m, S, a, st);
       }
       auto centers = std::make_unique<DevBuf<double>>();
       centers->alloc(std::max(nfold, 1));
-      ck(launch_centers(S, nfold, cfg->warmup, centers->p, D, ctx->stream), "centers");
+      ck(launch_centers(S, nfold, cfg->warmup, centers->p, D, st), "centers");
       ctx->launches += 2;
       ctx->chains.push_back(std::move(cs));
       ctx->centers.push_back(std::move(centers));
     }
+    ck(cudaEventRecord(ctx->evj, ctx->stream2), "event");
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->evj, 0), "wait");
     ck(cudaEventRecord(ctx->ev1, ctx->stream), "event");
     ck(cudaEventSynchronize(ctx->ev1), "warmup");
     float ms = 0.f;
@@ -905,6 +937,7 @@ pcvg_status pcvg_advance(pcvg_ctx* ctx, int64_t n_iters) {
     require_device(ctx);
     const pcvg_run_config& cfg = ctx->cfg;
     ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
+    ck(cudaStreamWaitEvent(ctx->stream2, ctx->ev0, 0), "wait");
     for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
       const HostModel& m = *ctx->models[mi];
       const uint64_t sm = cfg.shared_streams ? 0u : static_cast<uint64_t>(m.model_id);
@@ -914,8 +947,10 @@ pcvg_status pcvg_advance(pcvg_ctx* ctx, int64_t n_iters) {
       a.planned_n = cfg.iters;
       a.D = ctx->chains[mi]->D;
       a.b = ctx->b;
-      if (n_iters > 0) launch_family(ctx, m, S, a);
+      if (n_iters > 0) launch_family(ctx, m, S, a, mi == 0 ? ctx->stream : ctx->stream2);
     }
+    ck(cudaEventRecord(ctx->evj, ctx->stream2), "event");
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->evj, 0), "wait");
     ck(cudaEventRecord(ctx->ev1, ctx->stream), "event");
     ck(cudaEventSynchronize(ctx->ev1), "advance");
     float ms = 0.f;

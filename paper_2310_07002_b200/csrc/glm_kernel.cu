@@ -1,0 +1,724 @@
+// Fused HMC kernel on FP64 tensor cores for every family whose per-observation predictor is a
+// GEMM across chains (sm_100a):
+//   logistic  (new family, BASELINE configs[1])          eta = X . theta,       r = y - sigmoid(eta)
+//   grouped regression with one group (cfg1, cfg5)       eta = alpha + X . beta, r = y - eta
+//       (grouped_regression.cpp:56-122 with J = 1)
+//   seasonal AR (cfg4; seasonal_ar.cpp:37-105)           eta = b0 + sum rho(u) lag + sum b d
+// For the 64 chains of a CTA and every gradient pass over N observations:
+//   eta = X_tile . W  ->  R = mask(y - mean(eta))  ->  G += X_tile^T . R
+// with X = [1, covariates] ([N][KP] row-major, KP in {8, 16, 52}), W the per-chain GEMM weights
+// (a family transform of the parameters), both contractions on DMMA (mma.sync.m8n8k4.f64). X row
+// tiles stream through a 3-stage TMA bulk-copy ring guarded by full/empty mbarriers; 16 warps =
+// 4 row quarters x 4 chain groups, each reading back only its own R block so warps drift and
+// overlap phases. Parameters live in shared memory, momenta in the registers of 8 owner threads per
+// chain, which also apply the family chain rule (gradient in parameter space from G, the residual
+// sum of squares and the priors). One chain thread per chain runs the reference RNG stream,
+// energies, Metropolis test, log_pred and accumulators. Semantics follow hmc.cpp:22-99 and
+// engine.cpp:342-381.
+// Few-chain configurations (cfg4: 800 chains; K-fold cfg2: 80 chains) split the rows over a
+// thread-block cluster of CS CTAs that replicate one 64-chain tile: each CTA streams 1/CS of the
+// row tiles and the partial X^T R / residual sums are reduced through distributed shared memory in
+// fixed rank order, so every CTA of the cluster holds bit-identical state; rank 0 writes it back.
+#include <cooperative_groups.h>
+#include <math_constants.h>
+
+#include "device_common.cuh"
+#include "tc_common.cuh"
+#include "types.cuh"
+
+namespace pcvg {
+
+int glm_cluster_size(int n, int kp, int nch);
+
+namespace {
+
+using namespace tc;
+
+constexpr int kC = 64;          // chains per CTA
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kLdS = 68;        // leading dim of [k][chain] / [row][chain] shared arrays
+constexpr int kOwners = kThreads / kC;  // owner threads per chain (8)
+constexpr int kStages = 3;      // TMA ring depth
+
+template <int KP>
+struct Geom {
+  static constexpr int KS = KP / 4;                       // k-steps of X . W
+  static constexpr int PT = (KP + 7) / 8;                 // 8-row tiles of X^T . R
+  static constexpr int TM = KP <= 8 ? 256 : (KP <= 16 ? 128 : 64);  // rows per TMA tile
+  static constexpr int ROWS_W = TM / 4;                   // rows per warp (row quarter)
+  static constexpr int CHUNKS = ROWS_W / 16;              // 16-row chunks per warp per tile
+  static constexpr int XPAD = PT * 8 - KP + 4;            // X^T p-tile overread
+  static constexpr int DIMP = KP + 4;                     // max parameters (incl. specials)
+  static constexpr int OWN = (DIMP + kOwners - 1) / kOwners;
+  static constexpr int TILE_BYTES = TM * KP * 8 + TM * 8 + TM * 4;
+};
+
+template <int KP>
+struct Smem {
+  using G = Geom<KP>;
+  double xs[kStages][G::TM * KP + G::XPAD];
+  double ys[kStages][G::TM];
+  int ks[kStages][G::TM];
+  double rs[(KP > 64 ? KP : 64) * kLdS];  // per-warp R blocks; reused as G and momentum staging
+  double qs[G::DIMP * kLdS];              // parameters, [k][chain]
+  double ws[KP * kLdS];                   // GEMM weights, [col][chain]
+  double llp[4][kC];                      // per row quarter: log-lik (logistic) / sum r^2 (gaussian)
+  double gt[KP * kLdS];                   // cluster-reduced G, [col][chain]
+  double lt[kC];                          // cluster-reduced residual statistic
+  double red[kOwners][kC];                // owner partial sums (kinetic)
+  double pri[kOwners][kC];                // owner partial sums (log joint)
+  double exp_tab[16];                     // 2^(-j/16)
+  int lo[kC], hi[kC], ntr[kC];
+  int bad[kC];
+  int cur[kC];
+  unsigned long long full[kStages];
+  unsigned long long empty[kStages];
+};
+
+// ------------------------------------------------------------------ family hooks
+__device__ __forceinline__ double logistic_fn(double u) { return 1.0 / (1.0 + exp(-u)); }
+
+// Design column of parameter k, or -1 for parameters outside the predictor.
+template <int FAM>
+__device__ __forceinline__ int col_of(const ModelDev& M, int k) {
+  if constexpr (FAM == kLogistic) return k < M.dim ? k : -1;
+  else if constexpr (FAM == kGrouped) return k <= M.nc ? k : -1;  // [alpha_0, beta_0..beta_{P-1}]
+  else return k < M.p ? k + 1 : (k == M.p ? 0 : (k <= M.p + M.q ? k : -1));
+}
+
+// GEMM weight of parameter k (the coefficient multiplying its design column).
+template <int FAM>
+__device__ __forceinline__ double w_of(const ModelDev& M, int k, double qk) {
+  if constexpr (FAM == kGrouped) return k == 0 ? qk : M.cmask[k - 1] * qk;
+  else if constexpr (FAM == kSeasonal) {
+    if (k < M.p) {
+      const double w = logistic_fn(qk);
+      return M.rho_sym ? 2.0 * w - 1.0 : 0.5 * (1.0 + w);
+    }
+    return qk;
+  } else return qk;
+}
+
+template <int KP>
+__device__ __forceinline__ double quarter_sum(const Smem<KP>& sm, int c) {
+  return sm.lt[c];  // reduced over row quarters and cluster ranks (reduce_pass)
+}
+
+// d log p / d q_k from the reduced G column, the parameters and the residual sum of squares.
+// grouped_regression.cpp:100-121 (J = 1), seasonal_ar.cpp:79-105, logistic plugin.
+template <int FAM, int KP>
+__device__ __forceinline__ double grad_of(const ModelDev& M, const Smem<KP>& sm, int k, int c,
+                                          double gk, double qk) {
+  if constexpr (FAM == kLogistic) {
+    return gk - qk;
+  } else if constexpr (FAM == kGrouped) {
+    const int P = M.nc;
+    const double sig_y = exp(sm.qs[(P + 3) * kLdS + c]);
+    const double v = sig_y * sig_y;
+    const double sig_a = exp(sm.qs[(P + 2) * kLdS + c]);
+    const double va = sig_a * sig_a;
+    const double mu = sm.qs[(P + 1) * kLdS + c];
+    const double dev = sm.qs[c] - mu;
+    if (k == 0) return gk / v - dev / va;
+    if (k <= P) return M.cmask[k - 1] * (gk / v) - qk;
+    if (k == P + 1) return dev / va - mu;
+    if (k == P + 2) return dev * dev / va - 1.0 - va / 10.0 + 1.0;
+    return quarter_sum(sm, c) / v - sm.ntr[c] - v / 10.0 + 1.0;
+  } else {
+    const int p = M.p, q = M.q;
+    const double sigma = exp(sm.qs[(p + q + 1) * kLdS + c]);
+    const double v = sigma * sigma;
+    if (k < p) {
+      const double w = logistic_fn(qk);
+      const double dw = w * (1.0 - w);
+      const double drho = M.rho_sym ? 2.0 * dw : 0.5 * dw;
+      return gk * drho / v + (4.0 * (1.0 - w) - 4.0 * w + 1.0 - 2.0 * w);
+    }
+    if (k <= p + q) return gk / v - qk;
+    return quarter_sum(sm, c) / v - sm.ntr[c] - v + 1.0;
+  }
+}
+
+// Log joint contribution owned by parameter k (priors; the Gaussian likelihood term rides on the
+// observation-variance parameter). grouped_regression.cpp:65-85, seasonal_ar.cpp:59-77.
+template <int FAM, int KP>
+__device__ __forceinline__ double logp_of(const ModelDev& M, const Smem<KP>& sm, int k, int c,
+                                          double qk) {
+  if constexpr (FAM == kLogistic) {
+    return -0.5 * (kLog2Pi + qk * qk);
+  } else if constexpr (FAM == kGrouped) {
+    const int P = M.nc;
+    if (k == 0) {
+      const double sig_a = exp(sm.qs[(P + 2) * kLdS + c]);
+      const double va = sig_a * sig_a;
+      const double dev = qk - sm.qs[(P + 1) * kLdS + c];
+      return -0.5 * (kLog2Pi + log(va) + dev * dev / va);
+    }
+    if (k <= P + 1) return -0.5 * (kLog2Pi + qk * qk);
+    const double s = exp(qk);
+    double l = M.c_lhn10 - s * s / 20.0 + qk;
+    if (k == P + 3) {
+      const double v = s * s;
+      l += -0.5 * (sm.ntr[c] * (kLog2Pi + log(v)) + quarter_sum(sm, c) / v);
+    }
+    return l;
+  } else {
+    const int p = M.p, q = M.q;
+    if (k < p) {
+      const double w = logistic_fn(qk);
+      return 4.0 * log(w) + 4.0 * log1p(-w) + M.c_lbeta55 + log(w) + log1p(-w);
+    }
+    if (k <= p + q) return -0.5 * (kLog2Pi + qk * qk);
+    const double sigma = exp(qk);
+    const double v = sigma * sigma;
+    return M.c_lhn1 - v / 2.0 + qk - 0.5 * (sm.ntr[c] * (kLog2Pi + log(v)) + quarter_sum(sm, c) / v);
+  }
+}
+
+// ------------------------------------------------------------------ TMA ring
+template <int KP>
+__device__ __forceinline__ void issue_tile(Smem<KP>& sm, const ModelDev& M, int t, uint32_t g) {
+  using G = Geom<KP>;
+  const int slot = g % kStages;
+  if (g >= kStages) mbar_wait(&sm.empty[slot], ((g - kStages) / kStages) & 1u);
+  mbar_expect_tx(&sm.full[slot], G::TILE_BYTES);
+  bulk_g2s(sm.xs[slot], M.xr + static_cast<size_t>(t) * G::TM * KP, G::TM * KP * 8, &sm.full[slot]);
+  bulk_g2s(sm.ys[slot], M.y + static_cast<size_t>(t) * G::TM, G::TM * 8, &sm.full[slot]);
+  bulk_g2s(sm.ks[slot], M.key + static_cast<size_t>(t) * G::TM, G::TM * 4, &sm.full[slot]);
+}
+
+// One pass over all observations for the 64 chains with weights sm.ws: G = X^T R into sm.rs as
+// [col][chain]; the per-chain residual statistic (logistic: log-likelihood when VALUE; Gaussian:
+// sum of squared training residuals, every pass) into sm.llp[quarter][chain].
+template <int FAM, int KP, bool VALUE>
+__device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int t0, int t1) {
+  using G = Geom<KP>;
+  constexpr bool kGauss = FAM != kLogistic;
+  const int tid = threadIdx.x;
+  const int w = tid >> 5, l = tid & 31;
+  const int cg = w & 3, rq = w >> 2;
+  const int ntiles = t1 - t0;
+  const uint32_t g0 = gtile;
+  if (tid == 0)
+    for (int t = 0; t < kStages && t < ntiles; ++t) issue_tile(sm, M, t0 + t, g0 + t);
+  int lo[2][2], hi[2][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int ch = 16 * cg + 8 * j + 2 * (l & 3) + e;
+      lo[j][e] = sm.lo[ch];
+      hi[j][e] = sm.hi[ch];
+    }
+  const double* wcol = sm.ws + 16 * cg + (l >> 2);
+  double gacc[G::PT][2][2];
+#pragma unroll
+  for (int pt = 0; pt < G::PT; ++pt)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) gacc[pt][j][0] = gacc[pt][j][1] = 0.0;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double* rblk = sm.rs + (16 * rq) * kLdS + 16 * cg;  // this warp's private 16 x 16 R block
+
+  for (int tl = 0; tl < ntiles; ++tl) {
+    const int t = t0 + tl;
+    const uint32_t g = g0 + tl;
+    const int slot = g % kStages;
+    mbar_wait(&sm.full[slot], (g / kStages) & 1u);
+    const double* xs = sm.xs[slot];
+#pragma unroll 1
+    for (int ch = 0; ch < G::CHUNKS; ++ch) {
+      const int row0 = rq * G::ROWS_W + 16 * ch;
+      double eta[2][2][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) eta[mt][j][0] = eta[mt][j][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < G::KS; ++ks) {
+        double b[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) b[j] = wcol[(4 * ks + (l & 3)) * kLdS + 8 * j];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const double a = xs[(row0 + 8 * mt + (l >> 2)) * KP + 4 * ks + (l & 3)];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma(eta[mt][j][0], eta[mt][j][1], a, b[j]);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = row0 + 8 * mt + (l >> 2);
+        const bool valid = t * G::TM + row < M.n;
+        const double yv = sm.ys[slot][row];
+        const int kv = sm.ks[slot][row];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double r2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double x = eta[mt][j][e];
+            const bool train = valid && static_cast<unsigned>(kv - lo[j][e]) >=
+                                            static_cast<unsigned>(hi[j][e] - lo[j][e]);
+            if constexpr (!kGauss) {
+              const double ex = exp_neg(fabs(x), sm.exp_tab);
+              const double inv = rcp_1_2(1.0 + ex);
+              const double sig = x >= 0.0 ? inv : ex * inv;
+              r2[e] = train ? yv - sig : 0.0;
+              if (VALUE) {
+                if (train) acc[j][e] += yv * x - (fmax(x, 0.0) + log1p(ex));
+                else if (valid && !isfinite(x)) acc[j][e] = CUDART_NAN;  // 0 * non-finite test term
+              }
+            } else {
+              const double r = yv - x;
+              r2[e] = train ? r : 0.0;
+              acc[j][e] = fma(r2[e], r, acc[j][e]);
+              if (VALUE && valid && !train && !isfinite(r)) acc[j][e] = CUDART_NAN;
+            }
+          }
+          *reinterpret_cast<double2*>(&rblk[(8 * mt + (l >> 2)) * kLdS + 8 * j + 2 * (l & 3)]) =
+              make_double2(r2[0], r2[1]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int m = 4 * ks + (l & 3);
+        double b[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) b[j] = rblk[m * kLdS + 8 * j + (l >> 2)];
+#pragma unroll
+        for (int pt = 0; pt < G::PT; ++pt) {
+          const double a = xs[(row0 + m) * KP + 8 * pt + (l >> 2)];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma(gacc[pt][j][0], gacc[pt][j][1], a, b[j]);
+        }
+      }
+      __syncwarp();
+    }
+    if (l == 0) mbar_arrive(&sm.empty[slot]);
+    if (tid == 0 && tl + kStages < ntiles) issue_tile(sm, M, t + kStages, g + kStages);
+  }
+  gtile = g0 + ntiles;
+  __syncthreads();
+  // Stage G [col][chain] into sm.rs: quarter 0 stores, quarters 1..3 add in order.
+#pragma unroll 1
+  for (int qq = 0; qq < 4; ++qq) {
+    if (rq == qq) {
+#pragma unroll
+      for (int pt = 0; pt < G::PT; ++pt) {
+        const int p = 8 * pt + (l >> 2);
+        if (p < KP) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            double2* dst = reinterpret_cast<double2*>(&sm.rs[p * kLdS + 16 * cg + 8 * j + 2 * (l & 3)]);
+            if (qq == 0) {
+              *dst = make_double2(gacc[pt][j][0], gacc[pt][j][1]);
+            } else {
+              const double2 v = *dst;
+              *dst = make_double2(v.x + gacc[pt][j][0], v.y + gacc[pt][j][1]);
+            }
+          }
+        }
+      }
+      if (VALUE || kGauss) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double v = acc[j][e];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (l < 4) sm.llp[qq][16 * cg + 8 * j + 2 * l + e] = v;
+          }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Sums the staged partials (G in sm.rs, residual statistic in sm.llp) over the CS CTAs of the
+// cluster in rank order into sm.gt / sm.lt (CS = 1: a local copy, same bits).
+template <int KP>
+__device__ void reduce_pass(Smem<KP>& sm, int cs) {
+  namespace cgr = cooperative_groups;
+  const int tid = threadIdx.x;
+  if (cs > 1) cgr::this_cluster().sync();
+  for (int i = tid; i < KP * kC; i += kThreads) {
+    const int k = i / kC, c = i % kC;
+    double s = 0.0;
+    for (int r = 0; r < cs; ++r) {
+      const Smem<KP>* rem = cs > 1 ? cgr::this_cluster().map_shared_rank(&sm, r) : &sm;
+      s += rem->rs[k * kLdS + c];
+    }
+    sm.gt[k * kLdS + c] = s;
+  }
+  if (tid < kC) {
+    double s = 0.0;
+    for (int r = 0; r < cs; ++r) {
+      const Smem<KP>* rem = cs > 1 ? cgr::this_cluster().map_shared_rank(&sm, r) : &sm;
+      s += (rem->llp[0][tid] + rem->llp[1][tid]) + (rem->llp[2][tid] + rem->llp[3][tid]);
+    }
+    sm.lt[tid] = s;
+  }
+  if (cs > 1) cgr::this_cluster().sync();  // remote reads done before rs / llp are reused
+  else __syncthreads();
+}
+
+__device__ __forceinline__ double bernoulli_logit(double y, double x) {
+  return y * x - (fmax(x, 0.0) + log1p(exp(-fabs(x))));
+}
+
+template <int FAM, int KP>
+__global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs) {
+  using G = Geom<KP>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem<KP>& sm = *reinterpret_cast<Smem<KP>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int nch = S.nch;
+  const int dim = M.dim;
+  const size_t plane = static_cast<size_t>(dim) * nch;
+  const int tile = blockIdx.x / cs, crank = blockIdx.x % cs;  // chain tile, rank in the cluster
+  const bool writer = crank == 0;                              // rank 0 owns all global writes
+  const int ntiles_all = (M.n + G::TM - 1) / G::TM;
+  const int t0 = crank * ntiles_all / cs, t1 = (crank + 1) * ntiles_all / cs;
+  const int oc = tid & (kC - 1), ok = tid / kC;  // owner: chain oc, params ok + 8j
+  const int ogc = tile * kC + oc;
+  const bool ovalid = ogc < nch;
+  const bool is_chain = tid < kC;
+  const int gc = tile * kC + tid;
+  const bool cvalid = is_chain && gc < nch;
+
+  if (tid < kStages) {
+    mbar_init(&sm.full[tid], 1);
+    mbar_init(&sm.empty[tid], kWarps);
+  }
+  if (tid < 16) sm.exp_tab[tid] = exp2(-tid / 16.0);
+  for (int i = tid; i < KP * kLdS; i += kThreads) sm.ws[i] = 0.0;
+  fence_mbar_init();
+  uint32_t gtile = 0;
+
+  ChainRng R;
+  double lp0 = 0.0, warm = 0.0;
+  int64_t div_count = 0;
+  int fold = M.K;
+  if (is_chain) {
+    if (cvalid) {
+      fold = S.fold_override ? S.fold_override[gc] : S.fold0 + gc / S.L;
+      sm.lo[tid] = M.fold_lo[fold];
+      sm.hi[tid] = M.fold_hi[fold];
+      sm.ntr[tid] = M.n_train[fold];
+      sm.cur[tid] = S.cur[gc];
+      lp0 = S.lp0[gc];
+      R.init(S.seed, S.rng_stream[gc], S.rng_pos[gc], S.rng_cached[gc], S.rng_has[gc] != 0);
+    } else {
+      sm.lo[tid] = 0;
+      sm.hi[tid] = 0;
+      sm.ntr[tid] = M.n;
+      sm.cur[tid] = 0;
+    }
+  }
+  __syncthreads();
+
+  // owners: publish parameters + GEMM weights of their slots
+  auto put_q = [&](int k, double q) {
+    sm.qs[k * kLdS + oc] = q;
+    const int col = col_of<FAM>(M, k);
+    if (col >= 0) sm.ws[col * kLdS + oc] = w_of<FAM>(M, k, q);
+  };
+  auto lp_from_partials = [&](int c) {
+    double pr = 0.0;
+#pragma unroll
+    for (int o = 0; o < kOwners; ++o) pr += sm.pri[o][c];
+    if constexpr (FAM == kLogistic) return quarter_sum(sm, c) + pr;
+    else return pr;
+  };
+
+  if (A.mode == kModeEval) {
+    {
+      const int cu = sm.cur[oc];
+#pragma unroll
+      for (int j = 0; j < G::OWN; ++j) {
+        const int k = ok + kOwners * j;
+        if (k < dim) put_q(k, ovalid ? S.pos[cu * plane + static_cast<size_t>(k) * nch + ogc] : 0.0);
+      }
+    }
+    __syncthreads();
+    grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
+    reduce_pass(sm, cs);
+    double pr = 0.0;
+    const int cu = sm.cur[oc];
+#pragma unroll
+    for (int j = 0; j < G::OWN; ++j) {
+      const int k = ok + kOwners * j;
+      if (k < dim) {
+        const double q = sm.qs[k * kLdS + oc];
+        const int col = col_of<FAM>(M, k);
+        const double gk = col >= 0 ? sm.gt[col * kLdS + oc] : 0.0;
+        if (ovalid && writer) S.grad[cu * plane + static_cast<size_t>(k) * nch + ogc] = grad_of<FAM, KP>(M, sm, k, oc, gk, q);
+        pr += logp_of<FAM, KP>(M, sm, k, oc, q);
+      }
+    }
+    sm.pri[ok][oc] = pr;
+    __syncthreads();
+    if (cvalid && writer) {
+      const double lp = lp_from_partials(tid);
+      S.lp0[gc] = lp;
+      if (A.out_a) A.out_a[gc] = lp;
+    }
+    return;
+  }
+
+  const double eps = M.step, half = 0.5 * M.step;
+  const int n_lf = M.n_lf;
+  for (int64_t it = 0; it < A.n_iters; ++it) {
+    if (A.mode != kModePred) {
+      // -- momentum refresh (chain thread, reference draw order) -> staging in sm.rs
+      double k0 = 0.0;
+      if (is_chain) {
+        for (int k = 0; k < dim; ++k) {
+          const double mk = __ldg(M.inv_mass + k);
+          double p;
+          if (A.mode == kModeProbe) p = cvalid ? A.probe_momentum[static_cast<size_t>(gc) * dim + k] : 0.0;
+          else p = R.normal() / sqrt(mk);
+          k0 += mk * p * p;
+          sm.rs[k * kLdS + tid] = p;
+        }
+        sm.bad[tid] = 0;
+      }
+      __syncthreads();
+      // -- half kick + first drift (owners)
+      double pown[G::OWN];
+      {
+        const int cu = sm.cur[oc];
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < G::OWN; ++j) {
+          const int k = ok + kOwners * j;
+          double q = 0.0, p = 0.0;
+          if (k < dim) {
+            if (ovalid) {
+              const size_t gi = cu * plane + static_cast<size_t>(k) * nch + ogc;
+              p = sm.rs[k * kLdS + oc] + half * S.grad[gi];
+              q = S.pos[gi] + eps * __ldg(M.inv_mass + k) * p;
+              bad |= !isfinite(q);
+            }
+            put_q(k, q);
+          }
+          pown[j] = p;
+        }
+        if (bad) sm.bad[oc] = 1;
+      }
+      __syncthreads();
+      // -- leapfrog: n_lf gradient passes
+      for (int s = 0; s < n_lf; ++s) {
+        const bool last = s == n_lf - 1;
+        if (last) grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
+        else grad_pass<FAM, KP, false>(sm, M, gtile, t0, t1);
+        reduce_pass(sm, cs);
+        const double scale = last ? half : eps;
+        const int cu = sm.cur[oc];
+        bool bad = false;
+        double part = 0.0, part2 = 0.0;
+        double gk_new[G::OWN];
+#pragma unroll
+        for (int j = 0; j < G::OWN; ++j) {
+          const int k = ok + kOwners * j;
+          gk_new[j] = 0.0;
+          if (k < dim) {
+            const double q = sm.qs[k * kLdS + oc];
+            const int col = col_of<FAM>(M, k);
+            const double g = grad_of<FAM, KP>(M, sm, k, oc, col >= 0 ? sm.gt[col * kLdS + oc] : 0.0, q);
+            gk_new[j] = g;
+            bad |= !isfinite(g);
+            pown[j] += scale * g;
+            bad |= !isfinite(pown[j]);
+            if (last) {
+              part += __ldg(M.inv_mass + k) * pown[j] * pown[j];
+              part2 += logp_of<FAM, KP>(M, sm, k, oc, q);
+              if (ovalid && writer) {
+                const size_t gi = (cu ^ 1) * plane + static_cast<size_t>(k) * nch + ogc;
+                S.pos[gi] = q;
+                S.grad[gi] = g;
+              }
+            }
+          }
+        }
+        (void)gk_new;
+        __syncthreads();  // every owner read G / q / llp before they change
+        if (!last) {
+#pragma unroll
+          for (int j = 0; j < G::OWN; ++j) {
+            const int k = ok + kOwners * j;
+            if (k < dim) {
+              const double q = sm.qs[k * kLdS + oc] + eps * __ldg(M.inv_mass + k) * pown[j];
+              bad |= !isfinite(q);
+              put_q(k, q);
+            }
+          }
+        } else {
+          sm.red[ok][oc] = part;
+          sm.pri[ok][oc] = part2;
+        }
+        if (bad) sm.bad[oc] = 1;
+        __syncthreads();
+      }
+      // -- energies, Metropolis (chain thread)
+      if (is_chain) {
+        double k1 = 0.0;
+#pragma unroll
+        for (int o = 0; o < kOwners; ++o) k1 += sm.red[o][tid];
+        const double lp1 = lp_from_partials(tid);
+        const bool bad = sm.bad[tid] != 0;
+        const double h0 = -lp0 + 0.5 * k0;
+        const double h1 = bad ? CUDART_NAN : -lp1 + 0.5 * k1;
+        const double dh = h1 - h0;
+        const bool divergent = bad || isnan(dh) || (isfinite(dh) && fabs(dh) > 1000.0);
+        bool accepted = false;
+        if (divergent) {
+          ++div_count;
+        } else {
+          const double u = A.mode == kModeProbe ? (cvalid ? A.probe_u[gc] : 0.5) : R.uniform();
+          if (log(u) < -dh) {
+            accepted = true;
+            sm.cur[tid] ^= 1;
+            lp0 = lp1;
+          }
+        }
+        if (cvalid && writer && A.mode == kModeProbe) {
+          A.out_a[gc] = h0;
+          A.out_b[gc] = h1;
+          A.out_flags[gc] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
+        }
+        if (cvalid && writer && A.mode == kModeChain) A.traj_div[it] = divergent ? 1 : 0;
+      }
+      // rank 0's proposal writes must be visible to the cluster before the next half kick
+      if (cs > 1) cooperative_groups::this_cluster().sync();
+      else __syncthreads();
+      if (A.mode == kModeProbe) continue;
+      if (A.mode == kModeChain) {
+        const int cu = sm.cur[oc];
+        if (ovalid && writer) {
+#pragma unroll
+          for (int j = 0; j < G::OWN; ++j) {
+            const int k = ok + kOwners * j;
+            if (k < dim) A.traj[it * dim + k] = S.pos[cu * plane + static_cast<size_t>(k) * nch + ogc];
+          }
+        }
+        continue;
+      }
+    }
+    // -- log_pred at the current position + accumulators (chain thread of rank 0)
+    if (cvalid && writer) {
+      double sp = 0.0;
+      if (fold < M.K) {
+        const int cu = sm.cur[tid];
+        const double* pos = S.pos + cu * plane + gc;
+        double v_pred = 1.0;
+        if constexpr (FAM == kGrouped) {
+          const double sy = exp(pos[static_cast<size_t>(M.nc + 3) * nch]);
+          v_pred = sy * sy;  // grouped_regression.cpp:240-241
+        } else if constexpr (FAM == kSeasonal) {
+          v_pred = exp(2.0 * pos[static_cast<size_t>(M.p + M.q + 1) * nch]);  // seasonal_ar.cpp:110
+        }
+        const int s0 = M.fold_seg[fold], s1 = M.fold_seg[fold + 1];
+        for (int s = s0; s < s1; ++s) {
+          for (int tt = M.seg_row[s]; tt < M.seg_row[s + 1]; ++tt) {
+            const int i = M.seg_rows[tt];
+            const double* xrow = M.xr + static_cast<size_t>(i) * KP;
+            double eta = 0.0;
+            for (int k = 0; k < dim; ++k) {
+              const int col = col_of<FAM>(M, k);
+              if (col >= 0) eta = fma(xrow[col], w_of<FAM>(M, k, pos[static_cast<size_t>(k) * nch]), eta);
+            }
+            if constexpr (FAM == kLogistic) sp += bernoulli_logit(M.y[i], eta);
+            else sp += normal_logpdf(M.y[i], eta, v_pred);
+          }
+        }
+      }
+      if (A.mode == kModePred) {
+        if (A.out_a) A.out_a[gc] = sp;
+      } else if (A.mode == kModeWarmup) {
+        warm += sp;
+      } else {
+        accum_observe(S.acc, gc, nch, sp, A.iter0 + it, A.planned_n, A.D, A.b);
+      }
+    }
+    if (A.mode == kModePred) break;
+  }
+  if (cvalid && writer && A.mode != kModePred) {
+    S.cur[gc] = static_cast<int8_t>(sm.cur[tid]);
+    S.lp0[gc] = lp0;
+    S.rng_pos[gc] = R.pos;
+    S.rng_cached[gc] = R.cached;
+    S.rng_has[gc] = R.has_cached ? 1 : 0;
+    S.divergences[gc] += div_count;
+    if (A.mode == kModeWarmup) S.warm_sum[gc] += warm;
+  }
+}
+
+template <int FAM, int KP>
+cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
+  const int tiles = (S.nch + kC - 1) / kC;
+  if (tiles == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(glm_kernel<FAM, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(Smem<KP>)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int cs = glm_cluster_size(M.n, KP, S.nch);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles * cs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sizeof(Smem<KP>);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = cs > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs);
+}
+
+}  // namespace
+
+// Cluster size: enough CTAs per 64-chain tile to cover the GPU, at most 8 (portable), and at least
+// two row tiles per CTA.
+int glm_cluster_size(int n, int kp, int nch) {
+  const int tm = kp <= 8 ? 256 : (kp <= 16 ? 128 : 64);
+  const int tiles = (nch + kC - 1) / kC;
+  const int ntiles = (n + tm - 1) / tm;
+  int cs = 1;
+  while (cs < 8 && tiles * cs * 2 <= 148 && ntiles >= 4 * cs) cs *= 2;
+  return cs;
+}
+
+// Padded design width for a model on the tensor-core path, or 0 if it does not qualify
+// (hierarchical families with J > 1 use gauss_kernel).
+int glm_width(int family, int J, int nc) {
+  const int cols = nc + 1;  // intercept + covariates
+  if (family == kLogistic) return cols <= 8 ? 8 : (cols <= 16 ? 16 : (cols <= 52 ? 52 : 0));
+  if (family == kGrouped && J == 1) return cols <= 8 ? 8 : (cols <= 16 ? 16 : 0);
+  if (family == kSeasonal) return cols <= 8 ? 8 : (cols <= 16 ? 16 : 0);
+  return 0;
+}
+
+cudaError_t launch_glm(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
+  switch (M.family * 100 + M.nc_pad) {
+    case kLogistic * 100 + 8: return launch_t<kLogistic, 8>(M, S, A, st);
+    case kLogistic * 100 + 16: return launch_t<kLogistic, 16>(M, S, A, st);
+    case kLogistic * 100 + 52: return launch_t<kLogistic, 52>(M, S, A, st);
+    case kGrouped * 100 + 8: return launch_t<kGrouped, 8>(M, S, A, st);
+    case kGrouped * 100 + 16: return launch_t<kGrouped, 16>(M, S, A, st);
+    case kSeasonal * 100 + 8: return launch_t<kSeasonal, 8>(M, S, A, st);
+    case kSeasonal * 100 + 16: return launch_t<kSeasonal, 16>(M, S, A, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pcvg

@@ -1,0 +1,96 @@
+// sm_100a building blocks of the tensor-core kernels: FP64 DMMA, mbarriers, TMA bulk copies,
+// and the cheap FP64 transcendentals the sigmoid needs (DMMA and DFMA share one FP64 datapath on
+// B200, measured in tools/probes/fp64_peak.cu, so elementwise FP64 work is taken from the GEMM).
+#pragma once
+#include <cstdint>
+
+namespace pcvg {
+namespace tc {
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS DMMA.8x8x4).
+// Fragments: lane l holds A[l>>2][l&3], B[l&3][l>>2], D[l>>2][2(l&3) + {0,1}].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
+               "r"(bytes));
+}
+
+// One TMA bulk copy global -> shared completing on `bar` (SASS UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// exp(-a) for a >= 0 with ~1 ulp error in 11 FP64 operations (CUDA's exp() spends ~17 plus a
+// special-case branch): -a = -(n/16) ln2 + r, |r| <= ln2/32, 2^(-j/16) from a 16-entry table,
+// e^r by a degree-6 Taylor polynomial (truncation < 4e-17), 2^(-m) assembled in the exponent.
+__device__ __forceinline__ double exp_neg(double a, const double* tab) {
+  constexpr double kInvLn2x16 = 23.083120654223414;      // 16 / ln 2
+  constexpr double kLn2d16Hi = 0.04332169877307024;      // ln2/16, leading 32 bits
+  constexpr double kLn2d16Lo = 1.1926343307941173e-11;   // ln2/16 - hi
+  constexpr double kShift = 6755399441055744.0;          // 1.5 * 2^52
+  if (a > 700.0) return 0.0;
+  const double t = fma(a, kInvLn2x16, kShift);
+  const int n = __double2loint(t);
+  const double nd = t - kShift;
+  double r = fma(nd, kLn2d16Hi, -a);
+  r = fma(nd, kLn2d16Lo, r);
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double scale = __hiloint2double((1023 - (n >> 4)) << 20, 0);
+  return (tab[n & 15] * scale) * p;
+}
+
+// 1 / d for d in [1, 2]: hardware approximation + two Newton steps (no special cases needed).
+__device__ __forceinline__ double rcp_1_2(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+}  // namespace tc
+}  // namespace pcvg

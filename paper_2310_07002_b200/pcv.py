@@ -93,6 +93,7 @@ def load():
     _sig(lib, "pcvg_add_model", i32, [vp, P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec),
                                       P(abi.Kernel), pf, i64, i32, pi32])
     _sig(lib, "pcvg_model_dim", i32, [vp, i32, pi32])
+    _sig(lib, "pcvg_set_kernel_policy", i32, [vp, i32])
     _sig(lib, "pcvg_model_test_size", i32, [vp, i32, i32, pi64])
     _sig(lib, "pcvg_eval", i32, [vp, i32, i64, pi32, pf, pf, pf])
     _sig(lib, "pcvg_eval_pred", i32, [vp, i32, i64, pi32, pf, pf])
@@ -358,6 +359,11 @@ class Context:
         self.models.append(model)
         self._keep.append((kern, bank))
         return slot.value
+
+    KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TENSOR = 0, 1, 2
+
+    def set_kernel_policy(self, policy):
+        self._chk(self.lib.pcvg_set_kernel_policy(self.h, policy))
 
     def dim(self, slot):
         d = C.c_int32()

@@ -22,20 +22,36 @@ def ctx():
 
 
 _cases = {}
+# fixtures whose models have both a tensor-core (GLM) and a generic kernel
+BOTH_KERNELS = {"cfg1_linreg_loo", "seasonal_timeblocks", "seasonal_hvblock"}
 
 
 def case_in(ctx, name):
-    """(Case, slots) with the case's models registered in a fresh context."""
+    """(Case, slots) with the case's models registered in a fresh context. A name suffixed with
+    ':tensor' / ':generic' forces that kernel."""
+    name, _, kernel = name.partition(":")
     if name not in _cases:
         _cases[name] = Case(name)
     case = _cases[name]
     c = pcv.Context(0)
+    if kernel:
+        c.set_kernel_policy(c.KERNEL_TENSOR if kernel == "tensor" else c.KERNEL_GENERIC)
     slots = [c.add_model(m, kp, bank, model_id=i)
              for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
     return case, c, slots
 
 
-@pytest.mark.parametrize("name", ALL_FIXTURES)
+def with_kernels(names):
+    out = []
+    for n in names:
+        if n in BOTH_KERNELS:
+            out += [n + ":tensor", n + ":generic"]
+        else:
+            out.append(n)
+    return out
+
+
+@pytest.mark.parametrize("name", with_kernels(ALL_FIXTURES))
 def test_log_joint_and_gradient(ctx, name):
     case, c, slots = case_in(ctx, name)
     worst = 0.0
@@ -56,7 +72,7 @@ def test_log_joint_and_gradient(ctx, name):
     print(f"{name}: worst scaled error {worst:.2e}")
 
 
-@pytest.mark.parametrize("name", ALL_FIXTURES)
+@pytest.mark.parametrize("name", with_kernels(ALL_FIXTURES))
 def test_log_pred(ctx, name):
     case, c, slots = case_in(ctx, name)
     for m, slot in enumerate(slots):
@@ -71,7 +87,7 @@ def test_log_pred(ctx, name):
     c.close()
 
 
-@pytest.mark.parametrize("name", ALL_FIXTURES)
+@pytest.mark.parametrize("name", with_kernels(ALL_FIXTURES))
 def test_hmc_step_injected(ctx, name):
     """hmc_step (hmc.cpp:53-99) with injected momentum and uniform: h0, h1, flags, new position."""
     case, c, slots = case_in(ctx, name)
@@ -99,8 +115,8 @@ def test_hmc_step_injected(ctx, name):
     c.close()
 
 
-@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
-                                  "seasonal_hvblock", "logistic_loo"])
+@pytest.mark.parametrize("name", with_kernels(["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
+                                               "seasonal_hvblock", "logistic_loo"]))
 def test_chain_trajectory_reference_stream(ctx, name):
     """Same reference Philox stream (seed, ChainSampling, model, fold, chain): the device chain
     reproduces the oracle chain (identical integer draws; momenta to ~1 ulp) until chaos."""
@@ -117,8 +133,8 @@ def test_chain_trajectory_reference_stream(ctx, name):
     c.close()
 
 
-@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
-                                  "seasonal_hvblock", "logistic_kfold"])
+@pytest.mark.parametrize("name", with_kernels(["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
+                                               "seasonal_hvblock", "logistic_kfold"]))
 def test_run_pcv_within_mcse(ctx, name):
     """End-to-end run_pcv on the device vs the oracle run_pcv on the same inputs: the headline
     elpd / delta within Monte Carlo error, identical report structure."""

@@ -41,9 +41,10 @@ def flops_per_chain_step(case, m):
     return n_lf * n * (4.0 * nc + 4.0)
 
 
-def gpu_run(case, L, steps, warmup):
+def gpu_run(case, L, steps, warmup, policy=0):
     from paper_2310_07002_b200 import abi, pcv
     ctx = pcv.Context(0)
+    ctx.set_kernel_policy(policy)
     for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks)):
         ctx.add_model(m, kp, bank, model_id=i)
     cfg = abi.run_config(chains=L, iters=steps, warmup=warmup, batch_size=min(50, steps), bench_draws=10, seed=1)
@@ -94,6 +95,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--policy", type=int, default=0, help="0 auto, 1 generic kernel, 2 tensor-core kernel")
     args = ap.parse_args()
     from parity_util import Case
     peak = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
@@ -102,14 +104,14 @@ def main():
         fixture, L, desc = CONFIGS[name]
         case = Case(fixture)
         steps = args.steps if name != "cfg5" else max(2, args.steps // 3)
-        ms, cols = gpu_run(case, L, steps, args.warmup)
+        ms, cols = gpu_run(case, L, steps, args.warmup, args.policy)
         chains = case.K * L * len(case.models)
         value = chains * steps / (ms / 1e3)
         flops = sum(flops_per_chain_step(case, m) for m in range(len(case.models))) / len(case.models)
         achieved = flops * value / 1e12
         is_logistic = name == "cfg2"
         pk = peak["dmma_tflops_bps8"] if is_logistic else peak["dfma_tflops_bps8"]
-        line = {"config": name, "workload": desc, "chains": chains, "steps": steps,
+        line = {"config": name, "policy": args.policy, "workload": desc, "chains": chains, "steps": steps,
                 "gpu_chain_steps_per_s": value, "gpu_ms_per_step": ms / steps,
                 "flop_per_chain_step": flops, "achieved_tflops": achieved,
                 "peak_tflops": pk, "peak_kind": "FP64 DMMA" if is_logistic else "FP64 DFMA",
