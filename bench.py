@@ -220,12 +220,12 @@ def main():
                   "ess_overall": rep["ess_overall"], "iters": int(done)}
     ctx.close()
 
-    # roofline of the dominant kernel (logistic_kernel: one launch per step)
+    # roofline of the dominant kernel (glm_kernel<logistic,52>: one launch per step)
     peak, peak_src = peak_fp64()
     per_launch_ms = local_ms / args.steps
     achieved = FLOP_PER_CHAIN_STEP * (fe - fb) * L / (per_launch_ms * 1e-3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_logistic.json")
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_glm.json")
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
@@ -242,7 +242,8 @@ def main():
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "flop_per_chain_step": FLOP_PER_CHAIN_STEP, "peak_source": peak_src,
-                             "kernel": "logistic_kernel (FP64 DMMA)"},
+                             "kernel": "glm_kernel<logistic,52> (FP64 DMMA)",
+                             "traffic_source": "profiles/r01_ncu_glm.json (ncu --set full, dram read+write per launch)"},
                 "clocks": clk.summary(), "gpu_launches": int(launches1 - launches0), "result": result}
     # e2e: the public API call with host buffers (pcvg_run: H2D of data/bank, Step 2 + Step 3,
     # per-fold + Step-4 statistics, D2H of the report), wall-clock, max over ranks.
