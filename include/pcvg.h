@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PCVG_ABI_VERSION 1
+#define PCVG_ABI_VERSION 2
 
 typedef enum {
   PCVG_OK = 0,
@@ -126,6 +126,7 @@ typedef struct {
   int64_t* batches;
   int32_t* fault;
   int32_t* failed;
+  int32_t* dss_ridged;         /* FoldSummary::dss_ridged (engine.hpp:73); may be NULL */
 } pcvg_fold_table;
 
 /* pcv::PcvReport (engine.hpp:86-109). Arrays are caller-allocated; sizes in comments. */

@@ -725,6 +725,74 @@ double pcvo_log_pred(const pcvo_model* m, const double* th, int32_t fold) {
   return lp;
 }
 
+/* Model::pred_derivs / pred_sample over the fold's test rows in fold_meta order:
+ * grouped_regression.cpp:190-213, radon.cpp:167-199, seasonal_ar.cpp:133-150. The logistic
+ * family (binary outcome) supports neither (Model defaults, model.hpp:54-66). */
+static int64_t test_row(const pcvo_model* m, int32_t fold, int64_t t) {
+  return m->rows[m->seg_row[m->fold_seg[fold]] + t];
+}
+static int pred_mean_scale(const pcvo_model* m, const double* th, int32_t fold, int64_t t,
+                           double* mean, double* var, double* sd) {
+  const int64_t i = test_row(m, fold, t);
+  const int J = m->J;
+  switch (m->family) {
+    case PCVG_FAMILY_GROUPED: {
+      const double sig_y = exp(th[J + m->P + 2]);
+      *var = sig_y * sig_y;
+      *sd = sig_y;
+      *mean = grouped_linpred(m, th, i);
+      return 1;
+    }
+    case PCVG_FAMILY_RADON: {
+      /* locate the test row's county: the segment holding t */
+      int64_t s = m->fold_seg[fold];
+      const int64_t pos = m->seg_row[m->fold_seg[fold]] + t;
+      while (m->seg_row[s + 1] <= pos) ++s;
+      const double beta = th[J], mu_a = th[J + 1];
+      const double sa = exp(0.5 * th[J + 2]);
+      const double bmask = m->include_floor ? 1.0 : 0.0;
+      *var = exp(th[J + 3]);
+      *sd = exp(0.5 * th[J + 3]);
+      *mean = mu_a + sa * th[m->seg_group[s]] + bmask * beta * xv(m, i, 0);
+      return 1;
+    }
+    case PCVG_FAMILY_SEASONAL_AR:
+      *var = exp(2.0 * th[m->p + m->q + 1]);
+      *sd = exp(th[m->p + m->q + 1]);
+      *mean = seasonal_mean(m, th, i);
+      return 1;
+  }
+  return 0;
+}
+int pcvo_supports_pred(const pcvo_model* m) { return m->family != PCVG_FAMILY_LOGISTIC; }
+void pcvo_pred_derivs(const pcvo_model* m, const double* th, int32_t fold, double* d1, double* d2) {
+  const int64_t n = pcvo_test_size(m, fold);
+  for (int64_t t = 0; t < n; ++t) {
+    double mean, var, sd;
+    pred_mean_scale(m, th, fold, t, &mean, &var, &sd);
+    d1[t] = -(m->y[test_row(m, fold, t)] - mean) / var;
+    d2[t] = -1.0 / var;
+  }
+}
+void pcvo_pred_sample(const pcvo_model* m, const double* th, int32_t fold, pcvo_rng* rng, double* out) {
+  const int64_t n = pcvo_test_size(m, fold);
+  for (int64_t t = 0; t < n; ++t) {
+    double mean, var, sd;
+    pred_mean_scale(m, th, fold, t, &mean, &var, &sd);
+    out[t] = mean + sd * pcvo_normal(rng);
+  }
+}
+
+int pcvo_pred_sample_stream(const pcvo_model* m, const double* theta, int32_t fold, uint64_t seed,
+                            uint64_t stream, int32_t times, double* out) {
+  if (!pcvo_supports_pred(m)) return PCVG_UNSUPPORTED_SCORE;
+  pcvo_rng rng;
+  pcvo_rng_init(&rng, seed, stream);
+  const int64_t n = pcvo_test_size(m, fold);
+  for (int32_t r = 0; r < times; ++r) pcvo_pred_sample(m, theta, fold, &rng, out + r * n);
+  return 0;
+}
+
 /* ------------------------------------------------------------------ hmc.cpp:22-99 */
 static int all_finite(const double* v, int n) {
   for (int i = 0; i < n; ++i)
@@ -1028,6 +1096,12 @@ typedef struct {
   long sampling_divergences;
   score_accum acc;
   score_accum* snaps;
+  /* HS / DSS (engine.cpp:322-373): WelfordDiag of xi (2m) or WelfordAccumulator of draws (m);
+   * warm-up sums (WarmupStats hs1/hs2/pred). x_acc = [a_x | a_x2] (HS) or [a_x | a_xx m*m] (DSS). */
+  int64_t msize;
+  double* x_warm;
+  double* x_acc;
+  double** x_snaps;
 } chain_task;
 
 typedef struct {
@@ -1041,6 +1115,7 @@ typedef struct {
   chain_task* tasks;
   long n_tasks;
   double** centers; /* [m][k] */
+  double*** x_centers; /* [m][k] -> hs_c (2m) / pred_c (m) */
   int b;
   long* checkpoints;
   int n_ckpt;
@@ -1063,12 +1138,26 @@ static void task_step2(run_ctx* rc, chain_task* t) { /* engine.cpp:296-313 */
   double* wp = malloc(sizeof(double) * d);
   const pcvg_kernel* kp = &rc->kernels[t->model];
   t->warm_logpred = 0.0; /* warmup_discard, hmc.cpp:121-149 */
+  const int64_t ms = t->msize;
+  double* d1 = malloc(sizeof(double) * (ms + 1));
+  double* d2 = malloc(sizeof(double) * (ms + 1));
   for (long i = 0; i < cfg->warmup; ++i) {
     int32_t acc;
     t->divergences += hmc_step_rng(m, t->fold, kp->step_size, kp->n_leapfrog, kp->inv_mass_diag,
                                    t->position, &t->rng, mom, wq, wp, &acc);
     t->warm_logpred += pcvo_log_pred(m, t->position, t->fold);
+    if (cfg->score == PCVG_SCORE_HS) {
+      pcvo_pred_derivs(m, t->position, t->fold, d1, d2);
+      for (int64_t o = 0; o < ms; ++o) {
+        t->x_warm[o] += d2[o] + d1[o] * d1[o];
+        t->x_warm[ms + o] += d1[o];
+      }
+    } else if (cfg->score == PCVG_SCORE_DSS) {
+      pcvo_pred_sample(m, t->position, t->fold, &t->rng, d1);
+      for (int64_t o = 0; o < ms; ++o) t->x_warm[o] += d1[o];
+    }
   }
+  free(d1); free(d2);
   free(mom); free(wq); free(wp);
 }
 
@@ -1083,15 +1172,43 @@ static void task_step3(run_ctx* rc, chain_task* t) { /* engine.cpp:342-381 */
   double* wp = malloc(sizeof(double) * d);
   const long before = t->divergences;
   int next_ck = 0;
+  const int64_t ms = t->msize;
+  const double* xc = cfg->score != PCVG_SCORE_LOGS ? rc->x_centers[t->model][t->fold] : NULL;
+  double* d1 = malloc(sizeof(double) * (2 * ms + 1));
+  double* d2 = malloc(sizeof(double) * (ms + 1));
+  const int64_t xlen = cfg->score == PCVG_SCORE_HS ? 4 * ms : (cfg->score == PCVG_SCORE_DSS ? ms + ms * ms : 0);
   for (long iter = 0; iter < cfg->iters; ++iter) {
     int32_t acc;
     t->divergences += hmc_step_rng(m, t->fold, kp->step_size, kp->n_leapfrog, kp->inv_mass_diag,
                                    t->position, &t->rng, mom, wq, wp, &acc);
     const double s = pcvo_log_pred(m, t->position, t->fold);
     accum_observe(&t->acc, s, iter);
-    if (next_ck < rc->n_ckpt && iter + 1 == rc->checkpoints[next_ck]) t->snaps[next_ck++] = t->acc;
+    if (cfg->score == PCVG_SCORE_HS) { /* WelfordDiag::add, accum.cpp:66-74 */
+      pcvo_pred_derivs(m, t->position, t->fold, d1, d2);
+      for (int64_t o = 0; o < ms; ++o) {
+        const double x1 = d2[o] + d1[o] * d1[o], x2 = d1[o];
+        const double a = x1 - xc[o], b = x2 - xc[ms + o];
+        t->x_acc[o] += a;
+        t->x_acc[2 * ms + o] += a * a;
+        t->x_acc[ms + o] += b;
+        t->x_acc[3 * ms + o] += b * b;
+      }
+    } else if (cfg->score == PCVG_SCORE_DSS) { /* WelfordAccumulator::add, accum.cpp:19-26 */
+      pcvo_pred_sample(m, t->position, t->fold, &t->rng, d1);
+      double* axx = t->x_acc + ms;
+      for (int64_t i = 0; i < ms; ++i) {
+        const double di = d1[i] - xc[i];
+        t->x_acc[i] += di;
+        for (int64_t j = 0; j <= i; ++j) axx[i * ms + j] += di * (d1[j] - xc[j]);
+      }
+    }
+    if (next_ck < rc->n_ckpt && iter + 1 == rc->checkpoints[next_ck]) {
+      if (xlen) memcpy(t->x_snaps[next_ck], t->x_acc, sizeof(double) * xlen);
+      t->snaps[next_ck++] = t->acc;
+    }
   }
   t->sampling_divergences = t->divergences - before;
+  free(d1); free(d2);
   free(mom); free(wq); free(wp);
 }
 
@@ -1122,20 +1239,118 @@ typedef struct {
   double delta_hat, mcse, sigma2, epistemic_se, prob, ess, rhat_max;
 } ckpt_stats;
 
-/* compute_stats, engine.cpp:117-253 (LogS). fs_out: [n_models*K], rhat_out same. */
+/* Cholesky pieces, math.hpp:46-76 (row-major, lower factor in place). */
+static int cholesky_in_place(double* a, int n) {
+  for (int j = 0; j < n; ++j) {
+    double d = a[j * n + j];
+    for (int k = 0; k < j; ++k) d -= a[j * n + k] * a[j * n + k];
+    if (!(d > 0.0) || !isfinite(d)) return 0;
+    const double l = sqrt(d);
+    a[j * n + j] = l;
+    for (int i = j + 1; i < n; ++i) {
+      double s = a[i * n + j];
+      for (int k = 0; k < j; ++k) s -= a[i * n + k] * a[j * n + k];
+      a[i * n + j] = s / l;
+    }
+  }
+  return 1;
+}
+
+/* Chain-merged HS / DSS estimate of one fold (engine.cpp:148-171): WelfordDiag/WelfordAccumulator
+ * ::merge in chain order (accum.cpp:28-34, 76-84), hs_fold_score negated (scoring.cpp:64-73),
+ * dss_fold_score (scoring.cpp:75-104). Returns 0 where the reference throws (NaN + fault). */
+static int extra_fold_estimate(const pcvg_run_config* cfg, const pcvo_model* mdl, int fold,
+                               const double* const* acc, int l, long count_total, int64_t ms,
+                               const double* xc, double* est, int* ridged) {
+  *ridged = 0;
+  if (cfg->score == PCVG_SCORE_HS) {
+    double score = 0.0;
+    for (int64_t i = 0; i < ms; ++i) {
+      double a1 = acc[0][i], a2 = acc[0][ms + i];
+      for (int c = 1; c < l; ++c) { a1 += acc[c][i]; a2 += acc[c][ms + i]; }
+      const double mu1 = a1 / count_total + xc[i];
+      const double mu2 = a2 / count_total + xc[ms + i];
+      score += 2.0 * mu1 - mu2 * mu2;
+    }
+    *est = -score;
+    return 1;
+  }
+  const int d = (int)ms;
+  if (count_total < d + 1 || count_total < 2) return 0;
+  double* ax = malloc(sizeof(double) * d);
+  double* axx = malloc(sizeof(double) * d * d);
+  double* cov = malloc(sizeof(double) * d * d);
+  double* fac = malloc(sizeof(double) * d * d);
+  double* r = malloc(sizeof(double) * d);
+  for (int i = 0; i < d; ++i) ax[i] = acc[0][i];
+  for (int i = 0; i < d * d; ++i) axx[i] = acc[0][d + i];
+  for (int c = 1; c < l; ++c) {
+    for (int i = 0; i < d; ++i) ax[i] += acc[c][i];
+    for (int i = 0; i < d * d; ++i) axx[i] += acc[c][d + i];
+  }
+  const double inv_n = 1.0 / (double)count_total, inv_nm1 = 1.0 / (double)(count_total - 1);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j <= i; ++j) {
+      const double v = (axx[i * d + j] - ax[i] * ax[j] * inv_n) * inv_nm1;
+      cov[i * d + j] = v;
+      cov[j * d + i] = v;
+    }
+  memcpy(fac, cov, sizeof(double) * d * d);
+  int ok = 1;
+  if (!cholesky_in_place(fac, d)) {
+    double tr = 0.0;
+    for (int i = 0; i < d; ++i) tr += cov[i * d + i];
+    const double ridge = 1e-8 * tr / d;
+    for (int i = 0; i < d; ++i) cov[i * d + i] += ridge;
+    memcpy(fac, cov, sizeof(double) * d * d);
+    *ridged = 1;
+    ok = cholesky_in_place(fac, d);
+  }
+  if (ok) {
+    const int64_t r0 = mdl->seg_row[mdl->fold_seg[fold]];
+    for (int i = 0; i < d; ++i) r[i] = mdl->y[mdl->rows[r0 + i]] - (ax[i] / count_total + xc[i]);
+    for (int i = 0; i < d; ++i) {
+      double sm = r[i];
+      for (int k = 0; k < i; ++k) sm -= fac[i * d + k] * r[k];
+      r[i] = sm / fac[i * d + i];
+    }
+    double quad = 0.0, ld = 0.0;
+    for (int i = 0; i < d; ++i) quad += r[i] * r[i];
+    for (int i = 0; i < d; ++i) ld += log(fac[i * d + i]);
+    *est = -(2.0 * ld) - quad;
+  }
+  free(ax); free(axx); free(cov); free(fac); free(r);
+  return ok;
+}
+
+/* compute_stats, engine.cpp:117-253. fs_out: [n_models*K], rhat_out same. */
 static ckpt_stats compute_stats(run_ctx* rc, int K, long iter_count, int ck, const char* failed,
                                 fold_score* fs_out, double* rhat_out, int* failed_out,
-                                double* delta_k) {
+                                double* delta_k, int* ridged_out) {
   const int nm = rc->n_models, l = rc->cfg->chains;
   ckpt_stats out;
   const score_accum* ch[256];
+  const double* xa[256];
   for (int m = 0; m < nm; ++m)
     for (int k = 0; k < K; ++k) {
       for (int c = 0; c < l; ++c) {
         const chain_task* t = &rc->tasks[((long)m * K + k) * l + c];
         ch[c] = &t->snaps[ck];
+        xa[c] = t->x_snaps ? t->x_snaps[ck] : NULL;
       }
       fs_out[m * K + k] = logs_fold_score(ch, l, iter_count);
+      ridged_out[m * K + k] = 0;
+      if (rc->cfg->score != PCVG_SCORE_LOGS) {
+        const chain_task* t0 = &rc->tasks[((long)m * K + k) * l];
+        double est;
+        if (extra_fold_estimate(rc->cfg, rc->models[m], k, xa, l, (long)l * iter_count, t0->msize,
+                                rc->x_centers[m][k], &est, &ridged_out[m * K + k])) {
+          fs_out[m * K + k].estimate = est;
+        } else {
+          fs_out[m * K + k].estimate = NAN;
+          fs_out[m * K + k].fault = 1;
+        }
+      }
       double rh;
       rhat_out[m * K + k] = rhat_from_blocks(ch, l, iter_count, &rh) ? rh : NAN;
       failed_out[m * K + k] = failed && failed[k];
@@ -1184,7 +1399,7 @@ static ckpt_stats compute_stats(run_ctx* rc, int K, long iter_count, int ck, con
     out.sigma2 = out.epistemic_se = out.prob = NAN;
   }
   const double ln = (double)l * iter_count;
-  out.mcse = mc_inf ? INFINITY : sqrt(mc_sum / ln);
+  out.mcse = rc->cfg->score != PCVG_SCORE_LOGS ? NAN : (mc_inf ? INFINITY : sqrt(mc_sum / ln));
   out.ess = mc_sum > 0.0 ? (double)l * iter_count * naive_sum / mc_sum : NAN;
   out.rhat_max = best < 0.0 ? NAN : best;
   free(inc);
@@ -1207,7 +1422,10 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
   if (cfg->bench_draws < 1) return set_err(PCVG_INVALID_INPUT, "need at least 1 benchmark draw");
   if (cfg->checkpoint_every < 0) return set_err(PCVG_INVALID_INPUT, "checkpoint_every must be >= 0");
   if (n_models < 1 || n_models > 2) return set_err(PCVG_INVALID_INPUT, "run_pcv takes one or two models");
-  if (cfg->score != PCVG_SCORE_LOGS) return set_err(PCVG_UNSUPPORTED_SCORE, "oracle implements LogS only");
+  if (cfg->score < PCVG_SCORE_LOGS || cfg->score > PCVG_SCORE_DSS) return set_err(PCVG_INVALID_INPUT, "unknown score");
+  for (int m = 0; m < n_models; ++m) /* Model::check_score_support, model.cpp:21-28 */
+    if (cfg->score != PCVG_SCORE_LOGS && !pcvo_supports_pred(models[m]))
+      return set_err(PCVG_UNSUPPORTED_SCORE, "model does not support the configured score");
   const int K = models[0]->K;
   for (int m = 0; m < n_models; ++m) {
     if (models[m]->K != K) return set_err(PCVG_INVALID_INPUT, "models must share one fold assignment");
@@ -1244,6 +1462,15 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
         t->chain = c;
         t->position = malloc(sizeof(double) * models[m]->dim);
         t->snaps = malloc(sizeof(score_accum) * rc.n_ckpt);
+        t->msize = pcvo_test_size(models[m], k);
+        if (cfg->score != PCVG_SCORE_LOGS) {
+          const int64_t ms = t->msize;
+          const int64_t xl = cfg->score == PCVG_SCORE_HS ? 4 * ms : ms + ms * ms;
+          t->x_warm = calloc(2 * ms + 1, sizeof(double));
+          t->x_acc = calloc(xl + 1, sizeof(double));
+          t->x_snaps = malloc(sizeof(double*) * rc.n_ckpt);
+          for (int ci = 0; ci < rc.n_ckpt; ++ci) t->x_snaps[ci] = calloc(xl + 1, sizeof(double));
+        }
       }
   run_phase(&rc, 2, threads);
   /* centering constants, engine.cpp:316-339 */
@@ -1254,6 +1481,26 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
     const double denom = (double)l * cfg->warmup;
     for (int k = 0; k < K; ++k)
       for (int c = 0; c < l; ++c) rc.centers[m][k] += rc.tasks[((long)m * K + k) * l + c].warm_logpred / denom;
+  }
+  /* HS / DSS centring vectors hs_c / pred_c (engine.cpp:324-338) */
+  if (cfg->score != PCVG_SCORE_LOGS) {
+    rc.x_centers = malloc(sizeof(double**) * n_models);
+    for (int m = 0; m < n_models; ++m) {
+      rc.x_centers[m] = malloc(sizeof(double*) * K);
+      for (int k = 0; k < K; ++k) {
+        const int64_t ms = pcvo_test_size(models[m], k);
+        const int64_t wl = cfg->score == PCVG_SCORE_HS ? 2 * ms : ms;
+        double* xc = calloc(wl + 1, sizeof(double));
+        if (cfg->warmup > 0) {
+          const double denom = (double)l * cfg->warmup;
+          for (int c = 0; c < l; ++c) {
+            const chain_task* t = &rc.tasks[((long)m * K + k) * l + c];
+            for (int64_t e = 0; e < wl; ++e) xc[e] += t->x_warm[e] / denom;
+          }
+        }
+        rc.x_centers[m][k] = xc;
+      }
+    }
   }
   run_phase(&rc, 3, threads);
   /* failed folds, engine.cpp:385-397 */
@@ -1268,11 +1515,12 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
   fold_score* fs = malloc(sizeof(fold_score) * n_models * K);
   double* rh = malloc(sizeof(double) * n_models * K);
   int* fl = malloc(sizeof(int) * n_models * K);
+  int* rg = malloc(sizeof(int) * n_models * K);
   rep->n_checkpoints = rc.n_ckpt;
   for (int ci = 0; ci < rc.n_ckpt; ++ci) {
     const int last = ci + 1 == rc.n_ckpt;
     const ckpt_stats st = compute_stats(&rc, K, rc.checkpoints[ci], ci, last ? failed : NULL, fs, rh, fl,
-                                        last ? rep->delta_k : NULL);
+                                        last ? rep->delta_k : NULL, rg);
     double* o = rep->snapshots ? rep->snapshots + 7 * ci : NULL;
     if (o) {
       o[0] = (double)rc.checkpoints[ci];
@@ -1306,6 +1554,7 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
           rep->folds.batches[i] = fs[i].batches;
           rep->folds.fault[i] = fs[i].fault;
           rep->folds.failed[i] = fl[i];
+          if (rep->folds.dss_ridged) rep->folds.dss_ridged[i] = rg[i];
           for (int c = 0; c < l; ++c)
             rep->divergences[i * l + c] = rc.tasks[i * l + c].sampling_divergences;
           if (!fl[i]) rep->score_total[m] += fs[i].estimate;
@@ -1370,9 +1619,23 @@ int pcvo_run_pcv(int32_t n_models, pcvo_model** models, const int32_t* model_ids
       }
     }
   }
-  for (long i = 0; i < rc.n_tasks; ++i) { free(rc.tasks[i].position); free(rc.tasks[i].snaps); }
+  for (long i = 0; i < rc.n_tasks; ++i) {
+    chain_task* t = &rc.tasks[i];
+    free(t->position); free(t->snaps);
+    if (t->x_snaps) {
+      for (int ci = 0; ci < rc.n_ckpt; ++ci) free(t->x_snaps[ci]);
+      free(t->x_snaps); free(t->x_acc); free(t->x_warm);
+    }
+  }
   for (int m = 0; m < n_models; ++m) free(rc.centers[m]);
-  free(rc.centers); free(rc.tasks); free(rc.checkpoints); free(failed); free(fs); free(rh); free(fl);
+  if (rc.x_centers) {
+    for (int m = 0; m < n_models; ++m) {
+      for (int k = 0; k < K; ++k) free(rc.x_centers[m][k]);
+      free(rc.x_centers[m]);
+    }
+    free(rc.x_centers);
+  }
+  free(rc.centers); free(rc.tasks); free(rc.checkpoints); free(failed); free(fs); free(rh); free(fl); free(rg);
   return 0;
 }
 

@@ -59,6 +59,15 @@ double pcvo_log_joint(const pcvo_model* m, const double* theta, int32_t fold);
 void pcvo_grad(const pcvo_model* m, const double* theta, int32_t fold, double* grad);
 double pcvo_log_pred(const pcvo_model* m, const double* theta, int32_t fold);
 
+/* Model::pred_derivs / pred_sample over the fold's test rows (model.hpp:54-66); the logistic
+ * family supports neither (pcvo_supports_pred = 0). */
+int pcvo_supports_pred(const pcvo_model* m);
+void pcvo_pred_derivs(const pcvo_model* m, const double* theta, int32_t fold, double* d1, double* d2);
+void pcvo_pred_sample(const pcvo_model* m, const double* theta, int32_t fold, pcvo_rng* rng, double* out);
+/* `times` consecutive pred_sample calls on one CounterRng(seed, stream): out[times * test_size]. */
+int pcvo_pred_sample_stream(const pcvo_model* m, const double* theta, int32_t fold, uint64_t seed,
+                            uint64_t stream, int32_t times, double* out);
+
 /* hmc.cpp:22-99. */
 int32_t pcvo_leapfrog(const pcvo_model* m, int32_t fold, double step, int32_t n_lf,
                       const double* inv_mass, double* q, double* p);

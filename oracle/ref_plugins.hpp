@@ -76,6 +76,18 @@ class HvSeasonalARModel : public pcv::Model {
     return full_->initial_draw(rng);
   }
   std::vector<double> test_values(int fold_id) const override;
+  // HS / DSS hooks: the unmodified SeasonalARModel on the fold's test partition
+  // (seasonal_ar.cpp:133-150), test rows in time order as log_pred uses them.
+  bool supports_pred_derivs() const override { return true; }
+  void pred_derivs(std::span<const double> theta, int fold_id, std::span<double> d1,
+                   std::span<double> d2) const override {
+    test_[fold_id]->pred_derivs(theta, 0, d1, d2);
+  }
+  bool supports_pred_sample() const override { return true; }
+  void pred_sample(std::span<const double> theta, int fold_id, pcv::CounterRng& rng,
+                   std::span<double> out) const override {
+    test_[fold_id]->pred_sample(theta, 0, rng, out);
+  }
 
  private:
   std::string name_;

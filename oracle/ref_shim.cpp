@@ -235,6 +235,22 @@ double pcvref_log_pred(void* h, const double* theta, int32_t fold) {
 double pcvref_log_lik_test(void* h, const double* theta, int32_t fold) {
   return M(h).log_lik_test({theta, static_cast<size_t>(M(h).dim())}, fold);
 }
+// Model::pred_derivs / pred_sample (model.hpp:54-66); returns 0, or 1 when unsupported.
+int pcvref_pred_derivs(void* h, const double* theta, int32_t fold, double* d1, double* d2) {
+  if (!M(h).supports_pred_derivs()) return 1;
+  const size_t n = M(h).test_size(fold);
+  M(h).pred_derivs({theta, static_cast<size_t>(M(h).dim())}, fold, {d1, n}, {d2, n});
+  return 0;
+}
+int pcvref_pred_sample(void* h, const double* theta, int32_t fold, uint64_t seed, uint64_t stream,
+                       int32_t times, double* out) {
+  if (!M(h).supports_pred_sample()) return 1;
+  const size_t n = M(h).test_size(fold);
+  pcv::CounterRng rng(seed, stream);
+  for (int32_t r = 0; r < times; ++r)
+    M(h).pred_sample({theta, static_cast<size_t>(M(h).dim())}, fold, rng, {out + r * n, n});
+  return 0;
+}
 void pcvref_initial_draw(void* h, uint64_t seed, uint64_t stream, double* out) {
   pcv::CounterRng rng(seed, stream);
   const auto v = M(h).initial_draw(rng);
@@ -336,6 +352,7 @@ int pcvref_run_pcv(int32_t n_models, void** models, const int32_t* model_ids,
         rep->folds.batches[i] = fs.batches;
         rep->folds.fault[i] = fs.fault;
         rep->folds.failed[i] = fs.failed;
+        if (rep->folds.dss_ridged) rep->folds.dss_ridged[i] = fs.dss_ridged;
         for (int ch = 0; ch < L; ++ch)
           rep->divergences[(i)*L + ch] = mr.divergences[k][ch];
       }

@@ -10,7 +10,7 @@ import os
 
 import numpy as np
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, INVALID_INPUT, NUMERIC_FAULT, ADAPTATION_FAILURE, UNDEFINED_DIAGNOSTIC, \
     UNSUPPORTED_SCORE, CUDA_ERROR, COMM_ERROR = range(8)
@@ -57,7 +57,7 @@ class RunConfig(C.Structure):
 class FoldTable(C.Structure):
     _fields_ = [("estimate", P_f64), ("log_f_hat", P_f64), ("mc_contribution", P_f64),
                 ("naive_contribution", P_f64), ("ess", P_f64), ("rhat", P_f64),
-                ("batches", P_i64), ("fault", P_i32), ("failed", P_i32)]
+                ("batches", P_i64), ("fault", P_i32), ("failed", P_i32), ("dss_ridged", P_i32)]
 
 
 class Report(C.Structure):
@@ -86,7 +86,7 @@ def ptr(a, ctype):
 FOLD_COLUMNS = [("estimate", np.float64), ("log_f_hat", np.float64),
                 ("mc_contribution", np.float64), ("naive_contribution", np.float64),
                 ("ess", np.float64), ("rhat", np.float64), ("batches", np.int64),
-                ("fault", np.int32), ("failed", np.int32)]
+                ("fault", np.int32), ("failed", np.int32), ("dss_ridged", np.int32)]
 _CT = {np.float64: C.c_double, np.int64: C.c_int64, np.int32: C.c_int32}
 
 

@@ -20,7 +20,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr"]
 SOURCES = ["gauss_kernel.cu", "glm_kernel.cu", "chain_kernels.cu", "api.cpp", "stats.cpp",
            "host_folds.cpp"]
-HEADERS = ["device_common.cuh", "types.cuh", "host_common.hpp", "tc_common.cuh"]
+HEADERS = ["device_common.cuh", "types.cuh", "host_common.hpp", "tc_common.cuh", "score_extra.cuh"]
 
 
 def _newer(target, deps):

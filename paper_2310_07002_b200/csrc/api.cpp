@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -18,6 +19,7 @@
 
 #include "../../include/pcvg.h"
 #include "host_common.hpp"
+#include "score_extra.cuh"
 #include "types.cuh"
 
 namespace pcvg {
@@ -38,6 +40,8 @@ cudaError_t launch_fold_stats(const ChainsDev& S, int nfold, int64_t n, int b, i
                               cudaStream_t st);
 cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, int D, int b,
                                 cudaStream_t st);
+cudaError_t launch_extra_centers(const ChainsDev& S, int nfold, int64_t warmup, cudaStream_t st);
+cudaError_t launch_extra_merge(const ChainsDev& S, int nfold, double* merged, cudaStream_t st);
 // host_folds.cpp
 void rng_sequence(uint64_t, uint64_t, int32_t, uint64_t, const char*, const uint64_t*, int64_t, double*);
 void make_loo(int64_t, int32_t*, int32_t*);
@@ -55,6 +59,9 @@ void simulate_logistic(int64_t, int32_t, uint64_t, double*, double*);
 void merge_stats(int32_t n_models, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
                  int32_t final_checkpoint, const pcvg_fold_table* folds, const double* y_x,
                  const double* y_x2, int D_used, pcvg_report* rep);
+double hs_fold_estimate(const double* a_x, const double* center, int m, int64_t count);
+bool dss_fold_estimate(const double* merged, const double* center, const double* y_test, int m,
+                       int64_t count, double* score, int* ridged);
 
 namespace {
 
@@ -101,7 +108,8 @@ struct HostModel {
   int model_id = 0;
   bool hv = false;
   std::vector<int> perm;  // device row -> original row
-  std::vector<int> fold_seg, seg_row;
+  std::vector<int> fold_seg, seg_row, seg_rows;  // host copies of the test layout
+  std::vector<double> y_host;                    // y in device row order (test_values)
   DevBuf<double> y, x, xr, inv_mass, bank;
   DevBuf<int> key, grp_ptr, lo, hi, ntrain, fseg, sgroup, sunseen, srow, srows;
   int64_t bank_rows = 0;
@@ -119,6 +127,13 @@ struct ChainSet {
   DevBuf<double> u_x, u_x2, z_x, v_x, v_x2, center, y_x, y_x2;
   DevBuf<int64_t> committed, count, faults;
   DevBuf<int32_t> pending;
+  // HS / DSS state (ExtraDev, types.cuh)
+  int xkind = 0;
+  std::vector<int> xm;
+  std::vector<int64_t> xbase_h, xwbase_h, xcbase_h;
+  DevBuf<int> xmsize;
+  DevBuf<int64_t> xbase, xwbase, xcbase;
+  DevBuf<double> xacc, xwarm, xdev, xcenter;
 
   void alloc(int n, int d, int blocks) {
     nch = n;
@@ -168,6 +183,7 @@ struct ChainSet {
     s.divergences = div.p;
     s.warm_sum = warm.p;
     s.acc = AccumDev{u_x.p, u_x2.p, z_x.p, v_x.p, v_x2.p, committed.p, pending.p, count.p, faults.p, center.p, y_x.p, y_x2.p};
+    s.X = ExtraDev{xkind, xmsize.p, xbase.p, xwbase.p, xcbase.p, xacc.p, xwarm.p, xdev.p, xcenter.p};
     return s;
   }
 };
@@ -432,6 +448,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
       m.seg_row.push_back(static_cast<int>(seg_rows.size()));
     }
   }
+  m.seg_rows = seg_rows;
+  m.y_host.assign(y.begin(), y.begin() + n);
   m.fold_seg[m.K] = static_cast<int>(seg_group.size());
   m.fold_seg[m.K + 1] = static_cast<int>(seg_group.size());
   m.fseg.upload(m.fold_seg);
@@ -541,15 +559,92 @@ void validate_run(const pcvg_ctx* ctx, const pcvg_run_config* c) {
   const int K = ctx->models[0]->K;
   for (const auto& m : ctx->models)
     if (m->K != K) throw Error(PCVG_INVALID_INPUT, "models must share one fold assignment");
-  if (c->score == PCVG_SCORE_HS || c->score == PCVG_SCORE_DSS)
-    throw Error(PCVG_UNSUPPORTED_SCORE, "score hs/dss is not yet implemented on device (LogS only)");
-  if (c->score != PCVG_SCORE_LOGS) throw Error(PCVG_INVALID_INPUT, "unknown score");
+  if (c->score != PCVG_SCORE_LOGS && c->score != PCVG_SCORE_HS && c->score != PCVG_SCORE_DSS)
+    throw Error(PCVG_INVALID_INPUT, "unknown score");
+  // Model::check_score_support (model.cpp:21-28): the Gaussian families implement pred_derivs /
+  // pred_sample; the logistic family (binary outcome) implements neither.
+  for (const auto& m : ctx->models)
+    if (c->score != PCVG_SCORE_LOGS && m->family == PCVG_FAMILY_LOGISTIC)
+      throw Error(PCVG_UNSUPPORTED_SCORE, std::string("model does not support score ") +
+                                              (c->score == PCVG_SCORE_HS ? "hs" : "dss"));
   if (K < 2) throw Error(PCVG_INVALID_INPUT, "uncertainty estimates need at least 2 folds");
   if (c->fold_begin < 0 || c->fold_end < c->fold_begin || c->fold_end > K)
     throw Error(PCVG_INVALID_INPUT, "bad fold shard");
   if (c->early_stop) {
     if (c->checkpoint_every <= 0 || c->iters % c->checkpoint_every != 0)
       throw Error(PCVG_INVALID_INPUT, "early_stop needs checkpoint_every dividing iters");
+  }
+}
+
+int test_size_of(const HostModel& m, int fold) {
+  return fold >= m.K ? 0 : m.seg_row[m.fold_seg[fold + 1]] - m.seg_row[m.fold_seg[fold]];
+}
+
+// HS / DSS state of a shard (ExtraDev layout, types.cuh): per local fold the test size, the
+// accumulator / warm-up / centre bases; accumulators and warm-up sums start at zero.
+void alloc_extra(ChainSet& cs, const HostModel& m, int kind, int fb, int nfold, int L) {
+  cs.xkind = kind;
+  cs.xm.resize(nfold);
+  cs.xbase_h.resize(nfold);
+  cs.xwbase_h.resize(nfold);
+  cs.xcbase_h.resize(nfold);
+  int64_t ab = 0, wb = 0, cb = 0;
+  for (int k = 0; k < nfold; ++k) {
+    const int mk = test_size_of(m, fb + k);
+    cs.xm[k] = mk;
+    cs.xbase_h[k] = ab;
+    cs.xwbase_h[k] = wb;
+    cs.xcbase_h[k] = cb;
+    ab += L * extra_acc_len(kind, mk);
+    wb += L * extra_warm_len(kind, mk);
+    cb += extra_warm_len(kind, mk);
+  }
+  cs.xmsize.upload(cs.xm);
+  cs.xbase.upload(cs.xbase_h);
+  cs.xwbase.upload(cs.xwbase_h);
+  cs.xcbase.upload(cs.xcbase_h);
+  cs.xacc.alloc(std::max<int64_t>(ab, 1));
+  cs.xwarm.alloc(std::max<int64_t>(wb, 1));
+  cs.xdev.alloc(std::max<int64_t>(wb, 1));
+  cs.xcenter.alloc(std::max<int64_t>(cb, 1));
+  ck(cudaMemset(cs.xacc.p, 0, sizeof(double) * cs.xacc.n), "memset");
+  ck(cudaMemset(cs.xwarm.p, 0, sizeof(double) * cs.xwarm.n), "memset");
+}
+
+// Per-fold HS / DSS estimates of a shard at `iters` sampling iterations (engine.cpp:148-171):
+// chain merge on device, scores on the host. Overwrites estimate, ORs DSS failures into fault.
+void extra_estimates(pcvg_ctx* ctx, const HostModel& m, const ChainSet& cs, int fb, int nfold,
+                     int L, int64_t iters, double* estimate, int32_t* fault, int32_t* ridged) {
+  const ChainsDev S = cs.view(L, fb, 0, 0);
+  DevBuf<double> merged;
+  merged.alloc(std::max<int64_t>(cs.xacc.n / L, 1));
+  ck(launch_extra_merge(S, nfold, merged.p, ctx->stream), "extra merge");
+  ++ctx->launches;
+  const auto mg = merged.download(ctx->stream);
+  const auto cen = cs.xcenter.download(ctx->stream);
+  const int64_t count = iters * L;
+  std::vector<double> yt;
+  for (int k = 0; k < nfold; ++k) {
+    const int mk = cs.xm[k];
+    const double* a = mg.data() + cs.xbase_h[k] / L;
+    const double* c = cen.data() + cs.xcbase_h[k];
+    int rg = 0;
+    if (cs.xkind == PCVG_SCORE_HS) {
+      estimate[k] = hs_fold_estimate(a, c, mk, count);
+    } else {
+      const int fold = fb + k;
+      yt.clear();  // Model::test_values (fold_meta order)
+      for (int t = m.seg_row[m.fold_seg[fold]]; t < m.seg_row[m.fold_seg[fold + 1]]; ++t)
+        yt.push_back(m.y_host[m.seg_rows[t]]);
+      double sc;
+      if (dss_fold_estimate(a, c, yt.data(), mk, count, &sc, &rg)) {
+        estimate[k] = sc;
+      } else {
+        estimate[k] = std::numeric_limits<double>::quiet_NaN();
+        fault[k] = 1;
+      }
+    }
+    if (ridged) ridged[k] = rg;
   }
 }
 
@@ -901,6 +996,7 @@ pcvg_status pcvg_begin(pcvg_ctx* ctx, const pcvg_run_config* cfg) {
       cudaStream_t st = mi == 0 ? ctx->stream : ctx->stream2;
       auto cs = std::make_unique<ChainSet>();
       cs->alloc(nfold * L, m.dim, D);
+      if (cfg->score != PCVG_SCORE_LOGS) alloc_extra(*cs, m, cfg->score, ctx->fb, nfold, L);
       const uint64_t sm = cfg->shared_streams ? 0u : static_cast<uint64_t>(m.model_id);
       const ChainsDev S = cs->view(L, ctx->fb, cfg->seed, sm);
       ck(launch_init_chains(m.md, S, m.bank.p, m.bank_rows, st), "init_chains");
@@ -914,6 +1010,10 @@ pcvg_status pcvg_begin(pcvg_ctx* ctx, const pcvg_run_config* cfg) {
       centers->alloc(std::max(nfold, 1));
       ck(launch_centers(S, nfold, cfg->warmup, centers->p, D, st), "centers");
       ctx->launches += 2;
+      if (cfg->score != PCVG_SCORE_LOGS) {
+        ck(launch_extra_centers(S, nfold, cfg->warmup, st), "extra centers");
+        ++ctx->launches;
+      }
       ctx->chains.push_back(std::move(cs));
       ctx->centers.push_back(std::move(centers));
     }
@@ -987,15 +1087,22 @@ pcvg_status pcvg_fold_stats(pcvg_ctx* ctx, pcvg_fold_table* out, int64_t* diverg
       const auto b = bt.download(ctx->stream);
       const auto f = ft.download(ctx->stream);
       const size_t off = static_cast<size_t>(mi) * nfold;
+      std::vector<double> ee = e;
+      std::vector<int32_t> fx = f;
+      std::vector<int32_t> rg(nfold, 0);
+      if (cfg.score != PCVG_SCORE_LOGS)
+        extra_estimates(ctx, *ctx->models[mi], cs, ctx->fb, nfold, L, ctx->iters_done, ee.data(),
+                        fx.data(), rg.data());
       for (int k = 0; k < nfold; ++k) {
-        if (out->estimate) out->estimate[off + k] = e[k];
+        if (out->dss_ridged) out->dss_ridged[off + k] = rg[k];
+        if (out->estimate) out->estimate[off + k] = ee[k];
         if (out->log_f_hat) out->log_f_hat[off + k] = l[k];
         if (out->mc_contribution) out->mc_contribution[off + k] = c[k];
         if (out->naive_contribution) out->naive_contribution[off + k] = v[k];
         if (out->ess) out->ess[off + k] = s[k];
         if (out->rhat) out->rhat[off + k] = r[k];
         if (out->batches) out->batches[off + k] = b[k];
-        if (out->fault) out->fault[off + k] = f[k];
+        if (out->fault) out->fault[off + k] = fx[k];
       }
       const auto dv = cs.div.download(ctx->stream);
       sdiv[mi].resize(dv.size());
@@ -1078,8 +1185,8 @@ pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
     const size_t rows = static_cast<size_t>(nm) * K;
     std::vector<double> est(rows), lf(rows), mc(rows), nv(rows), ess(rows), rh(rows);
     std::vector<int64_t> bt(rows);
-    std::vector<int32_t> ft(rows), fl(rows);
-    pcvg_fold_table tab{est.data(), lf.data(), mc.data(), nv.data(), ess.data(), rh.data(), bt.data(), ft.data(), fl.data()};
+    std::vector<int32_t> ft(rows), fl(rows), rg(rows);
+    pcvg_fold_table tab{est.data(), lf.data(), mc.data(), nv.data(), ess.data(), rh.data(), bt.data(), ft.data(), fl.data(), rg.data()};
     std::vector<double> yx(rows * L * D), yx2(rows * L * D);
     int64_t dropped = 0, done = 0;
     std::vector<int64_t> divs(rows * L);
@@ -1138,6 +1245,7 @@ pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
       rep->folds.rhat[i] = rh[i];
       rep->folds.batches[i] = bt[i];
       rep->folds.fault[i] = ft[i];
+      if (rep->folds.dss_ridged) rep->folds.dss_ridged[i] = rg[i];
     }
     // failed flags after exclusions are written by merge_stats into rep->folds.failed
     std::copy(divs.begin(), divs.end(), rep->divergences);

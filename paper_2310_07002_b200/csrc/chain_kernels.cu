@@ -7,9 +7,14 @@
 //  * fold_stats    - LogS fold score + R-hat of each fold from its L chain accumulators
 //                    (scoring.cpp:10-62, diagnostics.cpp:11-44), same operation order as the
 //                    reference; one thread per fold.
+//  * extra_centers - HS / DSS centring vectors hs_c / pred_c = sum_c warm_c / (L N_wu) in chain
+//                    order (engine.cpp:324-338); one block per fold.
+//  * extra_merge   - per-fold WelfordDiag / WelfordAccumulator::merge over the L chains in chain
+//                    order (engine.cpp:150-156, accum.cpp:28-34, 76-84); one block per fold.
 #include <math_constants.h>
 
 #include "device_common.cuh"
+#include "score_extra.cuh"
 #include "types.cuh"
 
 namespace pcvg {
@@ -168,7 +173,46 @@ __global__ void feed_streams_kernel(ChainsDev S, const double* s, int64_t n, int
   for (int64_t i = 0; i < n; ++i) accum_observe(S.acc, c, S.nch, s[c * n + i], i, n, D, b);
 }
 
+__global__ void extra_centers_kernel(ExtraDev X, int L, int nfold, int64_t warmup) {
+  const int k = blockIdx.x;
+  if (k >= nfold) return;
+  const int64_t len = extra_warm_len(X.kind, X.msize[k]);
+  const double denom = static_cast<double>(L) * static_cast<double>(warmup);
+  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+    double c = 0.0;
+    if (warmup > 0)
+      for (int ch = 0; ch < L; ++ch) c += X.warm[X.wbase[k] + e * L + ch] / denom;
+    X.center[X.cbase[k] + e] = c;
+  }
+}
+
+// merged[base[k] / L + e] = sum over chains (in order) of entry e.
+__global__ void extra_merge_kernel(ExtraDev X, int L, int nfold, double* merged) {
+  const int k = blockIdx.x;
+  if (k >= nfold) return;
+  const int64_t len = extra_acc_len(X.kind, X.msize[k]);
+  const double* A = X.acc + X.base[k];
+  double* out = merged + X.base[k] / L;
+  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+    double s = A[e * L];
+    for (int ch = 1; ch < L; ++ch) s += A[e * L + ch];
+    out[e] = s;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_extra_centers(const ChainsDev& S, int nfold, int64_t warmup, cudaStream_t st) {
+  if (nfold == 0 || S.X.kind == 0) return cudaSuccess;
+  extra_centers_kernel<<<nfold, 64, 0, st>>>(S.X, S.L, nfold, warmup);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_extra_merge(const ChainsDev& S, int nfold, double* merged, cudaStream_t st) {
+  if (nfold == 0 || S.X.kind == 0) return cudaSuccess;
+  extra_merge_kernel<<<nfold, 128, 0, st>>>(S.X, S.L, nfold, merged);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, int D, int b,
                                 cudaStream_t st) {

@@ -17,6 +17,7 @@
 #include <math_constants.h>
 
 #include "device_common.cuh"
+#include "score_extra.cuh"
 #include "types.cuh"
 
 namespace pcvg {
@@ -394,6 +395,64 @@ __device__ double log_pred(const ModelDev& M, const ChainsDev& S, int c, int t, 
   return lp;
 }
 
+// HS / DSS state after hmc_step + log_pred (engine.cpp:360-373; warm-up hmc.cpp:133-145):
+// pred_derivs / pred_sample of grouped_regression.cpp:190-213, radon.cpp:167-199 and
+// seasonal_ar.cpp:133-150 over the fold's test rows in fold_meta order. The lanes of the chain
+// split the rows; DSS draws come from the chain stream in row order on every lane (so all lanes
+// keep identical stream state), the lane owning row t uses normal t.
+template <int FAM, int T, int NCM, int NGM>
+__device__ void score_extra(const ModelDev& M, const ChainsDev& S, int c, int t, unsigned mask,
+                            int fold, int cur, const double* qG, bool warm, ChainRng& R) {
+  const ExtraDev& X = S.X;
+  const int L = S.L, kf = fold - S.fold0, cl = c % L;
+  Prep<NCM> P;
+  prepare<FAM, NCM, NGM>(M, qG, P);
+  double vy, sy, sa = 0.0;
+  if constexpr (FAM == kGrouped) {
+    sy = exp(qG[2]);  // sig_y
+    vy = sy * sy;
+  } else if constexpr (FAM == kRadon) {
+    vy = exp(qG[3]);
+    sy = exp(0.5 * qG[3]);
+    sa = exp(0.5 * qG[2]);
+  } else {
+    vy = exp(2.0 * qG[1]);
+    sy = exp(qG[1]);
+  }
+  const size_t plane = static_cast<size_t>(M.dim) * S.nch;
+  const int s0 = __ldg(M.fold_seg + fold), s1 = __ldg(M.fold_seg + fold + 1);
+  int rt = 0;
+  for (int s = s0; s < s1; ++s) {
+    const int r0 = __ldg(M.seg_row + s), r1 = __ldg(M.seg_row + s + 1);
+    double qg = 0.0;
+    if constexpr (FAM != kSeasonal) qg = S.pos[cur * plane + static_cast<size_t>(__ldg(M.seg_group + s)) * S.nch + c];
+    for (int tt = r0; tt < r1; ++tt, ++rt) {
+      const double z = X.kind == 2 ? R.normal() : 0.0;
+      if (rt % T != t) continue;
+      const int i = __ldg(M.seg_rows + tt);
+      double mean;
+      if constexpr (FAM == kRadon) {
+        mean = qG[1] + sa * qg + (M.include_floor ? 1.0 : 0.0) * qG[0] * __ldg(M.x + i);
+      } else {
+        mean = FAM == kGrouped ? qg : P.off0;
+#pragma unroll
+        for (int k = 0; k < NCM; ++k)
+          if (k < M.nc) mean = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), mean);
+      }
+      if (X.kind == 1) {
+        const double d1 = -(__ldg(M.y + i) - mean) / vy;
+        extra_hs_row(X, kf, cl, L, rt, d1, -1.0 / vy, warm);
+      } else {
+        extra_dss_row(X, kf, cl, L, rt, mean + sy * z, warm);
+      }
+    }
+  }
+  if (X.kind == 2 && !warm) {
+    __syncwarp(mask);  // staged deviations of every lane's rows
+    extra_dss_cov(X, kf, cl, L, t, T);
+  }
+}
+
 template <int FAM, int T, int NCM, int NGM>
 __global__ void __launch_bounds__(kBlock) gauss_kernel(ModelDev M, ChainsDev S, RunArgs A) {
   constexpr int kChains = kBlock / T;
@@ -544,6 +603,8 @@ __global__ void __launch_bounds__(kBlock) gauss_kernel(ModelDev M, ChainsDev S, 
 #pragma unroll
     for (int i = 0; i < NGM; ++i) qG[i] = i < ng ? S.pos[gaddr(cur, i)] : 0.0;
     const double sp = log_pred<FAM, T, NCM, NGM>(M, S, c, t, mask, fold, cur, qG);
+    if (S.X.kind != 0 && fold < M.K)
+      score_extra<FAM, T, NCM, NGM>(M, S, c, t, mask, fold, cur, qG, A.mode == kModeWarmup, R);
     if (A.mode == kModeWarmup) {
       warm += sp;
     } else if (t == 0) {

@@ -23,6 +23,7 @@
 #include <math_constants.h>
 
 #include "device_common.cuh"
+#include "score_extra.cuh"
 #include "tc_common.cuh"
 #include "types.cuh"
 
@@ -370,6 +371,44 @@ __device__ __forceinline__ double bernoulli_logit(double y, double x) {
   return y * x - (fmax(x, 0.0) + log1p(exp(-fabs(x))));
 }
 
+// HS / DSS state of one chain after hmc_step + log_pred (engine.cpp:360-373; warm-up
+// hmc.cpp:133-145), run by the chain thread over the fold's test rows in order: pred_derivs /
+// pred_sample of grouped_regression.cpp:190-213 (J = 1) and seasonal_ar.cpp:133-150. Every rank
+// of a cluster draws the DSS normals (identical stream state); only the writer rank stores.
+template <int FAM, int KP>
+__device__ void glm_score_extra(const ModelDev& M, const ChainsDev& S, int gc, int fold,
+                                const double* pos, bool warm, bool writer, ChainRng& R) {
+  const ExtraDev& X = S.X;
+  const int nch = S.nch, L = S.L, kf = fold - S.fold0, cl = gc % L;
+  double vy, sy;
+  if constexpr (FAM == kGrouped) {
+    sy = exp(pos[static_cast<size_t>(M.nc + 3) * nch]);
+    vy = sy * sy;
+  } else {
+    const double u = pos[static_cast<size_t>(M.p + M.q + 1) * nch];
+    vy = exp(2.0 * u);
+    sy = exp(u);
+  }
+  const int s0 = M.fold_seg[fold], s1 = M.fold_seg[fold + 1];
+  int rt = 0;
+  for (int s = s0; s < s1; ++s) {
+    for (int tt = M.seg_row[s]; tt < M.seg_row[s + 1]; ++tt, ++rt) {
+      const double z = X.kind == 2 ? R.normal() : 0.0;
+      if (!writer) continue;
+      const int i = M.seg_rows[tt];
+      const double* xrow = M.xr + static_cast<size_t>(i) * KP;
+      double mean = 0.0;
+      for (int k = 0; k < M.dim; ++k) {
+        const int col = col_of<FAM>(M, k);
+        if (col >= 0) mean = fma(xrow[col], w_of<FAM>(M, k, pos[static_cast<size_t>(k) * nch]), mean);
+      }
+      if (X.kind == 1) extra_hs_row(X, kf, cl, L, rt, -(M.y[i] - mean) / vy, -1.0 / vy, warm);
+      else extra_dss_row(X, kf, cl, L, rt, mean + sy * z, warm);
+    }
+  }
+  if (X.kind == 2 && !warm && writer) extra_dss_cov(X, kf, cl, L, 0, 1);
+}
+
 template <int FAM, int KP>
 __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs) {
   using G = Geom<KP>;
@@ -644,6 +683,11 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
       } else {
         accum_observe(S.acc, gc, nch, sp, A.iter0 + it, A.planned_n, A.D, A.b);
       }
+    }
+    if constexpr (FAM != kLogistic) {
+      if (cvalid && S.X.kind != 0 && fold < M.K && A.mode != kModePred)
+        glm_score_extra<FAM, KP>(M, S, gc, fold, S.pos + sm.cur[tid] * plane + gc,
+                                 A.mode == kModeWarmup, writer, R);
     }
     if (A.mode == kModePred) break;
   }

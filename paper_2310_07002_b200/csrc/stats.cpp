@@ -36,7 +36,82 @@ bool rhat_from_sums(const double* sx, const double* sxx, int l, int64_t n, doubl
   return true;
 }
 
+// Cholesky helpers, math.hpp:46-76 (row-major n x n, lower factor in place).
+bool cholesky_in_place(std::vector<double>& a, int n) {
+  for (int j = 0; j < n; ++j) {
+    double d = a[j * n + j];
+    for (int k = 0; k < j; ++k) d -= a[j * n + k] * a[j * n + k];
+    if (!(d > 0.0) || !std::isfinite(d)) return false;
+    const double l = std::sqrt(d);
+    a[j * n + j] = l;
+    for (int i = j + 1; i < n; ++i) {
+      double s = a[i * n + j];
+      for (int k = 0; k < j; ++k) s -= a[i * n + k] * a[j * n + k];
+      a[i * n + j] = s / l;
+    }
+  }
+  return true;
+}
+
 }  // namespace
+
+// hs_fold_score (scoring.cpp:64-73) on the chain-merged WelfordDiag of xi = (d2 + d1^2, d1):
+// mu = a_x / count + c; the report carries the negation (engine.cpp:157-158).
+double hs_fold_estimate(const double* a_x, const double* center, int m, int64_t count) {
+  double score = 0.0;
+  for (int i = 0; i < m; ++i) {
+    const double mu1 = a_x[i] / static_cast<double>(count) + center[i];
+    const double mu2 = a_x[m + i] / static_cast<double>(count) + center[m + i];
+    score += 2.0 * mu1 - mu2 * mu2;
+  }
+  return -score;
+}
+
+// dss_fold_score (scoring.cpp:75-104) on the chain-merged WelfordAccumulator (a_x[m], packed lower
+// triangle a_xx): mean / covariance as WelfordAccumulator::mean/covariance (accum.cpp:36-57), a
+// ridge of 1e-8 tr/m on a failed factorisation. Returns false where the reference throws
+// (too few draws, singular covariance): the fold becomes NaN + fault (engine.cpp:162-170).
+bool dss_fold_estimate(const double* merged, const double* center, const double* y_test, int m,
+                       int64_t count, double* score, int* ridged) {
+  *ridged = 0;
+  if (count < m + 1) return false;
+  if (count < 2) return false;
+  const double* a_x = merged;
+  const double* a_xx = merged + m;
+  std::vector<double> mu(m), cov(static_cast<size_t>(m) * m);
+  for (int i = 0; i < m; ++i) mu[i] = a_x[i] / count + center[i];
+  const double inv_n = 1.0 / static_cast<double>(count);
+  const double inv_nm1 = 1.0 / static_cast<double>(count - 1);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j <= i; ++j) {
+      const double v = (a_xx[static_cast<int64_t>(i) * (i + 1) / 2 + j] - a_x[i] * a_x[j] * inv_n) * inv_nm1;
+      cov[i * m + j] = v;
+      cov[j * m + i] = v;
+    }
+  std::vector<double> factor = cov;
+  if (!cholesky_in_place(factor, m)) {
+    double tr = 0.0;
+    for (int i = 0; i < m; ++i) tr += cov[i * m + i];
+    const double ridge = 1e-8 * tr / m;
+    for (int i = 0; i < m; ++i) cov[i * m + i] += ridge;
+    factor = cov;
+    *ridged = 1;
+    if (!cholesky_in_place(factor, m)) return false;
+  }
+  std::vector<double> r(m);
+  for (int i = 0; i < m; ++i) r[i] = y_test[i] - mu[i];
+  for (int i = 0; i < m; ++i) {  // forward_solve, math.hpp:63-70
+    double s = r[i];
+    for (int k = 0; k < i; ++k) s -= factor[i * m + k] * r[k];
+    r[i] = s / factor[i * m + i];
+  }
+  double quad = 0.0;
+  for (int i = 0; i < m; ++i) quad += r[i] * r[i];
+  double ld = 0.0;  // chol_logdet, math.hpp:72-76
+  for (int i = 0; i < m; ++i) ld += std::log(factor[i * m + i]);
+  *score = -(2.0 * ld) - quad;
+  return true;
+}
 
 // final_checkpoint: 0 = intermediate snapshot (no exclusions), 1 = final (exclusions, per-model
 // report, benchmark + verdict), 2 = early-stop probe (no exclusions, benchmark + verdict on the
@@ -97,7 +172,8 @@ void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter
     rep->sigma2_delta = rep->epistemic_se = rep->prob_a_better = kNaN;
   }
   const double ln = static_cast<double>(l) * iter_count;
-  rep->mcse = mc_inf ? kInf : std::sqrt(mc_sum / ln);
+  // MCSE is defined for LogS only (engine.cpp:229-235)
+  rep->mcse = cfg->score != PCVG_SCORE_LOGS ? kNaN : (mc_inf ? kInf : std::sqrt(mc_sum / ln));
   rep->ess_overall = mc_sum > 0.0 ? static_cast<double>(l) * iter_count * naive_sum / mc_sum : kNaN;
   rep->rhat_max = best < 0.0 ? kNaN : best;
 

@@ -56,6 +56,26 @@ struct ModelDev {
   double c_log4;           // log(4)
 };
 
+// HS / DSS score state (ScoreKind::HS / DSS, engine.cpp:322-373; accum.cpp:10-99). Per local fold
+// kf with test size m = msize[kf], the L chains of the fold are interleaved entry-major: entry e of
+// chain cl sits at base[kf] + e * L + cl (one 8*L-byte segment per entry).
+//   HS : acc  e in [0,2m) WelfordDiag a_x of xi = (d2 + d1^2, d1), [2m,4m) a_x2
+//        warm [0,m) hs1_sum, [m,2m) hs2_sum (WarmupStats, hmc.cpp:133-140); centre 2m per fold
+//   DSS: acc  [0,m) WelfordAccumulator a_x, then the packed lower triangle a_xx (row i: i+1 entries)
+//        warm [0,m) pred_sum; dev [0,m) staging of x - c for the triangle update; centre m per fold
+// The observation count is the ScoreAccum count (both advance once per sampling iteration).
+struct ExtraDev {
+  int kind;              // pcvg_score: 0 = LogS (no extra state), 1 = HS, 2 = DSS
+  const int* msize;      // [nfold] test size
+  const int64_t* base;   // [nfold] accumulator base
+  const int64_t* wbase;  // [nfold] warm-up sum / staging base
+  const int64_t* cbase;  // [nfold] centre base
+  double* acc;
+  double* warm;
+  double* dev;
+  double* center;
+};
+
 struct ChainsDev {
   int nch;        // chains on this device (task order restricted to the shard)
   int L;          // chains per fold
@@ -75,6 +95,7 @@ struct ChainsDev {
   int64_t* divergences;  // cumulative (warm-up + sampling), hmc.hpp:20-24
   double* warm_sum;      // WarmupStats::logpred_sum
   AccumDev acc;
+  ExtraDev X;
 };
 
 struct RunArgs {

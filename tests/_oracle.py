@@ -60,6 +60,9 @@ def oracle():
         _sig(lib, "pcvo_time_tasks", C.c_int, [vp, i32, pi32, i32, i64, i64, u64, i32, P(abi.Kernel), pf64,
                                                 i64, i32, pf64, pf64, pf64])
         _sig(lib, "pcvo_score_streams", C.c_int, [i32, i64, pf64, f64, i32, i32, pf64])
+        _sig(lib, "pcvo_supports_pred", C.c_int, [vp])
+        _sig(lib, "pcvo_pred_derivs", None, [vp, pf64, i32, pf64, pf64])
+        _sig(lib, "pcvo_pred_sample_stream", C.c_int, [vp, pf64, i32, u64, u64, i32, pf64])
         _sig(lib, "pcvo_last_error", C.c_char_p, [])
         _oracle = lib
     return _oracle
@@ -92,6 +95,8 @@ def ref():
         _sig(lib, "pcvref_log_pred", f64, [vp, pf64, i32])
         _sig(lib, "pcvref_log_lik_test", f64, [vp, pf64, i32])
         _sig(lib, "pcvref_initial_draw", None, [vp, u64, u64, pf64])
+        _sig(lib, "pcvref_pred_derivs", C.c_int, [vp, pf64, i32, pf64, pf64])
+        _sig(lib, "pcvref_pred_sample", C.c_int, [vp, pf64, i32, u64, u64, i32, pf64])
         _sig(lib, "pcvref_leapfrog", i32, [vp, i32, f64, i32, pf64, pf64, pf64])
         _sig(lib, "pcvref_hmc_chain", C.c_int, [vp, i32, f64, i32, pf64, u64, u64, pf64, i64, pf64,
                                                  pi32, pi32, pf64])
@@ -141,6 +146,21 @@ class OModel:
 
     def test_size(self, fold):
         return self.lib.pcvo_test_size(self.h, fold)
+
+    def pred_derivs(self, th, fold):
+        th = np.ascontiguousarray(th, dtype=np.float64)
+        n = self.test_size(fold)
+        d1, d2 = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        self.lib.pcvo_pred_derivs(self.h, _p(th), fold, _p(d1), _p(d2))
+        return d1[:n], d2[:n]
+
+    def pred_sample(self, th, fold, seed, stream, times=1):
+        th = np.ascontiguousarray(th, dtype=np.float64)
+        n = self.test_size(fold)
+        out = np.zeros(max(n * times, 1))
+        rc = self.lib.pcvo_pred_sample_stream(self.h, _p(th), fold, seed, stream, times, _p(out))
+        assert rc == 0
+        return out[:n * times].reshape(times, n)
 
     def leapfrog(self, fold, step, n_lf, inv_mass, q, p):
         q = np.array(q, dtype=np.float64)
@@ -206,6 +226,20 @@ class RModel:
 
     def test_size(self, fold):
         return self.lib.pcvref_test_size(self.h, fold)
+
+    def pred_derivs(self, th, fold):
+        th = np.ascontiguousarray(th, dtype=np.float64)
+        n = self.test_size(fold)
+        d1, d2 = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        assert self.lib.pcvref_pred_derivs(self.h, _p(th), fold, _p(d1), _p(d2)) == 0
+        return d1[:n], d2[:n]
+
+    def pred_sample(self, th, fold, seed, stream, times=1):
+        th = np.ascontiguousarray(th, dtype=np.float64)
+        n = self.test_size(fold)
+        out = np.zeros(max(n * times, 1))
+        assert self.lib.pcvref_pred_sample(self.h, _p(th), fold, seed, stream, times, _p(out)) == 0
+        return out[:n * times].reshape(times, n)
 
     def initial_draw(self, seed, stream):
         out = np.zeros(self.dim)

@@ -212,8 +212,50 @@ def load(name):
     return d, f, models, z
 
 
+# HS / DSS reference reports (engine.cpp:322-373, scoring.cpp:64-104) on the inputs of a base
+# fixture: tests/golden/<base>_<hs|dss>.npz holds only the reference report for that score.
+SCORE_FIXTURES = {
+    "cfg1_linreg_loo": (abi.SCORE_HS, abi.SCORE_DSS),
+    "ex1_grouped_logo": (abi.SCORE_HS, abi.SCORE_DSS),
+    "radon_logo": (abi.SCORE_HS, abi.SCORE_DSS),
+    "seasonal_timeblocks": (abi.SCORE_HS, abi.SCORE_DSS),
+    "seasonal_hvblock": (abi.SCORE_HS, abi.SCORE_DSS),
+}
+SCORE_NAME = {abi.SCORE_HS: "hs", abi.SCORE_DSS: "dss"}
+
+
+def score_run_config(z, score):
+    rc = z["run_cfg"]
+    return abi.run_config(chains=int(rc[0]), iters=int(rc[1]), warmup=int(rc[2]), batch_size=int(rc[3]),
+                          blocks=int(rc[4]), bench_draws=int(rc[5]), checkpoint_every=int(rc[6]), seed=1,
+                          score=score)
+
+
+def make_score(base, score):
+    d, f, models, z = load(base)
+    fa = f.arrays()
+    rmodels = [O.RModel(d, fa, abi.SpecArrays(**kw)) for kw, _, _ in models]
+    kernels = [abi.KernelArrays(kp.step_size, kp.n_leapfrog, kp.inv_mass_diag) for _, kp, _ in models]
+    cfg = score_run_config(z, score)
+    rep = O.run_pcv_ref(rmodels, list(range(len(models))), kernels, [b for _, _, b in models], cfg, threads=0)
+    out = {"score": np.int64(score)}
+    for k in ("delta_hat", "mcse", "sigma2_delta", "epistemic_se", "prob_a_better", "ess_overall",
+              "rhat_max", "dropped_batch_draws", "verdict_pass", "verdict_quantile_value"):
+        out[f"ref_{k}"] = np.float64(rep[k])
+    for k in ("estimate", "log_f_hat", "mc_contribution", "ess", "rhat", "batches", "fault",
+              "failed", "dss_ridged", "divergences", "delta_k", "snapshots", "benchmark"):
+        out[f"ref_{k}"] = rep[k]
+    out["ref_score_total"] = np.array(rep["score_total"])
+    np.savez_compressed(os.path.join(HERE, f"{base}_{SCORE_NAME[score]}.npz"), **out)
+
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(CONFIGS)
+    names = sys.argv[1:] or list(CONFIGS) + ["scores"]
     for nm in names:
         print(nm, flush=True)
-        make(nm)
+        if nm == "scores":
+            for base, scores in SCORE_FIXTURES.items():
+                for sc in scores:
+                    make_score(base, sc)
+        else:
+            make(nm)

@@ -74,8 +74,8 @@ def test_run_config_validation():  # RunConfig::validate, engine.cpp:21-30; run_
         base.update(kw)
         with pytest.raises(pcv.InvalidInput):
             c.run(abi.run_config(**base))
-    with pytest.raises(pcv.UnsupportedScore):
-        c.run(abi.run_config(chains=4, iters=100, warmup=10, batch_size=10, score=abi.SCORE_HS))
+    with pytest.raises(pcv.InvalidInput):
+        c.run(abi.run_config(chains=4, iters=100, warmup=10, batch_size=10, score=7))
     c.close()
 
 

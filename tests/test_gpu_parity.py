@@ -157,3 +157,63 @@ def test_run_pcv_within_mcse(ctx, name):
     est, oest = rep["estimate"], orep["estimate"]
     assert est.shape == oest.shape
     c.close()
+
+
+SCORE_BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock"]
+
+
+def _score_cfg(case, score, iters=None, warmup=None, seed=1):
+    rc = case.z["run_cfg"]
+    return abi.run_config(chains=int(rc[0]), iters=int(iters or rc[1]), warmup=int(rc[2] if warmup is None else warmup),
+                          batch_size=int(rc[3]) if iters is None else 5, blocks=int(rc[4]),
+                          bench_draws=int(rc[5]), checkpoint_every=int(rc[6]) if iters is None else 0,
+                          seed=seed, score=score)
+
+
+@pytest.mark.parametrize("name", with_kernels(SCORE_BASES))
+@pytest.mark.parametrize("score", [abi.SCORE_HS, abi.SCORE_DSS])
+def test_score_short_horizon_matches_oracle(ctx, name, score):
+    """HS / DSS state on device (pred_derivs / pred_sample after every hmc_step, warm-up centring,
+    chain merge, hs/dss fold scores) vs the oracle on the same streams over a horizon short enough
+    that the chains have not decorrelated: per-fold estimates agree to ~1e-9."""
+    case, c, slots = case_in(ctx, name)
+    cfg = _score_cfg(case, score, iters=20, warmup=4)
+    rep = c.run(cfg)
+    orep = O.run_pcv_oracle(case.omodels, list(range(len(case.omodels))),
+                            [abi.KernelArrays(k.step_size, k.n_leapfrog, k.inv_mass_diag) for k in case.kparams],
+                            case.banks, cfg)
+    est, oest = rep["estimate"], orep["estimate"]
+    np.testing.assert_array_equal(np.isnan(est), np.isnan(oest))
+    np.testing.assert_array_equal(rep["fault"], orep["fault"])
+    ok = np.isfinite(oest)
+    rel = np.abs(est[ok] - oest[ok]) / (1.0 + np.abs(oest[ok]))
+    assert np.mean(rel <= 1e-8) >= 0.9, (name, np.sort(rel)[-5:])
+    assert np.isnan(rep["mcse"])
+    c.close()
+
+
+@pytest.mark.parametrize("name", SCORE_BASES)
+@pytest.mark.parametrize("score", [abi.SCORE_HS, abi.SCORE_DSS])
+def test_score_run_within_mc_error_of_reference(ctx, name, score):
+    """Full fixture run (N = 100-200) vs the reference report (tests/golden/<name>_<score>.npz): the
+    headline delta-hat agrees within 5 Monte Carlo standard deviations, the MC sd estimated from
+    independent device runs (seeds 2..6) of the same configuration."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden",
+                             f"{name}_{'hs' if score == abi.SCORE_HS else 'dss'}.npz"))
+    case, c, slots = case_in(ctx, name)
+    rep = c.run(_score_cfg(case, score))
+    others = [c.run(_score_cfg(case, score, seed=s))["delta_hat"] for s in range(2, 7)]
+    sd = np.std(others, ddof=1)
+    ref = float(z["ref_delta_hat"])
+    assert abs(rep["delta_hat"] - ref) <= 5.0 * np.sqrt(2.0) * sd + 1e-9 * abs(ref), (rep["delta_hat"], ref, sd)
+    np.testing.assert_array_equal(np.isnan(rep["estimate"]), np.isnan(z["ref_estimate"]))
+    c.close()
+
+
+def test_score_unsupported_for_logistic(ctx):  # Model::check_score_support, model.cpp:21-28
+    case, c, slots = case_in(ctx, "logistic_loo")
+    for sc in (abi.SCORE_HS, abi.SCORE_DSS):
+        with pytest.raises(pcv.UnsupportedScore):
+            c.run(abi.run_config(chains=4, iters=20, warmup=2, batch_size=5, score=sc))
+    c.close()

@@ -298,3 +298,66 @@ def test_hmc_trajectory_matches_reference_bitwise(name):
     a, da = om.hmc_chain(1, kp.step_size, kp.n_leapfrog, kp.inv_mass_diag, 3, stream, th0, 40)
     b, db = rm.hmc_chain(1, kp.step_size, kp.n_leapfrog, kp.inv_mass_diag, 3, stream, th0, 40)
     assert np.array_equal(a, b) and np.array_equal(da, db)
+
+
+# ---------------------------------------------------------------- HS / DSS (engine.cpp:322-373)
+SCORE_CASES = [(base, sc) for base in ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
+                                       "seasonal_timeblocks", "seasonal_hvblock"] for sc in ("hs", "dss")]
+
+
+def score_fixture(base, sc):
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", f"{base}_{sc}.npz"))
+    return z
+
+
+@pytest.mark.parametrize("base,sc", SCORE_CASES)
+def test_oracle_reproduces_reference_score_report(base, sc):
+    """Oracle run_pcv with score HS / DSS == the reference run_pcv report (make_golden.py
+    make_score): same chain streams (DSS draws consume them), same Welford arithmetic, same
+    hs_fold_score / dss_fold_score."""
+    case = Case(base)
+    z = score_fixture(base, sc)
+    rc = case.z["run_cfg"]
+    cfg = abi.run_config(chains=int(rc[0]), iters=int(rc[1]), warmup=int(rc[2]), batch_size=int(rc[3]),
+                         blocks=int(rc[4]), bench_draws=int(rc[5]), checkpoint_every=int(rc[6]), seed=1,
+                         score=int(z["score"]))
+    rep = O.run_pcv_oracle(case.omodels, list(range(len(case.omodels))),
+                           [abi.KernelArrays(k.step_size, k.n_leapfrog, k.inv_mass_diag) for k in case.kparams],
+                           case.banks, cfg, threads=4)
+    for k in ("delta_hat", "sigma2_delta", "epistemic_se", "ess_overall", "rhat_max"):
+        assert rep[k] == float(z[f"ref_{k}"]) or (np.isnan(rep[k]) and np.isnan(z[f"ref_{k}"])), k
+    assert np.isnan(rep["mcse"]) and np.isnan(z["ref_mcse"])  # MCSE is LogS-only
+    np.testing.assert_array_equal(rep["estimate"], z["ref_estimate"])
+    np.testing.assert_array_equal(rep["fault"], z["ref_fault"])
+    np.testing.assert_array_equal(rep["dss_ridged"], z["ref_dss_ridged"])
+    np.testing.assert_array_equal(rep["divergences"], z["ref_divergences"])
+    np.testing.assert_array_equal(rep["snapshots"], z["ref_snapshots"])
+
+
+def test_hs_closed_forms():  # test_scoring.cpp:44-62 via the oracle's pred_derivs on a 1-row fold
+    case = Case("cfg1_linreg_loo")
+    om = case.omodels[0]
+    th = case.banks[0][3].copy()
+    d1, d2 = om.pred_derivs(th, 7)
+    vy = np.exp(th[-1]) ** 2
+    mean = th[0] + case.data.x[7] @ th[1:6]
+    assert d2[0] == -1.0 / vy
+    assert abs(d1[0] + (case.data.y[7] - mean) / vy) <= 1e-13 * abs(d1[0])
+    # HS of a point mass at the predictive derivatives: 2(d2 + d1^2) - d1^2 (scoring.cpp:64-73)
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
+                                  "seasonal_timeblocks", "seasonal_hvblock"])
+def test_pred_hooks_match_reference_bitwise(name):
+    """Model::pred_derivs / pred_sample of the oracle == the reference (same stream)."""
+    case = Case(name)
+    for m, om in enumerate(case.omodels):
+        rm = O.RModel(case.data, case.fa, abi.SpecArrays(**case.kws[m]))
+        for fold in sorted({0, 1, case.K // 2, case.K - 1}):
+            for t in sample_thetas(case, m, 2, seed=fold):
+                a1, a2 = om.pred_derivs(t, fold)
+                b1, b2 = rm.pred_derivs(t, fold)
+                assert np.array_equal(a1, b1) and np.array_equal(a2, b2)
+                assert np.array_equal(om.pred_sample(t, fold, 3, 11, 3), rm.pred_sample(t, fold, 3, 11, 3))
