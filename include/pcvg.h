@@ -276,6 +276,29 @@ pcvg_status pcvg_merge(int32_t n_models, int32_t K, const pcvg_run_config* cfg,
                        const pcvg_fold_table* folds, const double* y_x, const double* y_x2,
                        pcvg_report* report);
 
+/* Shuffle benchmark (diagnostics.cpp:76-101, engine.cpp:464-480) of this context's shard on
+ * device. Replicate r consumes CounterRng(seed, stream_key(Benchmark, r, 0, 0)) sequentially over
+ * (model, non-failed fold, chain, block), one below(L) each; this shard's non-failed folds are
+ * global items m * nonfailed_total + nonfailed_before + j. failed: [shard folds] or NULL (none).
+ * rep_max[bench_draws]: max R-hat over the shard's items (0 = none; all-reduce MAX across shards);
+ * needs_host[bench_draws]: 1 where a below() rejection (probability < L / 2^64 per draw) makes the
+ * positional stream differ from the sequential one - run the sequential host path for it. */
+pcvg_status pcvg_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_before,
+                           int64_t nonfailed_total, int32_t blocks_used, double* rep_max,
+                           int32_t* needs_host);
+/* The same positional benchmark on host block sums y_x/y_x2 [n_models][nfold][L][D_stride]
+ * (multi-process CPU tests of the sharding arithmetic). */
+pcvg_status pcvg_benchmark_host(int32_t n_models, int32_t nfold, int32_t L, int32_t D_stride,
+                                int32_t blocks_used, int64_t iter_count, uint64_t seed,
+                                int32_t bench_draws, const double* y_x, const double* y_x2,
+                                const int32_t* failed, int64_t nonfailed_before,
+                                int64_t nonfailed_total, double* rep_max, int32_t* needs_host);
+/* pcvg_merge with precomputed benchmark replicate maxima (all shards reduced by MAX). */
+pcvg_status pcvg_merge_bench(int32_t n_models, int32_t K, const pcvg_run_config* cfg,
+                             int64_t iter_count, int32_t final_checkpoint,
+                             const pcvg_fold_table* folds, const double* bench_max,
+                             pcvg_report* report);
+
 #ifdef __cplusplus
 }
 #endif

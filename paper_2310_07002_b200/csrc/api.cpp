@@ -42,6 +42,9 @@ cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, 
                                 cudaStream_t st);
 cudaError_t launch_extra_centers(const ChainsDev& S, int nfold, int64_t warmup, cudaStream_t st);
 cudaError_t launch_extra_merge(const ChainsDev& S, int nfold, double* merged, cudaStream_t st);
+cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int D_used,
+                         int D_stride, int64_t n, unsigned long long* rep_max, int* reject,
+                         cudaStream_t st);
 // host_folds.cpp
 void rng_sequence(uint64_t, uint64_t, int32_t, uint64_t, const char*, const uint64_t*, int64_t, double*);
 void make_loo(int64_t, int32_t*, int32_t*);
@@ -58,7 +61,11 @@ void simulate_logistic(int64_t, int32_t, uint64_t, double*, double*);
 // stats.cpp
 void merge_stats(int32_t n_models, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
                  int32_t final_checkpoint, const pcvg_fold_table* folds, const double* y_x,
-                 const double* y_x2, int D_used, pcvg_report* rep);
+                 const double* y_x2, int D_used, pcvg_report* rep, const double* bench_max);
+void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t D_used, int64_t n,
+                 uint64_t seed, int32_t R, const double* y_x, const double* y_x2,
+                 const int32_t* failed, int64_t nonfailed_before, int64_t nonfailed_total,
+                 double* rep_max, int32_t* needs_host);
 double hs_fold_estimate(const double* a_x, const double* center, int m, int64_t count);
 bool dss_fold_estimate(const double* merged, const double* center, const double* y_test, int m,
                        int64_t count, double* score, int* ridged);
@@ -648,6 +655,40 @@ void extra_estimates(pcvg_ctx* ctx, const HostModel& m, const ChainSet& cs, int 
   }
 }
 
+// Shuffle benchmark of the shard on device (bench_kernel): replicate maxima + rejection flags.
+void device_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_before,
+                      int64_t nonfailed_total, int D_used, double* rep_max, int32_t* needs_host) {
+  const pcvg_run_config& cfg = ctx->cfg;
+  const int nfold = ctx->fe - ctx->fb, L = cfg.chains, R = cfg.bench_draws;
+  DevBuf<unsigned long long> mx;
+  DevBuf<int> rj;
+  mx.alloc(std::max(R, 1));
+  rj.alloc(std::max(R, 1));
+  ck(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long) * mx.n, ctx->stream), "memset");
+  ck(cudaMemsetAsync(rj.p, 0, sizeof(int) * rj.n, ctx->stream), "memset");
+  for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+    std::vector<int64_t> item(nfold, -1);
+    int64_t j = 0;
+    for (int k = 0; k < nfold; ++k)
+      if (!(failed && failed[k])) item[k] = static_cast<int64_t>(mi) * nonfailed_total + nonfailed_before + j++;
+    DevBuf<int64_t> it;
+    it.upload(item);
+    const ChainSet& cs = *ctx->chains[mi];
+    ck(launch_bench(cs.view(L, ctx->fb, cfg.seed, 0), nfold, it.p, R, D_used, cs.D, ctx->iters_done,
+                    mx.p, rj.p, ctx->stream), "benchmark");
+    ++ctx->launches;
+    ck(cudaStreamSynchronize(ctx->stream), "benchmark");  // `it` is freed at scope exit
+  }
+  const auto m = mx.download(ctx->stream);
+  const auto r = rj.download(ctx->stream);
+  for (int i = 0; i < R; ++i) {
+    double v;
+    std::memcpy(&v, &m[i], sizeof v);
+    rep_max[i] = v;
+    needs_host[i] = r[i];
+  }
+}
+
 void require_device(pcvg_ctx* ctx) {
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
 }
@@ -1162,7 +1203,47 @@ pcvg_status pcvg_merge(int32_t n_models, int32_t K, const pcvg_run_config* cfg, 
     if (!cfg || !folds || !report || n_models < 1 || n_models > 2 || K < 2)
       throw Error(PCVG_INVALID_INPUT, "bad merge arguments");
     const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
-    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, y_x, y_x2, D, report);
+    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, y_x, y_x2, D, report, nullptr);
+  }));
+}
+
+pcvg_status pcvg_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_before,
+                           int64_t nonfailed_total, int32_t blocks_used, double* rep_max,
+                           int32_t* needs_host) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !ctx->begun) throw Error(PCVG_INVALID_INPUT, "pcvg_begin first");
+    if (ctx->iters_done < 1) throw Error(PCVG_INVALID_INPUT, "no sampling iterations yet");
+    if (!rep_max || !needs_host || nonfailed_before < 0 || nonfailed_total < 0)
+      throw Error(PCVG_INVALID_INPUT, "bad benchmark arguments");
+    if (blocks_used < 1 || blocks_used > ctx->chains[0]->D) throw Error(PCVG_INVALID_INPUT, "blocks_used out of range");
+    require_device(ctx);
+    device_benchmark(ctx, failed, nonfailed_before, nonfailed_total, blocks_used, rep_max, needs_host);
+  }));
+}
+
+pcvg_status pcvg_benchmark_host(int32_t n_models, int32_t nfold, int32_t L, int32_t D_stride,
+                                int32_t blocks_used, int64_t iter_count, uint64_t seed,
+                                int32_t bench_draws, const double* y_x, const double* y_x2,
+                                const int32_t* failed, int64_t nonfailed_before,
+                                int64_t nonfailed_total, double* rep_max, int32_t* needs_host) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] {
+    if (n_models < 1 || n_models > 2 || nfold < 0 || L < 2 || blocks_used < 1 || blocks_used > D_stride ||
+        bench_draws < 0 || !y_x || !y_x2 || !rep_max || !needs_host)
+      throw Error(PCVG_INVALID_INPUT, "bad benchmark arguments");
+    bench_shard(n_models, nfold, L, D_stride, blocks_used, iter_count, seed, bench_draws, y_x, y_x2,
+                failed, nonfailed_before, nonfailed_total, rep_max, needs_host);
+  }));
+}
+
+pcvg_status pcvg_merge_bench(int32_t n_models, int32_t K, const pcvg_run_config* cfg,
+                             int64_t iter_count, int32_t final_checkpoint,
+                             const pcvg_fold_table* folds, const double* bench_max,
+                             pcvg_report* report) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] {
+    if (!cfg || !folds || !report || !bench_max || n_models < 1 || n_models > 2 || K < 2)
+      throw Error(PCVG_INVALID_INPUT, "bad merge arguments");
+    const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
+    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, nullptr, nullptr, D, report, bench_max);
   }));
 }
 
@@ -1201,8 +1282,6 @@ pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
       bool final_ck = last;
       if (cfg->early_stop && !last) {
         // Early-stop rule: blocks are the completed check intervals.
-        st = pcvg_block_sums(ctx, yx.data(), yx2.data());
-        if (st != PCVG_OK) throw Error(st, ctx->err);
         pcvg_report probe = *rep;
         std::vector<double> bench(cfg->bench_draws);
         probe.benchmark = bench.data();
@@ -1210,18 +1289,38 @@ pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
         probe.delta_k = nullptr;
         pcvg_fold_table t2 = tab;
         t2.failed = nullptr;
-        merge_stats(nm, K, cfg, done, 2, &t2, yx.data(), yx2.data(), static_cast<int>(ci + 1), &probe);
+        std::vector<double> bmax(cfg->bench_draws);
+        std::vector<int32_t> bhost(cfg->bench_draws);
+        device_benchmark(ctx, nullptr, 0, K, static_cast<int>(ci + 1), bmax.data(), bhost.data());
+        const bool host_path = std::any_of(bhost.begin(), bhost.end(), [](int32_t v) { return v != 0; });
+        if (host_path) {
+          st = pcvg_block_sums(ctx, yx.data(), yx2.data());
+          if (st != PCVG_OK) throw Error(st, ctx->err);
+        }
+        merge_stats(nm, K, cfg, done, 2, &t2, yx.data(), yx2.data(), static_cast<int>(ci + 1), &probe,
+                    host_path ? nullptr : bmax.data());
         if (probe.verdict_pass && std::isfinite(probe.rhat_max) && probe.mcse < probe.epistemic_se) final_ck = true;
       }
       if (final_ck) {
-        st = pcvg_block_sums(ctx, yx.data(), yx2.data());
-        if (st != PCVG_OK) throw Error(st, ctx->err);
-        merge_stats(nm, K, cfg, done, 1, &tab, yx.data(), yx2.data(), last ? D : static_cast<int>(ci + 1), rep);
+        // shuffle benchmark on device over the non-failed folds (failed flags from fold_stats)
+        const int D_used = last ? D : static_cast<int>(ci + 1);
+        int64_t nonfailed = 0;
+        for (int k = 0; k < K; ++k) nonfailed += fl[k] ? 0 : 1;
+        std::vector<double> bmax(cfg->bench_draws);
+        std::vector<int32_t> bhost(cfg->bench_draws);
+        device_benchmark(ctx, fl.data(), 0, nonfailed, D_used, bmax.data(), bhost.data());
+        const bool host_path = std::any_of(bhost.begin(), bhost.end(), [](int32_t v) { return v != 0; });
+        if (host_path) {  // a below() rejection: the reference's sequential stream on the host
+          st = pcvg_block_sums(ctx, yx.data(), yx2.data());
+          if (st != PCVG_OK) throw Error(st, ctx->err);
+        }
+        merge_stats(nm, K, cfg, done, 1, &tab, yx.data(), yx2.data(), D_used, rep,
+                    host_path ? nullptr : bmax.data());
         stopped = true;
       } else {
         pcvg_fold_table t2 = tab;
         t2.failed = nullptr;
-        merge_stats(nm, K, cfg, done, 0, &t2, nullptr, nullptr, D, rep);
+        merge_stats(nm, K, cfg, done, 0, &t2, nullptr, nullptr, D, rep, nullptr);
       }
       if (rep->snapshots) {
         double* o = rep->snapshots + 7 * ci;

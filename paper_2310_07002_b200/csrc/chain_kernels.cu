@@ -83,6 +83,27 @@ __device__ double logsumexp_dev(const double* v, int n) {  // math.hpp:24-32
   return m + log(s);
 }
 
+// rhat_from_sums (diagnostics.cpp:11-33) with the reference's rounding: explicit _rn products and
+// sums keep nvcc from contracting dev*dev + b or (n-1)/n*w + b/n into FMAs.
+__device__ bool rhat_from_sums_dev(const double* sx, const double* sxx, int l, int64_t n, double* rhat) {
+  if (l < 2 || n < 2) return false;
+  const double nd = static_cast<double>(n);
+  double w = 0.0, grand = 0.0;
+  for (int c = 0; c < l; ++c) {
+    w = __dadd_rn(w, (sxx[c] - __dmul_rn(sx[c], sx[c]) / nd) / (nd - 1.0) / l);
+    grand = __dadd_rn(grand, sx[c] / nd / l);
+  }
+  double bb = 0.0;
+  for (int c = 0; c < l; ++c) {
+    const double dev = sx[c] / nd - grand;
+    bb = __dadd_rn(bb, __dmul_rn(dev, dev));
+  }
+  bb = __dmul_rn(bb, nd / (l - 1.0));
+  if (!isfinite(w) || !isfinite(bb) || !(w > 0.0)) return false;
+  *rhat = sqrt(__dadd_rn(__dmul_rn((nd - 1.0) / nd, w), bb / nd) / w);
+  return true;
+}
+
 struct FoldOut {
   double *estimate, *log_f_hat, *mc, *naive, *ess, *rhat;
   int64_t* batches;
@@ -143,18 +164,8 @@ __global__ void fold_stats_kernel(ChainsDev S, int nfold, int64_t n, int b, int 
       sx[c] = s;
       sxx[c] = s2;
     }
-    double w = 0.0, grand = 0.0;
-    for (int c = 0; c < l; ++c) {
-      w += (sxx[c] - sx[c] * sx[c] / n) / (n - 1.0) / l;
-      grand += sx[c] / n / l;
-    }
-    double bb = 0.0;
-    for (int c = 0; c < l; ++c) {
-      const double dev = sx[c] / n - grand;
-      bb += dev * dev;
-    }
-    bb *= static_cast<double>(n) / (l - 1.0);
-    if (isfinite(w) && isfinite(bb) && w > 0.0) rhat = sqrt(((n - 1.0) / n * w + bb / n) / w);
+    double rh;
+    if (rhat_from_sums_dev(sx, sxx, l, n, &rh)) rhat = rh;
   }
   out.estimate[k] = lf;
   out.log_f_hat[k] = lf;
@@ -200,7 +211,68 @@ __global__ void extra_merge_kernel(ExtraDev X, int L, int nfold, double* merged)
   }
 }
 
+// Shuffle benchmark replicate maxima (diagnostics.cpp:76-101, engine.cpp:464-480) for the shard's
+// folds of one model; thread = (replicate r, local fold k). The reference consumes replicate r's
+// stream CounterRng(seed, stream_key(Benchmark, r, 0, 0)) sequentially, one below(L) per (model,
+// non-failed fold, chain, block). below() takes one u64 per try and rejects only v >= L*floor(
+// (2^64-1)/L) (probability < L/2^64), so without a rejection draw j of the stream is the u64 at
+// words 2j, 2j+1: every item computes its draws at its global position and flags a rejection
+// (the caller then runs the sequential host path for that replicate). R-hat > 0 always, so the
+// maximum is kept as the bit pattern of a non-negative double (0 = no item) via atomicMax.
+__global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R, int D_used,
+                             int D_stride, int64_t n, unsigned long long* rep_max, int* reject) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int k = static_cast<int>(idx % nfold);
+  const int r = static_cast<int>(idx / nfold);
+  if (r >= R || item[k] < 0) return;
+  const int l = S.L;
+  const uint64_t L64 = static_cast<uint64_t>(l);
+  const uint64_t bound = L64 * ((~0ull) / L64);
+  const uint64_t stream = stream_key(6 /*Benchmark*/, static_cast<uint64_t>(r), 0, 0);
+  const uint32_t k0 = static_cast<uint32_t>(S.seed), k1 = static_cast<uint32_t>(S.seed >> 32);
+  uint64_t word = 2ull * static_cast<uint64_t>(item[k]) * L64 * static_cast<uint64_t>(D_used);
+  uint64_t blk_cached = ~0ull;
+  uint4 buf = make_uint4(0, 0, 0, 0);
+  bool rej = false;
+  double sx[64], sxx[64];
+  const size_t c0 = static_cast<size_t>(k) * l;
+  for (int c = 0; c < l; ++c) {
+    double a = 0.0, b = 0.0;
+    for (int d = 0; d < D_used; ++d, word += 2) {
+      const uint64_t blk = word >> 2;
+      if (blk != blk_cached) {
+        buf = philox_block(blk, stream, k0, k1);
+        blk_cached = blk;
+      }
+      const uint64_t v = (word & 2) ? (static_cast<uint64_t>(buf.z) | (static_cast<uint64_t>(buf.w) << 32))
+                                    : (static_cast<uint64_t>(buf.x) | (static_cast<uint64_t>(buf.y) << 32));
+      rej |= v >= bound;
+      const size_t src = c0 + static_cast<size_t>(v % L64);
+      a += S.acc.y_x[static_cast<size_t>(d) * S.nch + src];
+      b += S.acc.y_x2[static_cast<size_t>(d) * S.nch + src];
+    }
+    sx[c] = a;
+    sxx[c] = b;
+  }
+  (void)D_stride;
+  if (rej) reject[r] = 1;
+  double rh;
+  if (!rhat_from_sums_dev(sx, sxx, l, n, &rh)) return;
+  atomicMax(rep_max + r, static_cast<unsigned long long>(__double_as_longlong(rh)));
+}
+
 }  // namespace
+
+cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int D_used,
+                         int D_stride, int64_t n, unsigned long long* rep_max, int* reject,
+                         cudaStream_t st) {
+  if (nfold == 0 || R == 0) return cudaSuccess;
+  if (S.L > 64) return cudaErrorInvalidValue;
+  const int64_t total = static_cast<int64_t>(nfold) * R;
+  bench_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, st>>>(S, nfold, item, R, D_used,
+                                                                         D_stride, n, rep_max, reject);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_extra_centers(const ChainsDev& S, int nfold, int64_t warmup, cudaStream_t st) {
   if (nfold == 0 || S.X.kind == 0) return cudaSuccess;

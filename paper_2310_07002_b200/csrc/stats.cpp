@@ -116,9 +116,55 @@ bool dss_fold_estimate(const double* merged, const double* center, const double*
 // final_checkpoint: 0 = intermediate snapshot (no exclusions), 1 = final (exclusions, per-model
 // report, benchmark + verdict), 2 = early-stop probe (no exclusions, benchmark + verdict on the
 // first D_used blocks).
+// Positional shuffle benchmark of one shard (the host restatement of bench_kernel,
+// chain_kernels.cu): y_x / y_x2 are the shard's block sums [m][k][c][D_stride]; item index of
+// (m, local non-failed fold j) = m * nonfailed_total + nonfailed_before + j. rep_max[r] is the max
+// R-hat over the shard's items (0 = none); needs_host[r] = 1 on a below() rejection.
+void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t D_used, int64_t n,
+                 uint64_t seed, int32_t R, const double* y_x, const double* y_x2,
+                 const int32_t* failed, int64_t nonfailed_before, int64_t nonfailed_total,
+                 double* rep_max, int32_t* needs_host) {
+  const uint64_t L64 = static_cast<uint64_t>(l);
+  const uint64_t bound = L64 * ((~uint64_t{0}) / L64);
+  std::vector<double> sx(l), sxx(l);
+  for (int r = 0; r < R; ++r) {
+    rep_max[r] = 0.0;
+    needs_host[r] = 0;
+    const uint64_t stream = stream_key(PCVG_STREAM_BENCHMARK, static_cast<uint64_t>(r), 0, 0);
+    for (int m = 0; m < nm; ++m) {
+      int64_t j = 0;
+      for (int k = 0; k < nfold; ++k) {
+        if (failed && failed[k]) continue;
+        const int64_t item = m * nonfailed_total + nonfailed_before + j++;
+        uint64_t word = 2ull * static_cast<uint64_t>(item) * L64 * static_cast<uint64_t>(D_used);
+        HostRng rng(seed, stream);
+        const size_t base = (static_cast<size_t>(m) * nfold + k) * l * D_stride;
+        for (int c = 0; c < l; ++c) {
+          sx[c] = 0.0;
+          sxx[c] = 0.0;
+          for (int blk = 0; blk < D_used; ++blk, word += 2) {
+            rng.skip_to(word >> 2);
+            if (word & 2) {
+              rng.next_u32();
+              rng.next_u32();
+            }
+            const uint64_t v = rng.next_u64();
+            if (v >= bound) needs_host[r] = 1;
+            const size_t src = static_cast<size_t>(v % L64);
+            sx[c] += y_x[base + src * D_stride + blk];
+            sxx[c] += y_x2[base + src * D_stride + blk];
+          }
+        }
+        double rr;
+        if (rhat_from_sums(sx.data(), sxx.data(), l, n, &rr)) rep_max[r] = std::max(rep_max[r], rr);
+      }
+    }
+  }
+}
+
 void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
                  int32_t final_checkpoint, const pcvg_fold_table* ft, const double* y_x,
-                 const double* y_x2, int D_used, pcvg_report* rep) {
+                 const double* y_x2, int D_used, pcvg_report* rep, const double* bench_max) {
   const int l = cfg->chains;
   const bool final = final_checkpoint == 1;
   const int D_stride = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
@@ -195,7 +241,10 @@ void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter
   // shuffle benchmark (diagnostics.cpp:76-101) over non-failed folds, model-major
   rep->benchmark_count = 0;
   const int64_t nbench = iter_count;  // = N for a full run (gather_block_sums(chains, n), engine.cpp:471)
-  if (y_x && y_x2 && rep->benchmark) {
+  if (bench_max && rep->benchmark) {  // replicate maxima from the device / sharded benchmark
+    for (int r = 0; r < cfg->bench_draws; ++r)
+      if (bench_max[r] > 0.0) rep->benchmark[rep->benchmark_count++] = bench_max[r];
+  } else if (y_x && y_x2 && rep->benchmark) {
     std::vector<double> sx(l), sxx(l);
     for (int r = 0; r < cfg->bench_draws; ++r) {
       HostRng rng(cfg->seed, stream_key(PCVG_STREAM_BENCHMARK, static_cast<uint64_t>(r), 0, 0));

@@ -56,6 +56,35 @@ def gather_rows(arr: np.ndarray, n_models: int, group=None) -> np.ndarray:
     return np.concatenate(per_model)
 
 
+def shard_benchmark_offsets(failed_local, group=None) -> tuple[int, int]:
+    """(non-failed folds before this shard, non-failed folds in total) from an all-gather of the
+    per-shard non-failed counts: the global stream position of this shard's benchmark items
+    (pcvg_benchmark, diagnostics.cpp:82-98)."""
+    import torch
+    import torch.distributed as dist
+
+    mine = int(np.sum(np.asarray(failed_local) == 0)) if failed_local is not None else None
+    world = dist.get_world_size(group)
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    rank = dist.get_rank(group)
+    return int(sum(parts[:rank])), int(sum(parts))
+
+
+def reduce_benchmark(rep_max: np.ndarray, needs_host: np.ndarray, device=None, group=None):
+    """All-reduce MAX of the per-shard replicate maxima and of the rejection flags."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.concatenate([rep_max, needs_host.astype(np.float64)]))
+    if device is not None:
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    t = t.cpu().numpy()
+    R = rep_max.shape[0]
+    return t[:R].copy(), t[R:].astype(np.int32)
+
+
 def failed_from_divergences(div: np.ndarray, n_models: int, K: int, L: int, iters: int) -> np.ndarray:
     """Failed folds (engine.cpp:385-397): every chain of some model divergent on > N/2 iterations."""
     d = div.reshape(n_models, K, L)

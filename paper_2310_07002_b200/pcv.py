@@ -109,6 +109,11 @@ def load():
     _sig(lib, "pcvg_timing", i32, [vp, pf, pi64])
     _sig(lib, "pcvg_merge", i32, [i32, i32, P(abi.RunConfig), i64, i32, P(abi.FoldTable), pf, pf,
                                   P(abi.Report)])
+    _sig(lib, "pcvg_benchmark", i32, [vp, pi32, i64, i64, i32, pf, pi32])
+    _sig(lib, "pcvg_benchmark_host", i32, [i32, i32, i32, i32, i32, i64, u64, i32, pf, pf, pi32, i64,
+                                           i64, pf, pi32])
+    _sig(lib, "pcvg_merge_bench", i32, [i32, i32, P(abi.RunConfig), i64, i32, P(abi.FoldTable), pf,
+                                        P(abi.Report)])
     if lib.pcvg_abi_version() != abi.ABI_VERSION:
         raise ImportError("libpcvg.so ABI version mismatch")
     _lib = lib
@@ -445,6 +450,18 @@ class Context:
                                            C.byref(done)))
         return cols, div, dropped.value, done.value
 
+    def benchmark(self, failed=None, nonfailed_before=0, nonfailed_total=None, blocks_used=None):
+        """pcvg_benchmark: the shard's shuffle-benchmark replicate maxima on device."""
+        R = self._cfg.bench_draws
+        nfold = (self._cfg.fold_end - self._cfg.fold_begin) or self.models[0].K
+        if nonfailed_total is None:
+            nonfailed_total = nfold if failed is None else int(np.sum(np.asarray(failed) == 0))
+        fl = None if failed is None else np.ascontiguousarray(failed, dtype=np.int32)
+        mx, nh = np.zeros(R), np.zeros(R, dtype=np.int32)
+        self._chk(self.lib.pcvg_benchmark(self.h, _p(fl, C.c_int32), nonfailed_before, nonfailed_total,
+                                          blocks_used or self._cfg.blocks, _p(mx), _p(nh, C.c_int32)))
+        return mx, nh
+
     def block_sums(self, nfold, D):
         nm = len(self.models)
         n = nm * nfold * self._cfg.chains * D
@@ -462,6 +479,32 @@ def merge(n_models, K, cfg, iter_count, final, cols, y_x=None, y_x2=None):
     _check(lib.pcvg_merge(n_models, K, C.byref(cfg), iter_count, int(final), C.byref(ft),
                           None if y_x is None else _p(y_x), None if y_x2 is None else _p(y_x2),
                           C.byref(rep)))
+    return abi.report_dict(rep, arrs, n_models)
+
+
+def benchmark_host(n_models, nfold, L, D_stride, blocks_used, iter_count, seed, bench_draws, y_x, y_x2,
+                   failed=None, nonfailed_before=0, nonfailed_total=None):
+    """pcvg_benchmark_host: positional shuffle benchmark of one shard from host block sums."""
+    if nonfailed_total is None:
+        nonfailed_total = nfold if failed is None else int(np.sum(np.asarray(failed) == 0))
+    fl = None if failed is None else np.ascontiguousarray(failed, dtype=np.int32)
+    mx, nh = np.zeros(bench_draws), np.zeros(bench_draws, dtype=np.int32)
+    _check(load().pcvg_benchmark_host(n_models, nfold, L, D_stride, blocks_used, iter_count, seed, bench_draws,
+                                      _p(np.ascontiguousarray(y_x)), _p(np.ascontiguousarray(y_x2)),
+                                      _p(fl, C.c_int32), nonfailed_before, nonfailed_total, _p(mx),
+                                      _p(nh, C.c_int32)))
+    return mx, nh
+
+
+def merge_bench(n_models, K, cfg, iter_count, final, cols, bench_max):
+    """pcvg_merge_bench: Step-4 statistics with precomputed benchmark replicate maxima."""
+    lib = load()
+    ft = abi.FoldTable(**{name: abi.ptr(np.ascontiguousarray(cols[name]), abi._CT[dt])
+                          for name, dt in abi.FOLD_COLUMNS})
+    rep, arrs = abi.new_report(n_models, K, cfg.chains, 1, cfg.bench_draws)
+    bm = np.ascontiguousarray(bench_max, dtype=np.float64)
+    _check(lib.pcvg_merge_bench(n_models, K, C.byref(cfg), iter_count, int(final), C.byref(ft), _p(bm),
+                                C.byref(rep)))
     return abi.report_dict(rep, arrs, n_models)
 
 

@@ -31,6 +31,8 @@ def _tables(n_models, K, L, D, seed=0):
     cols["mc_contribution"] = np.abs(cols["mc_contribution"])
     cols["naive_contribution"] = np.abs(cols["naive_contribution"])
     cols["rhat"] = 1.0 + np.abs(cols["rhat"])
+    for k in (3, 20):  # failed folds (both models): excluded from the benchmark stream
+        cols["failed"][k] = cols["failed"][K + k] = 1
     y_x = rng.standard_normal(n_models * K * L * D)
     y_x2 = y_x ** 2 + np.abs(rng.standard_normal(y_x.shape))
     return cols, y_x, y_x2
@@ -53,8 +55,17 @@ def _worker(rank, world, port, out_q):
     g_yx2 = dist.gather_rows(yx2m, n_models)
     cfg = abi.run_config(chains=L, iters=100, batch_size=10, blocks=D, bench_draws=50)
     rep = pcv.merge(n_models, K, cfg, 100, True, full, g_yx, g_yx2)
+    # sharded benchmark: each rank consumes its own items at their global stream positions
+    # (pcvg_benchmark's arithmetic on host block sums), then MAX across ranks
+    failed_local = cols["failed"][fb:fe]
+    before, total = dist.shard_benchmark_offsets(failed_local)
+    mx, nh = pcv.benchmark_host(n_models, fe - fb, L, D, D, 100, cfg.seed, cfg.bench_draws, yxm, yx2m,
+                                failed_local, before, total)
+    mx, nh = dist.reduce_benchmark(mx, nh)
+    rep2 = pcv.merge_bench(n_models, K, cfg, 100, True, full, mx)
     out_q.put((rank, rep["delta_hat"], rep["mcse"], rep["epistemic_se"], rep["rhat_max"],
-               rep["benchmark"].tolist(), {k: v.tolist() for k, v in full.items()}))
+               rep["benchmark"].tolist(), {k: v.tolist() for k, v in full.items()},
+               rep2["benchmark"].tolist(), int(nh.max())))
     tdist.destroy_process_group()
 
 
@@ -75,7 +86,9 @@ def test_sharded_merge_is_gpu_count_invariant():
     cols, y_x, y_x2 = _tables(n_models, K, L, D)
     cfg = abi.run_config(chains=L, iters=100, batch_size=10, blocks=D, bench_draws=50)
     single = pcv.merge(n_models, K, cfg, 100, True, cols, y_x, y_x2)
-    for rank, dh, mcse, ese, rmax, bench, full in results:
+    for rank, dh, mcse, ese, rmax, bench, full, bench2, rejected in results:
+        assert rejected == 0
+        assert np.array_equal(np.asarray(bench2), single["benchmark"])  # sharded == sequential
         for k, v in cols.items():
             assert np.array_equal(np.asarray(full[k], dtype=v.dtype), v), k
         assert dh == single["delta_hat"] and mcse == single["mcse"] and ese == single["epistemic_se"]
@@ -89,3 +102,19 @@ def test_shard_ranges_partition():
             r = [dist.shard_range(K, i, world) for i in range(world)]
             assert r[0][0] == 0 and r[-1][1] == K
             assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+
+
+def test_positional_benchmark_equals_sequential():
+    """pcvg_benchmark's positional stream == the reference's sequential below() stream
+    (diagnostics.cpp:82-98) on one shard, with failed folds and fewer blocks used than stored."""
+    from paper_2310_07002_b200 import pcv
+    n_models, K, L, D = 2, 23, 6, 5
+    cols, y_x, y_x2 = _tables(n_models, K, L, D, seed=3)
+    cfg = abi.run_config(chains=L, iters=80, batch_size=10, blocks=D, bench_draws=40, seed=9)
+    single = pcv.merge(n_models, K, cfg, 80, True, cols, y_x, y_x2)
+    failed = cols["failed"][:K]
+    mx, nh = pcv.benchmark_host(n_models, K, L, D, D, 80, cfg.seed, cfg.bench_draws, y_x, y_x2, failed)
+    assert nh.max() == 0
+    rep = pcv.merge_bench(n_models, K, cfg, 80, True, cols, mx)
+    assert np.array_equal(rep["benchmark"], single["benchmark"])
+    assert rep["verdict_quantile_value"] == single["verdict_quantile_value"]

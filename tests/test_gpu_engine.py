@@ -139,3 +139,28 @@ def test_early_stop_rule():
     if rep["iters_run"] < 400:
         assert rep["mcse"] < rep["epistemic_se"] and rep["verdict_pass"] == 1
     c.close()
+
+
+def test_device_benchmark_equals_host_sequential():
+    """bench_kernel (positional Philox stream per item) == the reference's sequential shuffle
+    benchmark (diagnostics.cpp:76-101) on the same block sums, with failed folds excluded and
+    with fewer blocks used than stored (early-stop probe)."""
+    case, c = _ctx_with("ex1_grouped_logo")
+    cfg = abi.run_config(chains=4, iters=60, warmup=10, batch_size=10, bench_draws=64, seed=5)
+    c.begin(cfg)
+    c.advance(60)
+    cols, divs, dropped, done = c.fold_stats(case.K)
+    yx, yx2 = c.block_sums(case.K, 5)
+    failed = np.zeros(case.K, np.int32)
+    failed[[2, 7, 31]] = 1
+    for blocks_used in (5, 3):
+        mx, nh = c.benchmark(failed, 0, int(np.sum(failed == 0)), blocks_used)
+        assert nh.max() == 0
+        hx, hh = pcv.benchmark_host(2, case.K, 4, 5, blocks_used, done, cfg.seed, cfg.bench_draws, yx, yx2, failed)
+        np.testing.assert_array_equal(mx, hx)
+    cols["failed"] = np.tile(failed, 2)
+    seq = pcv.merge(2, case.K, cfg, done, True, cols, yx, yx2)
+    mx, _ = c.benchmark(failed, 0, int(np.sum(failed == 0)), 5)
+    dev = pcv.merge_bench(2, case.K, cfg, done, True, cols, mx)
+    np.testing.assert_array_equal(dev["benchmark"], seq["benchmark"])
+    c.close()
