@@ -74,7 +74,7 @@ struct Smem {
   int bad[kC];
   int cur[kC];
   unsigned long long full[kStages];
-  unsigned long long empty[kStages];
+  unsigned int rel[kStages];  // warps done with each ring slot (monotonic; last arrival refills)
 };
 
 // ------------------------------------------------------------------ family hooks
@@ -178,11 +178,15 @@ __device__ __forceinline__ double logp_of(const ModelDev& M, const Smem<KP>& sm,
 }
 
 // ------------------------------------------------------------------ TMA ring
+// Tile g of the kernel's sequence goes to slot g % kStages. The first kStages tiles of a pass are
+// issued by thread 0 (every warp is past the previous pass's closing __syncthreads, so the slots
+// are free); tile g + kStages is issued by the last warp to release tile g (counted in rel[]), so
+// no thread ever blocks on a slot and the refill starts the moment the slot frees.
 template <int KP>
 __device__ __forceinline__ void issue_tile(Smem<KP>& sm, const ModelDev& M, int t, uint32_t g) {
   using G = Geom<KP>;
   const int slot = g % kStages;
-  if (g >= kStages) mbar_wait(&sm.empty[slot], ((g - kStages) / kStages) & 1u);
+  fence_proxy_async();  // generic-proxy reads of the slot before the async-proxy refill
   mbar_expect_tx(&sm.full[slot], G::TILE_BYTES);
   bulk_g2s(sm.xs[slot], M.xr + static_cast<size_t>(t) * G::TM * KP, G::TM * KP * 8, &sm.full[slot]);
   bulk_g2s(sm.ys[slot], M.y + static_cast<size_t>(t) * G::TM, G::TM * 8, &sm.full[slot]);
@@ -297,8 +301,12 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
       }
       __syncwarp();
     }
-    if (l == 0) mbar_arrive(&sm.empty[slot]);
-    if (tid == 0 && tl + kStages < ntiles) issue_tile(sm, M, t + kStages, g + kStages);
+    if (l == 0 && tl + kStages < ntiles) {
+      const unsigned int old = atomicAdd(&sm.rel[slot], 1u);
+      if ((old + 1u) % kWarps == 0u) issue_tile(sm, M, t + kStages, g + kStages);
+    } else if (l == 0) {
+      atomicAdd(&sm.rel[slot], 1u);
+    }
   }
   gtile = g0 + ntiles;
   __syncthreads();
@@ -431,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
 
   if (tid < kStages) {
     mbar_init(&sm.full[tid], 1);
-    mbar_init(&sm.empty[tid], kWarps);
+    sm.rel[tid] = 0u;
   }
   if (tid < 16) sm.exp_tab[tid] = exp2(-tid / 16.0);
   for (int i = tid; i < KP * kLdS; i += kThreads) sm.ws[i] = 0.0;

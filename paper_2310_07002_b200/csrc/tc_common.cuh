@@ -27,6 +27,10 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
 }
 
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
 }
@@ -66,7 +70,7 @@ __device__ __forceinline__ double exp_neg(double a, const double* tab) {
   constexpr double kLn2d16Hi = 0.04332169877307024;      // ln2/16, leading 32 bits
   constexpr double kLn2d16Lo = 1.1926343307941173e-11;   // ln2/16 - hi
   constexpr double kShift = 6755399441055744.0;          // 1.5 * 2^52
-  if (a > 700.0) return 0.0;
+  a = fmin(a, 700.0);  // exp(-700) ~ 1e-304 stands in for the underflow; keeps 2^-m in range
   const double t = fma(a, kInvLn2x16, kShift);
   const int n = __double2loint(t);
   const double nd = t - kShift;
