@@ -119,6 +119,8 @@ struct HostModel {
   std::vector<double> y_host;                    // y in device row order (test_values)
   DevBuf<double> y, x, xr, inv_mass, bank;
   DevBuf<int> key, grp_ptr, lo, hi, ntrain, fseg, sgroup, sunseen, srow, srows;
+  DevBuf<double> yb, xb;         // group-batched layout (ModelDev::nb > 0)
+  DevBuf<int> keyb, bgroup, boff;
   int64_t bank_rows = 0;
   ModelDev md{};
 };
@@ -384,6 +386,48 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   }
   m.grp_ptr.upload(hier ? grp_ptr : std::vector<int>{0});
 
+  // Group-batched layout for the hierarchical kernel (types.cuh): groups sorted by row count
+  // (descending, stable), 32 per batch; batch b is padded to its largest group.
+  int nb = 0, bstride = 0;
+  if (hier && m.J > 1 && m.J <= 32 * kMaxBatches) {
+    std::vector<int> order(m.J);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return grp_ptr[a + 1] - grp_ptr[a] > grp_ptr[b + 1] - grp_ptr[b];
+    });
+    nb = (m.J + 31) / 32;
+    std::vector<int> bgroup(static_cast<size_t>(nb) * 32, -1), boff(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) {
+      int rows = 0;
+      for (int i = 0; i < 32 && 32 * b + i < m.J; ++i) {
+        const int g = order[32 * b + i];
+        bgroup[32 * b + i] = g;
+        rows = std::max(rows, grp_ptr[g + 1] - grp_ptr[g]);
+      }
+      boff[b + 1] = boff[b] + rows;
+    }
+    bstride = boff[nb];
+    const size_t tot = static_cast<size_t>(bstride) * 32;
+    std::vector<double> ybv(tot, 0.0), xbv(static_cast<size_t>(std::max(m.nc, 1)) * tot, 0.0);
+    std::vector<int> kbv(tot, -1);
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < 32; ++i) {
+        const int g = bgroup[32 * b + i];
+        if (g < 0) continue;
+        for (int r = grp_ptr[g]; r < grp_ptr[g + 1]; ++r) {
+          const size_t idx = static_cast<size_t>(boff[b] + (r - grp_ptr[g])) * 32 + i;
+          ybv[idx] = y[r];
+          kbv[idx] = key[r];
+          for (int c = 0; c < m.nc; ++c) xbv[c * tot + idx] = xc[static_cast<size_t>(c) * n + r];
+        }
+      }
+    m.yb.upload(ybv);
+    m.xb.upload(xbv);
+    m.keyb.upload(kbv);
+    m.bgroup.upload(bgroup);
+    m.boff.upload(boff);
+  }
+
   // fold tables (index K = sentinel: nothing held out)
   std::vector<int> lo(m.K + 1, 0), hi(m.K + 1, 0), ntr(m.K + 1, static_cast<int>(n));
   for (int k = 0; k < m.K; ++k) {
@@ -509,6 +553,13 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.c_lgamma10_10 = 10.0 * std::log(10.0) - std::lgamma(10.0);
   md.c_lbeta55 = std::lgamma(10.0) - std::lgamma(5.0) - std::lgamma(5.0);
   md.c_log4 = std::log(4.0);
+  md.nb = nb;
+  md.bstride = bstride;
+  md.bgroup = m.bgroup.p;
+  md.boff = m.boff.p;
+  md.yb = m.yb.p;
+  md.xb = m.xb.p;
+  md.keyb = m.keyb.p;
   return hm;
 }
 
@@ -529,6 +580,8 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
   cudaError_t e;
   if (use_glm(ctx, m, S.nch)) {
     e = launch_glm(m.md, S, A, st);
+  } else if (m.md.nb > 0 && ctx->policy != PCVG_KERNEL_GENERIC) {
+    e = launch_gauss(m.md, S, A, 0, st);  // group-batched hierarchical kernel
   } else {
     const int T = gauss_lanes_per_chain(m.md, S.nch);
     e = launch_gauss(m.md, S, A, T, st);

@@ -341,6 +341,120 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
   __syncwarp(mask);  // group-dim stores of lane 0 become visible to the chain's lanes
 }
 
+// Group-batched gradient pass for the hierarchical families (grouped J > 1, radon), one warp per
+// chain: lane i owns group slot b of every batch (M.bgroup[b*32 + i], groups sorted by size so a
+// batch's groups have similar row counts) and keeps that group's position / momentum in registers
+// (qb[b * kBlock], pb[b * kBlock]: per-thread shared-memory slots) across the n_lf passes of a transition. Rows come from the lane-interleaved batch
+// layout (M.yb/xb/keyb: row j of batch b for lane i at (boff[b] + j) * 32 + i), so every row step
+// is one coalesced warp load and no per-group reduction is needed; only the global sums are
+// butterfly-reduced once per pass. Same semantics as grad_pass (kinds 0/1/2); k0g / k1g / bad
+// are warp-reduced here so every lane leaves with identical values.
+template <int FAM, int NB, int NCM, int NGM, bool VALUE>
+__device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S, int c, int t,
+                                           int lo, int hi, int n_train, const double* qG, int kind,
+                                           bool last, double scale, int cur, NormalCursor& nc,
+                                           ChainRng& R, const double* probe_p, double* gG, double& lp,
+                                           double& k0g, double& k1g, bool& bad, double* qb,
+                                           double* pb) {
+  constexpr unsigned kFull = 0xffffffffu;
+  Prep<NCM> P;
+  prepare<FAM, NCM, NGM>(M, qG, P);
+  const int nch = S.nch;
+  const double eps = M.step, half = 0.5 * M.step;
+  const size_t plane = static_cast<size_t>(M.dim) * nch;
+  const size_t bstride = static_cast<size_t>(M.bstride) * 32;
+  double sxr[NCM];
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) sxr[k] = 0.0;
+  double srr = 0.0, k0l = 0.0, k1l = 0.0;
+  bool poison = false, badl = false;
+  GroupAcc G{0.0, 0.0, 0.0};
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (b >= M.nb) break;
+    const int g = __ldg(M.bgroup + b * 32 + t);
+    const bool valid = g >= 0;
+    double qg = 0.0;
+    if (valid) {
+      const size_t gi = static_cast<size_t>(g) * nch + c;
+      const double mg = __ldg(M.inv_mass + g);
+      if (kind == 0) {
+        qg = S.pos[cur * plane + gi];
+      } else if (kind == 1) {
+        const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + g] : nc.at(R, g) / sqrt(mg);
+        k0l += mg * p0 * p0;
+        pb[b * kBlock] = p0 + half * S.grad[cur * plane + gi];
+        qg = S.pos[cur * plane + gi] + eps * mg * pb[b * kBlock];
+      } else {
+        qg = qb[b * kBlock] + eps * mg * pb[b * kBlock];
+      }
+      badl |= !isfinite(qg);
+      qb[b * kBlock] = qg;
+    }
+    const double off = group_offset<FAM, NCM>(P, qg);
+    double srg = 0.0;
+    const int r0 = __ldg(M.boff + b), r1 = __ldg(M.boff + b + 1);
+    const double* yp = M.yb + static_cast<size_t>(r0) * 32 + t;
+    const double* xp = M.xb + static_cast<size_t>(r0) * 32 + t;
+    const int* kp = M.keyb + static_cast<size_t>(r0) * 32 + t;
+#pragma unroll 8
+    for (int j = r0; j < r1; ++j, yp += 32, xp += 32, kp += 32) {
+      const double yi = __ldg(yp);
+      const int ki = __ldg(kp);
+      double m = off;
+      double xs[NCM];
+#pragma unroll
+      for (int k = 0; k < NCM; ++k) {
+        if (k < M.nc) {
+          xs[k] = __ldg(xp + k * bstride);
+          m = fma(P.w[k], xs[k], m);
+        } else {
+          xs[k] = 0.0;
+        }
+      }
+      const double r = yi - m;
+      // padding rows (key < 0) neither train nor test
+      const bool train = ki >= 0 && static_cast<unsigned>(ki - lo) >= static_cast<unsigned>(hi - lo);
+      const double wr = train ? r : 0.0;
+      srg += wr;
+#pragma unroll
+      for (int k = 0; k < NCM; ++k) sxr[k] = fma(xs[k], wr, sxr[k]);
+      srr = fma(wr, r, srr);
+      if (VALUE && !train && ki >= 0) poison |= !isfinite(P.logv + r * r * P.inv_v);
+    }
+    if (valid) {
+      const double gg = group_grad<FAM, NCM, NGM>(P, qG, M, qg, srg, G);
+      const size_t gi = static_cast<size_t>(g) * nch + c;
+      badl |= !isfinite(gg);
+      if (kind == 0) {
+        S.grad[cur * plane + gi] = gg;
+      } else {
+        const double pn = pb[b * kBlock] + scale * gg;
+        pb[b * kBlock] = pn;
+        badl |= !isfinite(pn);
+        if (last) {
+          S.pos[(cur ^ 1) * plane + gi] = qg;
+          S.grad[(cur ^ 1) * plane + gi] = gg;
+          k1l += __ldg(M.inv_mass + g) * pn * pn;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) sxr[k] = lane_sum<32>(sxr[k], kFull);
+  srr = lane_sum<32>(srr, kFull);
+  G.a0 = lane_sum<32>(G.a0, kFull);
+  G.a1 = lane_sum<32>(G.a1, kFull);
+  G.a2 = lane_sum<32>(G.a2, kFull);
+  if (kind == 1) k0g += lane_sum<32>(k0l, kFull);
+  if (last) k1g += lane_sum<32>(k1l, kFull);
+  bad |= __any_sync(kFull, badl);
+  if (VALUE) poison = __any_sync(kFull, poison);
+  global_grad<FAM, NCM, NGM>(M, P, qG, sxr, 0.0, srr, G, n_train, gG, VALUE, lp);
+  if (VALUE && poison) lp = CUDART_NAN;
+  __syncwarp(kFull);  // group-dim stores become visible to the chain's lanes
+}
+
 // Model::log_pred at the stored position (grouped_regression.cpp:124-163, radon.cpp:109-138,
 // seasonal_ar.cpp:107-115), observations split across the chain's lanes.
 template <int FAM, int T, int NCM, int NGM>
@@ -453,8 +567,10 @@ __device__ void score_extra(const ModelDev& M, const ChainsDev& S, int c, int t,
   }
 }
 
-template <int FAM, int T, int NCM, int NGM>
-__global__ void __launch_bounds__(kBlock) gauss_kernel(ModelDev M, ChainsDev S, RunArgs A) {
+// NB = 0: row-split passes (grad_pass, T lanes per chain); NB > 0: group-batched passes
+// (hgrad_pass, T = 32, up to 32 * NB groups).
+template <int FAM, int T, int NCM, int NGM, int NB>
+__global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev M, ChainsDev S, RunArgs A) {
   constexpr int kChains = kBlock / T;
   const int t = threadIdx.x % T;
   const int local = threadIdx.x / T;
@@ -482,13 +598,21 @@ __global__ void __launch_bounds__(kBlock) gauss_kernel(ModelDev M, ChainsDev S, 
   ChainRng R;
   R.init(S.seed, S.rng_stream[c], S.rng_pos[c], S.rng_cached[c], S.rng_has[c] != 0);
   NormalCursor nc;
+  constexpr int kNB = NB > 0 ? NB : 1;
+  __shared__ double sqb[kNB * kBlock], spb[kNB * kBlock];  // group slots of each thread (NB > 0)
+  double* qb = sqb + threadIdx.x;
+  double* pb = spb + threadIdx.x;
 
   if (A.mode == kModeEval || A.mode == kModePred) {
     if (A.mode == kModeEval) {
       double lp = 0.0, k0 = 0.0, k1 = 0.0;
       bool bad = false;
-      grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, 0, false, 0.0,
-                                        cur, nc, R, nullptr, gG, lp, k0, k1, bad);
+      if constexpr (NB > 0)
+        hgrad_pass<FAM, kNB, NCM, NGM, true>(M, S, c, t, lo, hi, n_train, qG, 0, false, 0.0, cur, nc,
+                                             R, nullptr, gG, lp, k0, k1, bad, qb, pb);
+      else
+        grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, 0, false, 0.0,
+                                          cur, nc, R, nullptr, gG, lp, k0, k1, bad);
       if (t == 0) {
 #pragma unroll
         for (int i = 0; i < NGM; ++i)
@@ -538,12 +662,20 @@ __global__ void __launch_bounds__(kBlock) gauss_kernel(ModelDev M, ChainsDev S, 
         }
       }
       const double scale = last ? half : eps;
-      if (last)
+      if constexpr (NB > 0) {
+        if (last)
+          hgrad_pass<FAM, kNB, NCM, NGM, true>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, true,
+                                               scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb);
+        else
+          hgrad_pass<FAM, kNB, NCM, NGM, false>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, false,
+                                                scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb);
+      } else if (last) {
         grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, first ? 1 : 2,
                                           true, scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad);
-      else
+      } else {
         grad_pass<FAM, T, NCM, NGM, false>(M, S, c, t, mask, lo, hi, n_train, qG, first ? 1 : 2,
                                            false, scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad);
+      }
 #pragma unroll
       for (int i = 0; i < NGM; ++i) {
         if (i < ng) {
@@ -629,12 +761,25 @@ cudaError_t launch_family(const ModelDev& M, const ChainsDev& S, const RunArgs& 
   const int grid = (S.nch + chains_per_block - 1) / chains_per_block;
   if (grid == 0) return cudaSuccess;
   switch (T) {
-    case 1: gauss_kernel<FAM, 1, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
-    case 4: gauss_kernel<FAM, 4, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
-    case 8: gauss_kernel<FAM, 8, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
-    case 32: gauss_kernel<FAM, 32, NCM, NGM><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 1: gauss_kernel<FAM, 1, NCM, NGM, 0><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 4: gauss_kernel<FAM, 4, NCM, NGM, 0><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 8: gauss_kernel<FAM, 8, NCM, NGM, 0><<<grid, kBlock, 0, st>>>(M, S, A); break;
+    case 32: gauss_kernel<FAM, 32, NCM, NGM, 0><<<grid, kBlock, 0, st>>>(M, S, A); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// Group-batched launch (hierarchical families with a batch layout): one warp per chain.
+template <int FAM, int NCM, int NGM>
+cudaError_t launch_batched(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
+  const int grid = (S.nch + kBlock / 32 - 1) / (kBlock / 32);
+  if (grid == 0) return cudaSuccess;
+  if (M.nb <= 2) gauss_kernel<FAM, 32, NCM, NGM, 2><<<grid, kBlock, 0, st>>>(M, S, A);
+  else if (M.nb <= 4) gauss_kernel<FAM, 32, NCM, NGM, 4><<<grid, kBlock, 0, st>>>(M, S, A);
+  else if (M.nb <= 8) gauss_kernel<FAM, 32, NCM, NGM, 8><<<grid, kBlock, 0, st>>>(M, S, A);
+  else if (M.nb <= 16) gauss_kernel<FAM, 32, NCM, NGM, 16><<<grid, kBlock, 0, st>>>(M, S, A);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
@@ -656,6 +801,12 @@ int gauss_lanes_per_chain(const ModelDev& M, int nch) {
 
 cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T,
                          cudaStream_t st) {
+  if (T == 0) {  // group-batched kernel
+    if (M.nb < 1 || M.nb > kMaxBatches) return cudaErrorInvalidValue;
+    if (M.family == kGrouped && M.nc <= 8) return launch_batched<kGrouped, 8, 11>(M, S, A, st);
+    if (M.family == kRadon) return launch_batched<kRadon, 1, 4>(M, S, A, st);
+    return cudaErrorInvalidValue;
+  }
   switch (M.family) {
     case kGrouped:
       if (M.nc > 8) return cudaErrorInvalidValue;

@@ -54,7 +54,20 @@ struct ModelDev {
   double c_lgamma10_10;    // 10 log 10 - lgamma(10)
   double c_lbeta55;        // lgamma(10) - 2 lgamma(5)
   double c_log4;           // log(4)
+  // group-batched layout (hierarchical families, gauss_kernel NB > 0): nb batches of 32 group
+  // slots; bgroup[b*32 + i] = group of lane i in batch b (-1 = none); rows of batch b are
+  // [boff[b], boff[b+1]) in lane-interleaved arrays (row j of lane i at j*32 + i), padded with
+  // key -1 rows; bstride = boff[nb] (rows per lane).
+  int nb;
+  int bstride;
+  const int* bgroup;
+  const int* boff;
+  const double* yb;
+  const double* xb;  // [nc][bstride*32]
+  const int* keyb;
 };
+
+constexpr int kMaxBatches = 16;
 
 // HS / DSS score state (ScoreKind::HS / DSS, engine.cpp:322-373; accum.cpp:10-99). Per local fold
 // kf with test size m = msize[kf], the L chains of the fold are interleaved entry-major: entry e of

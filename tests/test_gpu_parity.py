@@ -22,20 +22,23 @@ def ctx():
 
 
 _cases = {}
-# fixtures whose models have both a tensor-core (GLM) and a generic kernel
-BOTH_KERNELS = {"cfg1_linreg_loo", "seasonal_timeblocks", "seasonal_hvblock"}
+# fixtures whose models have two device kernels: the tensor-core GLM kernel or the group-batched
+# hierarchical kernel (policy AUTO / TENSOR), and the generic row-split kernel (GENERIC)
+BOTH_KERNELS = {"cfg1_linreg_loo": "tensor", "seasonal_timeblocks": "tensor", "seasonal_hvblock": "tensor",
+                "ex1_grouped_logo": "batched", "radon_logo": "batched"}
 
 
 def case_in(ctx, name):
     """(Case, slots) with the case's models registered in a fresh context. A name suffixed with
-    ':tensor' / ':generic' forces that kernel."""
+    ':tensor' / ':batched' / ':generic' forces that kernel."""
     name, _, kernel = name.partition(":")
     if name not in _cases:
         _cases[name] = Case(name)
     case = _cases[name]
     c = pcv.Context(0)
     if kernel:
-        c.set_kernel_policy(c.KERNEL_TENSOR if kernel == "tensor" else c.KERNEL_GENERIC)
+        c.set_kernel_policy({"tensor": c.KERNEL_TENSOR, "batched": c.KERNEL_AUTO,
+                             "generic": c.KERNEL_GENERIC}[kernel])
     slots = [c.add_model(m, kp, bank, model_id=i)
              for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
     return case, c, slots
@@ -45,7 +48,7 @@ def with_kernels(names):
     out = []
     for n in names:
         if n in BOTH_KERNELS:
-            out += [n + ":tensor", n + ":generic"]
+            out += [n + ":" + BOTH_KERNELS[n], n + ":generic"]
         else:
             out.append(n)
     return out
