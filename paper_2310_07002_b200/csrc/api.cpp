@@ -120,7 +120,7 @@ struct HostModel {
   DevBuf<double> y, x, xr, inv_mass, bank;
   DevBuf<int> key, grp_ptr, lo, hi, ntrain, fseg, sgroup, sunseen, srow, srows;
   DevBuf<double> yb, xb;         // group-batched layout (ModelDev::nb > 0)
-  DevBuf<int> keyb, bgroup, boff;
+  DevBuf<int> keyb, bgroup, boff, tfirst, tr0, trows, bkey, bgrows, buni;
   int64_t bank_rows = 0;
   ModelDev md{};
 };
@@ -388,7 +388,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
 
   // Group-batched layout for the hierarchical kernel (types.cuh): groups sorted by row count
   // (descending, stable), 32 per batch; batch b is padded to its largest group.
-  int nb = 0, bstride = 0;
+  int nb = 0, bstride = 0, ntile = 0, rt = 0, bkey_uniform = 0;
   if (hier && m.J > 1 && m.J <= 32 * kMaxBatches) {
     std::vector<int> order(m.J);
     std::iota(order.begin(), order.end(), 0);
@@ -426,6 +426,38 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
     m.keyb.upload(kbv);
     m.bgroup.upload(bgroup);
     m.boff.upload(boff);
+    // per-slot group key when every group's rows share one key (LOGO-style folds)
+    std::vector<int> bkey(static_cast<size_t>(nb) * 32, -1), bgrows(static_cast<size_t>(nb) * 32, 0);
+    bkey_uniform = 1;
+    for (int s2 = 0; s2 < nb * 32; ++s2) {
+      const int g = bgroup[s2];
+      if (g < 0) continue;
+      bkey[s2] = key[grp_ptr[g]];
+      bgrows[s2] = grp_ptr[g + 1] - grp_ptr[g];
+      for (int r = grp_ptr[g]; r < grp_ptr[g + 1]; ++r)
+        if (key[r] != bkey[s2]) bkey_uniform = 0;
+    }
+    m.bkey.upload(bkey);
+    m.bgrows.upload(bgrows);
+    std::vector<int> buni(nb, 1);
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < 32; ++i)
+        if (bgroup[32 * b + i] >= 0 && bgrows[32 * b + i] != boff[b + 1] - boff[b]) buni[b] = 0;
+    m.buni.upload(buni);
+    // row tiles staged through shared memory (<= 12 KB per slot, kRing slots)
+    rt = std::max(1, 12288 / (32 * (12 + 8 * std::max(m.nc, 1))));
+    std::vector<int> tfirst(nb + 1, 0), tr0, trows;
+    for (int b = 0; b < nb; ++b) {
+      for (int r = boff[b]; r < boff[b + 1]; r += rt) {
+        tr0.push_back(r);
+        trows.push_back(std::min(rt, boff[b + 1] - r));
+      }
+      tfirst[b + 1] = static_cast<int>(tr0.size());
+    }
+    ntile = static_cast<int>(tr0.size());
+    m.tfirst.upload(tfirst);
+    m.tr0.upload(tr0.empty() ? std::vector<int>{0} : tr0);
+    m.trows.upload(trows.empty() ? std::vector<int>{0} : trows);
   }
 
   // fold tables (index K = sentinel: nothing held out)
@@ -560,6 +592,15 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.yb = m.yb.p;
   md.xb = m.xb.p;
   md.keyb = m.keyb.p;
+  md.ntile = ntile;
+  md.rt = rt;
+  md.tile_first = m.tfirst.p;
+  md.tile_r0 = m.tr0.p;
+  md.tile_rows = m.trows.p;
+  md.bkey_uniform = bkey_uniform;
+  md.bkey = m.bkey.p;
+  md.bgrows = m.bgrows.p;
+  md.buniform = m.buni.p;
   return hm;
 }
 

@@ -18,6 +18,7 @@
 
 #include "device_common.cuh"
 #include "score_extra.cuh"
+#include "tc_common.cuh"
 #include "types.cuh"
 
 namespace pcvg {
@@ -341,6 +342,94 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
   __syncwarp(mask);  // group-dim stores of lane 0 become visible to the chain's lanes
 }
 
+// Row-tile ring of the group-batched kernel: the CTA's warps (one chain each) share one staged copy
+// of every batch row tile. Tile g of the launch's sequence (pass-major, M.ntile tiles per pass)
+// lives in slot g & 1 as [y: rt*32][x: nc][rt*32][key: rt*32]; TMA bulk copies fill it (full[]
+// mbarrier), the last of the CTA's W warps to release a tile refills its slot with tile g + 2.
+constexpr int kRing = 4;  // ring depth (slots)
+
+struct BatchRing {
+  unsigned char* base;
+  size_t slot_bytes;
+  unsigned long long* full;
+  unsigned int* rel;
+  uint32_t g;       // next tile of this warp
+  uint32_t total;   // tiles consumed by this launch
+  unsigned int W;   // valid warps of the CTA
+  double* qslots;   // [2][nb][kBlock] group position / momentum slots
+};
+
+__device__ __forceinline__ void ring_issue(const ModelDev& M, BatchRing& rg, uint32_t g) {
+  using namespace tc;
+  const int s = g % kRing;
+  const int tl = static_cast<int>(g % static_cast<uint32_t>(M.ntile));
+  const int r0 = __ldg(M.tile_r0 + tl), rows = __ldg(M.tile_rows + tl);
+  const size_t tot = static_cast<size_t>(M.bstride) * 32;
+  const uint32_t yb = rows * 32 * 8;
+  fence_proxy_async();
+  mbar_expect_tx(&rg.full[s], yb * (1 + M.nc) + (M.bkey_uniform ? 0 : rows * 32 * 4));
+  unsigned char* dst = rg.base + s * rg.slot_bytes;
+  bulk_g2s(dst, M.yb + static_cast<size_t>(r0) * 32, yb, &rg.full[s]);
+  for (int k = 0; k < M.nc; ++k)
+    bulk_g2s(dst + static_cast<size_t>(M.rt) * 32 * 8 * (1 + k), M.xb + k * tot + static_cast<size_t>(r0) * 32,
+             yb, &rg.full[s]);
+  if (!M.bkey_uniform)
+    bulk_g2s(dst + static_cast<size_t>(M.rt) * 32 * 8 * (1 + M.nc), M.keyb + static_cast<size_t>(r0) * 32,
+             rows * 32 * 4, &rg.full[s]);
+}
+
+// Rows of one staged tile for one lane (its group, offset `off`). KEYS: 0 = per-row fold keys,
+// 1 = group-uniform key and equal group lengths in the batch (no per-row test at all),
+// 2 = group-uniform key, rows past the group's end masked by count. NCX: exact covariate count
+// (0 = M.nc at run time, up to NCM). Two interleaved partial sums per accumulator.
+template <int FAM, int NCX, int NCM, int KEYS, bool VALUE>
+__device__ __forceinline__ void tile_rows_loop(const ModelDev& M, const Prep<NCM>& P, const double* yp,
+                                               const double* xp, const int* kp, int xstride, int rows,
+                                               int jb0, int grows, bool gtrain, int gkey, int lo, int hi,
+                                               double off, double& srg, double* sxr, double& srr,
+                                               double& srg1, double* sxr1, double& srr1, bool& poison) {
+  constexpr int kNc = NCX > 0 ? NCX : NCM;
+  const int nc = NCX > 0 ? NCX : M.nc;
+  auto row = [&](const double* yq, const double* xq, const int* kq, int jb, double& a_rg, double* a_xr,
+                 double& a_rr) {
+    double m = off;
+    double xs[kNc];
+#pragma unroll
+    for (int k = 0; k < kNc; ++k) {
+      xs[k] = (NCX > 0 || k < nc) ? xq[k * xstride] : 0.0;
+      m = fma(P.w[k], xs[k], m);
+    }
+    const double r = *yq - m;
+    bool train, test;
+    if constexpr (KEYS == 0) {
+      const int ki = *kq;  // padding rows (key < 0) neither train nor test
+      train = ki >= 0 && static_cast<unsigned>(ki - lo) >= static_cast<unsigned>(hi - lo);
+      test = ki >= 0 && !train;
+    } else if constexpr (KEYS == 1) {
+      train = gtrain;
+      test = gkey >= 0 && !gtrain;
+    } else {
+      const bool in = jb < grows;
+      train = gtrain && in;
+      test = gkey >= 0 && !gtrain && in;
+    }
+    if (train) {
+      a_rg += r;
+#pragma unroll
+      for (int k = 0; k < kNc; ++k) a_xr[k] = fma(xs[k], r, a_xr[k]);
+      a_rr = fma(r, r, a_rr);
+    }
+    if (VALUE && test) poison |= !isfinite(P.logv + r * r * P.inv_v);
+  };
+  int j = 0;
+#pragma unroll 4
+  for (; j + 1 < rows; j += 2, yp += 64, xp += 64, kp += 64) {
+    row(yp, xp, kp, jb0 + j, srg, sxr, srr);
+    row(yp + 32, xp + 32, kp + 32, jb0 + j + 1, srg1, sxr1, srr1);
+  }
+  if (j < rows) row(yp, xp, kp, jb0 + j, srg, sxr, srr);
+}
+
 // Group-batched gradient pass for the hierarchical families (grouped J > 1, radon), one warp per
 // chain: lane i owns group slot b of every batch (M.bgroup[b*32 + i], groups sorted by size so a
 // batch's groups have similar row counts) and keeps that group's position / momentum in registers
@@ -349,29 +438,27 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
 // is one coalesced warp load and no per-group reduction is needed; only the global sums are
 // butterfly-reduced once per pass. Same semantics as grad_pass (kinds 0/1/2); k0g / k1g / bad
 // are warp-reduced here so every lane leaves with identical values.
-template <int FAM, int NB, int NCM, int NGM, bool VALUE>
+template <int FAM, int NB, int NCM, int NGM, bool VALUE, int NCX>
 __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S, int c, int t,
                                            int lo, int hi, int n_train, const double* qG, int kind,
                                            bool last, double scale, int cur, NormalCursor& nc,
                                            ChainRng& R, const double* probe_p, double* gG, double& lp,
                                            double& k0g, double& k1g, bool& bad, double* qb,
-                                           double* pb) {
+                                           double* pb, BatchRing& rg) {
   constexpr unsigned kFull = 0xffffffffu;
   Prep<NCM> P;
   prepare<FAM, NCM, NGM>(M, qG, P);
   const int nch = S.nch;
   const double eps = M.step, half = 0.5 * M.step;
   const size_t plane = static_cast<size_t>(M.dim) * nch;
-  const size_t bstride = static_cast<size_t>(M.bstride) * 32;
   double sxr[NCM];
 #pragma unroll
   for (int k = 0; k < NCM; ++k) sxr[k] = 0.0;
   double srr = 0.0, k0l = 0.0, k1l = 0.0;
   bool poison = false, badl = false;
   GroupAcc G{0.0, 0.0, 0.0};
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    if (b >= M.nb) break;
+#pragma unroll 1
+  for (int b = 0; b < M.nb; ++b) {
     const int g = __ldg(M.bgroup + b * 32 + t);
     const bool valid = g >= 0;
     double qg = 0.0;
@@ -392,36 +479,50 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
       qb[b * kBlock] = qg;
     }
     const double off = group_offset<FAM, NCM>(P, qg);
-    double srg = 0.0;
-    const int r0 = __ldg(M.boff + b), r1 = __ldg(M.boff + b + 1);
-    const double* yp = M.yb + static_cast<size_t>(r0) * 32 + t;
-    const double* xp = M.xb + static_cast<size_t>(r0) * 32 + t;
-    const int* kp = M.keyb + static_cast<size_t>(r0) * 32 + t;
-#pragma unroll 8
-    for (int j = r0; j < r1; ++j, yp += 32, xp += 32, kp += 32) {
-      const double yi = __ldg(yp);
-      const int ki = __ldg(kp);
-      double m = off;
-      double xs[NCM];
+    double srg = 0.0, srg1 = 0.0, srr1 = 0.0;
+    double sxr1[NCM];
 #pragma unroll
-      for (int k = 0; k < NCM; ++k) {
-        if (k < M.nc) {
-          xs[k] = __ldg(xp + k * bstride);
-          m = fma(P.w[k], xs[k], m);
-        } else {
-          xs[k] = 0.0;
-        }
-      }
-      const double r = yi - m;
-      // padding rows (key < 0) neither train nor test
-      const bool train = ki >= 0 && static_cast<unsigned>(ki - lo) >= static_cast<unsigned>(hi - lo);
-      const double wr = train ? r : 0.0;
-      srg += wr;
-#pragma unroll
-      for (int k = 0; k < NCM; ++k) sxr[k] = fma(xs[k], wr, sxr[k]);
-      srr = fma(wr, r, srr);
-      if (VALUE && !train && ki >= 0) poison |= !isfinite(P.logv + r * r * P.inv_v);
+    for (int k = 0; k < NCM; ++k) sxr1[k] = 0.0;
+    // group-uniform fold keys (e.g. LOGO): one train test per group, rows past the group's end
+    // (batch padding) masked by count instead of a per-row key
+    const int gkey = __ldg(M.bkey + b * 32 + t);
+    const int grows = __ldg(M.bgrows + b * 32 + t);
+    const bool gtrain = gkey >= 0 && static_cast<unsigned>(gkey - lo) >= static_cast<unsigned>(hi - lo);
+    const int tl1 = __ldg(M.tile_first + b + 1);
+    const int bstart = __ldg(M.boff + b);
+    for (int tl = __ldg(M.tile_first + b); tl < tl1; ++tl) {
+    const int s = rg.g % kRing;
+    tc::mbar_wait(&rg.full[s], (rg.g / kRing) & 1u);
+    const int rows = __ldg(M.tile_rows + tl);
+    const int jb0 = __ldg(M.tile_r0 + tl) - bstart;  // row of the batch at tile row 0
+    const double* yp = reinterpret_cast<const double*>(rg.base + s * rg.slot_bytes) + t;
+    const int xstride = M.rt * 32;
+    const double* xp = yp + xstride;
+    const int* kp = reinterpret_cast<const int*>(yp - t + static_cast<size_t>(xstride) * (1 + M.nc)) + t;
+    if (M.bkey_uniform) {
+      // group-uniform keys: one train flag per group; rows past the group's end only in batches
+      // whose groups differ in length (buniform[b] == 0)
+      if (__ldg(M.buniform + b))
+        tile_rows_loop<FAM, NCX, NCM, 1, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
+                                               lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
+      else
+        tile_rows_loop<FAM, NCX, NCM, 2, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
+                                               lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
+    } else {
+      tile_rows_loop<FAM, NCX, NCM, 0, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
+                                             lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
     }
+    __syncwarp(kFull);
+    if (t == 0) {  // release the slot; the CTA's last warp refills it
+      const unsigned int old = atomicAdd(&rg.rel[s], 1u);
+      if ((old + 1u) % rg.W == 0u && rg.g + kRing < rg.total) ring_issue(M, rg, rg.g + kRing);
+    }
+    ++rg.g;
+    }
+    srg += srg1;
+    srr += srr1;
+#pragma unroll
+    for (int k = 0; k < NCM; ++k) sxr[k] += sxr1[k];
     if (valid) {
       const double gg = group_grad<FAM, NCM, NGM>(P, qG, M, qg, srg, G);
       const size_t gi = static_cast<size_t>(g) * nch + c;
@@ -575,6 +676,28 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
   const int t = threadIdx.x % T;
   const int local = threadIdx.x / T;
   const int c = blockIdx.x * kChains + local;
+  BatchRing rg{};
+  if constexpr (NB > 0) {
+    extern __shared__ __align__(128) unsigned char ring_raw[];
+    const size_t slot_bytes = static_cast<size_t>(M.rt) * 32 * (12 + 8 * M.nc);
+    rg.base = ring_raw;
+    rg.slot_bytes = slot_bytes;
+    rg.full = reinterpret_cast<unsigned long long*>(ring_raw + kRing * slot_bytes);
+    rg.rel = reinterpret_cast<unsigned int*>(rg.full + kRing);
+    rg.qslots = reinterpret_cast<double*>(ring_raw + kRing * slot_bytes + 16 * kRing);
+    rg.g = 0;
+    const uint32_t passes = A.mode == kModeEval ? 1u : (A.mode == kModePred ? 0u : static_cast<uint32_t>(A.n_iters * M.n_lf));
+    rg.total = passes * static_cast<uint32_t>(M.ntile);
+    rg.W = static_cast<unsigned int>(min(kChains, S.nch - static_cast<int>(blockIdx.x) * kChains));
+    if (threadIdx.x < kRing) {
+      tc::mbar_init(&rg.full[threadIdx.x], 1);
+      rg.rel[threadIdx.x] = 0u;
+    }
+    tc::fence_mbar_init();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (uint32_t g = 0; g < kRing && g < rg.total; ++g) ring_issue(M, rg, g);
+  }
   if (c >= S.nch) return;
   const unsigned mask =
       T == 32 ? 0xffffffffu : (((1u << T) - 1u) << ((threadIdx.x & 31) & ~(T - 1)));
@@ -598,18 +721,19 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
   ChainRng R;
   R.init(S.seed, S.rng_stream[c], S.rng_pos[c], S.rng_cached[c], S.rng_has[c] != 0);
   NormalCursor nc;
-  constexpr int kNB = NB > 0 ? NB : 1;
-  __shared__ double sqb[kNB * kBlock], spb[kNB * kBlock];  // group slots of each thread (NB > 0)
-  double* qb = sqb + threadIdx.x;
-  double* pb = spb + threadIdx.x;
+  constexpr int kNB = 1;
+  constexpr int NCX = NB > 0 ? NB - 1 : 0;  // exact covariate count of the batched variant (0 = run time)
+  // group slots of each thread (NB > 0): [nb][kBlock] position / momentum after the ring
+  double* qb = rg.qslots + threadIdx.x;
+  double* pb = rg.qslots + static_cast<size_t>(M.nb) * kBlock + threadIdx.x;
 
   if (A.mode == kModeEval || A.mode == kModePred) {
     if (A.mode == kModeEval) {
       double lp = 0.0, k0 = 0.0, k1 = 0.0;
       bool bad = false;
       if constexpr (NB > 0)
-        hgrad_pass<FAM, kNB, NCM, NGM, true>(M, S, c, t, lo, hi, n_train, qG, 0, false, 0.0, cur, nc,
-                                             R, nullptr, gG, lp, k0, k1, bad, qb, pb);
+        hgrad_pass<FAM, kNB, NCM, NGM, true, NCX>(M, S, c, t, lo, hi, n_train, qG, 0, false, 0.0, cur, nc,
+                                             R, nullptr, gG, lp, k0, k1, bad, qb, pb, rg);
       else
         grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, 0, false, 0.0,
                                           cur, nc, R, nullptr, gG, lp, k0, k1, bad);
@@ -664,11 +788,11 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
       const double scale = last ? half : eps;
       if constexpr (NB > 0) {
         if (last)
-          hgrad_pass<FAM, kNB, NCM, NGM, true>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, true,
-                                               scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb);
+          hgrad_pass<FAM, kNB, NCM, NGM, true, NCX>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, true,
+                                               scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb, rg);
         else
-          hgrad_pass<FAM, kNB, NCM, NGM, false>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, false,
-                                                scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb);
+          hgrad_pass<FAM, kNB, NCM, NGM, false, NCX>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, false,
+                                                scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb, rg);
       } else if (last) {
         grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, first ? 1 : 2,
                                           true, scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad);
@@ -771,16 +895,28 @@ cudaError_t launch_family(const ModelDev& M, const ChainsDev& S, const RunArgs& 
 }
 
 // Group-batched launch (hierarchical families with a batch layout): one warp per chain.
+template <int FAM, int NCM, int NGM, int NB>
+cudaError_t launch_nb(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st, int grid) {
+  const size_t smem = kRing * static_cast<size_t>(M.rt) * 32 * (12 + 8 * M.nc) + 16 * kRing +
+                      2 * static_cast<size_t>(M.nb) * kBlock * sizeof(double);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, 32, NCM, NGM, NB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  gauss_kernel<FAM, 32, NCM, NGM, NB><<<grid, kBlock, smem, st>>>(M, S, A);
+  return cudaGetLastError();
+}
+
 template <int FAM, int NCM, int NGM>
 cudaError_t launch_batched(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
   const int grid = (S.nch + kBlock / 32 - 1) / (kBlock / 32);
   if (grid == 0) return cudaSuccess;
-  if (M.nb <= 2) gauss_kernel<FAM, 32, NCM, NGM, 2><<<grid, kBlock, 0, st>>>(M, S, A);
-  else if (M.nb <= 4) gauss_kernel<FAM, 32, NCM, NGM, 4><<<grid, kBlock, 0, st>>>(M, S, A);
-  else if (M.nb <= 8) gauss_kernel<FAM, 32, NCM, NGM, 8><<<grid, kBlock, 0, st>>>(M, S, A);
-  else if (M.nb <= 16) gauss_kernel<FAM, 32, NCM, NGM, 16><<<grid, kBlock, 0, st>>>(M, S, A);
-  else return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  if (M.nb > kMaxBatches) return cudaErrorInvalidValue;
+  if (M.nc == NCM) return launch_nb<FAM, NCM, NGM, 1 + NCM>(M, S, A, st, grid);  // exact width
+  return launch_nb<FAM, NCM, NGM, 1>(M, S, A, st, grid);
 }
 
 }  // namespace
@@ -803,6 +939,7 @@ cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A
                          cudaStream_t st) {
   if (T == 0) {  // group-batched kernel
     if (M.nb < 1 || M.nb > kMaxBatches) return cudaErrorInvalidValue;
+    if (M.family == kGrouped && M.nc <= 4) return launch_batched<kGrouped, 4, 7>(M, S, A, st);
     if (M.family == kGrouped && M.nc <= 8) return launch_batched<kGrouped, 8, 11>(M, S, A, st);
     if (M.family == kRadon) return launch_batched<kRadon, 1, 4>(M, S, A, st);
     return cudaErrorInvalidValue;

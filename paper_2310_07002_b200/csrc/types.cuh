@@ -65,6 +65,16 @@ struct ModelDev {
   const double* yb;
   const double* xb;  // [nc][bstride*32]
   const int* keyb;
+  // row tiles of a pass (at most rt rows each, batch order): tile_first[b] .. tile_first[b+1]
+  int ntile;
+  int rt;
+  const int* tile_first;  // [nb+1]
+  const int* tile_r0;     // [ntile] first row (batch layout)
+  const int* tile_rows;   // [ntile]
+  int bkey_uniform;       // every group's rows share one fold key (LOGO): per-slot key below
+  const int* bkey;        // [nb*32] the group's key (-1 = no group)
+  const int* bgrows;      // [nb*32] the group's row count
+  const int* buniform;    // [nb] 1 if every group of the batch has the batch's row count
 };
 
 constexpr int kMaxBatches = 16;
