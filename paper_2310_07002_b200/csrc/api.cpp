@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -388,7 +389,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
 
   // Group-batched layout for the hierarchical kernel (types.cuh): groups sorted by row count
   // (descending, stable), 32 per batch; batch b is padded to its largest group.
-  int nb = 0, bstride = 0, ntile = 0, rt = 0, bkey_uniform = 0;
+  int nb = 0, bstride = 0, ntile = 0, rt = 0, bkey_uniform = 0, ring = 0;
   if (hier && m.J > 1 && m.J <= 32 * kMaxBatches) {
     std::vector<int> order(m.J);
     std::iota(order.begin(), order.end(), 0);
@@ -444,8 +445,11 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
       for (int i = 0; i < 32; ++i)
         if (bgroup[32 * b + i] >= 0 && bgrows[32 * b + i] != boff[b + 1] - boff[b]) buni[b] = 0;
     m.buni.upload(buni);
-    // row tiles staged through shared memory (<= 12 KB per slot, kRing slots)
-    rt = std::max(1, 12288 / (32 * (12 + 8 * std::max(m.nc, 1))));
+    // row tiles: staged through a shared-memory ring (<= 16 KB per slot) or, ring off, one tile
+    // per batch read through L1 (PCVG_BATCH_RING=0/1 overrides; default on)
+    const char* ring_env = std::getenv("PCVG_BATCH_RING");
+    ring = ring_env ? std::atoi(ring_env) != 0 : 1;
+    rt = ring ? std::max(1, 16384 / (32 * (8 + 8 * std::max(m.nc, 1) + (bkey_uniform ? 0 : 4)))) : 1 << 30;
     std::vector<int> tfirst(nb + 1, 0), tr0, trows;
     for (int b = 0; b < nb; ++b) {
       for (int r = boff[b]; r < boff[b + 1]; r += rt) {
@@ -601,6 +605,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.bkey = m.bkey.p;
   md.bgrows = m.bgrows.p;
   md.buniform = m.buni.p;
+  md.ring = ring;
   return hm;
 }
 

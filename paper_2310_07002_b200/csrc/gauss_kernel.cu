@@ -346,7 +346,14 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
 // of every batch row tile. Tile g of the launch's sequence (pass-major, M.ntile tiles per pass)
 // lives in slot g & 1 as [y: rt*32][x: nc][rt*32][key: rt*32]; TMA bulk copies fill it (full[]
 // mbarrier), the last of the CTA's W warps to release a tile refills its slot with tile g + 2.
-constexpr int kRing = 4;  // ring depth (slots)
+constexpr int kRing = 3;  // ring depth (slots)
+
+// Bytes of one ring slot: y and nc covariate columns of rt rows x 32 lanes, plus the keys unless
+// they are group-uniform (0 when the ring is off).
+__host__ __device__ inline size_t ring_slot_bytes(const ModelDev& M) {
+  if (!M.ring) return 0;
+  return static_cast<size_t>(M.rt) * 32 * (8 + 8 * M.nc + (M.bkey_uniform ? 0 : 4));
+}
 
 struct BatchRing {
   unsigned char* base;
@@ -492,13 +499,25 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
     const int bstart = __ldg(M.boff + b);
     for (int tl = __ldg(M.tile_first + b); tl < tl1; ++tl) {
     const int s = rg.g % kRing;
-    tc::mbar_wait(&rg.full[s], (rg.g / kRing) & 1u);
     const int rows = __ldg(M.tile_rows + tl);
-    const int jb0 = __ldg(M.tile_r0 + tl) - bstart;  // row of the batch at tile row 0
-    const double* yp = reinterpret_cast<const double*>(rg.base + s * rg.slot_bytes) + t;
-    const int xstride = M.rt * 32;
-    const double* xp = yp + xstride;
-    const int* kp = reinterpret_cast<const int*>(yp - t + static_cast<size_t>(xstride) * (1 + M.nc)) + t;
+    const int tr0 = __ldg(M.tile_r0 + tl);
+    const int jb0 = tr0 - bstart;  // row of the batch at tile row 0
+    const double* yp;
+    const double* xp;
+    const int* kp;
+    int xstride;
+    if (M.ring) {  // staged tile in shared memory
+      tc::mbar_wait(&rg.full[s], (rg.g / kRing) & 1u);
+      yp = reinterpret_cast<const double*>(rg.base + s * rg.slot_bytes) + t;
+      xstride = M.rt * 32;
+      xp = yp + xstride;
+      kp = reinterpret_cast<const int*>(yp - t + static_cast<size_t>(xstride) * (1 + M.nc)) + t;
+    } else {  // straight from L2 / L1 (read-only path)
+      yp = M.yb + static_cast<size_t>(tr0) * 32 + t;
+      xstride = M.bstride * 32;
+      xp = M.xb + static_cast<size_t>(tr0) * 32 + t;
+      kp = M.keyb + static_cast<size_t>(tr0) * 32 + t;
+    }
     if (M.bkey_uniform) {
       // group-uniform keys: one train flag per group; rows past the group's end only in batches
       // whose groups differ in length (buniform[b] == 0)
@@ -512,12 +531,14 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
       tile_rows_loop<FAM, NCX, NCM, 0, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
                                              lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
     }
+    if (M.ring) {
     __syncwarp(kFull);
     if (t == 0) {  // release the slot; the CTA's last warp refills it
       const unsigned int old = atomicAdd(&rg.rel[s], 1u);
       if ((old + 1u) % rg.W == 0u && rg.g + kRing < rg.total) ring_issue(M, rg, rg.g + kRing);
     }
     ++rg.g;
+    }
     }
     srg += srg1;
     srr += srr1;
@@ -679,7 +700,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
   BatchRing rg{};
   if constexpr (NB > 0) {
     extern __shared__ __align__(128) unsigned char ring_raw[];
-    const size_t slot_bytes = static_cast<size_t>(M.rt) * 32 * (12 + 8 * M.nc);
+    const size_t slot_bytes = ring_slot_bytes(M);
     rg.base = ring_raw;
     rg.slot_bytes = slot_bytes;
     rg.full = reinterpret_cast<unsigned long long*>(ring_raw + kRing * slot_bytes);
@@ -687,7 +708,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
     rg.qslots = reinterpret_cast<double*>(ring_raw + kRing * slot_bytes + 16 * kRing);
     rg.g = 0;
     const uint32_t passes = A.mode == kModeEval ? 1u : (A.mode == kModePred ? 0u : static_cast<uint32_t>(A.n_iters * M.n_lf));
-    rg.total = passes * static_cast<uint32_t>(M.ntile);
+    rg.total = M.ring ? passes * static_cast<uint32_t>(M.ntile) : 0u;
     rg.W = static_cast<unsigned int>(min(kChains, S.nch - static_cast<int>(blockIdx.x) * kChains));
     if (threadIdx.x < kRing) {
       tc::mbar_init(&rg.full[threadIdx.x], 1);
@@ -897,8 +918,7 @@ cudaError_t launch_family(const ModelDev& M, const ChainsDev& S, const RunArgs& 
 // Group-batched launch (hierarchical families with a batch layout): one warp per chain.
 template <int FAM, int NCM, int NGM, int NB>
 cudaError_t launch_nb(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st, int grid) {
-  const size_t smem = kRing * static_cast<size_t>(M.rt) * 32 * (12 + 8 * M.nc) + 16 * kRing +
-                      2 * static_cast<size_t>(M.nb) * kBlock * sizeof(double);
+  const size_t smem = kRing * ring_slot_bytes(M) + 16 * kRing + 2 * static_cast<size_t>(M.nb) * kBlock * sizeof(double);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, 32, NCM, NGM, NB>,

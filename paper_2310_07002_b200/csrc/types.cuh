@@ -75,6 +75,7 @@ struct ModelDev {
   const int* bkey;        // [nb*32] the group's key (-1 = no group)
   const int* bgrows;      // [nb*32] the group's row count
   const int* buniform;    // [nb] 1 if every group of the batch has the batch's row count
+  int ring;               // 1: row tiles staged through a shared-memory TMA ring; 0: read via L1
 };
 
 constexpr int kMaxBatches = 16;
