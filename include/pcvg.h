@@ -276,6 +276,43 @@ pcvg_status pcvg_merge(int32_t n_models, int32_t K, const pcvg_run_config* cfg,
                        const pcvg_fold_table* folds, const double* y_x, const double* y_x2,
                        pcvg_report* report);
 
+/* ---------------------------------------------------------------- Step 1: full-data fit
+ * adapt_full_data (adapt.hpp:64-69, adapt.cpp:96-221) on the device: L_fd chains from the model's
+ * prior (Model::initial_draw on CounterRng(seed, stream_key(FullData, model_id, c)), host), the
+ * StepInit doubling search for the first step size, dual-averaging step-size adaptation
+ * (adapt.hpp:15-44) with windowed diagonal mass estimation on the full-data sentinel fold, then
+ * `draws` frozen-kernel transitions that fill the warm-start bank. Every transition of every chain
+ * runs in the fused HMC kernels; the window / dual-averaging arithmetic (a few doubles per
+ * iteration) stays on the host, as in the reference coordinator. */
+typedef struct {
+  int32_t chains;          /* L_fd */
+  int64_t warmup;
+  int64_t draws;
+  int32_t n_leapfrog;
+  double target_accept;
+  double init_step_size;   /* 0 = StepInit search */
+} pcvg_adapt_config;       /* AdaptConfig, adapt.hpp:47-54 */
+
+typedef struct {
+  double step_size;
+  double* inv_mass_diag;   /* [dim] */
+  double* draws;           /* [chains*draws*dim]: row iter*chains + chain (adapt.cpp:204-209) */
+  double* rhat;            /* [dim] param_rhat (adapt.cpp:45-66), may be NULL */
+  double* ess;             /* [dim] param_ess (adapt.cpp:69-92), may be NULL */
+  double* step_trace;      /* [warmup] step size used at each warm-up iteration, may be NULL */
+  int64_t divergences;     /* sampling phase */
+  double mean_accept;
+  double device_ms;        /* device time of all transitions */
+} pcvg_fit;                /* FullDataFit, adapt.hpp:56-62 */
+
+/* Model::initial_draw (model.hpp:44) on CounterRng(seed, stream): host, bit-exact. */
+pcvg_status pcvg_initial_draw(const pcvg_dataset* data, const pcvg_folds* folds,
+                              const pcvg_model_spec* spec, uint64_t seed, uint64_t stream,
+                              double* theta);
+pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_folds* folds,
+                                 const pcvg_model_spec* spec, const pcvg_adapt_config* cfg,
+                                 uint64_t seed, int32_t model_id, pcvg_fit* out);
+
 /* Shuffle benchmark (diagnostics.cpp:76-101, engine.cpp:464-480) of this context's shard on
  * device. Replicate r consumes CounterRng(seed, stream_key(Benchmark, r, 0, 0)) sequentially over
  * (model, non-failed fold, chain, block), one below(L) each; this shard's non-failed folds are

@@ -306,6 +306,93 @@ int pcvref_adapt(void* h, int32_t chains, int64_t warmup, int64_t draws, int32_t
   });
 }
 
+// Test oracle: adapt_full_data (adapt.cpp:96-185) restated over the reference's public pieces
+// (hmc_step, DualAveraging, WelfordDiag) with per-iteration traces, to localise differences
+// between the device adaptation and the reference. Returns the initial step size.
+int pcvref_adapt_trace(void* h, int32_t chains, int64_t warmup, int32_t n_lf, double target,
+                       uint64_t seed, int32_t model_id, double* init_step, double* step_trace,
+                       double* ap_trace, double* inv_mass_out, double* pos_out) {
+  return guarded([&] {
+    const pcv::Model& model = M(h);
+    const int d = model.dim(), sentinel = model.fold_count(), l = chains;
+    std::vector<pcv::ChainState> cs;
+    for (int c = 0; c < l; ++c) {
+      pcv::CounterRng rng(seed, pcv::stream_key(pcv::StreamKind::FullData,
+                                                static_cast<std::uint64_t>(model_id),
+                                                static_cast<std::uint64_t>(c)));
+      cs.push_back(pcv::ChainState{model.initial_draw(rng), rng, 0});
+    }
+    if (pos_out)
+      for (int c = 0; c < l; ++c) std::memcpy(pos_out + c * d, cs[c].position.data(), sizeof(double) * d);
+    pcv::KernelParams kp;
+    kp.n_leapfrog = n_lf;
+    kp.inv_mass_diag.assign(d, 1.0);
+    pcv::HmcWorkspace ws;
+    auto probe = [&](double e) {  // find_initial_step, adapt.cpp:17-43
+      pcv::ChainState ps{cs[0].position,
+                         pcv::CounterRng(seed, pcv::stream_key(pcv::StreamKind::StepInit,
+                                                               static_cast<std::uint64_t>(model_id))),
+                         0};
+      pcv::KernelParams k1{e, 1, kp.inv_mass_diag};
+      const auto info = pcv::hmc_step(ps, model, sentinel, k1, ws);
+      return info.divergent ? 0.0 : info.accept_prob;
+    };
+    double eps = 1.0;
+    const bool go_up = probe(eps) > 0.5;
+    bool done = false;
+    for (int i = 0; i < 50 && !done; ++i) {
+      if (go_up) {
+        eps *= 2.0;
+        if (probe(eps) <= 0.5) { eps /= 2.0; done = true; }
+      } else {
+        eps *= 0.5;
+        if (probe(eps) > 0.5) done = true;
+      }
+    }
+    kp.step_size = done ? eps : (go_up ? eps : 1e-8);
+    *init_step = kp.step_size;
+    pcv::DualAveraging da;
+    da.target = target;
+    da.restart(kp.step_size);
+    const long w_total = warmup;
+    const long w_init = std::min<long>(75, std::max<long>(1, w_total * 15 / 100));
+    const long w_final = std::min<long>(50, std::max<long>(1, w_total / 10));
+    long window = 25;
+    long window_end = std::min(w_total - w_final, w_init + window);
+    pcv::WelfordDiag acc(d);
+    for (long iter = 0; iter < w_total; ++iter) {
+      kp.step_size = da.current();
+      step_trace[iter] = kp.step_size;
+      double ap = 0.0;
+      for (auto& ch : cs) {
+        const auto info = pcv::hmc_step(ch, model, sentinel, kp, ws);
+        ap += info.divergent ? 0.0 : info.accept_prob;
+      }
+      ap /= l;
+      ap_trace[iter] = ap;
+      da.update(ap);
+      const bool in_slow = iter >= w_init && iter < w_total - w_final;
+      if (in_slow)
+        for (const auto& ch : cs) acc.add(ch.position);
+      if (in_slow && iter + 1 == window_end) {
+        if (acc.count() >= 2) {
+          const auto var = acc.variance();
+          const double n = static_cast<double>(acc.count());
+          for (int i = 0; i < d; ++i)
+            kp.inv_mass_diag[i] = std::max(var[i] * (n / (n + 5.0)) + 1e-3 * (5.0 / (n + 5.0)), 1e-10);
+        }
+        acc = pcv::WelfordDiag(d);
+        da.restart(da.current());
+        window *= 2;
+        long next_end = window_end + window;
+        if (next_end + 2 * window > w_total - w_final) next_end = w_total - w_final;
+        window_end = next_end;
+      }
+    }
+    std::memcpy(inv_mass_out, kp.inv_mass_diag.data(), sizeof(double) * d);
+  });
+}
+
 int pcvref_run_pcv(int32_t n_models, void** models, const int32_t* model_ids,
                    const pcvg_kernel* kernels, const double* const* banks,
                    const int64_t* bank_rows, const pcvg_run_config* c, int32_t threads,

@@ -75,6 +75,18 @@ class Report(C.Structure):
                 ("gpu_launches", C.c_int64)]
 
 
+class AdaptConfig(C.Structure):
+    _fields_ = [("chains", C.c_int32), ("warmup", C.c_int64), ("draws", C.c_int64),
+                ("n_leapfrog", C.c_int32), ("target_accept", C.c_double),
+                ("init_step_size", C.c_double)]
+
+
+class Fit(C.Structure):
+    _fields_ = [("step_size", C.c_double), ("inv_mass_diag", P_f64), ("draws", P_f64),
+                ("rhat", P_f64), ("ess", P_f64), ("step_trace", P_f64),
+                ("divergences", C.c_int64), ("mean_accept", C.c_double), ("device_ms", C.c_double)]
+
+
 def ptr(a, ctype):
     """Pointer into a contiguous numpy array (None passes NULL)."""
     if a is None:

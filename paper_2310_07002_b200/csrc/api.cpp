@@ -620,17 +620,20 @@ bool use_glm(const pcvg_ctx* ctx, const HostModel& m, int nch) {
   return tiles * glm_cluster_size(m.md.n, m.md.nc_pad, nch) >= 24;
 }
 
+// md_override: the model with a different kernel (step size, n_leapfrog, inverse mass) - used by
+// the full-data adaptation, whose kernel changes between transitions.
 void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const RunArgs& A,
-                   cudaStream_t st = nullptr) {
+                   cudaStream_t st = nullptr, const ModelDev* md_override = nullptr) {
   if (!st) st = ctx->stream;
+  const ModelDev& md = md_override ? *md_override : m.md;
   cudaError_t e;
   if (use_glm(ctx, m, S.nch)) {
-    e = launch_glm(m.md, S, A, st);
-  } else if (m.md.nb > 0 && ctx->policy != PCVG_KERNEL_GENERIC) {
-    e = launch_gauss(m.md, S, A, 0, st);  // group-batched hierarchical kernel
+    e = launch_glm(md, S, A, st);
+  } else if (md.nb > 0 && ctx->policy != PCVG_KERNEL_GENERIC) {
+    e = launch_gauss(md, S, A, 0, st);  // group-batched hierarchical kernel
   } else {
-    const int T = gauss_lanes_per_chain(m.md, S.nch);
-    e = launch_gauss(m.md, S, A, T, st);
+    const int T = gauss_lanes_per_chain(md, S.nch);
+    e = launch_gauss(md, S, A, T, st);
   }
   ++ctx->launches;
   ck(e, "kernel launch");
@@ -1066,7 +1069,8 @@ pcvg_status pcvg_hmc_chain(pcvg_ctx* ctx, int32_t slot, int32_t fold, int32_t ch
     const auto t = tr.download(ctx->stream);
     const auto d = dv.download(ctx->stream);
     std::copy(t.begin(), t.end(), trajectory);
-    if (divergent) std::copy(d.begin(), d.end(), divergent);
+    if (divergent)
+      for (size_t i = 0; i < d.size(); ++i) divergent[i] = (d[i] >> 1) & 1;
   }));
 }
 
@@ -1456,3 +1460,386 @@ pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
 }
 
 }  // extern "C"
+
+// ============================================================================ Step 1 on device
+namespace {
+
+// Model::initial_draw of each family (grouped_regression.cpp:177-188, radon.cpp:157-165,
+// seasonal_ar.cpp:122-131, logistic plugin) on the chain's FullData stream (host, glibc math).
+std::vector<double> initial_draw(const HostModel& m, const pcvg_model_spec* s, HostRng& rng) {
+  std::vector<double> th(m.dim, 0.0);
+  const int J = m.J;
+  switch (m.family) {
+    case PCVG_FAMILY_GROUPED: {
+      const int P = m.nc;
+      const double mu_a = rng.normal();
+      const double sig_a = std::fabs(rng.normal()) * std::sqrt(10.0);
+      const double sig_y = std::fabs(rng.normal()) * std::sqrt(10.0);
+      for (int g = 0; g < J; ++g) th[g] = mu_a + sig_a * rng.normal();
+      for (int p = 0; p < P; ++p) th[J + p] = rng.normal();
+      th[J + P] = mu_a;
+      th[J + P + 1] = std::log(sig_a);
+      th[J + P + 2] = std::log(sig_y);
+      break;
+    }
+    case PCVG_FAMILY_RADON:
+      for (int g = 0; g < J; ++g) th[g] = rng.normal();
+      th[J] = rng.normal();
+      th[J + 1] = 2.0 * rng.normal();
+      th[J + 2] = std::log(gamma_draw(rng, 6.0, 9.0));
+      th[J + 3] = std::log(gamma_draw(rng, 10.0, 10.0));
+      break;
+    case PCVG_FAMILY_SEASONAL_AR: {
+      const int p = s->ar_order, q = s->dummies;
+      for (int i = 0; i < p; ++i) {
+        const double w = beta_draw(rng, 5.0, 5.0);
+        th[i] = std::log(w) - std::log1p(-w);
+      }
+      for (int j = 0; j <= q; ++j) th[p + j] = rng.normal();
+      th[p + q + 1] = std::log(std::fabs(rng.normal()));
+      break;
+    }
+    default:  // logistic plugin: independent standard normals
+      for (double& t : th) t = rng.normal();
+  }
+  return th;
+}
+
+// DualAveraging, adapt.hpp:15-44.
+struct DualAveraging {
+  double target = 0.8, gamma = 0.05, t0 = 10.0, kappa = 0.75;
+  double mu = 0.0, log_eps = 0.0, log_eps_bar = 0.0, h_bar = 0.0;
+  long iter = 0;
+  void restart(double step) {
+    mu = std::log(10.0 * step);
+    log_eps = std::log(step);
+    log_eps_bar = log_eps;
+    h_bar = 0.0;
+    iter = 0;
+  }
+  void update(double ap) {
+    ++iter;
+    const double w = 1.0 / (iter + t0);
+    h_bar = (1.0 - w) * h_bar + w * (target - ap);
+    log_eps = mu - std::sqrt(static_cast<double>(iter)) / gamma * h_bar;
+    const double w2 = std::pow(static_cast<double>(iter), -kappa);
+    log_eps_bar = w2 * log_eps + (1.0 - w2) * log_eps_bar;
+  }
+  double current() const { return std::exp(log_eps); }
+  double averaged() const { return std::exp(log_eps_bar); }
+};
+
+// StepInfo::accept_prob from the kernel's energies (hmc.cpp:79-92): 0 when divergent.
+double accept_prob(double h0, double h1, int32_t flags) {
+  if (flags & 2) return 0.0;
+  const double dh = h1 - h0;
+  return dh <= 0.0 ? 1.0 : std::exp(-dh);
+}
+
+// Chains of the adaptation: positions from the host, device streams continuing each host stream.
+std::unique_ptr<ChainSet> adapt_chains(const HostModel& m, const std::vector<std::vector<double>>& pos,
+                                       const std::vector<HostRng>& rngs, uint64_t stream0) {
+  const int L = static_cast<int>(pos.size());
+  auto cs = std::make_unique<ChainSet>();
+  cs->alloc(L, m.dim, 1);
+  std::vector<double> p(2 * static_cast<size_t>(m.dim) * L, 0.0);
+  std::vector<uint64_t> st(L), rp(L);
+  std::vector<double> cached(L);
+  std::vector<int8_t> has(L);
+  for (int c = 0; c < L; ++c) {
+    for (int d = 0; d < m.dim; ++d) p[static_cast<size_t>(d) * L + c] = pos[c][d];
+    st[c] = stream0 == 0 ? 0 : stream0;
+    rp[c] = rngs[c].position();
+    cached[c] = rngs[c].cached();
+    has[c] = rngs[c].has_cached() ? 1 : 0;
+  }
+  ck(cudaMemcpy(cs->pos.p, p.data(), sizeof(double) * p.size(), cudaMemcpyHostToDevice), "upload");
+  ck(cudaMemset(cs->grad.p, 0, sizeof(double) * cs->grad.n), "memset");
+  ck(cudaMemset(cs->cur.p, 0, L), "memset");
+  ck(cudaMemset(cs->div.p, 0, sizeof(int64_t) * L), "memset");
+  ck(cudaMemset(cs->warm.p, 0, sizeof(double) * L), "memset");
+  ck(cudaMemcpy(cs->rpos.p, rp.data(), sizeof(uint64_t) * L, cudaMemcpyHostToDevice), "upload");
+  ck(cudaMemcpy(cs->cached.p, cached.data(), sizeof(double) * L, cudaMemcpyHostToDevice), "upload");
+  ck(cudaMemcpy(cs->has.p, has.data(), L, cudaMemcpyHostToDevice), "upload");
+  cs->fold_override.upload(std::vector<int>(L, m.K));  // full-data sentinel fold
+  return cs;
+}
+
+// param_rhat / param_ess (adapt.cpp:45-92) of parameter p over the bank [draws][L][dim].
+double param_rhat(const std::vector<double>& bank, int L, int64_t n, int dim, int p) {
+  double w = 0.0, grand = 0.0;
+  std::vector<double> means(L);
+  for (int c = 0; c < L; ++c) {
+    double mm = 0.0;
+    for (int64_t i = 0; i < n; ++i) mm += bank[(i * L + c) * dim + p];
+    mm /= n;
+    means[c] = mm;
+    grand += mm / L;
+    double ss = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double v = bank[(i * L + c) * dim + p];
+      ss += (v - mm) * (v - mm);
+    }
+    w += ss / (n - 1) / L;
+  }
+  double b = 0.0;
+  for (int c = 0; c < L; ++c) b += (means[c] - grand) * (means[c] - grand);
+  b *= static_cast<double>(n) / (L - 1);
+  if (!(w > 0.0)) return std::numeric_limits<double>::quiet_NaN();
+  return std::sqrt(((n - 1.0) / n * w + b / n) / w);
+}
+
+double param_ess(const std::vector<double>& bank, int L, int64_t n, int dim, int p, int bsz) {
+  const int64_t a = n / bsz;
+  if (a < 2) return std::numeric_limits<double>::quiet_NaN();
+  double grand = 0.0;
+  for (int c = 0; c < L; ++c)
+    for (int64_t i = 0; i < n; ++i) grand += bank[(i * L + c) * dim + p];
+  grand /= static_cast<double>(L) * n;
+  double ss_naive = 0.0, ss_batch = 0.0;
+  for (int c = 0; c < L; ++c) {
+    for (int64_t i = 0; i < n; ++i) {
+      const double v = bank[(i * L + c) * dim + p];
+      ss_naive += (v - grand) * (v - grand);
+    }
+    for (int64_t h = 0; h < a; ++h) {
+      double bm = 0.0;
+      for (int64_t i = h * bsz; i < (h + 1) * bsz; ++i) bm += bank[(i * L + c) * dim + p];
+      bm /= bsz;
+      ss_batch += (bm - grand) * (bm - grand);
+    }
+  }
+  const double s2 = ss_naive / (static_cast<double>(L) * n - 1);
+  const double sigma2 = bsz * ss_batch / (static_cast<double>(L) * a - 1);
+  if (!(sigma2 > 0.0)) return std::numeric_limits<double>::quiet_NaN();
+  return static_cast<double>(L) * n * s2 / sigma2;
+}
+
+}  // namespace
+
+extern "C" pcvg_status pcvg_initial_draw(const pcvg_dataset* data, const pcvg_folds* folds,
+                                         const pcvg_model_spec* spec, uint64_t seed, uint64_t stream,
+                                         double* theta) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] {
+    if (!data || !folds || !spec || !theta) throw Error(PCVG_INVALID_INPUT, "null argument");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+    // host-only: the model layout is needed for the dimensions, not the device
+    HostModel m;
+    m.family = spec->family;
+    switch (spec->family) {
+      case PCVG_FAMILY_GROUPED: m.J = n_groups(data); m.nc = data->n_cov; m.ng = data->n_cov + 3; break;
+      case PCVG_FAMILY_RADON: m.J = n_groups(data); m.nc = 1; m.ng = 4; break;
+      case PCVG_FAMILY_SEASONAL_AR: m.J = 0; m.nc = spec->ar_order + spec->dummies; m.ng = m.nc + 2; break;
+      case PCVG_FAMILY_LOGISTIC: m.J = 0; m.nc = data->n_cov; m.ng = data->n_cov + 1; break;
+      default: throw Error(PCVG_INVALID_INPUT, "model family not available");
+    }
+    m.dim = m.J + m.ng;
+    HostRng rng(seed, stream);
+    const auto th = initial_draw(m, spec, rng);
+    std::copy(th.begin(), th.end(), theta);
+    (void)folds;
+    (void)count;
+  }));
+}
+
+extern "C" pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* data,
+                                            const pcvg_folds* folds, const pcvg_model_spec* spec,
+                                            const pcvg_adapt_config* cfg, uint64_t seed,
+                                            int32_t model_id, pcvg_fit* out) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !cfg || !out || !data || !spec) throw Error(PCVG_INVALID_INPUT, "null argument");
+    if (cfg->chains < 1 || cfg->warmup < 1 || cfg->draws < 1)  // adapt.cpp:97-99
+      throw Error(PCVG_INVALID_INPUT, "full-data config needs chains, warmup, draws >= 1");
+    if (cfg->n_leapfrog < 1) throw Error(PCVG_INVALID_INPUT, "n_leapfrog must be >= 1");
+    if (cfg->chains > 64) throw Error(PCVG_INVALID_INPUT, "at most 64 full-data chains on device");
+    if (!out->inv_mass_diag || !out->draws) throw Error(PCVG_INVALID_INPUT, "fit output buffers missing");
+    require_device(ctx);
+    // the model in device layout; kernel and bank are placeholders until adapted
+    const int dim_cap = (data->group_id ? n_groups(data) : 0) + data->n_cov + 8;
+    std::vector<double> ones(dim_cap, 1.0), zero(dim_cap, 0.0);
+    pcvg_kernel k0{1.0, cfg->n_leapfrog, ones.data()};
+    auto hm = build_model(data, folds, spec, &k0, zero.data(), 1, model_id);
+    const HostModel& m = *hm;
+    const int d = m.dim, L = cfg->chains;
+    if (d < 1) throw Error(PCVG_INVALID_INPUT, "model has no parameters");
+    ModelDev md = m.md;
+    DevBuf<double> im;
+    std::vector<double> inv_mass(d, 1.0);
+    im.upload(inv_mass);
+    md.inv_mass = im.p;
+    md.n_lf = cfg->n_leapfrog;
+
+    // chains from the prior on their FullData streams (adapt.cpp:104-110)
+    std::vector<std::vector<double>> pos;
+    std::vector<HostRng> rngs;
+    for (int c = 0; c < L; ++c) {
+      HostRng rng(seed, stream_key(PCVG_STREAM_FULL_DATA, static_cast<uint64_t>(model_id),
+                                   static_cast<uint64_t>(c), 0));
+      pos.push_back(initial_draw(m, spec, rng));
+      rngs.push_back(rng);
+    }
+    auto cs = adapt_chains(m, pos, rngs, 0);
+    {
+      std::vector<uint64_t> st(L);
+      for (int c = 0; c < L; ++c)
+        st[c] = stream_key(PCVG_STREAM_FULL_DATA, static_cast<uint64_t>(model_id), static_cast<uint64_t>(c), 0);
+      ck(cudaMemcpy(cs->stream.p, st.data(), sizeof(uint64_t) * L, cudaMemcpyHostToDevice), "upload");
+    }
+    const ChainsDev S = cs->view(1, 0, seed, 0);
+    DevBuf<double> h0b, h1b;
+    DevBuf<int32_t> flb;
+    DevBuf<double> trb;
+    float ms_total = 0.f;
+    auto trace = [&](const ChainSet& set, const ChainsDev& SS, int64_t n_iters, bool positions,
+                     std::vector<double>& h0, std::vector<double>& h1, std::vector<int32_t>& fl,
+                     std::vector<double>* traj) {
+      const size_t rows = static_cast<size_t>(n_iters) * SS.nch;
+      if (h0b.n < rows) { h0b.alloc(rows); h1b.alloc(rows); flb.alloc(rows); }
+      if (positions && trb.n < rows * d) trb.alloc(rows * d);
+      RunArgs a = make_args(kModeChain, n_iters);
+      a.out_a = h0b.p;
+      a.out_b = h1b.p;
+      a.traj_div = flb.p;
+      a.traj = positions ? trb.p : nullptr;
+      ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
+      launch_family(ctx, m, SS, a, ctx->stream, &md);
+      ck(cudaEventRecord(ctx->ev1, ctx->stream), "event");
+      ck(cudaEventSynchronize(ctx->ev1), "adapt");
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+      ms_total += ms;
+      h0.resize(rows);
+      h1.resize(rows);
+      fl.resize(rows);
+      ck(cudaMemcpy(h0.data(), h0b.p, sizeof(double) * rows, cudaMemcpyDeviceToHost), "download");
+      ck(cudaMemcpy(h1.data(), h1b.p, sizeof(double) * rows, cudaMemcpyDeviceToHost), "download");
+      ck(cudaMemcpy(fl.data(), flb.p, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost), "download");
+      if (positions && traj) {
+        traj->resize(rows * d);
+        ck(cudaMemcpy(traj->data(), trb.p, sizeof(double) * rows * d, cudaMemcpyDeviceToHost), "download");
+      }
+      (void)set;
+    };
+    std::vector<double> h0, h1, tr;
+    std::vector<int32_t> fl;
+
+    // first step size: doubling search on chain 0's start (adapt.cpp:17-43)
+    double step = cfg->init_step_size;
+    if (!(step > 0.0)) {
+      const uint64_t sst = stream_key(PCVG_STREAM_STEP_INIT, static_cast<uint64_t>(model_id), 0, 0);
+      auto probe = [&](double e) {
+        HostRng fresh(seed, sst);
+        auto ps = adapt_chains(m, {pos[0]}, {fresh}, 0);
+        ck(cudaMemcpy(ps->stream.p, &sst, sizeof sst, cudaMemcpyHostToDevice), "upload");
+        ModelDev saved = md;
+        md.step = e;
+        md.n_lf = 1;
+        const ChainsDev PS = ps->view(1, 0, seed, 0);
+        launch_family(ctx, m, PS, make_args(kModeEval, 0), ctx->stream, &md);
+        trace(*ps, PS, 1, false, h0, h1, fl, nullptr);
+        md = saved;
+        return accept_prob(h0[0], h1[0], fl[0]);
+      };
+      double eps = 1.0;
+      const bool go_up = probe(eps) > 0.5;
+      bool done = false;
+      for (int i = 0; i < 50 && !done; ++i) {
+        if (go_up) {
+          eps *= 2.0;
+          if (probe(eps) <= 0.5) { eps /= 2.0; done = true; }
+        } else {
+          eps *= 0.5;
+          if (probe(eps) > 0.5) done = true;
+        }
+      }
+      step = done ? eps : (go_up ? eps : 1e-8);
+    }
+    md.step = step;
+    launch_family(ctx, m, S, make_args(kModeEval, 0), ctx->stream, &md);  // grad / lp0 at the starts
+
+    // windowed adaptation (adapt.cpp:112-185)
+    DualAveraging da;
+    da.target = cfg->target_accept;
+    da.restart(step);
+    const int64_t w_total = cfg->warmup;
+    const int64_t w_init = std::min<int64_t>(75, std::max<int64_t>(1, w_total * 15 / 100));
+    const int64_t w_final = std::min<int64_t>(50, std::max<int64_t>(1, w_total / 10));
+    int64_t window = 25;
+    int64_t window_end = std::min(w_total - w_final, w_init + window);
+    std::vector<double> wx(d, 0.0), wx2(d, 0.0);  // WelfordDiag(d), centre 0 (accum.cpp:59-74)
+    int64_t wcount = 0;
+    int64_t window_div = 0, window_steps = 0;
+    for (int64_t iter = 0; iter < w_total; ++iter) {
+      md.step = da.current();
+      if (out->step_trace) out->step_trace[iter] = md.step;
+      const bool in_slow = iter >= w_init && iter < w_total - w_final;
+      trace(*cs, S, 1, in_slow, h0, h1, fl, &tr);
+      double ap = 0.0;
+      int64_t n_div = 0;
+      for (int c = 0; c < L; ++c) {
+        ap += accept_prob(h0[c], h1[c], fl[c]);
+        n_div += (fl[c] >> 1) & 1;
+      }
+      ap /= L;
+      da.update(ap);
+      window_div += n_div;
+      window_steps += L;
+      if (in_slow) {
+        for (int c = 0; c < L; ++c)
+          for (int i = 0; i < d; ++i) {
+            const double v = tr[static_cast<size_t>(c) * d + i];
+            wx[i] += v;
+            wx2[i] += v * v;
+          }
+        wcount += L;
+      }
+      if (in_slow && iter + 1 == window_end) {
+        if (wcount >= 2) {
+          const double n = static_cast<double>(wcount);
+          for (int i = 0; i < d; ++i) {
+            const double var = (wx2[i] - wx[i] * wx[i] / wcount) / (wcount - 1);
+            const double v = var * (n / (n + 5.0)) + 1e-3 * (5.0 / (n + 5.0));
+            inv_mass[i] = std::max(v, 1e-10);
+          }
+          ck(cudaMemcpy(im.p, inv_mass.data(), sizeof(double) * d, cudaMemcpyHostToDevice), "upload");
+        }
+        std::fill(wx.begin(), wx.end(), 0.0);
+        std::fill(wx2.begin(), wx2.end(), 0.0);
+        wcount = 0;
+        da.restart(da.current());
+        window *= 2;
+        int64_t next_end = window_end + window;
+        if (next_end + 2 * window > w_total - w_final) next_end = w_total - w_final;
+        window_end = next_end;
+      }
+      if (window_steps >= 100 * L) {  // persistent-failure check (adapt.cpp:169-180)
+        if (window_div > window_steps / 2)
+          throw Error(PCVG_ADAPTATION_FAILURE, "full-data adaptation failed: chains diverging persistently");
+        window_div = 0;
+        window_steps = 0;
+      }
+    }
+    md.step = da.averaged();
+
+    // frozen-kernel draws fill the bank (adapt.cpp:194-210), one launch
+    trace(*cs, S, cfg->draws, true, h0, h1, fl, &tr);
+    double acc = 0.0;
+    int64_t ndiv = 0;
+    for (size_t r = 0; r < h0.size(); ++r) {
+      acc += accept_prob(h0[r], h1[r], fl[r]);
+      ndiv += (fl[r] >> 1) & 1;
+    }
+    out->step_size = md.step;
+    std::copy(inv_mass.begin(), inv_mass.end(), out->inv_mass_diag);
+    std::copy(tr.begin(), tr.end(), out->draws);
+    out->divergences = ndiv;
+    out->mean_accept = acc / (static_cast<double>(L) * cfg->draws);
+    const int ess_b = std::max(1, static_cast<int>(std::sqrt(static_cast<double>(cfg->draws))));
+    for (int p = 0; p < d; ++p) {
+      if (out->rhat) out->rhat[p] = L >= 2 ? param_rhat(tr, L, cfg->draws, d, p) : std::numeric_limits<double>::quiet_NaN();
+      if (out->ess) out->ess[p] = param_ess(tr, L, cfg->draws, d, p, ess_b);
+    }
+    out->device_ms = ms_total;
+  }));
+}

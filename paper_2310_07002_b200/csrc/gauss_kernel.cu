@@ -869,11 +869,15 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
       }
       continue;
     }
-    if (A.mode == kModeChain) {
+    if (A.mode == kModeChain) {  // trace: record (it, chain) = it * nch + c
       if (t == 0) {
-        for (int d = 0; d < M.dim; ++d)
-          A.traj[it * M.dim + d] = S.pos[cur * plane + static_cast<size_t>(d) * nch + c];
-        A.traj_div[it] = divergent ? 1 : 0;
+        const size_t row = static_cast<size_t>(it) * nch + c;
+        if (A.traj)
+          for (int d = 0; d < M.dim; ++d)
+            A.traj[row * M.dim + d] = S.pos[cur * plane + static_cast<size_t>(d) * nch + c];
+        if (A.traj_div) A.traj_div[row] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
+        if (A.out_a) A.out_a[row] = h0;
+        if (A.out_b) A.out_b[row] = h1;
       }
       continue;
     }

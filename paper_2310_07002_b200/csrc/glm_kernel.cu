@@ -638,7 +638,12 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
           A.out_b[gc] = h1;
           A.out_flags[gc] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
         }
-        if (cvalid && writer && A.mode == kModeChain) A.traj_div[it] = divergent ? 1 : 0;
+        if (cvalid && writer && A.mode == kModeChain) {  // trace row (it, chain) = it * nch + gc
+          const size_t row = static_cast<size_t>(it) * nch + gc;
+          if (A.traj_div) A.traj_div[row] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
+          if (A.out_a) A.out_a[row] = h0;
+          if (A.out_b) A.out_b[row] = h1;
+        }
       }
       // rank 0's proposal writes must be visible to the cluster before the next half kick
       if (cs > 1) cooperative_groups::this_cluster().sync();
@@ -650,7 +655,8 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
 #pragma unroll
           for (int j = 0; j < G::OWN; ++j) {
             const int k = ok + kOwners * j;
-            if (k < dim) A.traj[it * dim + k] = S.pos[cu * plane + static_cast<size_t>(k) * nch + ogc];
+            if (k < dim && A.traj)
+              A.traj[(static_cast<size_t>(it) * nch + ogc) * dim + k] = S.pos[cu * plane + static_cast<size_t>(k) * nch + ogc];
           }
         }
         continue;

@@ -55,6 +55,12 @@ class HostRng {
     have_ = 0;
     has_cached_ = false;
   }
+  // Device stream state (device_common.cuh ChainRng): u32 words consumed, Box-Muller cache.
+  uint64_t position() const {
+    return 4 * ((static_cast<uint64_t>(ctr_[1]) << 32) | ctr_[0]) - static_cast<uint64_t>(have_);
+  }
+  double cached() const { return cached_; }
+  bool has_cached() const { return has_cached_; }
   uint64_t below(uint64_t n) {
     const uint64_t bound = n * ((~uint64_t{0}) / n);
     for (;;) {
@@ -111,6 +117,13 @@ inline double gamma_draw(HostRng& rng, double a, double r) {
     const double u = rng.uniform();
     if (std::log(u) < 0.5 * x * x + d - d * v + d * std::log(v)) return boost * d * v / r;
   }
+}
+
+// beta_draw (priors.hpp:50-54).
+inline double beta_draw(HostRng& rng, double a, double b) {
+  const double x = gamma_draw(rng, a, 1.0);
+  const double y = gamma_draw(rng, b, 1.0);
+  return x / (x + y);
 }
 
 // Stable argsort by time (std::stable_sort in folds.cpp:95-98).

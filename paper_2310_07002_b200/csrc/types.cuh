@@ -14,7 +14,8 @@ enum Mode : int {
   kModeWarmup = 1,  // Step 2: hmc steps, Sigma log_pred into warm_sum (hmc.cpp:121-149)
   kModeSample = 2,  // Step 3: hmc steps, ScoreAccum::observe (engine.cpp:342-381)
   kModeProbe = 3,   // one hmc step with injected momentum / uniform (parity probe)
-  kModeChain = 4,   // hmc steps writing the trajectory (parity probe)
+  kModeChain = 4,   // hmc steps recording every (transition, chain): position, flags, h0, h1
+                    // (parity probe, full-data adaptation)
   kModePred = 5     // log_pred at the stored position (parity probe)
 };
 
@@ -134,8 +135,8 @@ struct RunArgs {
   double* out_a;  // probe: h0 / eval: log joint / pred: log_pred   [nch]
   double* out_b;  // probe: h1                                      [nch]
   int32_t* out_flags;  // probe: accepted | divergent << 1           [nch]
-  double* traj;        // chain mode: [n_iters][dim]
-  int32_t* traj_div;   // chain mode: [n_iters]
+  double* traj;        // chain mode: [n_iters][nch][dim] or null
+  int32_t* traj_div;   // chain mode: [n_iters][nch] accepted | divergent << 1, or null
 };
 
 }  // namespace pcvg

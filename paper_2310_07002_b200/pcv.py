@@ -114,6 +114,9 @@ def load():
                                            i64, pf, pi32])
     _sig(lib, "pcvg_merge_bench", i32, [i32, i32, P(abi.RunConfig), i64, i32, P(abi.FoldTable), pf,
                                         P(abi.Report)])
+    _sig(lib, "pcvg_adapt_full_data", i32, [vp, P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec),
+                                            P(abi.AdaptConfig), u64, i32, P(abi.Fit)])
+    _sig(lib, "pcvg_initial_draw", i32, [P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec), u64, u64, pf])
     if lib.pcvg_abi_version() != abi.ABI_VERSION:
         raise ImportError("libpcvg.so ABI version mismatch")
     _lib = lib
@@ -317,6 +320,17 @@ class ModelInput:
     model_id: int = 0
 
 
+@dataclass
+class AdaptConfig:
+    """pcv::AdaptConfig (adapt.hpp:47-54)."""
+    chains: int = 4
+    warmup: int = 1000
+    draws: int = 2000
+    n_leapfrog: int = 32
+    target_accept: float = 0.8
+    init_step_size: float = 0.0
+
+
 def RunConfig(**kw):
     """pcv::RunConfig defaults (engine.hpp:21-45) as a pcvg_run_config struct."""
     return abi.run_config(**kw)
@@ -369,6 +383,29 @@ class Context:
 
     def set_kernel_policy(self, policy):
         self._chk(self.lib.pcvg_set_kernel_policy(self.h, policy))
+
+    def adapt_full_data(self, model, cfg=None, seed=1, model_id=0, trace=False):
+        """pcv::adapt_full_data (adapt.cpp:96-221) on the device: returns a FullDataFit with the
+        tuned kernel and the (chains*draws) x dim bank, plus rhat / ess per parameter."""
+        cfg = cfg or AdaptConfig()
+        ac = abi.AdaptConfig(chains=cfg.chains, warmup=cfg.warmup, draws=cfg.draws,
+                             n_leapfrog=cfg.n_leapfrog, target_accept=cfg.target_accept,
+                             init_step_size=cfg.init_step_size)
+        d = model.dim()
+        im = np.zeros(d)
+        bank = np.zeros((cfg.chains * cfg.draws, d))
+        rh, es = np.zeros(d), np.zeros(d)
+        st = np.zeros(cfg.warmup) if trace else None
+        fit = abi.Fit(inv_mass_diag=_p(im), draws=_p(bank), rhat=_p(rh), ess=_p(es), step_trace=_p(st))
+        self._chk(self.lib.pcvg_adapt_full_data(self.h, C.byref(model.data.struct),
+                                                C.byref(model.fold_arrays.struct),
+                                                C.byref(model.spec.struct), C.byref(ac), seed, model_id,
+                                                C.byref(fit)))
+        out = FullDataFit(KernelParams(fit.step_size, cfg.n_leapfrog, im), bank)
+        out.rhat_per_param, out.ess_per_param = rh, es
+        out.divergences, out.mean_accept, out.device_ms = fit.divergences, fit.mean_accept, fit.device_ms
+        out.step_trace = st
+        return out
 
     def dim(self, slot):
         d = C.c_int32()
@@ -506,6 +543,20 @@ def merge_bench(n_models, K, cfg, iter_count, final, cols, bench_max):
     _check(lib.pcvg_merge_bench(n_models, K, C.byref(cfg), iter_count, int(final), C.byref(ft), _p(bm),
                                 C.byref(rep)))
     return abi.report_dict(rep, arrs, n_models)
+
+
+def initial_draw(model, seed, stream):
+    """Model::initial_draw (model.hpp:44) on CounterRng(seed, stream) (host, bit-exact)."""
+    out = np.zeros(model.dim())
+    _check(load().pcvg_initial_draw(C.byref(model.data.struct), C.byref(model.fold_arrays.struct),
+                                    C.byref(model.spec.struct), seed, stream, _p(out)))
+    return out
+
+
+def adapt_full_data(model, cfg=None, seed=1, model_id=0, device=0):
+    """pcv::adapt_full_data (adapt.hpp:64-69) on one GPU."""
+    with Context(device) as ctx:
+        return ctx.adapt_full_data(model, cfg, seed, model_id)
 
 
 def run_pcv(inputs, cfg, device=0):

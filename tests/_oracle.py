@@ -96,6 +96,8 @@ def ref():
         _sig(lib, "pcvref_log_lik_test", f64, [vp, pf64, i32])
         _sig(lib, "pcvref_initial_draw", None, [vp, u64, u64, pf64])
         _sig(lib, "pcvref_pred_derivs", C.c_int, [vp, pf64, i32, pf64, pf64])
+        _sig(lib, "pcvref_adapt_trace", C.c_int, [vp, i32, i64, i32, f64, u64, i32, pf64, pf64, pf64,
+                                                   pf64, pf64])
         _sig(lib, "pcvref_pred_sample", C.c_int, [vp, pf64, i32, u64, u64, i32, pf64])
         _sig(lib, "pcvref_leapfrog", i32, [vp, i32, f64, i32, pf64, pf64, pf64])
         _sig(lib, "pcvref_hmc_chain", C.c_int, [vp, i32, f64, i32, pf64, u64, u64, pf64, i64, pf64,
@@ -264,6 +266,16 @@ class RModel:
                                        n_steps, _p(traj), _p(div, C.c_int32), _p(acc, C.c_int32), _p(dh))
         assert rc == 0, self.lib.pcvref_last_error()
         return traj, div
+
+    def adapt_trace(self, chains=4, warmup=30, n_lf=32, target=0.8, seed=1, model_id=0):
+        init = f64()
+        st, ap = np.zeros(warmup), np.zeros(warmup)
+        im = np.zeros(self.dim)
+        pos = np.zeros((chains, self.dim))
+        rc = self.lib.pcvref_adapt_trace(self.h, chains, warmup, n_lf, target, seed, model_id, C.byref(init),
+                                         _p(st), _p(ap), _p(im), _p(pos))
+        assert rc == 0, self.lib.pcvref_last_error()
+        return dict(init_step=init.value, step_trace=st, ap_trace=ap, inv_mass=im, start=pos)
 
     def adapt(self, chains=4, warmup=1000, draws=2000, n_lf=32, target=0.8, init_step=0.0,
               seed=1, model_id=0):

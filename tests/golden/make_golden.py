@@ -249,11 +249,41 @@ def make_score(base, score):
     np.savez_compressed(os.path.join(HERE, f"{base}_{SCORE_NAME[score]}.npz"), **out)
 
 
+# Short full-data adaptations by the reference (adapt.cpp:96-221) on fixture inputs, short enough
+# that the device run follows the same chain trajectories: tests/golden/adapt_short.npz.
+ADAPT_SHORT = dict(chains=4, warmup=30, draws=10, n_lf=32)
+ADAPT_BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks",
+               "seasonal_hvblock", "logistic_loo"]
+
+
+def make_adapt_short():
+    out = {}
+    for base in ADAPT_BASES:
+        d, f, models, z = load(base)
+        fa = f.arrays()
+        for m, (kw, _, _) in enumerate(models):
+            rm = O.RModel(d, fa, abi.SpecArrays(**kw))
+            fit = rm.adapt(seed=3, model_id=m, **ADAPT_SHORT)
+            out[f"{base}:{m}:step"] = np.float64(fit["step_size"])
+            out[f"{base}:{m}:inv_mass"] = fit["inv_mass_diag"]
+            out[f"{base}:{m}:bank"] = fit["bank"]
+            out[f"{base}:{m}:accept"] = np.float64(fit["mean_accept"])
+            out[f"{base}:{m}:div"] = np.int64(fit["divergences"])
+            if m == 0:  # per-iteration traces of the restated loop (ref_shim pcvref_adapt_trace)
+                tr = rm.adapt_trace(chains=4, warmup=30, seed=3, model_id=m)
+                out[f"{base}:{m}:init_step"] = np.float64(tr["init_step"])
+                out[f"{base}:{m}:step_trace"] = tr["step_trace"]
+                out[f"{base}:{m}:ap_trace"] = tr["ap_trace"]
+    np.savez_compressed(os.path.join(HERE, "adapt_short.npz"), **out)
+
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(CONFIGS) + ["scores"]
+    names = sys.argv[1:] or list(CONFIGS) + ["scores", "adapt"]
     for nm in names:
         print(nm, flush=True)
-        if nm == "scores":
+        if nm == "adapt":
+            make_adapt_short()
+        elif nm == "scores":
             for base, scores in SCORE_FIXTURES.items():
                 for sc in scores:
                     make_score(base, sc)

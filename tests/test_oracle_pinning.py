@@ -361,3 +361,31 @@ def test_pred_hooks_match_reference_bitwise(name):
                 b1, b2 = rm.pred_derivs(t, fold)
                 assert np.array_equal(a1, b1) and np.array_equal(a2, b2)
                 assert np.array_equal(om.pred_sample(t, fold, 3, 11, 3), rm.pred_sample(t, fold, 3, 11, 3))
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks",
+                                  "seasonal_hvblock", "logistic_loo"])
+def test_initial_draw_matches_reference_bitwise(name):
+    """pcvg_initial_draw (host, the full-data chains' starts) == Model::initial_draw of the
+    reference (grouped_regression.cpp:177-188, radon.cpp:157-165, seasonal_ar.cpp:122-131)."""
+    from paper_2310_07002_b200 import pcv
+    case = Case(name)
+    for m, model in enumerate(case.models):
+        rm = O.RModel(case.data, case.fa, abi.SpecArrays(**case.kws[m]))
+        for c in range(4):
+            st = pcv.stream_key(abi.STREAM_FULL_DATA, m, c)
+            assert np.array_equal(pcv.initial_draw(model, 7, st), rm.initial_draw(7, st))
+
+
+@pytest.mark.ref
+def test_adapt_trace_oracle_matches_reference():
+    """The traced restatement of adapt_full_data (ref_shim pcvref_adapt_trace, used to pin the
+    device adaptation step by step) reproduces the reference's own inverse mass."""
+    z = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "adapt_short.npz"))
+    for name in ("cfg1_linreg_loo", "radon_logo"):
+        case = Case(name)
+        rm = O.RModel(case.data, case.fa, abi.SpecArrays(**case.kws[0]))
+        tr = rm.adapt_trace(chains=4, warmup=30, seed=3, model_id=0)
+        assert np.array_equal(tr["inv_mass"], z[f"{name}:0:inv_mass"])
+        assert np.array_equal(tr["step_trace"], z[f"{name}:0:step_trace"])
