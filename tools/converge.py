@@ -1,0 +1,61 @@
+"""Wall-clock to R-hat-converged elpd (the second half of BASELINE.json's metric): a full PCV run
+with the early-stop rule (R-hat max within the 0.99 benchmark quantile and MCSE below
+the epistemic SE, checked every `--every` iterations) through the public API, with host inputs.
+
+  python tools/converge.py [--config cfg2] [--iters 1000] [--every 50]
+
+Prints one JSON line: iterations run, wall-clock, device time, the elpd / delta and its errors,
+and the reference CPU path's projected time for the same chain-steps (measured rate on a sample).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in (ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "tests", "golden"), os.path.join(ROOT, "tools")):
+    sys.path.insert(0, p)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--every", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    from bench_configs import CONFIGS, cpu_sample
+    from parity_util import Case
+    from paper_2310_07002_b200 import abi, pcv
+    fixture, L, desc = CONFIGS[args.config]
+    case = Case(fixture)
+    cfg = abi.run_config(chains=L, iters=args.iters, warmup=args.warmup, batch_size=args.every, blocks=5,
+                         bench_draws=500, seed=1, checkpoint_every=args.every, early_stop=1)
+    inputs = [pcv.ModelInput(m, pcv.FullDataFit(kp, bank), i)
+              for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
+    t0 = time.perf_counter()
+    rep = pcv.run_pcv(inputs, cfg)
+    wall = time.perf_counter() - t0
+    chains = case.K * L * len(case.models)
+    steps = rep["iters_run"] + args.warmup
+    line = {"config": args.config, "workload": desc, "chains": chains, "iters_run": int(rep["iters_run"]),
+            "warmup": args.warmup, "check_every": args.every, "max_iters": args.iters,
+            "stopped_early": bool(rep["iters_run"] < args.iters), "wall_s": wall,
+            "device_s": (rep["warmup_ms"] + rep["sampling_ms"]) / 1e3,
+            "delta_hat": rep["delta_hat"], "mcse": rep["mcse"], "epistemic_se": rep["epistemic_se"],
+            "rhat_max": rep["rhat_max"], "verdict_quantile_value": rep["verdict_quantile_value"],
+            "verdict_pass": int(rep["verdict_pass"]), "chain_steps": chains * steps}
+    if not args.no_cpu:
+        threads = os.cpu_count() or 1
+        rate, kind, sample = cpu_sample(case, L, 8, 3, threads)
+        line["cpu"] = {"chain_steps_per_s": rate, "kind": kind, "cores": threads, "sample": sample,
+                       "projected_s_same_chain_steps": chains * steps / rate}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
