@@ -46,7 +46,7 @@ typedef enum {
   PCVG_FAMILY_RADON = 1,       /* RadonStyleModel         radon.hpp:18-64 */
   PCVG_FAMILY_SEASONAL_AR = 2, /* SeasonalARModel         seasonal_ar.hpp:22-61 */
   PCVG_FAMILY_LOGISTIC = 3,    /* new: Bernoulli-logit regression (BASELINE configs[1]) */
-  PCVG_FAMILY_RAT_GROWTH = 4   /* RatGrowthModel (rat_growth.hpp) - not yet on device */
+  PCVG_FAMILY_RAT_GROWTH = 4   /* RatGrowthModel (rat_growth.hpp:20-63); per_subject_slope = M_A */
 } pcvg_family;
 
 typedef enum { PCVG_SCORE_LOGS = 0, PCVG_SCORE_HS = 1, PCVG_SCORE_DSS = 2 } pcvg_score; /* model.hpp:12 */
@@ -189,6 +189,8 @@ pcvg_status pcvg_simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_o
 /* simulate_radon_style (radon.cpp:216-240): n = houses, x = floor. */
 pcvg_status pcvg_simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y,
                                 double* x, int32_t* group_id);
+/* simulate_rat_growth (rat_growth.cpp:310-336): n = 5 * subjects, x = time. */
+pcvg_status pcvg_simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* group_id);
 /* simulate_seasonal_ar (seasonal_ar.cpp:167-205): n = months - p, n_cov = p + q. */
 pcvg_status pcvg_simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho,
                                    double seasonal_amp, double sigma, uint64_t seed, double* y,

@@ -273,6 +273,7 @@ struct pcvo_model {
   int J, P, dim;
   int32_t* mask; /* grouped covariate mask */
   int include_floor, p, q, rho_sym;
+  int per_subject; /* rat growth M_A (rat_growth.hpp:22-27) */
   /* per-fold test layout (fold_meta_, grouped_regression.cpp:27-47): segments of test rows
    * grouped by group in increasing group order, rows increasing within a group. */
   int64_t* fold_seg; /* [K+1] */
@@ -361,6 +362,11 @@ pcvo_model* pcvo_model_create(const pcvg_dataset* d, const pcvg_folds* f,
       m->dim = m->P + 1;
       m->J = 0;
       break;
+    case PCVG_FAMILY_RAT_GROWTH: /* rat_growth.cpp:13-48 */
+      if (!m->g || d->n_cov < 1) { set_err(PCVG_INVALID_INPUT, "growth model needs a group column and a time covariate"); pcvo_model_destroy(m); return NULL; }
+      m->per_subject = s->per_subject_slope != 0;
+      m->dim = m->per_subject ? 2 * m->J + 5 : m->J + 4;
+      break;
     default:
       set_err(PCVG_INVALID_INPUT, "family not in the oracle");
       pcvo_model_destroy(m);
@@ -368,7 +374,8 @@ pcvo_model* pcvo_model_create(const pcvg_dataset* d, const pcvg_folds* f,
   }
   /* Per-fold test segments. */
   const int K = m->K;
-  const int hier = (m->family == PCVG_FAMILY_GROUPED || m->family == PCVG_FAMILY_RADON);
+  const int hier = (m->family == PCVG_FAMILY_GROUPED || m->family == PCVG_FAMILY_RADON ||
+                    m->family == PCVG_FAMILY_RAT_GROWTH);
   const int J = hier ? m->J : 1;
   int64_t* grp_size = calloc(J, sizeof(int64_t));
   for (int64_t i = 0; i < n; ++i) grp_size[hier ? m->g[i] : 0]++;
@@ -477,6 +484,42 @@ static double seasonal_mean(const pcvo_model* m, const double* th, int64_t i) {
   for (int j = 0; j < m->q; ++j) mm += th[m->p + 1 + j] * xv(m, i, m->p + j);
   return mm;
 }
+/* rat_growth.cpp:50-63: layout M_A [alpha(J), beta(J), mu_a, mu_b, log s_a, log s_b, log s_y],
+ * M_B [alpha(J), beta, mu_a, log s_a, log s_y] */
+static int rat_mu_a(const pcvo_model* m) { return m->J + (m->per_subject ? m->J : 1); }
+static double rat_mean(const pcvo_model* m, const double* th, int64_t i) {
+  const int g = m->g[i];
+  const double t = xv(m, i, 0);
+  const double slope = m->per_subject ? th[m->J + g] : th[m->J];
+  return th[g] + slope * t;
+}
+/* math.hpp:46-90 dense Cholesky MVN (mvn_logpdf_chol), n <= 64 */
+static double mvn_logpdf_chol(const double* x, const double* mean, double* cov, int n) {
+  for (int j = 0; j < n; ++j) {
+    double dd = cov[j * n + j];
+    for (int k = 0; k < j; ++k) dd -= cov[j * n + k] * cov[j * n + k];
+    if (!(dd > 0.0) || !isfinite(dd)) return NEG_INF;
+    const double l = sqrt(dd);
+    cov[j * n + j] = l;
+    for (int i = j + 1; i < n; ++i) {
+      double sm = cov[i * n + j];
+      for (int k = 0; k < j; ++k) sm -= cov[i * n + k] * cov[j * n + k];
+      cov[i * n + j] = sm / l;
+    }
+  }
+  double r[64];
+  for (int i = 0; i < n; ++i) r[i] = x[i] - mean[i];
+  for (int i = 0; i < n; ++i) {
+    double sm = r[i];
+    for (int k = 0; k < i; ++k) sm -= cov[i * n + k] * r[k];
+    r[i] = sm / cov[i * n + i];
+  }
+  double q = 0.0, ld = 0.0;
+  for (int i = 0; i < n; ++i) q += r[i] * r[i];
+  for (int i = 0; i < n; ++i) ld += log(cov[i * n + i]);
+  return -0.5 * (n * kLog2Pi + 2.0 * ld + q);
+}
+
 /* logistic plugin (oracle/ref_plugins.cpp) */
 static double softplus(double t) { return (t > 0.0 ? t : 0.0) + log1p(exp(-fabs(t))); }
 static double sigmoid(double t) {
@@ -542,6 +585,40 @@ double pcvo_log_joint(const pcvo_model* m, const double* th, int32_t fold) {
       }
       for (int j = 0; j <= q; ++j) lp += normal_logpdf(th[p + j], 0.0, 1.0);
       lp += log_half_normal(sigma, 1.0) + th[p + q + 1];
+      return lp;
+    }
+    case PCVG_FAMILY_RAT_GROWTH: { /* rat_growth.cpp:65-109 */
+      const int base = rat_mu_a(m);
+      const double mu_a = th[base];
+      if (m->per_subject) {
+        const double mu_b = th[base + 1];
+        const double s_a = exp(th[base + 2]), s_b = exp(th[base + 3]), s_y = exp(th[base + 4]);
+        const double vy = s_y * s_y;
+        for (int64_t i = 0; i < m->n; ++i) {
+          const double mask = excluded(m, i, fold) ? 0.0 : 1.0;
+          lp += mask * normal_logpdf(m->y[i], rat_mean(m, th, i), vy);
+        }
+        for (int g = 0; g < J; ++g) {
+          lp += normal_logpdf(th[g], mu_a, s_a * s_a);
+          lp += normal_logpdf(th[J + g], mu_b, s_b * s_b);
+        }
+        lp += normal_logpdf(mu_a, 250.0, 20.0) + normal_logpdf(mu_b, 6.0, 2.0);
+        lp += log_gamma_pdf(s_a, 25.0, 2.0) + th[base + 2];
+        lp += log_gamma_pdf(s_b, 5.0, 10.0) + th[base + 3];
+        lp += log_gamma_pdf(s_y, 1.0, 2.0) + th[base + 4];
+      } else {
+        const double s_a = exp(th[base + 1]), s_y = exp(th[base + 2]);
+        const double vy = s_y * s_y;
+        for (int64_t i = 0; i < m->n; ++i) {
+          const double mask = excluded(m, i, fold) ? 0.0 : 1.0;
+          lp += mask * normal_logpdf(m->y[i], rat_mean(m, th, i), vy);
+        }
+        for (int g = 0; g < J; ++g) lp += normal_logpdf(th[g], mu_a, s_a * s_a);
+        lp += normal_logpdf(th[J], 6.0, 2.0);
+        lp += normal_logpdf(mu_a, 250.0, 20.0);
+        lp += log_gamma_pdf(s_a, 25.0, 2.0) + th[base + 1];
+        lp += log_gamma_pdf(s_y, 1.0, 2.0) + th[base + 2];
+      }
       return lp;
     }
     case PCVG_FAMILY_LOGISTIC: { /* oracle/ref_plugins.cpp LogisticModel::log_joint */
@@ -641,6 +718,69 @@ void pcvo_grad(const pcvo_model* m, const double* th, int32_t fold, double* grad
       grad[p + q + 1] = sum_r2 / v - n_train - v + 1.0;
       return;
     }
+    case PCVG_FAMILY_RAT_GROWTH: { /* rat_growth.cpp:111-172 */
+      const int base = rat_mu_a(m);
+      const double mu_a = th[base];
+      if (m->per_subject) {
+        const double mu_b = th[base + 1];
+        const double s_a = exp(th[base + 2]), s_b = exp(th[base + 3]), s_y = exp(th[base + 4]);
+        const double va = s_a * s_a, vb = s_b * s_b, vy = s_y * s_y;
+        double sum_r2 = 0.0;
+        long n_train = 0;
+        for (int64_t i = 0; i < m->n; ++i) {
+          if (excluded(m, i, fold)) continue;
+          const int g = m->g[i];
+          const double t = xv(m, i, 0);
+          const double r = m->y[i] - rat_mean(m, th, i);
+          grad[g] += r / vy;
+          grad[J + g] += t * r / vy;
+          sum_r2 += r * r;
+          ++n_train;
+        }
+        double sum_a2 = 0.0, sum_b2 = 0.0;
+        for (int g = 0; g < J; ++g) {
+          const double da = th[g] - mu_a, db = th[J + g] - mu_b;
+          grad[g] -= da / va;
+          grad[J + g] -= db / vb;
+          grad[base] += da / va;
+          grad[base + 1] += db / vb;
+          sum_a2 += da * da;
+          sum_b2 += db * db;
+        }
+        grad[base] -= (mu_a - 250.0) / 20.0;
+        grad[base + 1] -= (mu_b - 6.0) / 2.0;
+        grad[base + 2] = sum_a2 / va - J + 25.0 - 2.0 * s_a;
+        grad[base + 3] = sum_b2 / vb - J + 5.0 - 10.0 * s_b;
+        grad[base + 4] = sum_r2 / vy - n_train + 1.0 - 2.0 * s_y;
+      } else {
+        const double s_a = exp(th[base + 1]), s_y = exp(th[base + 2]);
+        const double va = s_a * s_a, vy = s_y * s_y;
+        double sum_r2 = 0.0;
+        long n_train = 0;
+        for (int64_t i = 0; i < m->n; ++i) {
+          if (excluded(m, i, fold)) continue;
+          const int g = m->g[i];
+          const double t = xv(m, i, 0);
+          const double r = m->y[i] - rat_mean(m, th, i);
+          grad[g] += r / vy;
+          grad[J] += t * r / vy;
+          sum_r2 += r * r;
+          ++n_train;
+        }
+        double sum_a2 = 0.0;
+        for (int g = 0; g < J; ++g) {
+          const double da = th[g] - mu_a;
+          grad[g] -= da / va;
+          grad[base] += da / va;
+          sum_a2 += da * da;
+        }
+        grad[J] -= (th[J] - 6.0) / 2.0;
+        grad[base] -= (mu_a - 250.0) / 20.0;
+        grad[base + 1] = sum_a2 / va - J + 25.0 - 2.0 * s_a;
+        grad[base + 2] = sum_r2 / vy - n_train + 1.0 - 2.0 * s_y;
+      }
+      return;
+    }
     case PCVG_FAMILY_LOGISTIC: { /* oracle/ref_plugins.cpp LogisticModel::grad_log_joint */
       for (int64_t i = 0; i < m->n; ++i) {
         if (excluded(m, i, fold)) continue;
@@ -720,6 +860,49 @@ double pcvo_log_pred(const pcvo_model* m, const double* th, int32_t fold) {
           lp += m->y[i] * e - softplus(e);
         }
         break;
+      case PCVG_FAMILY_RAT_GROWTH: { /* rat_growth.cpp:174-226 */
+        const int base = rat_mu_a(m);
+        const double mu_a = th[base];
+        if (m->per_subject) {
+          const double mu_b = th[base + 1];
+          const double va = exp(2.0 * th[base + 2]), vb = exp(2.0 * th[base + 3]);
+          const double vy = exp(2.0 * th[base + 4]);
+          if (m->seg_unseen[s]) {
+            const int nn = (int)(r1 - r0);
+            if (nn > 64) return NAN;
+            double cov[64 * 64];
+            for (int a = 0; a < nn; ++a) {
+              const double ta = xv(m, m->rows[r0 + a], 0);
+              yv[a] = m->y[m->rows[r0 + a]];
+              mv[a] = mu_a + mu_b * ta;
+              for (int b = 0; b < nn; ++b) {
+                const double tb = xv(m, m->rows[r0 + b], 0);
+                cov[a * nn + b] = va + vb * ta * tb + (a == b ? vy : 0.0);
+              }
+            }
+            lp += mvn_logpdf_chol(yv, mv, cov, nn);
+          } else {
+            for (int64_t t = r0; t < r1; ++t)
+              lp += normal_logpdf(m->y[m->rows[t]], rat_mean(m, th, m->rows[t]), vy);
+          }
+        } else {
+          const double va = exp(2.0 * th[base + 1]), vy = exp(2.0 * th[base + 2]);
+          const double beta = th[J];
+          if (m->seg_unseen[s]) {
+            int nn = 0;
+            for (int64_t t = r0; t < r1 && nn < 4096; ++t, ++nn) {
+              const int64_t i = m->rows[t];
+              yv[nn] = m->y[i];
+              mv[nn] = mu_a + beta * xv(m, i, 0);
+            }
+            lp += mvn_logpdf_compound(yv, mv, nn, vy, va);
+          } else {
+            for (int64_t t = r0; t < r1; ++t)
+              lp += normal_logpdf(m->y[m->rows[t]], rat_mean(m, th, m->rows[t]), vy);
+          }
+        }
+        break;
+      }
     }
   }
   return lp;
@@ -761,6 +944,13 @@ static int pred_mean_scale(const pcvo_model* m, const double* th, int32_t fold, 
       *sd = exp(th[m->p + m->q + 1]);
       *mean = seasonal_mean(m, th, i);
       return 1;
+    case PCVG_FAMILY_RAT_GROWTH: { /* rat_growth.cpp:267-290 */
+      const double s_y = exp(th[m->dim - 1]);
+      *var = s_y * s_y;
+      *sd = s_y;
+      *mean = rat_mean(m, th, i);
+      return 1;
+    }
   }
   return 0;
 }

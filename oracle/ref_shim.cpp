@@ -22,6 +22,7 @@
 #include "pcv/hmc.hpp"
 #include "pcv/models/grouped_regression.hpp"
 #include "pcv/models/radon.hpp"
+#include "pcv/models/rat_growth.hpp"
 #include "pcv/models/seasonal_ar.hpp"
 #include "pcv/rng.hpp"
 #include "ref_plugins.hpp"
@@ -136,6 +137,15 @@ int pcvref_simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_beta, u
   });
 }
 
+int pcvref_simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* g) {
+  return guarded([&] {
+    const auto r = pcv::simulate_rat_growth(subjects, seed);
+    std::memcpy(y, r.data.y.data(), sizeof(double) * r.data.y.size());
+    std::memcpy(x, r.data.x.data(), sizeof(double) * r.data.x.size());
+    for (size_t i = 0; i < r.data.group_id.size(); ++i) g[i] = r.data.group_id[i];
+  });
+}
+
 int pcvref_simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y, double* x,
                           int32_t* g) {
   return guarded([&] {
@@ -205,6 +215,10 @@ void* pcvref_model_create(const pcvg_dataset* ds, const pcvg_folds* fs,
           break;
         case PCVG_FAMILY_LOGISTIC:
           rm->model = std::make_unique<pcvoracle::LogisticModel>(nm, std::move(d), std::move(f));
+          break;
+        case PCVG_FAMILY_RAT_GROWTH:
+          rm->model = std::make_unique<pcv::RatGrowthModel>(nm, std::move(d), std::move(f),
+                                                            spec->per_subject_slope != 0);
           break;
         default:
           throw pcv::invalid_input("family not wired in the reference shim");

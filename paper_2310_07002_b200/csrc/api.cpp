@@ -56,6 +56,7 @@ void make_hv_block(const pcvg_dataset*, int32_t, int64_t, int64_t*);
 void make_hv_racine(const pcvg_dataset*, int64_t, int64_t, int64_t*);
 void simulate_grouped(int32_t, int32_t, int32_t, double, uint64_t, double*, double*, int32_t*);
 void simulate_radon(int32_t, int32_t, uint64_t, double*, double*, int32_t*);
+void simulate_rat(int32_t, uint64_t, double*, double*, int32_t*);
 void simulate_seasonal(int64_t, int32_t, int32_t, double, double, double, uint64_t, double*, double*, int64_t*);
 void simulate_linreg(int64_t, int32_t, uint64_t, double*, double*, int32_t*);
 void simulate_logistic(int64_t, int32_t, uint64_t, double*, double*);
@@ -266,7 +267,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   m.hv = f->intervals != nullptr;
   if (!f->test_index && !f->intervals) throw Error(PCVG_INVALID_INPUT, "folds need test_index or intervals");
   if (f->K < 1) throw Error(PCVG_INVALID_INPUT, "fold count must be at least 1");
-  const bool hier = s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON;
+  const bool hier = s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON ||
+                    s->family == PCVG_FAMILY_RAT_GROWTH;
   if (d->group_id) {  // Dataset::validate (dataset.cpp:19-39)
     std::vector<char> seen(n_groups(d), 0);
     for (int64_t i = 0; i < n; ++i) {
@@ -307,10 +309,20 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
       m.nc = d->n_cov;
       m.ng = d->n_cov + 1;
       break;
+    case PCVG_FAMILY_RAT_GROWTH:  // rat_growth.cpp:13-48
+      if (!d->group_id || d->n_cov < 1)
+        throw Error(PCVG_INVALID_INPUT, "growth model needs a group column and a time covariate");
+      m.J = n_groups(d);
+      m.nc = 1;
+      m.ng = s->per_subject_slope ? 5 : 4;
+      if (m.J > 32 * kMaxBatches)
+        throw Error(PCVG_INVALID_INPUT, "growth model supports at most 512 subjects on device");
+      break;
     default:
-      throw Error(PCVG_INVALID_INPUT, "model family not available on device (rat-growth is a next-round item)");
+      throw Error(PCVG_INVALID_INPUT, "unknown model family");
   }
-  m.dim = m.J + m.ng;
+  const int gdims = (s->family == PCVG_FAMILY_RAT_GROWTH && s->per_subject_slope) ? 2 : 1;
+  m.dim = m.J * gdims + m.ng;
   if (!kp->inv_mass_diag) throw Error(PCVG_INVALID_INPUT, "inverse mass diagonal missing");
   if (kp->n_leapfrog < 1) throw Error(PCVG_INVALID_INPUT, "n_leapfrog must be >= 1");
   for (int i = 0; i < m.dim; ++i)
@@ -550,7 +562,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   m.bank_rows = bank_rows;
 
   ModelDev& md = m.md;
-  md.family = s->family;
+  md.family = s->family == PCVG_FAMILY_RAT_GROWTH ? (s->per_subject_slope ? kRatA : kRatB) : s->family;
+  md.goff = m.dim - m.ng;
   md.n = static_cast<int>(n);
   md.nc = m.nc;
   md.J = m.J;
@@ -589,6 +602,15 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.c_lgamma10_10 = 10.0 * std::log(10.0) - std::lgamma(10.0);
   md.c_lbeta55 = std::lgamma(10.0) - std::lgamma(5.0) - std::lgamma(5.0);
   md.c_log4 = std::log(4.0);
+  md.c_lg25_2 = 25.0 * std::log(2.0) - std::lgamma(25.0);
+  md.c_lg5_10 = 5.0 * std::log(10.0) - std::lgamma(5.0);
+  md.c_lg1_2 = 1.0 * std::log(2.0) - std::lgamma(1.0);
+  md.c_log20 = std::log(20.0);
+  md.c_log2 = std::log(2.0);
+  if (md.family == kRatA)  // the dense unseen-subject predictive runs in registers
+    for (size_t sg = 0; sg < seg_unseen.size(); ++sg)
+      if (seg_unseen[sg] && m.seg_row[sg + 1] - m.seg_row[sg] > 16)
+        throw Error(PCVG_INVALID_INPUT, "per-subject growth model supports at most 16 observations per unseen subject on device");
   md.nb = nb;
   md.bstride = bstride;
   md.bgroup = m.bgroup.p;
@@ -629,7 +651,7 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
   cudaError_t e;
   if (use_glm(ctx, m, S.nch)) {
     e = launch_glm(md, S, A, st);
-  } else if (md.nb > 0 && ctx->policy != PCVG_KERNEL_GENERIC) {
+  } else if (md.nb > 0 && (ctx->policy != PCVG_KERNEL_GENERIC || md.family >= kRatB)) {
     e = launch_gauss(md, S, A, 0, st);  // group-batched hierarchical kernel
   } else {
     const int T = gauss_lanes_per_chain(md, S.nch);
@@ -848,6 +870,9 @@ pcvg_status pcvg_simulate_grouped(int32_t J, int32_t Nj, int32_t P, double mb, u
 pcvg_status pcvg_simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y,
                                 double* x, int32_t* g) {
   return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_radon(houses, counties, seed, y, x, g); }));
+}
+pcvg_status pcvg_simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* g) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] { simulate_rat(subjects, seed, y, x, g); }));
 }
 pcvg_status pcvg_simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho, double amp,
                                    double sigma, uint64_t seed, double* y, double* x, int64_t* t) {
@@ -1499,6 +1524,29 @@ std::vector<double> initial_draw(const HostModel& m, const pcvg_model_spec* s, H
       th[p + q + 1] = std::log(std::fabs(rng.normal()));
       break;
     }
+    case PCVG_FAMILY_RAT_GROWTH: {  // rat_growth.cpp:228-254
+      const double mu_a = 250.0 + std::sqrt(20.0) * rng.normal();
+      const double mu_b = 6.0 + std::sqrt(2.0) * rng.normal();
+      const double s_a = gamma_draw(rng, 25.0, 2.0);
+      const double s_b = gamma_draw(rng, 5.0, 10.0);
+      const double s_y = gamma_draw(rng, 1.0, 2.0);
+      for (int g = 0; g < J; ++g) th[g] = mu_a + s_a * rng.normal();
+      const int base = s->per_subject_slope ? 2 * J : J + 1;  // idx_mu_a (rat_growth.hpp:61)
+      if (s->per_subject_slope) {
+        for (int g = 0; g < J; ++g) th[J + g] = mu_b + s_b * rng.normal();
+        th[base] = mu_a;
+        th[base + 1] = mu_b;
+        th[base + 2] = std::log(s_a);
+        th[base + 3] = std::log(s_b);
+        th[base + 4] = std::log(s_y);
+      } else {
+        th[J] = 6.0 + std::sqrt(2.0) * rng.normal();
+        th[base] = mu_a;
+        th[base + 1] = std::log(s_a);
+        th[base + 2] = std::log(s_y);
+      }
+      break;
+    }
     default:  // logistic plugin: independent standard normals
       for (double& t : th) t = rng.normal();
   }
@@ -1632,9 +1680,10 @@ extern "C" pcvg_status pcvg_initial_draw(const pcvg_dataset* data, const pcvg_fo
       case PCVG_FAMILY_RADON: m.J = n_groups(data); m.nc = 1; m.ng = 4; break;
       case PCVG_FAMILY_SEASONAL_AR: m.J = 0; m.nc = spec->ar_order + spec->dummies; m.ng = m.nc + 2; break;
       case PCVG_FAMILY_LOGISTIC: m.J = 0; m.nc = data->n_cov; m.ng = data->n_cov + 1; break;
+      case PCVG_FAMILY_RAT_GROWTH: m.J = n_groups(data); m.nc = 1; m.ng = spec->per_subject_slope ? 5 : 4; break;
       default: throw Error(PCVG_INVALID_INPUT, "model family not available");
     }
-    m.dim = m.J + m.ng;
+    m.dim = m.J * ((spec->family == PCVG_FAMILY_RAT_GROWTH && spec->per_subject_slope) ? 2 : 1) + m.ng;
     HostRng rng(seed, stream);
     const auto th = initial_draw(m, spec, rng);
     std::copy(th.begin(), th.end(), theta);
@@ -1656,7 +1705,7 @@ extern "C" pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* d
     if (!out->inv_mass_diag || !out->draws) throw Error(PCVG_INVALID_INPUT, "fit output buffers missing");
     require_device(ctx);
     // the model in device layout; kernel and bank are placeholders until adapted
-    const int dim_cap = (data->group_id ? n_groups(data) : 0) + data->n_cov + 8;
+    const int dim_cap = (data->group_id ? 2 * n_groups(data) : 0) + data->n_cov + 8;
     std::vector<double> ones(dim_cap, 1.0), zero(dim_cap, 0.0);
     pcvg_kernel k0{1.0, cfg->n_leapfrog, ones.data()};
     auto hm = build_model(data, folds, spec, &k0, zero.data(), 1, model_id);

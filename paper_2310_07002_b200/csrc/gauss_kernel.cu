@@ -93,17 +93,19 @@ struct Prep {
   double off0;    // offset without the group term
   double v, inv_v, logv;
   double va, sa;  // group scale (grouped: va = sig_a^2; radon: va, sa = sqrt(va))
+  double vb;      // rat M_A: slope scale s_b^2
 };
 
 // Register slot -> global parameter index. Slots put the parameters whose position depends
 // on runtime sizes (P, p, q) at fixed registers so no register array is indexed dynamically:
 //   grouped  [mu_alpha, log sigma_alpha, log sigma_y, beta_0..beta_{P-1}]
 //   radon    [beta, mu_alpha, log sigma_alpha^2, log sigma_y^2]           (reference order)
+//   rat M_B  [beta, mu_a, log s_a, log s_y]; rat M_A [mu_a, mu_b, log s_a, log s_b, log s_y]
 //   seasonal [beta_0, log sigma, cov 0..p+q-1 -> u_1..u_p, beta_1..beta_q]
 template <int FAM>
 __device__ __forceinline__ int gidx(const ModelDev& M, int r) {
   if constexpr (FAM == kGrouped) return r < 3 ? M.nc + r : r - 3;
-  else if constexpr (FAM == kRadon) return r;
+  else if constexpr (FAM == kRadon || FAM == kRatA || FAM == kRatB) return r;
   else return r == 0 ? M.p : (r == 1 ? M.p + M.q + 1 : (r - 2 < M.p ? r - 2 : r - 1));
 }
 
@@ -123,6 +125,19 @@ __device__ __forceinline__ void prepare(const ModelDev& M, const double* qG, Pre
     P.va = exp(qG[2]);
     P.sa = sqrt(P.va);
     P.v = exp(qG[3]);
+  } else if constexpr (FAM == kRatB) {  // rat_growth.cpp:148-172
+    P.w[0] = qG[0];
+    P.off0 = 0.0;
+    const double s_a = exp(qG[2]), s_y = exp(qG[3]);
+    P.va = s_a * s_a;
+    P.v = s_y * s_y;
+  } else if constexpr (FAM == kRatA) {  // rat_growth.cpp:117-147 (slope per group)
+    P.w[0] = 0.0;
+    P.off0 = 0.0;
+    const double s_a = exp(qG[2]), s_b = exp(qG[3]), s_y = exp(qG[4]);
+    P.va = s_a * s_a;
+    P.vb = s_b * s_b;
+    P.v = s_y * s_y;
   } else {  // seasonal
 #pragma unroll
     for (int c = 0; c < NCM; ++c) {
@@ -143,14 +158,14 @@ __device__ __forceinline__ void prepare(const ModelDev& M, const double* qG, Pre
 
 template <int FAM, int NCM>
 __device__ __forceinline__ double group_offset(const Prep<NCM>& P, double qg) {
-  if constexpr (FAM == kGrouped) return qg;
+  if constexpr (FAM == kGrouped || FAM == kRatA || FAM == kRatB) return qg;
   else if constexpr (FAM == kRadon) return P.off0 + P.sa * qg;
   else return P.off0;
 }
 
 // Replicated (not lane-reduced) per-group accumulators.
 struct GroupAcc {
-  double a0, a1, a2;
+  double a0, a1, a2, a3;
 };
 
 // d log p / d q_g given the lane-reduced residual sum of group g; updates replicated sums.
@@ -162,6 +177,11 @@ __device__ __forceinline__ double group_grad(const Prep<NCM>& P, const double* q
     const double dev = qg - qG[0];
     G.a0 += dev / P.va;  // -> d/d mu_alpha
     G.a1 += dev * dev;   // -> d/d log sigma_alpha, prior
+    return srg / P.v - dev / P.va;
+  } else if constexpr (FAM == kRatB || FAM == kRatA) {  // rat_growth.cpp:129-137, 159-164 (alpha_g)
+    const double dev = qg - (FAM == kRatB ? qG[1] : qG[0]);
+    G.a0 += dev / P.va;  // -> d/d mu_a
+    G.a1 += dev * dev;   // -> d/d log s_a, prior
     return srg / P.v - dev / P.va;
   } else {  // radon.cpp:93-105
     G.a0 += srg;       // sum r (-> d/d mu_alpha)
@@ -209,6 +229,41 @@ __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& 
       l += -0.5 * (kLog2Pi + M.c_log4 + qG[1] * qG[1] / 4.0);
       l += M.c_lgamma6_9 + 5.0 * qG[2] - 9.0 * P.va + qG[2];
       l += M.c_lgamma10_10 + 9.0 * qG[3] - 10.0 * P.v + qG[3];
+      lp = l;
+    }
+  } else if constexpr (FAM == kRatB) {  // rat_growth.cpp:148-172, 88-107
+    const double s_a = exp(qG[2]), s_y = exp(qG[3]);
+    gG[0] = sxr[0] / P.v - (qG[0] - 6.0) / 2.0;
+    gG[1] = G.a0 - (qG[1] - 250.0) / 20.0;
+    gG[2] = G.a1 / P.va - M.J + 25.0 - 2.0 * s_a;
+    gG[3] = srr / P.v - ntr + 1.0 - 2.0 * s_y;
+    if (value) {
+      double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
+      l += -0.5 * (M.J * (kLog2Pi + log(P.va)) + G.a1 / P.va);
+      const double d6 = qG[0] - 6.0, d250 = qG[1] - 250.0;
+      l += -0.5 * (kLog2Pi + M.c_log2 + d6 * d6 / 2.0);
+      l += -0.5 * (kLog2Pi + M.c_log20 + d250 * d250 / 20.0);
+      l += M.c_lg25_2 + 25.0 * qG[2] - 2.0 * s_a;
+      l += M.c_lg1_2 + 1.0 * qG[3] - 2.0 * s_y;
+      lp = l;
+    }
+  } else if constexpr (FAM == kRatA) {  // rat_growth.cpp:117-147, 72-87
+    const double s_a = exp(qG[2]), s_b = exp(qG[3]), s_y = exp(qG[4]);
+    gG[0] = G.a0 - (qG[0] - 250.0) / 20.0;
+    gG[1] = G.a2 - (qG[1] - 6.0) / 2.0;
+    gG[2] = G.a1 / P.va - M.J + 25.0 - 2.0 * s_a;
+    gG[3] = G.a3 / P.vb - M.J + 5.0 - 10.0 * s_b;
+    gG[4] = srr / P.v - ntr + 1.0 - 2.0 * s_y;
+    if (value) {
+      double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
+      l += -0.5 * (M.J * (kLog2Pi + log(P.va)) + G.a1 / P.va);
+      l += -0.5 * (M.J * (kLog2Pi + log(P.vb)) + G.a3 / P.vb);
+      const double d250 = qG[0] - 250.0, d6 = qG[1] - 6.0;
+      l += -0.5 * (kLog2Pi + M.c_log20 + d250 * d250 / 20.0);
+      l += -0.5 * (kLog2Pi + M.c_log2 + d6 * d6 / 2.0);
+      l += M.c_lg25_2 + 25.0 * qG[2] - 2.0 * s_a;
+      l += M.c_lg5_10 + 5.0 * qG[3] - 10.0 * s_b;
+      l += M.c_lg1_2 + 1.0 * qG[4] - 2.0 * s_y;
       lp = l;
     }
   } else {  // seasonal_ar.cpp:79-105, 59-77
@@ -259,7 +314,7 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
   for (int k = 0; k < NCM; ++k) sxr[k] = 0.0;
   double sr_tot = 0.0, srr = 0.0;
   bool poison = false;
-  GroupAcc G{0.0, 0.0, 0.0};
+  GroupAcc G{0.0, 0.0, 0.0, 0.0};
   const int ngroups = M.J > 0 ? M.J : 1;
   for (int g = 0; g < ngroups; ++g) {
     double qg = 0.0, pg = 0.0;
@@ -363,7 +418,7 @@ struct BatchRing {
   uint32_t g;       // next tile of this warp
   uint32_t total;   // tiles consumed by this launch
   unsigned int W;   // valid warps of the CTA
-  double* qslots;   // [2][nb][kBlock] group position / momentum slots
+  double* qslots;   // [2 or 4][nb][kBlock] group position / momentum slots (rat M_A: + slopes)
 };
 
 __device__ __forceinline__ void ring_issue(const ModelDev& M, BatchRing& rg, uint32_t g) {
@@ -463,7 +518,7 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
   for (int k = 0; k < NCM; ++k) sxr[k] = 0.0;
   double srr = 0.0, k0l = 0.0, k1l = 0.0;
   bool poison = false, badl = false;
-  GroupAcc G{0.0, 0.0, 0.0};
+  GroupAcc G{0.0, 0.0, 0.0, 0.0};
 #pragma unroll 1
   for (int b = 0; b < M.nb; ++b) {
     const int g = __ldg(M.bgroup + b * 32 + t);
@@ -485,6 +540,35 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
       badl |= !isfinite(qg);
       qb[b * kBlock] = qg;
     }
+    // rat M_A: the subject's slope beta_g (dim J + g) is a second group parameter, slots qb2/pb2
+    double qs = 0.0;
+    double* qb2 = qb + 2 * static_cast<size_t>(M.nb) * kBlock;
+    double* pb2 = pb + 2 * static_cast<size_t>(M.nb) * kBlock;
+    if constexpr (FAM == kRatA) {
+      if (valid) {
+        const int gs = M.J + g;
+        const size_t si = static_cast<size_t>(gs) * nch + c;
+        const double ms = __ldg(M.inv_mass + gs);
+        if (kind == 0) {
+          qs = S.pos[cur * plane + si];
+        } else if (kind == 1) {
+          const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + gs] : nc.at(R, gs) / sqrt(ms);
+          k0l += ms * p0 * p0;
+          pb2[b * kBlock] = p0 + half * S.grad[cur * plane + si];
+          qs = S.pos[cur * plane + si] + eps * ms * pb2[b * kBlock];
+        } else {
+          qs = qb2[b * kBlock] + eps * ms * pb2[b * kBlock];
+        }
+        badl |= !isfinite(qs);
+        qb2[b * kBlock] = qs;
+      }
+    }
+    Prep<NCM> Pg = P;  // the row predictor: rat M_A uses the subject's own slope
+    if constexpr (FAM == kRatA) Pg.w[0] = qs;
+    double sxg[NCM];   // rat M_A: per-subject sum t r (-> d/d beta_g) instead of the global sum
+#pragma unroll
+    for (int k = 0; k < NCM; ++k) sxg[k] = 0.0;
+    double* sxr_tgt = FAM == kRatA ? sxg : sxr;
     const double off = group_offset<FAM, NCM>(P, qg);
     double srg = 0.0, srg1 = 0.0, srr1 = 0.0;
     double sxr1[NCM];
@@ -522,14 +606,14 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
       // group-uniform keys: one train flag per group; rows past the group's end only in batches
       // whose groups differ in length (buniform[b] == 0)
       if (__ldg(M.buniform + b))
-        tile_rows_loop<FAM, NCX, NCM, 1, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
-                                               lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
+        tile_rows_loop<FAM, NCX, NCM, 1, VALUE>(M, Pg, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
+                                               lo, hi, off, srg, sxr_tgt, srr, srg1, sxr1, srr1, poison);
       else
-        tile_rows_loop<FAM, NCX, NCM, 2, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
-                                               lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
+        tile_rows_loop<FAM, NCX, NCM, 2, VALUE>(M, Pg, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
+                                               lo, hi, off, srg, sxr_tgt, srr, srg1, sxr1, srr1, poison);
     } else {
-      tile_rows_loop<FAM, NCX, NCM, 0, VALUE>(M, P, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
-                                             lo, hi, off, srg, sxr, srr, srg1, sxr1, srr1, poison);
+      tile_rows_loop<FAM, NCX, NCM, 0, VALUE>(M, Pg, yp, xp, kp, xstride, rows, jb0, grows, gtrain, gkey,
+                                             lo, hi, off, srg, sxr_tgt, srr, srg1, sxr1, srr1, poison);
     }
     if (M.ring) {
     __syncwarp(kFull);
@@ -543,7 +627,30 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
     srg += srg1;
     srr += srr1;
 #pragma unroll
-    for (int k = 0; k < NCM; ++k) sxr[k] += sxr1[k];
+    for (int k = 0; k < NCM; ++k) sxr_tgt[k] += sxr1[k];
+    if constexpr (FAM == kRatA) {  // slope beta_g: t r / vy - (beta_g - mu_b) / vb (rat_growth.cpp:127-137)
+      if (valid) {
+        const int gs = M.J + g;
+        const size_t si = static_cast<size_t>(gs) * nch + c;
+        const double db = qs - qG[1];
+        G.a2 += db / P.vb;
+        G.a3 += db * db;
+        const double gsl = sxg[0] / P.v - db / P.vb;
+        badl |= !isfinite(gsl);
+        if (kind == 0) {
+          S.grad[cur * plane + si] = gsl;
+        } else {
+          const double pn = pb2[b * kBlock] + scale * gsl;
+          pb2[b * kBlock] = pn;
+          badl |= !isfinite(pn);
+          if (last) {
+            S.pos[(cur ^ 1) * plane + si] = qs;
+            S.grad[(cur ^ 1) * plane + si] = gsl;
+            k1l += __ldg(M.inv_mass + gs) * pn * pn;
+          }
+        }
+      }
+    }
     if (valid) {
       const double gg = group_grad<FAM, NCM, NGM>(P, qG, M, qg, srg, G);
       const size_t gi = static_cast<size_t>(g) * nch + c;
@@ -568,6 +675,7 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
   G.a0 = lane_sum<32>(G.a0, kFull);
   G.a1 = lane_sum<32>(G.a1, kFull);
   G.a2 = lane_sum<32>(G.a2, kFull);
+  G.a3 = lane_sum<32>(G.a3, kFull);
   if (kind == 1) k0g += lane_sum<32>(k0l, kFull);
   if (last) k1g += lane_sum<32>(k1l, kFull);
   bad |= __any_sync(kFull, badl);
@@ -575,6 +683,42 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
   global_grad<FAM, NCM, NGM>(M, P, qG, sxr, 0.0, srr, G, n_train, gG, VALUE, lp);
   if (VALUE && poison) lp = CUDART_NAN;
   __syncwarp(kFull);  // group-dim stores become visible to the chain's lanes
+}
+
+// Unseen subject of the per-subject-slope growth model: log N(y; mu_a + mu_b t, va + vb t t' +
+// vy I) by a dense Cholesky (mvn_logpdf_chol, math.hpp:46-90); -inf when not positive definite.
+// Subjects have at most kRatMaxObs rows on device (checked at upload).
+constexpr int kRatMaxObs = 16;
+__device__ double rat_unseen_logpdf(const ModelDev& M, int r0, int r1, double mu_a, double mu_b,
+                                    double va, double vb, double vy) {
+  const int n = r1 - r0;
+  double L[kRatMaxObs * (kRatMaxObs + 1) / 2], tv[kRatMaxObs], r[kRatMaxObs];
+  for (int a = 0; a < n; ++a) {
+    const int i = __ldg(M.seg_rows + r0 + a);
+    tv[a] = __ldg(M.x + i);
+    r[a] = __ldg(M.y + i) - (mu_a + mu_b * tv[a]);
+  }
+  for (int j = 0; j < n; ++j) {  // packed lower triangle, row i at i(i+1)/2
+    double d = va + vb * tv[j] * tv[j] + vy;
+    for (int k = 0; k < j; ++k) d -= L[j * (j + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
+    if (!(d > 0.0) || !isfinite(d)) return -CUDART_INF;
+    const double l = sqrt(d);
+    L[j * (j + 1) / 2 + j] = l;
+    for (int i = j + 1; i < n; ++i) {
+      double sm = va + vb * tv[i] * tv[j];
+      for (int k = 0; k < j; ++k) sm -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
+      L[i * (i + 1) / 2 + j] = sm / l;
+    }
+  }
+  double q = 0.0, ld = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double sm = r[i];
+    for (int k = 0; k < i; ++k) sm -= L[i * (i + 1) / 2 + k] * r[k];
+    r[i] = sm / L[i * (i + 1) / 2 + i];
+    q += r[i] * r[i];
+    ld += log(L[i * (i + 1) / 2 + i]);
+  }
+  return -0.5 * (n * kLog2Pi + 2.0 * ld + q);
 }
 
 // Model::log_pred at the stored position (grouped_regression.cpp:124-163, radon.cpp:109-138,
@@ -587,8 +731,17 @@ __device__ double log_pred(const ModelDev& M, const ChainsDev& S, int c, int t, 
   prepare<FAM, NCM, NGM>(M, qG, P);
   const size_t plane = static_cast<size_t>(M.dim) * S.nch;
   const int s0 = __ldg(M.fold_seg + fold), s1 = __ldg(M.fold_seg + fold + 1);
-  double v_pred = P.v;
+  double v_pred = P.v, va_pred = P.va, vb_pred = 0.0;
   if constexpr (FAM == kSeasonal) v_pred = exp(2.0 * qG[1]);
+  if constexpr (FAM == kRatB) {  // rat_growth.cpp:204-205 (exp(2 theta) forms)
+    va_pred = exp(2.0 * qG[2]);
+    v_pred = exp(2.0 * qG[3]);
+  }
+  if constexpr (FAM == kRatA) {  // rat_growth.cpp:181-183
+    va_pred = exp(2.0 * qG[2]);
+    vb_pred = exp(2.0 * qG[3]);
+    v_pred = exp(2.0 * qG[4]);
+  }
   double lp = 0.0;
   for (int s = s0; s < s1; ++s) {
     const int r0 = __ldg(M.seg_row + s), r1 = __ldg(M.seg_row + s + 1);
@@ -596,12 +749,23 @@ __device__ double log_pred(const ModelDev& M, const ChainsDev& S, int c, int t, 
     const bool unseen = __ldg(M.seg_unseen + s) != 0;
     double qg = 0.0;
     if (FAM != kSeasonal && !unseen) qg = S.pos[cur * plane + static_cast<size_t>(g) * S.nch + c];
+    if constexpr (FAM == kRatA) {
+      if (unseen) {  // dense N(mu_a + mu_b t, va + vb t t' + vy I) over the subject (rat_growth.cpp:184-199)
+        double part = 0.0;
+        if (t == 0) part = rat_unseen_logpdf(M, r0, r1, qG[0], qG[1], va_pred, vb_pred, v_pred);
+        lp += lane_sum<T>(part, mask);
+        continue;
+      }
+      P.w[0] = S.pos[cur * plane + static_cast<size_t>(M.J + g) * S.nch + c];  // the subject's slope
+    }
     double a = 0.0, b = 0.0;
     for (int tt = r0 + t; tt < r1; tt += T) {
       const int i = __ldg(M.seg_rows + tt);
       double m;
       if constexpr (FAM == kGrouped) m = unseen ? qG[0] : qg;
       else if constexpr (FAM == kRadon) m = unseen ? P.off0 : P.off0 + sqrt(P.va) * qg;
+      else if constexpr (FAM == kRatB) m = unseen ? qG[1] : qg;
+      else if constexpr (FAM == kRatA) m = qg;
       else m = P.off0;
 #pragma unroll
       for (int k = 0; k < NCM; ++k)
@@ -617,7 +781,7 @@ __device__ double log_pred(const ModelDev& M, const ChainsDev& S, int c, int t, 
     a = lane_sum<T>(a, mask);
     if (unseen) {  // mvn_logpdf_compound, math.hpp:94-109, sigma2 = vy, tau2 = va
       b = lane_sum<T>(b, mask);
-      const double sigma2 = P.v, tau2 = P.va;
+      const double sigma2 = FAM == kRatB ? v_pred : P.v, tau2 = FAM == kRatB ? va_pred : P.va;
       const int nn = r1 - r0;
       if (!(sigma2 > 0.0) || tau2 < 0.0) return CUDART_NAN;  // numeric_fault in the reference
       const double denom = sigma2 + nn * tau2;
@@ -647,6 +811,9 @@ __device__ void score_extra(const ModelDev& M, const ChainsDev& S, int c, int t,
   if constexpr (FAM == kGrouped) {
     sy = exp(qG[2]);  // sig_y
     vy = sy * sy;
+  } else if constexpr (FAM == kRatA || FAM == kRatB) {  // rat_growth.cpp:267-290
+    sy = exp(qG[NGM - 1]);
+    vy = sy * sy;
   } else if constexpr (FAM == kRadon) {
     vy = exp(qG[3]);
     sy = exp(0.5 * qG[3]);
@@ -669,8 +836,11 @@ __device__ void score_extra(const ModelDev& M, const ChainsDev& S, int c, int t,
       double mean;
       if constexpr (FAM == kRadon) {
         mean = qG[1] + sa * qg + (M.include_floor ? 1.0 : 0.0) * qG[0] * __ldg(M.x + i);
+      } else if constexpr (FAM == kRatA) {
+        const double slope = S.pos[cur * plane + static_cast<size_t>(M.J + __ldg(M.seg_group + s)) * S.nch + c];
+        mean = fma(slope, __ldg(M.x + i), qg);
       } else {
-        mean = FAM == kGrouped ? qg : P.off0;
+        mean = (FAM == kGrouped || FAM == kRatB) ? qg : P.off0;
 #pragma unroll
         for (int k = 0; k < NCM; ++k)
           if (k < M.nc) mean = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), mean);
@@ -729,7 +899,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
   const int J = M.J, ng = M.ng;
   const size_t plane = static_cast<size_t>(M.dim) * nch;
   // address of global parameter slot i of chain c in plane b
-  auto gaddr = [&](int b, int i) { return b * plane + static_cast<size_t>(J + gidx<FAM>(M, i)) * nch + c; };
+  auto gaddr = [&](int b, int i) { return b * plane + static_cast<size_t>(M.goff + gidx<FAM>(M, i)) * nch + c; };
   int cur = S.cur[c];
 
   double qG[NGM], pG[NGM], gG[NGM];
@@ -784,7 +954,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
 #pragma unroll
     for (int i = 0; i < NGM; ++i) {
       if (i < ng) {
-        const int gi = J + gidx<FAM>(M, i);
+        const int gi = M.goff + gidx<FAM>(M, i);
         const double mi = __ldg(M.inv_mass + gi);
         const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + gi]
                                   : nc.at(R, gi) / sqrt(mi);
@@ -800,7 +970,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
       for (int i = 0; i < NGM; ++i) {
         if (i < ng) {
           const double base = first ? S.pos[gaddr(cur, i)] : qG[i];
-          qG[i] = base + eps * __ldg(M.inv_mass + J + gidx<FAM>(M, i)) * pG[i];
+          qG[i] = base + eps * __ldg(M.inv_mass + M.goff + gidx<FAM>(M, i)) * pG[i];
           bad |= !isfinite(qG[i]);
         } else {
           qG[i] = 0.0;
@@ -834,7 +1004,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
     double k1G = 0.0;
 #pragma unroll
     for (int i = 0; i < NGM; ++i)
-      if (i < ng) k1G += __ldg(M.inv_mass + J + gidx<FAM>(M, i)) * pG[i] * pG[i];
+      if (i < ng) k1G += __ldg(M.inv_mass + M.goff + gidx<FAM>(M, i)) * pG[i] * pG[i];
     // proposal (q', grad(q')) of the global dims into the working plane; accept flips `cur`
     if (t == 0) {
 #pragma unroll
@@ -922,7 +1092,8 @@ cudaError_t launch_family(const ModelDev& M, const ChainsDev& S, const RunArgs& 
 // Group-batched launch (hierarchical families with a batch layout): one warp per chain.
 template <int FAM, int NCM, int NGM, int NB>
 cudaError_t launch_nb(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st, int grid) {
-  const size_t smem = kRing * ring_slot_bytes(M) + 16 * kRing + 2 * static_cast<size_t>(M.nb) * kBlock * sizeof(double);
+  const size_t smem = kRing * ring_slot_bytes(M) + 16 * kRing +
+                      (FAM == kRatA ? 4 : 2) * static_cast<size_t>(M.nb) * kBlock * sizeof(double);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, 32, NCM, NGM, NB>,
@@ -966,6 +1137,8 @@ cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A
     if (M.family == kGrouped && M.nc <= 4) return launch_batched<kGrouped, 4, 7>(M, S, A, st);
     if (M.family == kGrouped && M.nc <= 8) return launch_batched<kGrouped, 8, 11>(M, S, A, st);
     if (M.family == kRadon) return launch_batched<kRadon, 1, 4>(M, S, A, st);
+    if (M.family == kRatB) return launch_batched<kRatB, 1, 4>(M, S, A, st);
+    if (M.family == kRatA) return launch_batched<kRatA, 1, 5>(M, S, A, st);
     return cudaErrorInvalidValue;
   }
   switch (M.family) {

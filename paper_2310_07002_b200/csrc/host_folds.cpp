@@ -169,6 +169,29 @@ void simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_beta, uint64_
 }
 
 // simulate_radon_style, radon.cpp:216-240.
+// simulate_rat_growth (rat_growth.cpp:310-336): n = 5 * subjects at times {8,15,22,29,36}.
+void simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* g) {
+  if (subjects < 2) throw Error(PCVG_INVALID_INPUT, "simulator needs at least 2 subjects");
+  HostRng rng(seed, stream_key(PCVG_STREAM_SIMULATE, 2, 0, 0));
+  const double mu_alpha = 250.0 + std::sqrt(20.0) * rng.normal();
+  const double mu_beta = 6.0 + std::sqrt(2.0) * rng.normal();
+  const double sigma_alpha = gamma_draw(rng, 25.0, 2.0);
+  const double sigma_beta = gamma_draw(rng, 5.0, 10.0);
+  const double sigma_y = gamma_draw(rng, 1.0, 2.0);
+  const double times[5] = {8, 15, 22, 29, 36};
+  int64_t i = 0;
+  for (int s = 0; s < subjects; ++s) {
+    const double a = mu_alpha + sigma_alpha * rng.normal();
+    const double b = mu_beta + sigma_beta * rng.normal();
+    for (double t : times) {
+      y[i] = a + b * t + sigma_y * rng.normal();
+      x[i] = t;
+      g[i] = s;
+      ++i;
+    }
+  }
+}
+
 void simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y, double* x,
                     int32_t* g) {
   if (counties < 2 || houses < counties)

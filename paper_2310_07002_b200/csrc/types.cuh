@@ -6,7 +6,8 @@
 
 namespace pcvg {
 
-enum Family : int { kGrouped = 0, kRadon = 1, kSeasonal = 2, kLogistic = 3 };
+// Device family codes: pcvg_family, with the rat-growth model split by slope structure.
+enum Family : int { kGrouped = 0, kRadon = 1, kSeasonal = 2, kLogistic = 3, kRatB = 4, kRatA = 5 };
 
 // Kernel modes.
 enum Mode : int {
@@ -25,7 +26,8 @@ struct ModelDev {
   int family;
   int n;     // observations (device row order: group-major for hierarchical families)
   int nc;    // covariate columns read by the kernel
-  int J;     // group parameters (first J dims); 0 if none
+  int J;     // groups (the first J dims are one parameter per group; kRatA: 2J dims)
+  int goff;  // index of the first global parameter (J, or 2J for kRatA)
   int ng;    // global parameters (dims J..dim-1)
   int dim;
   int K;     // folds; index K is the full-data sentinel
@@ -55,6 +57,8 @@ struct ModelDev {
   double c_lgamma10_10;    // 10 log 10 - lgamma(10)
   double c_lbeta55;        // lgamma(10) - 2 lgamma(5)
   double c_log4;           // log(4)
+  double c_lg25_2, c_lg5_10, c_lg1_2;  // a log r - lgamma(a): Gamma(25,2), Gamma(5,10), Gamma(1,2)
+  double c_log20, c_log2;              // log 20, log 2 (rat-growth normal hyper-priors)
   // group-batched layout (hierarchical families, gauss_kernel NB > 0): nb batches of 32 group
   // slots; bgroup[b*32 + i] = group of lane i in batch b (-1 = none); rows of batch b are
   // [boff[b], boff[b+1]) in lane-interleaved arrays (row j of lane i at j*32 + i), padded with

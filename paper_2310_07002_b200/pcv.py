@@ -85,6 +85,7 @@ def load():
     _sig(lib, "pcvg_make_hv_racine", i32, [P(abi.Dataset), i64, i64, pi64])
     _sig(lib, "pcvg_simulate_grouped", i32, [i32, i32, i32, f64, u64, pf, pf, pi32])
     _sig(lib, "pcvg_simulate_radon", i32, [i32, i32, u64, pf, pf, pi32])
+    _sig(lib, "pcvg_simulate_rat", i32, [i32, u64, pf, pf, pi32])
     _sig(lib, "pcvg_simulate_seasonal", i32, [i64, i32, i32, f64, f64, f64, u64, pf, pf, pi64])
     _sig(lib, "pcvg_simulate_linreg", i32, [i64, i32, u64, pf, pf, pi32])
     _sig(lib, "pcvg_simulate_logistic", i32, [i64, i32, u64, pf, pf])
@@ -217,6 +218,14 @@ def simulate_radon_style(houses, counties, seed):
     return Dataset(y, x.reshape(houses, 1), g)
 
 
+def simulate_rat_growth(subjects=30, seed=1):
+    """simulate_rat_growth (rat_growth.cpp:310-336): 5 weights per subject at t = 8..36."""
+    n = 5 * subjects
+    y, x, g = np.zeros(n), np.zeros(n), np.zeros(n, dtype=np.int32)
+    _check(load().pcvg_simulate_rat(subjects, seed, _p(y), _p(x), _p(g, C.c_int32)))
+    return Dataset(y, x.reshape(n, 1), g)
+
+
 def simulate_seasonal_ar(months=432, ar_order=1, dummies=11, rho=0.6, seasonal_amp=1.0, sigma=1.0, seed=1):
     n = months - ar_order
     nc = ar_order + dummies
@@ -290,6 +299,19 @@ class SeasonalARModel(Model):
 
     def dim(self):
         return self.p + self.q + 2
+
+
+class RatGrowthModel(Model):
+    """RatGrowthModel (rat_growth.hpp:20-63): per_subject_slope = M_A, else the shared-slope M_B."""
+    family = abi.FAMILY_RAT_GROWTH
+
+    def __init__(self, name, data, folds, per_subject_slope=True):
+        super().__init__(name, data, folds, per_subject_slope=int(per_subject_slope))
+        self.per_subject_slope = bool(per_subject_slope)
+
+    def dim(self):
+        J = self.data.n_groups
+        return 2 * J + 5 if self.per_subject_slope else J + 4
 
 
 class LogisticModel(Model):

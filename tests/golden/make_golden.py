@@ -58,6 +58,13 @@ def _seasonal_hv():
     return d, f, [dict(family=abi.FAMILY_SEASONAL_AR, ar_order=2, dummies=11)]
 
 
+def _rat():  # paper Ex-2 style: 30 rats x 5 weights, leave-one-subject-out, M_A vs M_B
+    d = pcv.simulate_rat_growth(30, seed=4)
+    f = pcv.make_logo_scheme(d)
+    return d, f, [dict(family=abi.FAMILY_RAT_GROWTH, per_subject_slope=1),
+                  dict(family=abi.FAMILY_RAT_GROWTH, per_subject_slope=0)]
+
+
 def _logistic():
     d = pcv.simulate_logistic(500, 10, seed=1)
     f = pcv.make_loo_scheme(d)
@@ -126,6 +133,7 @@ CONFIGS = {
     "radon_logo": (_radon, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
     "seasonal_timeblocks": (_seasonal_tb, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
     "seasonal_hvblock": (_seasonal_hv, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
+    "rat_logo": (_rat, dict(chains=4, warmup=1000, draws=250), dict(chains=4, iters=200, warmup=50, batch_size=20, bench_draws=50, checkpoint_every=100)),
     "logistic_loo": (_logistic, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
     "logistic_kfold": (_logistic_kfold, dict(chains=4, warmup=600, draws=250), dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50)),
     # bench input only (no reference run: 80k chains is the GPU workload)
@@ -159,7 +167,8 @@ def make(name):
         rm = O.RModel(d, fa, sa)
         fit = rm.adapt(seed=1, model_id=m, **akw)
         out[f"spec{m}"] = np.array([s.get("family"), s.get("include_floor", 1), s.get("ar_order", 1),
-                                    s.get("dummies", 0), s.get("rho_transform", 0)], dtype=np.int64)
+                                    s.get("dummies", 0), s.get("rho_transform", 0),
+                                    s.get("per_subject_slope", 0)], dtype=np.int64)
         if s.get("covariate_mask") is not None:
             out[f"mask{m}"] = np.array(s["covariate_mask"], dtype=np.int32)
         out[f"step{m}"] = np.float64(fit["step_size"])
@@ -203,8 +212,11 @@ def load(name):
                                z["intervals"] if "intervals" in z else None)
     models = []
     for m in range(int(z["n_models"])):
-        fam, floor, p, q, rho = (int(v) for v in z[f"spec{m}"])
+        sp = [int(v) for v in z[f"spec{m}"]]
+        fam, floor, p, q, rho = sp[:5]
         kw = dict(family=fam, include_floor=floor, ar_order=p, dummies=q, rho_transform=rho)
+        if fam == abi.FAMILY_RAT_GROWTH:
+            kw["per_subject_slope"] = sp[5]
         if f"mask{m}" in z:
             kw["covariate_mask"] = z[f"mask{m}"]
         kp = pcv.KernelParams(float(z[f"step{m}"]), 32, z[f"inv_mass{m}"])
@@ -220,6 +232,7 @@ SCORE_FIXTURES = {
     "radon_logo": (abi.SCORE_HS, abi.SCORE_DSS),
     "seasonal_timeblocks": (abi.SCORE_HS, abi.SCORE_DSS),
     "seasonal_hvblock": (abi.SCORE_HS, abi.SCORE_DSS),
+    "rat_logo": (abi.SCORE_HS, abi.SCORE_DSS),
 }
 SCORE_NAME = {abi.SCORE_HS: "hs", abi.SCORE_DSS: "dss"}
 
@@ -253,7 +266,7 @@ def make_score(base, score):
 # that the device run follows the same chain trajectories: tests/golden/adapt_short.npz.
 ADAPT_SHORT = dict(chains=4, warmup=30, draws=10, n_lf=32)
 ADAPT_BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks",
-               "seasonal_hvblock", "logistic_loo"]
+               "seasonal_hvblock", "logistic_loo", "rat_logo"]
 
 
 def make_adapt_short():

@@ -9,7 +9,7 @@ from make_golden import load
 LOG2PI = 1.8378770664093454835606594728112
 
 GAUSS_FIXTURES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks",
-                  "seasonal_hvblock"]
+                  "seasonal_hvblock", "rat_logo"]
 ALL_FIXTURES = GAUSS_FIXTURES + ["logistic_loo", "logistic_kfold"]
 
 _MODEL_CLS = {
@@ -17,6 +17,7 @@ _MODEL_CLS = {
     abi.FAMILY_RADON: lambda nm, d, f, kw: pcv.RadonStyleModel(nm, d, f, kw["include_floor"]),
     abi.FAMILY_SEASONAL_AR: lambda nm, d, f, kw: pcv.SeasonalARModel(nm, d, f, kw["ar_order"], kw["dummies"], kw["rho_transform"]),
     abi.FAMILY_LOGISTIC: lambda nm, d, f, kw: pcv.LogisticModel(nm, d, f),
+    abi.FAMILY_RAT_GROWTH: lambda nm, d, f, kw: pcv.RatGrowthModel(nm, d, f, kw.get("per_subject_slope", 1)),
 }
 
 
@@ -77,6 +78,15 @@ def term_scales(case, m, theta, fold):
         v = np.exp(th[J + P + 2]) ** 2
         va = np.exp(th[J + P + 1]) ** 2
         extra = np.sum(np.abs(th[:J] - th[J + P]) / va + (th[:J] - th[J + P]) ** 2 / va) + J + va
+    elif fam == abi.FAMILY_RAT_GROWTH:
+        J = d.n_groups
+        A = kw.get("per_subject_slope", 1)
+        base = 2 * J if A else J + 1
+        slope = th[J + d.group_id] if A else th[J]
+        mean = th[d.group_id] + slope * x[:, 0]
+        v = np.exp(th[-1]) ** 2
+        va = np.exp(th[base + (2 if A else 1)]) ** 2
+        extra = np.sum(np.abs(th[:2 * J if A else J + 1]) * (1 + np.abs(x).max())) / min(va, 1.0) + 1e4 + J * 100
     elif fam == abi.FAMILY_RADON:
         J = d.n_groups
         va, v = np.exp(th[J + 2]), np.exp(th[J + 3])

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 SHORT = np.load(os.path.join(HERE, "golden", "adapt_short.npz"))
 BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock",
-         "logistic_loo"]
+         "logistic_loo", "rat_logo"]
 
 
 @pytest.mark.parametrize("name", BASES)
@@ -40,7 +40,7 @@ def test_short_adaptation_follows_reference(name):
             assert np.all(np.isfinite(fit.draws)) and fit.kparams.step_size > 0
 
 
-@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "radon_logo", "seasonal_timeblocks", "logistic_loo"])
+@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "radon_logo", "seasonal_timeblocks", "logistic_loo", "rat_logo"])
 def test_full_adaptation_within_mc_error_of_reference(name):
     case = Case(name)
     import make_golden

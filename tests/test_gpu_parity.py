@@ -119,7 +119,7 @@ def test_hmc_step_injected(ctx, name):
 
 
 @pytest.mark.parametrize("name", with_kernels(["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
-                                               "seasonal_hvblock", "logistic_loo"]))
+                                               "seasonal_hvblock", "logistic_loo", "rat_logo"]))
 def test_chain_trajectory_reference_stream(ctx, name):
     """Same reference Philox stream (seed, ChainSampling, model, fold, chain): the device chain
     reproduces the oracle chain (identical integer draws; momenta to ~1 ulp) until chaos."""
@@ -137,7 +137,7 @@ def test_chain_trajectory_reference_stream(ctx, name):
 
 
 @pytest.mark.parametrize("name", with_kernels(["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
-                                               "seasonal_hvblock", "logistic_kfold"]))
+                                               "seasonal_hvblock", "logistic_kfold", "rat_logo"]))
 def test_run_pcv_within_mcse(ctx, name):
     """End-to-end run_pcv on the device vs the oracle run_pcv on the same inputs: the headline
     elpd / delta within Monte Carlo error, identical report structure."""
@@ -162,7 +162,8 @@ def test_run_pcv_within_mcse(ctx, name):
     c.close()
 
 
-SCORE_BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock"]
+SCORE_BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock",
+               "rat_logo"]
 
 
 def _score_cfg(case, score, iters=None, warmup=None, seed=1):

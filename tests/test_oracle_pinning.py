@@ -302,7 +302,8 @@ def test_hmc_trajectory_matches_reference_bitwise(name):
 
 # ---------------------------------------------------------------- HS / DSS (engine.cpp:322-373)
 SCORE_CASES = [(base, sc) for base in ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
-                                       "seasonal_timeblocks", "seasonal_hvblock"] for sc in ("hs", "dss")]
+                                       "seasonal_timeblocks", "seasonal_hvblock", "rat_logo"]
+               for sc in ("hs", "dss")]
 
 
 def score_fixture(base, sc):
@@ -349,7 +350,7 @@ def test_hs_closed_forms():  # test_scoring.cpp:44-62 via the oracle's pred_deri
 
 @pytest.mark.ref
 @pytest.mark.parametrize("name", ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
-                                  "seasonal_timeblocks", "seasonal_hvblock"])
+                                  "seasonal_timeblocks", "seasonal_hvblock", "rat_logo"])
 def test_pred_hooks_match_reference_bitwise(name):
     """Model::pred_derivs / pred_sample of the oracle == the reference (same stream)."""
     case = Case(name)
@@ -365,7 +366,7 @@ def test_pred_hooks_match_reference_bitwise(name):
 
 @pytest.mark.ref
 @pytest.mark.parametrize("name", ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks",
-                                  "seasonal_hvblock", "logistic_loo"])
+                                  "seasonal_hvblock", "logistic_loo", "rat_logo"])
 def test_initial_draw_matches_reference_bitwise(name):
     """pcvg_initial_draw (host, the full-data chains' starts) == Model::initial_draw of the
     reference (grouped_regression.cpp:177-188, radon.cpp:157-165, seasonal_ar.cpp:122-131)."""
