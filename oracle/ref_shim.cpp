@@ -16,6 +16,9 @@
 
 #include "../include/pcvg.h"
 #include "pcv/adapt.hpp"
+#include "pcv/models/registry.hpp"
+#include "pcv/report_io.hpp"
+#include "pcv/config.hpp"
 #include "pcv/engine.hpp"
 #include "pcv/errors.hpp"
 #include "pcv/folds.hpp"
@@ -404,6 +407,73 @@ int pcvref_adapt_trace(void* h, int32_t chains, int64_t warmup, int32_t n_lf, do
       }
     }
     std::memcpy(inv_mass_out, kp.inv_mass_diag.data(), sizeof(double) * d);
+  });
+}
+
+// The reference's own file writers/readers (registry.cpp:98-165, report_io.cpp), for the CLI
+// format tests: run_simulator with "key=value;..." arguments; read_full_data_fit.
+int pcvref_run_simulator(const char* family, const char* args, uint64_t seed, const char* out_dir) {
+  return guarded([&] {
+    pcv::ConfigMap a;
+    std::string s(args ? args : "");
+    size_t pos = 0;
+    while (pos < s.size()) {
+      size_t end = s.find(';', pos);
+      if (end == std::string::npos) end = s.size();
+      const std::string kv = s.substr(pos, end - pos);
+      const size_t eq = kv.find('=');
+      if (eq != std::string::npos) a.set(kv.substr(0, eq), kv.substr(eq + 1));
+      pos = end + 1;
+    }
+    pcv::run_simulator(family, a, seed, out_dir);
+  });
+}
+
+int pcvref_read_fit(const char* dir, const char* stem, int64_t* rows, int64_t* cols, double* step,
+                    double* first_row) {
+  return guarded([&] {
+    const auto fit = pcv::read_full_data_fit(dir, stem);
+    *rows = static_cast<int64_t>(fit.draws.size());
+    *cols = fit.draws.empty() ? 0 : static_cast<int64_t>(fit.draws[0].size());
+    *step = fit.kparams.step_size;
+    if (first_row && !fit.draws.empty())
+      std::memcpy(first_row, fit.draws[0].data(), sizeof(double) * fit.draws[0].size());
+  });
+}
+
+// Reference run_pcv written with the reference writers (report.json, progressive.csv, benchmark.csv).
+int pcvref_run_pcv_files(int32_t n_models, void** models, const int32_t* model_ids,
+                         const pcvg_kernel* kernels, const double* const* banks, const int64_t* bank_rows,
+                         const pcvg_run_config* c, int32_t threads, const char* out_dir) {
+  return guarded([&] {
+    pcv::RunConfig cfg;
+    cfg.chains = c->chains;
+    cfg.iters = c->iters;
+    cfg.warmup = c->warmup;
+    cfg.batch_size = c->batch_size;
+    cfg.blocks = c->blocks;
+    cfg.bench_draws = c->bench_draws;
+    cfg.bench_quantile = c->bench_quantile;
+    cfg.seed = c->seed;
+    cfg.score = static_cast<pcv::ScoreKind>(c->score);
+    cfg.checkpoint_every = c->checkpoint_every;
+    cfg.thread_budget = threads;
+    std::vector<pcv::FullDataFit> fits(n_models);
+    std::vector<pcv::ModelInput> inputs;
+    for (int m = 0; m < n_models; ++m) {
+      const size_t d = M(models[m]).dim();
+      fits[m].kparams.step_size = kernels[m].step_size;
+      fits[m].kparams.n_leapfrog = kernels[m].n_leapfrog;
+      fits[m].kparams.inv_mass_diag.assign(kernels[m].inv_mass_diag, kernels[m].inv_mass_diag + d);
+      for (int64_t r = 0; r < bank_rows[m]; ++r)
+        fits[m].draws.emplace_back(banks[m] + r * d, banks[m] + (r + 1) * d);
+      inputs.push_back({&M(models[m]), &fits[m], model_ids[m]});
+    }
+    const pcv::PcvReport r = pcv::run_pcv(inputs, cfg);
+    const std::string dir(out_dir);
+    pcv::write_report_json(dir + "/report.json", r);
+    pcv::write_progressive_csv(dir + "/progressive.csv", r);
+    pcv::write_benchmark_csv(dir + "/benchmark.csv", r);
   });
 }
 

@@ -59,7 +59,30 @@ def build(force=False, verbose=False):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    build_cli(force)
     return LIB
+
+
+# The command-line front end (cli/pcvg_main.cpp) over libpcvg.so; JSON via nlohmann/json, the
+# reference's own dependency, from the image (3.11.3 under cudnn_frontend).
+CLI_SRC = os.path.join(PKG, "cli", "pcvg_main.cpp")
+CLI = os.path.join(OUT, "pcvg")
+JSON_DIRS = ["/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"]
+
+
+def build_cli(force=False):
+    deps = [CLI_SRC, LIB, os.path.join(CSRC, "host_common.hpp"), os.path.join(PKG, "..", "include", "pcvg.h")]
+    if not force and not _newer(CLI, deps):
+        return CLI
+    inc = [d for d in JSON_DIRS if os.path.exists(os.path.join(d, "nlohmann", "json.hpp"))]
+    if not inc:
+        return None  # no JSON header in this image: the CLI is optional
+    cmd = [NVCC, "-O2", "-std=c++17", "-x", "cu", "-I" + inc[0], CLI_SRC, "-o", CLI, "-L" + OUT, "-lpcvg",
+           "-Xlinker", "-rpath=$ORIGIN"] + ARCH
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

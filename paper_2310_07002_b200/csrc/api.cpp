@@ -54,10 +54,6 @@ void make_kfold(int64_t, int32_t, uint64_t, int32_t*);
 void make_time_blocks(const pcvg_dataset*, int32_t, int32_t*);
 void make_hv_block(const pcvg_dataset*, int32_t, int64_t, int64_t*);
 void make_hv_racine(const pcvg_dataset*, int64_t, int64_t, int64_t*);
-void simulate_grouped(int32_t, int32_t, int32_t, double, uint64_t, double*, double*, int32_t*);
-void simulate_radon(int32_t, int32_t, uint64_t, double*, double*, int32_t*);
-void simulate_rat(int32_t, uint64_t, double*, double*, int32_t*);
-void simulate_seasonal(int64_t, int32_t, int32_t, double, double, double, uint64_t, double*, double*, int64_t*);
 void simulate_linreg(int64_t, int32_t, uint64_t, double*, double*, int32_t*);
 void simulate_logistic(int64_t, int32_t, uint64_t, double*, double*);
 // stats.cpp

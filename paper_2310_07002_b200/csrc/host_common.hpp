@@ -126,6 +126,23 @@ inline double beta_draw(HostRng& rng, double a, double b) {
   return x / (x + y);
 }
 
+// Ground truth of a simulated dataset (the `<family>_truth.json` sidecar, registry.cpp:99-160):
+// vectors and scalars by name.
+struct SimTruth {
+  std::vector<std::pair<std::string, std::vector<double>>> vectors;
+  std::vector<std::pair<std::string, double>> scalars;
+};
+
+// Host simulators (host_folds.cpp); `truth` may be null.
+void simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_beta, uint64_t seed, double* y,
+                      double* x, int32_t* g, SimTruth* truth = nullptr);
+void simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* g,
+                  SimTruth* truth = nullptr);
+void simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y, double* x,
+                    int32_t* g, SimTruth* truth = nullptr);
+void simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho, double amp, double sigma,
+                       uint64_t seed, double* y, double* x, int64_t* t, SimTruth* truth = nullptr);
+
 // Stable argsort by time (std::stable_sort in folds.cpp:95-98).
 std::vector<int64_t> time_order(const int64_t* t, int64_t n);
 

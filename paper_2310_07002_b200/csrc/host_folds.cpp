@@ -142,7 +142,7 @@ void make_hv_racine(const pcvg_dataset* d, int64_t v, int64_t h, int64_t* iv) {
 
 // simulate_grouped_regression, grouped_regression.cpp:232-268.
 void simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_beta, uint64_t seed, double* y,
-                      double* x, int32_t* g) {
+                      double* x, int32_t* g, SimTruth* truth) {
   if (J < 2) throw Error(PCVG_INVALID_INPUT, "simulator needs at least 2 groups");
   if (Nj < 1 || P < 1) throw Error(PCVG_INVALID_INPUT, "simulator needs per_group and covariates >= 1");
   HostRng rng(seed, stream_key(PCVG_STREAM_SIMULATE, 1, 0, 0));
@@ -166,11 +166,15 @@ void simulate_grouped(int32_t J, int32_t Nj, int32_t P, double min_beta, uint64_
       for (int p = 0; p < P; ++p) x[row * P + p] = xg[gg * P + p];
       g[row] = gg;
     }
+  if (truth) {
+    truth->vectors = {{"alpha", alpha}, {"beta", beta}};
+    truth->scalars = {{"mu_alpha", mu_alpha}, {"sigma_alpha", sigma_alpha}, {"sigma_y", sigma_y}};
+  }
 }
 
 // simulate_radon_style, radon.cpp:216-240.
 // simulate_rat_growth (rat_growth.cpp:310-336): n = 5 * subjects at times {8,15,22,29,36}.
-void simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* g) {
+void simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t* g, SimTruth* truth) {
   if (subjects < 2) throw Error(PCVG_INVALID_INPUT, "simulator needs at least 2 subjects");
   HostRng rng(seed, stream_key(PCVG_STREAM_SIMULATE, 2, 0, 0));
   const double mu_alpha = 250.0 + std::sqrt(20.0) * rng.normal();
@@ -180,9 +184,12 @@ void simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t
   const double sigma_y = gamma_draw(rng, 1.0, 2.0);
   const double times[5] = {8, 15, 22, 29, 36};
   int64_t i = 0;
+  std::vector<double> alpha, beta;
   for (int s = 0; s < subjects; ++s) {
     const double a = mu_alpha + sigma_alpha * rng.normal();
     const double b = mu_beta + sigma_beta * rng.normal();
+    alpha.push_back(a);
+    beta.push_back(b);
     for (double t : times) {
       y[i] = a + b * t + sigma_y * rng.normal();
       x[i] = t;
@@ -190,10 +197,15 @@ void simulate_rat(int32_t subjects, uint64_t seed, double* y, double* x, int32_t
       ++i;
     }
   }
+  if (truth) {
+    truth->vectors = {{"alpha", alpha}, {"beta", beta}};
+    truth->scalars = {{"mu_alpha", mu_alpha}, {"mu_beta", mu_beta}, {"sigma_alpha", sigma_alpha},
+                      {"sigma_beta", sigma_beta}, {"sigma_y", sigma_y}};
+  }
 }
 
 void simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y, double* x,
-                    int32_t* g) {
+                    int32_t* g, SimTruth* truth) {
   if (counties < 2 || houses < counties)
     throw Error(PCVG_INVALID_INPUT, "simulator needs counties >= 2 and houses >= counties");
   HostRng rng(seed, stream_key(PCVG_STREAM_SIMULATE, 3, 0, 0));
@@ -210,11 +222,16 @@ void simulate_radon(int32_t houses, int32_t counties, uint64_t seed, double* y, 
     x[i] = floor;
     g[i] = gg;
   }
+  if (truth) {
+    truth->vectors = {{"alpha", alpha}};
+    truth->scalars = {{"beta", beta}, {"mu_alpha", mu_alpha}, {"sigma_alpha2", sigma_alpha2},
+                      {"sigma_y2", sigma_y2}};
+  }
 }
 
 // simulate_seasonal_ar, seasonal_ar.cpp:167-205.
 void simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho, double amp, double sigma,
-                       uint64_t seed, double* y, double* x, int64_t* t) {
+                       uint64_t seed, double* y, double* x, int64_t* t, SimTruth* truth) {
   if (months <= p + q) throw Error(PCVG_INVALID_INPUT, "series too short for the requested AR order and dummies");
   if (p < 1) throw Error(PCVG_INVALID_INPUT, "AR order must be at least 1");
   HostRng rng(seed, stream_key(PCVG_STREAM_SIMULATE, 4, 0, 0));
@@ -238,6 +255,10 @@ void simulate_seasonal(int64_t months, int32_t p, int32_t q, double rho, double 
     const int month = static_cast<int>(s % 12);
     for (int j = 1; j <= q; ++j) x[row * nc + p + j - 1] = month == j ? 1.0 : 0.0;
     t[row] = s;
+  }
+  if (truth) {
+    truth->vectors = {{"beta", beta}, {"rho", rhos}};
+    truth->scalars = {{"sigma", sigma}};
   }
 }
 
