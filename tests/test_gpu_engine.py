@@ -164,3 +164,19 @@ def test_device_benchmark_equals_host_sequential():
     dev = pcv.merge_bench(2, case.K, cfg, done, True, cols, mx)
     np.testing.assert_array_equal(dev["benchmark"], seq["benchmark"])
     c.close()
+
+
+def test_shared_streams_identical_models_give_zero_delta():
+    """test_engine.cpp:187-201: two identical models with shared_streams consume the same chain
+    streams (engine.cpp:299-300), so every fold difference is exactly zero."""
+    case = Case("ex1_grouped_logo")
+    c = pcv.Context(0)
+    m, kp, bank = case.models[0], case.kparams[0], case.banks[0]
+    c.add_model(m, kp, bank, model_id=0)
+    c.add_model(m, kp, bank, model_id=1)
+    rep = c.run(abi.run_config(chains=4, iters=40, warmup=10, batch_size=10, bench_draws=10, seed=2,
+                               shared_streams=1))
+    assert np.all(rep["delta_k"] == 0.0) and rep["delta_hat"] == 0.0
+    rep2 = c.run(abi.run_config(chains=4, iters=40, warmup=10, batch_size=10, bench_draws=10, seed=2))
+    assert np.any(rep2["delta_k"] != 0.0)  # independent streams otherwise
+    c.close()
