@@ -255,13 +255,14 @@ def main():
                                             batch_size=min(50, args.steps), blocks=5, bench_draws=100,
                                             seed=1), device=local)
             d2h = sum(v.nbytes for v in rep.values() if isinstance(v, np.ndarray))
-        else:
-            with pcv.Context(local) as c2:
-                c2.add_model(model, kp, bank, model_id=0)
-                c2.begin(cfg)
-                c2.advance(args.steps)
-                cols2, _, _, done2 = c2.fold_stats(fe - fb)
-                d2h = sum(v.nbytes for v in cols2.values())
+        else:  # the fold-sharded multi-GPU driver (dist.run_pcv_sharded): tables gathered, device
+            # shuffle benchmark at global stream offsets, MAX-reduced
+            from paper_2310_07002_b200 import dist as pdist
+            rep = pdist.run_pcv_sharded([pcv.ModelInput(model, pcv.FullDataFit(kp, bank), 0)],
+                                        pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup,
+                                                      batch_size=min(50, args.steps), blocks=5,
+                                                      bench_draws=100, seed=1), device=local)
+            d2h = sum(v.nbytes for v in rep.values() if isinstance(v, np.ndarray))
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         if dist:
@@ -274,8 +275,9 @@ def main():
             line["e2e"] = {"value": chains_total * steps_all / e2e_s, "unit": "chain-steps/s",
                            "h2d_bytes_per_step": int(h2d / steps_all), "d2h_bytes_per_step": int(d2h / steps_all),
                            "wall_s": e2e_s, "chain_steps": chains_total * steps_all,
-                           "note": "pcvg_run with host inputs: upload, warm start, warm-up + sampling, "
-                                   "per-fold stats, shuffle benchmark (R=100), report download"}
+                           "note": "run_pcv (1 GPU: pcvg_run; N GPUs: dist.run_pcv_sharded) with host "
+                                   "inputs: upload, warm start, warm-up + sampling, per-fold stats, "
+                                   "shuffle benchmark (R=100, on device), report download"}
     if line is not None and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         cv, kind, sample = cpu_sample(K, 12, 1, threads)

@@ -91,3 +91,77 @@ def failed_from_divergences(div: np.ndarray, n_models: int, K: int, L: int, iter
     bad = np.all(d * 2 > iters, axis=2)  # [m, k]
     f = np.any(bad, axis=0).astype(np.int32)
     return np.tile(f, n_models)
+
+
+def run_pcv_sharded(inputs, cfg, device=0, group=None):
+    """run_pcv (engine.cpp:257-483) with the folds sharded across the ranks of `group` (one
+    process per GPU): every rank samples its contiguous fold range on its own device; at each
+    checkpoint the per-fold tables are all-gathered in fold order and merged identically on every
+    rank; the shuffle benchmark runs on each rank's own block sums at its global stream offset and
+    the replicate maxima are MAX-reduced. No block sums or chain states leave their GPU. Returns
+    the report dict (pcv.Context.run's layout) on every rank."""
+    import copy
+
+    import torch.distributed as dist
+
+    from . import pcv
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    K = inputs[0].model.K
+    nm = len(inputs)
+    fb, fe = shard_range(K, rank, world)
+    if cfg.early_stop:
+        raise pcv.InvalidInput("early stop is not available in the sharded driver")
+    cfg_s = copy.copy(cfg)
+    cfg_s.fold_begin, cfg_s.fold_end = fb, fe
+    if fe == fb:
+        raise pcv.InvalidInput("more ranks than folds")
+    checkpoints = list(range(cfg.checkpoint_every, cfg.iters, cfg.checkpoint_every)) if cfg.checkpoint_every > 0 else []
+    checkpoints.append(cfg.iters)
+    snaps = []
+    dev = None
+    try:
+        import torch
+        if torch.cuda.is_available() and dist.get_backend(group) == "nccl":
+            dev = torch.device("cuda", device)
+    except Exception:
+        dev = None
+    with pcv.Context(device) as ctx:
+        for mi in inputs:
+            ctx.add_model(mi.model, mi.fit.kparams, mi.fit.draws, mi.model_id)
+        ctx.begin(cfg_s)
+        done = 0
+        for ci, t in enumerate(checkpoints):
+            ctx.advance(t - done)
+            done = t
+            cols, div, dropped, iters = ctx.fold_stats(fe - fb)
+            full = gather_fold_tables(cols, nm, group)
+            last = ci + 1 == len(checkpoints)
+            if not last:
+                part = dict(full)
+                part["failed"] = np.zeros_like(part["failed"])
+                rep = pcv.merge(nm, K, cfg, iters, False, part)
+            else:
+                failed_local = cols["failed"][: fe - fb]
+                before, total = shard_benchmark_offsets(failed_local, group)
+                mx, nh = ctx.benchmark(failed_local, before, total, cfg.blocks)
+                mx, nh = reduce_benchmark(mx, nh, dev, group)
+                if nh.max() > 0:  # a below() rejection: the sequential stream needs all block sums
+                    yx, yx2 = ctx.block_sums(fe - fb, cfg.blocks)
+                    rep = pcv.merge(nm, K, cfg, iters, True, full, gather_rows(yx, nm, group),
+                                    gather_rows(yx2, nm, group))
+                else:
+                    rep = pcv.merge_bench(nm, K, cfg, iters, True, full, mx)
+                for name, _ in abi.FOLD_COLUMNS:  # per-fold columns (merge writes only `failed`)
+                    if name != "failed":
+                        rep[name] = full[name]
+                rep["divergences"] = gather_rows(div, nm, group)
+                parts = [None] * world
+                dist.all_gather_object(parts, int(dropped), group=group)
+                rep["dropped_batch_draws"] = int(sum(parts))
+                rep["iters_run"] = iters
+            snaps.append([iters, rep["delta_hat"], rep["mcse"], rep["epistemic_se"], rep["prob_a_better"],
+                          rep["ess_overall"], rep["rhat_max"]])
+    rep["snapshots"] = np.array(snaps)
+    rep["n_checkpoints"] = len(snaps)
+    return rep

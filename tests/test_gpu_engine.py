@@ -180,3 +180,34 @@ def test_shared_streams_identical_models_give_zero_delta():
     rep2 = c.run(abi.run_config(chains=4, iters=40, warmup=10, batch_size=10, bench_draws=10, seed=2))
     assert np.any(rep2["delta_k"] != 0.0)  # independent streams otherwise
     c.close()
+
+
+def test_sharded_driver_single_rank_equals_run():
+    """dist.run_pcv_sharded (fold-sharded multi-GPU driver: per-checkpoint table gathers, device
+    benchmark at global stream offsets, MAX reduction) in a one-rank process group reproduces
+    pcvg_run bit for bit."""
+    import os
+    import socket
+    import torch.distributed as tdist
+    from paper_2310_07002_b200 import dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        case = Case("ex1_grouped_logo")
+        inputs = [pcv.ModelInput(m, pcv.FullDataFit(kp, b), i)
+                  for i, (m, kp, b) in enumerate(zip(case.models, case.kparams, case.banks))]
+        cfg = abi.run_config(chains=4, iters=60, warmup=10, batch_size=10, bench_draws=30, seed=4,
+                             checkpoint_every=30)
+        rep = pcv.run_pcv(inputs, cfg)
+        rep2 = dist.run_pcv_sharded(inputs, cfg, device=0)
+        for k in ("delta_hat", "mcse", "epistemic_se", "rhat_max", "prob_a_better", "verdict_quantile_value"):
+            assert rep[k] == rep2[k], k
+        for k in ("estimate", "rhat", "failed", "divergences", "benchmark"):
+            np.testing.assert_array_equal(rep[k], rep2[k])
+        np.testing.assert_array_equal(rep["snapshots"], rep2["snapshots"])
+    finally:
+        tdist.destroy_process_group()
