@@ -166,6 +166,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "PCVG_FORCE_DEVICE" in os.environ:  # N ranks sharing one GPU (test of the multi-rank path)
+        local = int(os.environ["PCVG_FORCE_DEVICE"])
     if args.impl == "reference":
         return run_reference(args, rank)
 
@@ -175,7 +177,13 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink between the GPUs; PCVG_DIST_BACKEND=gloo runs the same multi-rank logic
+        # with host collectives (used to exercise N ranks on one GPU: no kernel waits on another)
+        backend = os.environ.get("PCVG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     d, f, kp, bank = load_inputs()
     K = args.folds or f.K
     from paper_2310_07002_b200.dist import shard_range
@@ -200,7 +208,7 @@ def main():
     _, launches1 = ctx.last_advance_ms()
     local_ms = float(np.sum(step_ms))
     if dist:
-        t = torch.tensor([local_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([local_ms], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     else:
@@ -266,7 +274,7 @@ def main():
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         if dist:
-            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            t = torch.tensor([e2e_s], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         h2d = d.y.nbytes + d.x.nbytes + f.test_index.nbytes + bank.nbytes + kp.inv_mass_diag.nbytes
