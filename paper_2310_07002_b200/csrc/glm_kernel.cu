@@ -266,8 +266,8 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
             const bool train = valid && static_cast<unsigned>(kv - lo[j][e]) >=
                                             static_cast<unsigned>(hi[j][e] - lo[j][e]);
             if constexpr (!kGauss) {
-              const double ex = exp_neg(fabs(x), sm.exp_tab);
-              const double inv = rcp_1_2(1.0 + ex);
+              const double ex = VALUE ? exp_neg(fabs(x), sm.exp_tab) : exp_neg_5(fabs(x), sm.exp_tab);
+              const double inv = VALUE ? rcp_1_2(1.0 + ex) : rcp_1_2_fast(1.0 + ex);
               const double sig = x >= 0.0 ? inv : ex * inv;
               r2[e] = train ? yv - sig : 0.0;
               if (VALUE) {

@@ -86,6 +86,38 @@ __device__ __forceinline__ double exp_neg(double a, const double* tab) {
   return (tab[n & 15] * scale) * p;
 }
 
+// exp(-a) for a >= 0 to ~1.5e-13 relative in 10 FP64 operations: exp_neg with a degree-5
+// polynomial (truncation |r|^6/720 <= 1.5e-13 at |r| <= ln2/32). Used where only the logistic
+// residual y - sigmoid(eta) needs it: an error d in sigmoid moves a gradient component by at most
+// sum_i |x_ij| d, far inside the 1e-12 * sum|terms| parity tolerance.
+__device__ __forceinline__ double exp_neg_5(double a, const double* tab) {
+  constexpr double kInvLn2x16 = 23.083120654223414;
+  constexpr double kLn2d16Hi = 0.04332169877307024;
+  constexpr double kLn2d16Lo = 1.1926343307941173e-11;
+  constexpr double kShift = 6755399441055744.0;
+  a = fmin(a, 700.0);
+  const double t = fma(a, kInvLn2x16, kShift);
+  const int n = __double2loint(t);
+  const double nd = t - kShift;
+  double r = fma(nd, kLn2d16Hi, -a);
+  r = fma(nd, kLn2d16Lo, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double scale = __hiloint2double((1023 - (n >> 4)) << 20, 0);
+  return (tab[n & 15] * scale) * p;
+}
+
+// 1 / d for d in [1, 2] to ~1e-13 relative: hardware approximation (~2^-22) + one Newton step.
+__device__ __forceinline__ double rcp_1_2_fast(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 // 1 / d for d in [1, 2]: hardware approximation + two Newton steps (no special cases needed).
 __device__ __forceinline__ double rcp_1_2(double d) {
   double r;
