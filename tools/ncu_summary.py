@@ -2,7 +2,7 @@
 """Summarises an ncu capture into profiles/ (tracked evidence).
 
   python tools/ncu_summary.py launches <launches.csv> <out.json>     # launch list -> per-kernel shares
-  python tools/ncu_summary.py full <prof.ncu-rep> <out.json> [tag]   # --set full -> key metrics
+  python tools/ncu_summary.py full <prof.ncu-rep | raw.csv> <out.json> [tag]   # --set full -> key metrics
 """
 import collections
 import csv
@@ -49,8 +49,11 @@ def launches(path, out):
 
 
 def full(path, out, tag=""):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if path.endswith(".csv"):  # raw page exported on the GPU box (ncu -i rep --page raw --csv)
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     res = {"source": path, "tag": tag, "launches": []}
