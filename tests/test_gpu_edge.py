@@ -1,0 +1,85 @@
+"""Edge cases of the device models against the CPU oracle: ragged group sizes and
+per-row fold keys in the group-batched kernel (the equal-size fixtures only exercise the
+uniform-key / equal-length path), poisoned (non-finite) test rows, and groups absent from a
+fold's training set (unseen-group predictive)."""
+import numpy as np
+import pytest
+
+from paper_2310_07002_b200 import abi, pcv
+import _oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def ragged_grouped(seed=3, J=45):
+    rng = np.random.default_rng(seed)
+    sizes = rng.integers(1, 12, J)
+    g = np.repeat(np.arange(J), sizes).astype(np.int32)
+    n = g.size
+    x = rng.standard_normal((n, 3))
+    alpha = rng.standard_normal(J)
+    y = alpha[g] + x @ np.array([0.5, -0.3, 0.2]) + 0.7 * rng.standard_normal(n)
+    return pcv.Dataset(y, x, g)
+
+
+def thetas(model, n, seed):
+    return np.array([pcv.initial_draw(model, seed, 100 + i) for i in range(n)]) * 0.5
+
+
+def scale(th):
+    return 1e4 * (1.0 + np.abs(th).max())
+
+
+@pytest.mark.parametrize("scheme", ["logo", "kfold", "loo"])
+@pytest.mark.parametrize("family", [abi.FAMILY_GROUPED, abi.FAMILY_RADON, abi.FAMILY_RAT_GROWTH])
+def test_ragged_groups_and_row_keys(scheme, family):
+    d = ragged_grouped()
+    if family == abi.FAMILY_RADON:
+        d = pcv.Dataset(d.y, (d.x[:, :1] > 0).astype(float), d.group_id)
+    if family == abi.FAMILY_RAT_GROWTH:
+        d = pcv.Dataset(d.y + 250.0, np.abs(d.x[:, :1]) * 10.0, d.group_id)
+    f = {"logo": pcv.make_logo_scheme, "kfold": lambda dd: pcv.make_kfold_scheme(dd, 7, 2),
+         "loo": pcv.make_loo_scheme}[scheme](d)
+    cls = {abi.FAMILY_GROUPED: lambda: pcv.GroupedRegressionModel("M", d, f),
+           abi.FAMILY_RADON: lambda: pcv.RadonStyleModel("M", d, f, True),
+           abi.FAMILY_RAT_GROWTH: lambda: pcv.RatGrowthModel("M", d, f, True)}[family]
+    model = cls()
+    om = O.OModel(d, f.arrays(), model.spec)
+    dim = model.dim()
+    kp = pcv.KernelParams(0.01, 8, np.ones(dim))
+    with pcv.Context(0) as ctx:
+        slot = ctx.add_model(model, kp, thetas(model, 2, 1))
+        folds = sorted({0, 1, f.K // 2, f.K - 1, f.K})
+        for fold in folds:
+            th = thetas(model, 3, fold + 7)
+            lp, g = ctx.eval(slot, np.full(3, fold), th)
+            for i in range(3):
+                olp, og = om.log_joint(th[i], fold), om.grad(th[i], fold)
+                s = scale(th[i])
+                assert abs(lp[i] - olp) <= 1e-12 * s * max(1.0, abs(olp)), (fold, lp[i], olp)
+                assert np.abs(g[i] - og).max() <= 1e-12 * s * max(1.0, np.abs(og).max()), fold
+            pr = ctx.eval_pred(slot, np.full(3, fold), th)
+            for i in range(3):
+                ref = om.log_pred(th[i], fold)
+                assert abs(pr[i] - ref) <= 1e-10 * (1.0 + abs(ref)), (fold, pr[i], ref)
+
+
+def test_poisoned_test_row():
+    """A non-finite y in a test row: the reference's log_joint multiplies the test term by 0,
+    which is NaN (grouped_regression.cpp:74-76); training folds stay finite."""
+    d = ragged_grouped(seed=5, J=20)
+    y = d.y.copy()
+    g = d.group_id
+    y[np.where(g == 3)[0][0]] = np.inf
+    d = pcv.Dataset(y, d.x, g)
+    f = pcv.make_logo_scheme(d)
+    model = pcv.GroupedRegressionModel("M", d, f)
+    om = O.OModel(d, f.arrays(), model.spec)
+    with pcv.Context(0) as ctx:
+        slot = ctx.add_model(model, pcv.KernelParams(0.01, 8, np.ones(model.dim())), thetas(model, 1, 1))
+        th = thetas(model, 1, 4)
+        for fold in (3, 4):
+            lp, _ = ctx.eval(slot, [fold], th)
+            olp = om.log_joint(th[0], fold)
+            assert (np.isnan(lp[0]) and np.isnan(olp)) or (not np.isfinite(olp) and lp[0] == olp) or \
+                abs(lp[0] - olp) <= 1e-10 * max(1.0, abs(olp)), (fold, lp[0], olp)
