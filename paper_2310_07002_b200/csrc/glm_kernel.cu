@@ -20,6 +20,7 @@
 // row tiles and the partial X^T R / residual sums are reduced through distributed shared memory in
 // fixed rank order, so every CTA of the cluster holds bit-identical state; rank 0 writes it back.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "device_common.cuh"
@@ -30,6 +31,7 @@
 namespace pcvg {
 
 int glm_cluster_size(int n, int kp, int nch);
+int glm_sm_count();
 
 namespace {
 
@@ -418,7 +420,8 @@ __device__ void glm_score_extra(const ModelDev& M, const ChainsDev& S, int gc, i
 }
 
 template <int FAM, int KP>
-__global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs) {
+__global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs,
+                                                           int tile0) {
   using G = Geom<KP>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem<KP>& sm = *reinterpret_cast<Smem<KP>*>(smem_raw);
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
   const int nch = S.nch;
   const int dim = M.dim;
   const size_t plane = static_cast<size_t>(dim) * nch;
-  const int tile = blockIdx.x / cs, crank = blockIdx.x % cs;  // chain tile, rank in the cluster
+  const int tile = tile0 + blockIdx.x / cs, crank = blockIdx.x % cs;  // chain tile, rank in the cluster
   const bool writer = crank == 0;                              // rank 0 owns all global writes
   const int ntiles_all = (M.n + G::TM - 1) / G::TM;
   const int t0 = crank * ntiles_all / cs, t1 = (crank + 1) * ntiles_all / cs;
@@ -727,23 +730,50 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int cs = glm_cluster_size(M.n, KP, S.nch);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles * cs);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = sizeof(Smem<KP>);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cs;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = cs > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs);
+  auto launch = [&](int tile0, int ntiles, int cs) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * cs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sizeof(Smem<KP>);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = cs > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs, tile0);
+  };
+  const int cs = glm_cluster_size(M.n, KP, S.nch);
+  const int sms = glm_sm_count();
+  static const bool no_split = std::getenv("PCVG_NO_TAIL_SPLIT") != nullptr;  // A/B tests only
+  if (cs == 1 && tiles > sms && tiles % sms != 0 && !no_split) {
+    // Wave tail: one CTA per SM per wave, so the last partial wave of r tiles would take as long
+    // as a full one. Its tiles run instead as row-split clusters of up to 8 CTAs (the cluster
+    // path of the few-chain configurations), same results bit for bit.
+    const int r = tiles % sms, ntiles_rows = (M.n + Geom<KP>::TM - 1) / Geom<KP>::TM;
+    int ct = 1;
+    while (ct < 8 && r * ct * 2 <= sms && ntiles_rows >= 4 * ct * 2) ct *= 2;
+    cudaError_t e = launch(0, tiles - r, 1);
+    if (e != cudaSuccess) return e;
+    return launch(tiles - r, r, ct);
+  }
+  return launch(0, tiles, cs);
 }
 
+
 }  // namespace
+
+int glm_sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 // Cluster size: enough CTAs per 64-chain tile to cover the GPU, at most 8 (portable), and at least
 // two row tiles per CTA.

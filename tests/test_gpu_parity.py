@@ -221,3 +221,34 @@ def test_score_unsupported_for_logistic(ctx):  # Model::check_score_support, mod
         with pytest.raises(pcv.UnsupportedScore):
             c.run(abi.run_config(chains=4, iters=20, warmup=2, batch_size=5, score=sc))
     c.close()
+
+
+def test_wave_tail_split_matches_unsplit():
+    """More than one wave of 64-chain tiles: the last partial wave runs as row-split clusters
+    (glm_kernel.cu launch_t). Its chains must follow the same trajectories as without the split
+    (same streams; the gradient differs only in summation order)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path[:0] = ["tests", "tests/golden", "."]
+from parity_util import Case
+from paper_2310_07002_b200 import abi, pcv
+case = Case("logistic_loo")
+with pcv.Context(0) as c:
+    c.add_model(case.models[0], case.kparams[0], case.banks[0], model_id=0)
+    rep = c.run(abi.run_config(chains=20, iters=10, warmup=2, batch_size=5, bench_draws=5, seed=2))
+np.save(sys.argv[1], rep["estimate"])
+'''
+    out = {}
+    for tag, env in (("split", {}), ("plain", {"PCVG_NO_TAIL_SPLIT": "1"})):
+        path = f"/tmp/pcvg_tail_{tag}.npy"
+        r = subprocess.run([sys.executable, "-c", code, path], env={**os.environ, **env}, capture_output=True,
+                           text=True, timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0, r.stderr
+        out[tag] = np.load(path)
+    a, b = out["split"], out["plain"]
+    assert a.shape == (500,)  # 500 folds x 20 chains = 157 tiles: 148 + a 9-tile tail
+    rel = np.abs(a - b) / (1.0 + np.abs(b))
+    assert np.mean(rel <= 1e-9) >= 0.95 and np.all(rel[:440] == 0.0), np.sort(rel)[-5:]
