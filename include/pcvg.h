@@ -236,6 +236,11 @@ pcvg_status pcvg_hmc_probe(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t
                            const double* theta, const double* momentum, const double* u,
                            double* theta_out, double* h0, double* h1, int32_t* accepted,
                            int32_t* divergent);
+/* leapfrog (hmc.cpp:22-51) from (theta, momentum) with the model's kernel: the end point
+ * (theta_out, momentum_out) of n_leapfrog steps; ok[c] = 0 where the trajectory went non-finite. */
+pcvg_status pcvg_leapfrog(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t* fold,
+                          const double* theta, const double* momentum, double* theta_out,
+                          double* momentum_out, int32_t* ok);
 /* n_steps consecutive hmc_step calls of chain (fold, chain) on its own reference stream
  * CounterRng(seed, stream_key(ChainSampling, model_id, fold, chain)) from theta0: writes the
  * position after every step [n_steps*dim] and the divergence flags [n_steps]. */

@@ -1064,6 +1064,52 @@ pcvg_status pcvg_hmc_probe(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t
   }));
 }
 
+pcvg_status pcvg_leapfrog(pcvg_ctx* ctx, int32_t slot, int64_t n, const int32_t* fold,
+                          const double* theta, const double* momentum, double* theta_out,
+                          double* momentum_out, int32_t* ok) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size())) throw Error(PCVG_INVALID_INPUT, "bad slot");
+    if (!theta || !momentum || !theta_out || !momentum_out) throw Error(PCVG_INVALID_INPUT, "null argument");
+    require_device(ctx);
+    const HostModel& m = *ctx->models[slot];
+    if (n < 1) return;
+    auto cs = probe_chains(ctx, m, n, fold, theta);
+    DevBuf<double> pout;
+    pout.alloc(static_cast<size_t>(n) * m.dim);
+    ChainsDev S = cs->view(1, 0, 0, 0);
+    S.probe_p_out = pout.p;
+    launch_family(ctx, m, S, make_args(kModeEval, 0));
+    DevBuf<double> mom, uu, oa, ob;
+    DevBuf<int32_t> fl;
+    mom.upload(std::vector<double>(momentum, momentum + n * m.dim));
+    uu.upload(std::vector<double>(n, 0.0));  // log(0) < -dH: every finite trajectory is accepted
+    oa.alloc(n);
+    ob.alloc(n);
+    fl.alloc(n);
+    RunArgs a = make_args(kModeProbe, 1);
+    a.probe_momentum = mom.p;
+    a.probe_u = uu.p;
+    a.out_a = oa.p;
+    a.out_b = ob.p;
+    a.out_flags = fl.p;
+    a.traj = pout.p;
+    launch_family(ctx, m, S, a);
+    ck(cudaStreamSynchronize(ctx->stream), "leapfrog");
+    const auto f0 = fl.download(ctx->stream);
+    const auto pos = cs->pos.download(ctx->stream);
+    const auto cur = cs->cur.download(ctx->stream);
+    const auto po = pout.download(ctx->stream);
+    const size_t plane = static_cast<size_t>(m.dim) * n;
+    for (int64_t c = 0; c < n; ++c) {
+      if (ok) ok[c] = (f0[c] >> 1) & 1 ? 0 : 1;
+      for (int d = 0; d < m.dim; ++d) {
+        theta_out[c * m.dim + d] = pos[cur[c] * plane + static_cast<size_t>(d) * n + c];
+        momentum_out[c * m.dim + d] = po[c * m.dim + d];
+      }
+    }
+  }));
+}
+
 pcvg_status pcvg_hmc_chain(pcvg_ctx* ctx, int32_t slot, int32_t fold, int32_t chain, uint64_t seed,
                            const double* theta0, int64_t n_steps, double* trajectory,
                            int32_t* divergent) {

@@ -647,6 +647,7 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
             S.pos[(cur ^ 1) * plane + si] = qs;
             S.grad[(cur ^ 1) * plane + si] = gsl;
             k1l += __ldg(M.inv_mass + gs) * pn * pn;
+            if (probe_p && S.probe_p_out) S.probe_p_out[static_cast<size_t>(c) * M.dim + gs] = pn;
           }
         }
       }
@@ -665,6 +666,7 @@ __device__ __forceinline__ void hgrad_pass(const ModelDev& M, const ChainsDev& S
           S.pos[(cur ^ 1) * plane + gi] = qg;
           S.grad[(cur ^ 1) * plane + gi] = gg;
           k1l += __ldg(M.inv_mass + g) * pn * pn;
+          if (probe_p && S.probe_p_out) S.probe_p_out[static_cast<size_t>(c) * M.dim + g] = pn;
         }
       }
     }
@@ -1036,6 +1038,13 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
         A.out_a[c] = h0;
         A.out_b[c] = h1;
         A.out_flags[c] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
+        if (A.traj) {  // final momentum of the trajectory (leapfrog probe)
+#pragma unroll
+          for (int i = 0; i < NGM; ++i)
+            if (i < ng) A.traj[static_cast<size_t>(c) * M.dim + M.goff + gidx<FAM>(M, i)] = pG[i];
+          if constexpr (NB == 0)
+            for (int g = 0; g < J; ++g) A.traj[static_cast<size_t>(c) * M.dim + g] = S.wp[static_cast<size_t>(g) * nch + c];
+        }
       }
       continue;
     }

@@ -591,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
                 const size_t gi = (cu ^ 1) * plane + static_cast<size_t>(k) * nch + ogc;
                 S.pos[gi] = q;
                 S.grad[gi] = g;
+                if (A.mode == kModeProbe && A.traj) A.traj[static_cast<size_t>(ogc) * dim + k] = pown[j];
               }
             }
           }

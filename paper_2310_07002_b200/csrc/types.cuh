@@ -125,6 +125,7 @@ struct ChainsDev {
   double* warm_sum;      // WarmupStats::logpred_sum
   AccumDev acc;
   ExtraDev X;
+  double* probe_p_out;  // leapfrog probe: final momentum [nch][dim] of group dims (batched kernel)
 };
 
 struct RunArgs {

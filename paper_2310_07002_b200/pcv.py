@@ -100,6 +100,7 @@ def load():
     _sig(lib, "pcvg_eval_pred", i32, [vp, i32, i64, pi32, pf, pf])
     _sig(lib, "pcvg_hmc_probe", i32, [vp, i32, i64, pi32, pf, pf, pf, pf, pf, pf, pi32, pi32])
     _sig(lib, "pcvg_hmc_chain", i32, [vp, i32, i32, i32, u64, pf, i64, pf, pi32])
+    _sig(lib, "pcvg_leapfrog", i32, [vp, i32, i64, pi32, pf, pf, pf, pf, pi32])
     _sig(lib, "pcvg_score_streams", i32, [vp, i32, i64, pf, f64, i32, i32, pf])
     _sig(lib, "pcvg_checkpoint_count", i32, [P(abi.RunConfig)])
     _sig(lib, "pcvg_run", i32, [vp, P(abi.RunConfig), P(abi.Report)])
@@ -462,6 +463,18 @@ class Context:
         self._chk(self.lib.pcvg_hmc_probe(self.h, slot, n, _p(folds, C.c_int32), _p(th), _p(mo), _p(u),
                                           _p(out), _p(h0), _p(h1), _p(acc, C.c_int32), _p(div, C.c_int32)))
         return out, h0, h1, acc, div
+
+    def leapfrog(self, slot, folds, thetas, momenta):
+        """leapfrog (hmc.cpp:22-51) end points (theta', p', ok) on the device."""
+        folds = np.ascontiguousarray(np.atleast_1d(folds), dtype=np.int32)
+        th = np.ascontiguousarray(np.atleast_2d(thetas), dtype=np.float64)
+        mo = np.ascontiguousarray(np.atleast_2d(momenta), dtype=np.float64)
+        n = th.shape[0]
+        qo, po = np.zeros_like(th), np.zeros_like(th)
+        ok = np.zeros(n, dtype=np.int32)
+        self._chk(self.lib.pcvg_leapfrog(self.h, slot, n, _p(folds, C.c_int32), _p(th), _p(mo), _p(qo), _p(po),
+                                         _p(ok, C.c_int32)))
+        return qo, po, ok
 
     def hmc_chain(self, slot, fold, chain, seed, theta0, n_steps):
         th = np.ascontiguousarray(theta0, dtype=np.float64)

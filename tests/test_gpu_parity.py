@@ -252,3 +252,42 @@ np.save(sys.argv[1], rep["estimate"])
     assert a.shape == (500,)  # 500 folds x 20 chains = 157 tiles: 148 + a 9-tile tail
     rel = np.abs(a - b) / (1.0 + np.abs(b))
     assert np.mean(rel <= 1e-9) >= 0.95 and np.all(rel[:440] == 0.0), np.sort(rel)[-5:]
+
+
+@pytest.mark.parametrize("name", with_kernels(["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo",
+                                               "seasonal_hvblock", "logistic_loo", "rat_logo"]))
+def test_leapfrog_endpoint_and_reversibility(ctx, name):
+    """leapfrog (hmc.cpp:22-51): the device end point (theta', p') matches the oracle's, and
+    integrating back from (theta', -p') returns to (theta, -p) within 1e-10 (test_hmc.cpp:134-147)."""
+    case, c, slots = case_in(ctx, name)
+    rng = np.random.default_rng(11)
+    m, slot = 0, slots[0]
+    om, kp = case.omodels[m], case.kparams[m]
+    th = sample_thetas(case, m, 4, seed=2)
+    mom = rng.standard_normal(th.shape) / np.sqrt(kp.inv_mass_diag)
+    folds = np.array([0, 1, case.K // 2, case.K], dtype=np.int32)
+    q1, p1, ok = c.leapfrog(slot, folds, th, mom)
+    assert ok.all()
+    for i in range(4):
+        okr, oq, op = om.leapfrog(int(folds[i]), kp.step_size, kp.n_leapfrog, kp.inv_mass_diag, th[i], mom[i])
+        np.testing.assert_allclose(q1[i], oq, rtol=1e-8, atol=1e-9)
+        np.testing.assert_allclose(p1[i], op, rtol=1e-8, atol=1e-8)
+    q2, p2, ok2 = c.leapfrog(slot, folds, q1, -p1)
+    assert ok2.all()
+    np.testing.assert_allclose(q2, th, rtol=0, atol=1e-10 * (1 + np.abs(th).max()))
+    np.testing.assert_allclose(-p2, mom, rtol=0, atol=1e-10 * (1 + np.abs(mom).max()) * 10)
+    c.close()
+
+
+def test_snapshots_prefix_stable(ctx):
+    """test_engine.cpp:150-173: the first snapshot of a 200-iteration run equals the final
+    statistics of a 100-iteration run (R-hat up to the block-boundary summation order)."""
+    case, c, slots = case_in(ctx, "ex1_grouped_logo")
+    base = dict(chains=4, warmup=20, batch_size=10, bench_draws=10, seed=6)
+    long = c.run(abi.run_config(iters=200, checkpoint_every=100, **base))
+    short = c.run(abi.run_config(iters=100, **base))
+    a, b = long["snapshots"][0], short["snapshots"][0]
+    assert a[0] == b[0] == 100
+    assert a[1] == b[1] and a[2] == b[2] and a[5] == b[5]  # delta_hat, mcse, ess
+    assert abs(a[6] - b[6]) <= 1e-12 * b[6]
+    c.close()
