@@ -39,6 +39,16 @@ FLOP_PER_CHAIN_STEP = N_LF * 4.0 * N_OBS * (P + 1)
 CPU_SAMPLE_FOLDS = 64
 
 
+def peak_tf32():
+    """Dense TF32 tensor peak: half the measured dense bf16 figure (tcgen05 kind::tf32 runs at half
+    the kind::f16 rate)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["bf16_tflops"] / 2.0, "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)"
+    except (OSError, KeyError, ValueError):
+        return 1125.0, "nominal dense TF32 (2.25 PF/s bf16 / 2; MEASURED_PEAKS.json absent)"
+
+
 def peak_fp64():
     path = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
     with open(path) as f:
@@ -162,6 +172,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--folds", type=int, default=0, help="debug: limit the fold count")
+    ap.add_argument("--fp32", action="store_true",
+                    help="the separately reported FP32 variant (glm32_kernel: tcgen05 kind::tf32, "
+                         "hi/lo split operands); device-timed only")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -192,6 +205,9 @@ def main():
     cfg = pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup, batch_size=min(50, args.steps),
                         blocks=5, bench_draws=100, seed=1, fold_begin=fb, fold_end=fe)
     ctx = pcv.Context(local)
+    if args.fp32:
+        ctx.set_kernel_policy(ctx.KERNEL_TF32)
+        args.no_e2e = args.no_cpu = True
     ctx.add_model(model, kp, bank, model_id=0)
     ctx.begin(cfg)  # Step 2: warm start + args.warmup untimed warm-up transitions
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -229,7 +245,7 @@ def main():
     ctx.close()
 
     # roofline of the dominant kernel (glm_kernel<logistic,52>: one launch per step)
-    peak, peak_src = peak_fp64()
+    peak, peak_src = peak_fp64() if not args.fp32 else peak_tf32()
     per_launch_ms = local_ms / args.steps
     achieved = FLOP_PER_CHAIN_STEP * (fe - fb) * L / (per_launch_ms * 1e-3) / 1e12
     traffic = None
@@ -241,7 +257,8 @@ def main():
     if rank == 0:
         line = {"metric": "chain-steps/sec", "value": value, "unit": "chain-steps/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 (tf32 hi/lo split; chain state f64)" if args.fp32 else "f64",
                 "data": "synthetic",
                 "config": {"workload": WORKLOAD, "folds": K, "chains_per_fold": L, "n_obs": N_OBS,
                            "covariates": P, "n_leapfrog": N_LF, "chains": chains_total,
@@ -250,7 +267,7 @@ def main():
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "flop_per_chain_step": FLOP_PER_CHAIN_STEP, "peak_source": peak_src,
-                             "kernel": "glm_kernel<logistic,52> (FP64 DMMA)",
+                             "kernel": "glm32_kernel (tcgen05 kind::tf32)" if args.fp32 else "glm_kernel<logistic,52> (FP64 DMMA)",
                              "traffic_source": "profiles/r01_ncu_glm.json (ncu --set full, dram read+write per launch)"},
                 "clocks": clk.summary(), "gpu_launches": int(launches1 - launches0), "result": result}
     # e2e: the public API call with host buffers (pcvg_run: H2D of data/bank, Step 2 + Step 3,

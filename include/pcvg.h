@@ -219,7 +219,10 @@ pcvg_status pcvg_model_dim(const pcvg_ctx* ctx, int32_t slot, int32_t* dim);
  * effects when enough chains (or a row-split cluster) fill the GPU, else the generic lane-split
  * kernel; GENERIC / TENSOR force one (tests run both). Logistic always uses the tensor kernel,
  * hierarchical families (J > 1) always the generic one. */
-enum { PCVG_KERNEL_AUTO = 0, PCVG_KERNEL_GENERIC = 1, PCVG_KERNEL_TENSOR = 2 };
+enum { PCVG_KERNEL_AUTO = 0, PCVG_KERNEL_GENERIC = 1, PCVG_KERNEL_TENSOR = 2, PCVG_KERNEL_TF32 = 3 };
+/* PCVG_KERNEL_TF32: the FP32 variant of the logistic family: both contractions on
+ * tcgen05 kind::tf32 with hi/lo-split operands (FP32-class accuracy, per-step values within 1e-5
+ * of the FP64 path); chain state, energies and accumulators stay FP64. Other families ignore it. */
 pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy);
 pcvg_status pcvg_model_test_size(const pcvg_ctx* ctx, int32_t slot, int32_t fold, int64_t* n);
 

@@ -31,6 +31,9 @@ cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A
 int glm_width(int family, int J, int nc);
 int glm_cluster_size(int n, int kp, int nch);
 cudaError_t launch_glm(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+size_t glm32_image_bytes(int64_t n);
+void glm32_tile_image(const double* xr, int kp, const double* y, const int* key, int64_t n, unsigned char* out);
 cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const double* bank,
                                int64_t bank_rows, cudaStream_t st);
 cudaError_t launch_centers(const ChainsDev& S, int nfold, int64_t warmup, double* centers, int D,
@@ -118,6 +121,7 @@ struct HostModel {
   DevBuf<double> y, x, xr, inv_mass, bank;
   DevBuf<int> key, grp_ptr, lo, hi, ntrain, fseg, sgroup, sunseen, srow, srows;
   DevBuf<double> yb, xb;         // group-batched layout (ModelDev::nb > 0)
+  DevBuf<unsigned char> x32;     // logistic FP32 variant tile images
   DevBuf<int> keyb, bgroup, boff, tfirst, tr0, trows, bkey, bgrows, buni;
   int64_t bank_rows = 0;
   ModelDev md{};
@@ -392,6 +396,11 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
       for (int c = 0; c < m.nc; ++c) xr[r * nc_pad + 1 + c] = d->x[m.perm[r] * d->n_cov + c];
     }
     m.xr.upload(xr);
+    if (s->family == PCVG_FAMILY_LOGISTIC && m.nc + 1 <= 56) {  // FP32 (tcgen05 TF32) variant
+      std::vector<unsigned char> img(glm32_image_bytes(n));
+      glm32_tile_image(xr.data(), nc_pad, y.data(), key.data(), n, img.data());
+      m.x32.upload(img);
+    }
   }
   m.grp_ptr.upload(hier ? grp_ptr : std::vector<int>{0});
 
@@ -624,6 +633,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.bgrows = m.bgrows.p;
   md.buniform = m.buni.p;
   md.ring = ring;
+  md.x32 = m.x32.p;
   return hm;
 }
 
@@ -645,7 +655,9 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
   if (!st) st = ctx->stream;
   const ModelDev& md = md_override ? *md_override : m.md;
   cudaError_t e;
-  if (use_glm(ctx, m, S.nch)) {
+  if (ctx->policy == PCVG_KERNEL_TF32 && md.family == kLogistic && md.x32) {
+    e = launch_glm32(md, S, A, st);  // FP32 variant: tcgen05 kind::tf32, split operands
+  } else if (use_glm(ctx, m, S.nch)) {
     e = launch_glm(md, S, A, st);
   } else if (md.nb > 0 && (ctx->policy != PCVG_KERNEL_GENERIC || md.family >= kRatB)) {
     e = launch_gauss(md, S, A, 0, st);  // group-batched hierarchical kernel
@@ -928,7 +940,7 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
 }
 
 pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy) {
-  if (!ctx || policy < PCVG_KERNEL_AUTO || policy > PCVG_KERNEL_TENSOR) return PCVG_INVALID_INPUT;
+  if (!ctx || policy < PCVG_KERNEL_AUTO || policy > PCVG_KERNEL_TF32) return PCVG_INVALID_INPUT;
   ctx->policy = policy;
   return PCVG_OK;
 }

@@ -81,6 +81,7 @@ struct ModelDev {
   const int* bgrows;      // [nb*32] the group's row count
   const int* buniform;    // [nb] 1 if every group of the batch has the batch's row count
   int ring;               // 1: row tiles staged through a shared-memory TMA ring; 0: read via L1
+  const unsigned char* x32;  // logistic FP32 variant: TF32-split tile images (glm32_kernel.cu)
 };
 
 constexpr int kMaxBatches = 16;
