@@ -1,28 +1,31 @@
 // FP32 variant of the logistic HMC kernel on the 5th-generation tensor cores (sm_100a), the
-// "FP32 variant reported separately" of SURVEY 8(d): the two contractions of every gradient pass,
-//   eta = X . Theta        (128 rows x 64 chains, K = 56)
-//   G   = X^T . R          (56 columns x 64 chains, K = 128 rows per tile)
-// run as tcgen05.mma kind::tf32 with both operands split exactly into a TF32 high part and an FP32
-// remainder (x = hi + lo, hi = round-to-TF32(x)); all four products are accumulated in FP32 in
-// tensor memory, which gives FP32-class accuracy (per-step gradients within 1e-5 of the FP64
-// path, the north star's FP32 tolerance). The split is folded into the operand shapes instead of
-// extra instructions:
-//   eta: B = [Theta_hi | Theta_lo] (N = 128), issued once with A = X_hi and once with A = X_lo;
-//        eta = D[:, c] + D[:, 64 + c].
-//   G:   A = [X_hi^T ; X_lo^T] (M = 128 stacked columns), issued once with B = R_hi and once with
-//        B = R_lo; G = D[k, :] + D[56 + k, :].
-// Every operand is K-major (SWIZZLE_NONE canonical layout, 16-byte core rows of 4 TF32 values), so
-// each 128-row tile of the design has two host-built images: the eta image ([16-byte column chunk]
-// [row][4], hi then lo) and the G image ([16-byte row chunk][stacked column][4]). They stream by
-// TMA bulk copies into two single buffers that are refilled as soon as the MMA reading them has
-// completed (the eta image during the epilogue and G, the G image during the next eta), with y and
-// the row keys double-buffered beside the eta image. Since the design does not depend on theta,
-// the copies run ahead across gradient passes. One elected thread issues the MMAs and commits them
-// to mbarriers; all 16 warps drain TMEM (warp w reads lane quadrant w%4, chain group w/4),
-// evaluate the sigmoid and the mask in FP32, and write R_hi / R_lo in the B layout of G. G is
-// flushed from TMEM into FP64 per-CTA accumulators every 16 tiles. The chain
-// state, integrator, energies, Metropolis test, RNG, log_pred and accumulators are FP64 and the
-// same as glm_kernel.cu (hmc.cpp:22-99, engine.cpp:342-381).
+// "FP32 variant reported separately" of SURVEY 8(d). A CTA runs 128 chains; per 128-row tile of the
+// design the two contractions of a gradient pass are computed transposed, chains on the TMEM lanes:
+//   eta^T = Theta^T . X^T   (M = 128 chains, N = 128 rows, K = 56 columns)   SS form
+//   G^T  += R^T . X         (M = 128 chains, N = 112 stacked columns, K = 128 rows)   TS form:
+//                           R^T is written by the epilogue straight into tensor memory and read
+//                           there as the A operand; it never touches shared memory.
+// Operands are split exactly as x = hi + lo (hi = x rounded to TF32, lo = the FP32 remainder):
+// eta^T = Th_hi.X_hi + Th_hi.X_lo + Th_lo.X_hi (3 MMAs per k-step) and
+// G^T = R_hi.[X_hi | X_lo] + R_lo.[X_hi | X_lo(0..7)] (N = 112 and N = 64), FP32 accumulation in
+// TMEM, flushed into FP64 per-CTA accumulators every 16 tiles. That gives FP32-class results (the
+// north star's 1e-5 tolerance).
+//
+// Warp specialisation (544 threads): 16 epilogue warps + 1 control warp.
+//  * Control thread (warp 16, lane 0): TMA bulk copies of the tile images and every tcgen05.mma.
+//    Tensor-pipe order: ..., G(g-1), eta(g+1), G(g), eta(g+2), ... so the eta of the next tile
+//    and the G of the previous one run while the epilogue warps work on tile g.
+//  * Epilogue warp w: TMEM lane quadrant w%4 (32 chains, one per thread) x row block w/4 (32 rows).
+//    Per tile: tcgen05.ld eta^T, residual r = mask(y - sigmoid(eta)) in FP32, tcgen05.st R_hi^T in
+//    place over eta^T (double-buffered by tile parity), R_lo^T into its own columns once G(g-1)
+//    has consumed the previous one, then one mbarrier arrive.
+// TMEM (512 columns): eta/R_hi buffers 0..127 and 128..255, R_lo 256..383, G^T 384..495.
+// Shared memory: Theta^T image (A of eta), eta image of X (B of eta), G image of X (B of G),
+// y/keys (double-buffered); all K-major SWIZZLE_NONE canonical layouts (a tf32 MMA with an
+// MN-major SWIZZLE_NONE operand returns zeros on B200: tools/probes/tf32_umma_probe.cu; the TS form
+// is checked by tools/probes/tf32_ts_probe.cu).
+// The chain state, integrator, energies, Metropolis test, RNG, log_pred and accumulators are FP64
+// and the same as glm_kernel.cu (hmc.cpp:22-99, engine.cpp:342-381).
 #include <math_constants.h>
 
 #include <cstdint>
@@ -38,43 +41,46 @@ namespace {
 
 using namespace tc;
 
-constexpr int kC = 64;                          // chains per CTA
-constexpr int kThreads = 512;                   // 16 warps
-constexpr int kOwners = kThreads / kC;          // owner threads per chain
-constexpr int kRows = 128;                      // rows per tile = UMMA M of eta = TMEM lanes
+constexpr int kC = 128;                         // chains per CTA (= UMMA M, TMEM lanes)
+constexpr int kEpiWarps = 16;
+constexpr int kEpiThreads = kEpiWarps * 32;     // 512
+constexpr int kThreads = kEpiThreads + 32;      // + control warp
+constexpr int kCtl = kEpiThreads;               // the control thread
+constexpr int kOwners = kEpiThreads / kC;       // owner threads per chain (4)
+constexpr int kRows = 128;                      // rows per tile (= N of eta, K of G)
 constexpr int kK = 56;                          // padded design width (1 + 50 covariates + pad)
-constexpr int kChunks = kK / 4;                 // 16-byte column chunks per row
+constexpr int kChunks = kK / 4;                 // 16-byte column chunks per row (14)
 constexpr int kOwn = (kK + kOwners - 1) / kOwners;
-constexpr int kChunkBytes = kRows * 16;         // one column chunk of a tile image (2048)
+constexpr int kChunkBytes = kRows * 16;         // one column chunk of the eta image (2048)
 constexpr int kXImg = 2 * kChunks * kChunkBytes;  // eta image: hi + lo (57344)
 constexpr int kYK = kRows * 8;                  // y (f32) + key (i32)
-constexpr int kGImg = (kRows / 4) * 128 * 16;   // G image: [row chunk][128 stacked columns][4] (65536)
+constexpr int kGN = 2 * kK;                     // stacked hi/lo columns (112) = N of G
+constexpr int kGChunk = kGN * 16;               // one row chunk of the G image (1792)
+constexpr int kGImg = (kRows / 4) * kGChunk;    // G image: [row chunk][112 stacked columns][4] (57344)
 constexpr int kTileBytes = kXImg + kYK + kGImg; // per tile in HBM: eta image, y/key, G image
-constexpr int kRLbo = kC * 16 + 16;             // R image chunk stride: +16 B keeps the stores conflict-free
-constexpr int kRImg = (kRows / 4) * kRLbo;
-constexpr int kThImg = kChunks * 2 * kC * 16;   // [chunk][hi chains | lo chains][4]
+constexpr int kThChunk = kC * 16;               // one column chunk of the Theta^T image (2048)
+constexpr int kThImg = 2 * kChunks * kThChunk;  // [hi chunks | lo chunks][chain][4] (57344)
 constexpr int kFlush = 16;                      // tiles between FP32 -> FP64 flushes of G
-constexpr uint32_t kTmemCols = 256;             // eta: 128 columns, G: 64 columns
-constexpr uint32_t kEtaCol = 0, kGCol = 128;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColE0 = 0, kColRL = 256, kColG = 384;
 
 static_assert(kTileBytes % 16 == 0 && kXImg % 16 == 0 && kYK % 16 == 0, "bulk copy granularity");
-static_assert(2 * kK <= 128, "stacked hi/lo columns fit one M = 128 operand");
+static_assert(kThImg == kK * kC * 8, "the momentum staging [k][chain] (FP64) aliases the Theta image");
+static_assert(kGN % 16 == 0 && kGN <= 128, "N of the G MMA");
 
 struct Smem32 {
-  alignas(128) unsigned char xa[kXImg];
-  alignas(128) unsigned char yk[2][kYK];
-  alignas(128) unsigned char xb[kGImg];
   alignas(128) unsigned char th[kThImg];
-  alignas(128) unsigned char r[2][kRImg];
+  alignas(128) unsigned char xa[kXImg];
+  alignas(128) unsigned char xb[kGImg];
+  alignas(128) unsigned char yk[2][kYK];
   double red[kOwners][kC];
   double pri[kOwners][kC];
   double llq[4][kC];
-  int lo[kC], hi[kC], ntr[kC], bad[kC], cur[kC];
+  int lo[kC], hi[kC], bad[kC], cur[kC];
   unsigned long long full_a, full_b, full_y[2];  // eta image, G image, y/key slots
-  unsigned long long mma_eta, mma_g;
+  unsigned long long eta_bar[2], g_bar, rdy;     // eta(g) done (per buffer), G(g) done, R(g) written
   uint32_t tmem_base;
 };
-
 static_assert(sizeof(Smem32) <= 232448, "fits the 227 KB opt-in shared memory of one CTA");
 
 // ------------------------------------------------------------------ tcgen05 helpers
@@ -85,18 +91,24 @@ __device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t 
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-// Instruction descriptor: kind::tf32, FP32 accumulate, M x N, operand majors (0 = K, 1 = MN).
-__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n, int a_mn, int b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
-         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+// Instruction descriptor: kind::tf32, FP32 accumulate, M x N, both operands K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
          (static_cast<uint32_t>(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, bool acc) {
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, bool acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc ? 1 : 0));
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc ? 1 : 0));
 }
 
 __device__ __forceinline__ void mma_commit(unsigned long long* bar) {
@@ -109,16 +121,21 @@ __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 
 // 16 consecutive 32-bit TMEM columns of this thread's lane.
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
 }
 
 __device__ __forceinline__ float tf32_hi(float x) {
@@ -127,22 +144,16 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ void split_store(unsigned char* hi_img, unsigned char* lo_img, uint32_t off, float v) {
-  const float h = tf32_hi(v);
-  *reinterpret_cast<float*>(hi_img + off) = h;
-  *reinterpret_cast<float*>(lo_img + off) = v - h;
-}
-
 __device__ __forceinline__ double bernoulli_logit32(double y, double x) {
   return y * x - (fmax(x, 0.0) + log1p(exp(-fabs(x))));
 }
 
-// ------------------------------------------------------------------ one gradient pass
-// Tile stream state: g = tiles consumed so far (over all passes), ia / ib = eta / G images issued.
-// Load j carries tile j % ntiles; the eta image buffer, the G image buffer and each y/key slot see
-// their loads complete in order, so the mbarrier parity of load j is j & 1 (y/key: (j >> 1) & 1).
+// ------------------------------------------------------------------ tile stream
+// g = tiles consumed so far (over all passes); ia / ib = eta / G images issued. Load j carries
+// tile j % ntiles. Every barrier completes once per tile in tile order, so the parity of tile g
+// is g & 1 (per-buffer barriers eta_bar[g & 1] and full_y[g & 1]: (g >> 1) & 1).
 struct Pipe32 {
-  uint32_t g = 0, ia = 0, ib = 0, n_eta = 0, n_g = 0;
+  uint32_t g = 0, ia = 0, ib = 0;
 };
 
 __device__ __forceinline__ const unsigned char* tile_src(const ModelDev& M, uint32_t j, int ntiles) {
@@ -162,109 +173,174 @@ __device__ __forceinline__ void load_g_image(Smem32& sm, const ModelDev& M, uint
   bulk_g2s(sm.xb, tile_src(M, j, ntiles) + kXImg + kYK, kGImg, &sm.full_b);
 }
 
-// Accumulates G (FP64, [stacked column m][chain] in gsc) over all tiles for the CTA's 64 chains
-// with the parameters in the theta image; VALUE adds the per-chain log-likelihood into sm.llq.
-// `more` = another pass follows (its first tile may be prefetched).
+// eta^T(g) into buffer g & 1: 7 k-steps x {hi.hi, hi.lo, lo.hi}.
+__device__ __forceinline__ void issue_eta(Smem32& sm, uint32_t g) {
+  constexpr uint32_t kId = idesc_tf32(128, kRows);
+  const uint32_t d = sm.tmem_base + kColE0 + (g & 1u) * 128u;
+#pragma unroll 1
+  for (int ks = 0; ks < kChunks / 2; ++ks) {
+    const uint64_t ah = sdesc(sm.th + (2 * ks) * kThChunk, kThChunk, 128);
+    const uint64_t al = sdesc(sm.th + (kChunks + 2 * ks) * kThChunk, kThChunk, 128);
+    const uint64_t bh = sdesc(sm.xa + (2 * ks) * kChunkBytes, kChunkBytes, 128);
+    const uint64_t bl = sdesc(sm.xa + (kChunks + 2 * ks) * kChunkBytes, kChunkBytes, 128);
+    mma_ss(d, ah, bh, kId, ks > 0);
+    mma_ss(d, ah, bl, kId, true);
+    mma_ss(d, al, bh, kId, true);
+  }
+  mma_commit(&sm.eta_bar[g & 1]);
+}
+
+// G^T += R_hi^T(g) . [X_hi | X_lo] + R_lo^T . [X_hi | X_lo(0..7)]: 16 k-steps of 8 rows.
+__device__ __forceinline__ void issue_g(Smem32& sm, uint32_t g, bool fresh) {
+  constexpr uint32_t kIdHi = idesc_tf32(128, kGN);
+  constexpr uint32_t kIdLo = idesc_tf32(128, 64);
+  const uint32_t d = sm.tmem_base + kColG;
+  const uint32_t rh = sm.tmem_base + kColE0 + (g & 1u) * 128u, rl = sm.tmem_base + kColRL;
+#pragma unroll 1
+  for (int ks = 0; ks < kRows / 8; ++ks) {
+    const uint64_t b = sdesc(sm.xb + (2 * ks) * kGChunk, kGChunk, 128);
+    mma_ts(d, rh + 8 * ks, b, kIdHi, !(fresh && ks == 0));
+    mma_ts(d, rl + 8 * ks, b, kIdLo, true);
+  }
+  mma_commit(&sm.g_bar);
+}
+
+// ------------------------------------------------------------------ one gradient pass
+// Accumulates G (FP64, [stacked column][chain] in gsc) over all tiles for the CTA's 128 chains
+// with the parameters in the Theta image; VALUE leaves the per-chain log-likelihood in sm.llq.
+// `more` = another pass follows (its first tile images may be prefetched).
 template <bool VALUE>
 __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& P, int ntiles, bool more) {
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int qd = w & 3, cg = w >> 2;  // TMEM lane quadrant, chain group (16 chains)
-  const uint32_t tmem = sm.tmem_base;
-  const uint32_t lane_off = static_cast<uint32_t>(32 * qd) << 16;
-  constexpr uint32_t kIdEta = idesc_tf32(128, 128, 0, 0);
-  constexpr uint32_t kIdG = idesc_tf32(128, 64, 0, 0);
-  if (VALUE) {
-    for (int i = tid; i < 4 * kC; i += kThreads) (&sm.llq[0][0])[i] = 0.0;
-    __syncthreads();
-  }
-  if (tid == 0) {  // first tile of the pass, unless the previous pass prefetched it
-    if (P.ia == P.g) load_eta_image(sm, M, P.ia++, ntiles);
-    if (P.ib == P.g) load_g_image(sm, M, P.ib++, ntiles);
-  }
-  bool first_flush = true;
-  for (int t = 0; t < ntiles; ++t) {
-    const uint32_t g = P.g + t;
-    const bool next = t + 1 < ntiles || more;
-    // ---- eta = X . [Th_hi | Th_lo]  (7 k-steps x {X_hi, X_lo})
-    if (tid == 0) {
-      mbar_wait(&sm.full_a, g & 1u);
-      tmem_fence_after();
-      for (int half = 0; half < 2; ++half)
-        for (int ks = 0; ks < kChunks / 2; ++ks) {
-          const uint64_t a = sdesc(sm.xa + (half * kChunks + 2 * ks) * kChunkBytes, kChunkBytes, 128);
-          const uint64_t b = sdesc(sm.th + 2 * ks * (2 * kC * 16), 2 * kC * 16, 128);
-          mma_tf32(tmem + kEtaCol, a, b, kIdEta, half > 0 || ks > 0);
-        }
-      mma_commit(&sm.mma_eta);
-    }
-    mbar_wait(&sm.mma_eta, P.n_eta & 1u);
-    ++P.n_eta;
-    if (tid == 0 && next) load_eta_image(sm, M, P.ia++, ntiles);  // eta(g) done: the buffer is free
-    mbar_wait(&sm.full_y[g & 1], (g >> 1) & 1u);
+  const int tid = threadIdx.x;
+  const uint32_t g0 = P.g;
+  if (tid == kCtl) {
+    // ---------------- control thread
+    if (P.ia == g0) load_eta_image(sm, M, P.ia++, ntiles);
+    if (P.ib == g0) load_g_image(sm, M, P.ib++, ntiles);
+    mbar_wait(&sm.full_a, g0 & 1u);
     tmem_fence_after();
-    // ---- residuals of this warp's 32 rows x 16 chains
-    {
-      float eh[16], el[16];
-      tmem_ld16(tmem + lane_off + kEtaCol + 16 * cg, eh);
-      tmem_ld16(tmem + lane_off + kEtaCol + kC + 16 * cg, el);
-      const int r = 32 * qd + l;
-      const float yv = reinterpret_cast<const float*>(sm.yk[g & 1])[r];
-      const int kv = reinterpret_cast<const int*>(sm.yk[g & 1] + kRows * 4)[r];
-      const uint32_t roff = (r >> 2) * kRLbo + (r & 3) * 4;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int c = 16 * cg + j;
-        const float eta = eh[j] + el[j];
-        const bool real = kv >= 0;
-        const bool train = real && static_cast<unsigned>(kv - sm.lo[c]) >= static_cast<unsigned>(sm.hi[c] - sm.lo[c]);
-        const float sig = 1.0f / (1.0f + __expf(-eta));
-        const float res = train ? yv - sig : 0.0f;
-        split_store(sm.r[0], sm.r[1], roff + c * 16, res);
-        if (VALUE) {
-          float ll = 0.0f;
-          if (train) ll = yv * eta - (fmaxf(eta, 0.0f) + log1pf(__expf(-fabsf(eta))));
-          else if (real && !isfinite(eta)) ll = CUDART_NAN_F;  // 0 * non-finite test term
-          for (int o = 16; o > 0; o >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, o);
-          if (l == 0) sm.llq[qd][c] += static_cast<double>(ll);
-        }
+    issue_eta(sm, g0);
+    if (ntiles > 1 || more) {
+      mbar_wait(&sm.eta_bar[g0 & 1u], (g0 >> 1) & 1u);  // the eta image buffer is free
+      load_eta_image(sm, M, P.ia++, ntiles);
+      if (ntiles > 1) {
+        mbar_wait(&sm.full_a, (g0 + 1) & 1u);
+        tmem_fence_after();
+        issue_eta(sm, g0 + 1);
       }
     }
-    tmem_fence_before();
-    fence_proxy_async();  // R image writes before the async-proxy MMA reads them
-    __syncthreads();
-    // ---- G += [X_hi^T ; X_lo^T] . R_hi + ... . R_lo  (16 k-steps of 8 rows)
-    const bool fresh = t % kFlush == 0;
-    if (tid == 0) {
+    for (int t = 0; t < ntiles; ++t) {
+      const uint32_t g = g0 + t;
+      mbar_wait(&sm.rdy, g & 1u);  // R^T(g) is in tensor memory
       mbar_wait(&sm.full_b, g & 1u);
       tmem_fence_after();
-      for (int ks = 0; ks < kRows / 8; ++ks) {
-        const uint64_t a = sdesc(sm.xb + 2 * ks * 2048, 2048, 128);
-        const uint64_t b0 = sdesc(sm.r[0] + 2 * ks * kRLbo, kRLbo, 128);
-        const uint64_t b1 = sdesc(sm.r[1] + 2 * ks * kRLbo, kRLbo, 128);
-        mma_tf32(tmem + kGCol, a, b0, kIdG, !(fresh && ks == 0));
-        mma_tf32(tmem + kGCol, a, b1, kIdG, true);
+      issue_g(sm, g, t % kFlush == 0);
+      if (t + 2 < ntiles || (t + 2 == ntiles && more)) {
+        mbar_wait(&sm.eta_bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);  // eta(g+1) read the buffer
+        load_eta_image(sm, M, P.ia++, ntiles);  // y/key slot g & 1: epilogue(g) is done
+        if (t + 2 < ntiles) {
+          mbar_wait(&sm.full_a, (g + 2) & 1u);
+          tmem_fence_after();
+          issue_eta(sm, g + 2);
+        }
       }
-      mma_commit(&sm.mma_g);
+      if (t + 1 < ntiles || more) {
+        mbar_wait(&sm.g_bar, g & 1u);  // G(g) read the G image buffer
+        load_g_image(sm, M, P.ib++, ntiles);
+      }
     }
-    mbar_wait(&sm.mma_g, P.n_g & 1u);
-    ++P.n_g;
-    if (tid == 0 && next) load_g_image(sm, M, P.ib++, ntiles);  // G(g) done: the buffer is free
-    const bool flush = (t + 1) % kFlush == 0 || t + 1 == ntiles;
-    if (flush) {  // G (FP32, TMEM) -> FP64 accumulators [m][chain]
+  } else if (tid < kEpiThreads) {
+    // ---------------- epilogue warps
+    const int w = tid >> 5, l = tid & 31;
+    const int q = w & 3, rb = w >> 2;
+    const int c = 32 * q + l;  // this thread's chain (TMEM lane)
+    const uint32_t lane = static_cast<uint32_t>(32 * q) << 16;
+    const int clo = sm.lo[c], chi = sm.hi[c];
+    const unsigned span = static_cast<unsigned>(chi - clo);
+    double llacc = 0.0;
+    bool first_flush = true;
+    auto flush = [&]() {  // G^T (FP32, TMEM) -> FP64 accumulators [column][chain]
       tmem_fence_after();
-      float gv[16];
-      tmem_ld16(tmem + lane_off + kGCol + 16 * cg, gv);
-      const int m = 32 * qd + l;
-      if (m < 2 * kK) {
-        double* dst = gsc + static_cast<size_t>(m) * kC + 16 * cg;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) dst[j] = first_flush ? static_cast<double>(gv[j]) : dst[j] + static_cast<double>(gv[j]);
+      for (int h = 0; h < 2; ++h) {
+        const int col0 = 32 * rb + 16 * h;
+        if (col0 >= kGN) break;
+        uint32_t gv[16];
+        tmem_ld16(sm.tmem_base + lane + kColG + col0, gv);
+        double* dst = gsc + static_cast<size_t>(col0) * kC + c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const double v = static_cast<double>(__uint_as_float(gv[j]));
+          dst[j * kC] = first_flush ? v : dst[j * kC] + v;
+        }
       }
       first_flush = false;
+    };
+    for (int t = 0; t < ntiles; ++t) {
+      const uint32_t g = g0 + t;
+      mbar_wait(&sm.eta_bar[g & 1u], (g >> 1) & 1u);
+      mbar_wait(&sm.full_y[g & 1u], (g >> 1) & 1u);
+      tmem_fence_after();
+      const uint32_t ebuf = sm.tmem_base + lane + kColE0 + (g & 1u) * 128u + 32 * rb;
+      const float4* yv4 = reinterpret_cast<const float4*>(sm.yk[g & 1u]) + 8 * rb;
+      const int4* kv4 = reinterpret_cast<const int4*>(sm.yk[g & 1u] + kRows * 4) + 8 * rb;
+      uint32_t rlo[32];
+      float ll = 0.0f;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t e[16];
+        tmem_ld16(ebuf + 16 * h, e);
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 y4 = yv4[4 * h + j4];
+          const int4 k4 = kv4[4 * h + j4];
+          const float ys[4] = {y4.x, y4.y, y4.z, y4.w};
+          const int ks[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * j4 + u;
+            const float eta = __uint_as_float(e[j]);
+            const bool real = ks[u] >= 0;
+            const bool train = real && static_cast<unsigned>(ks[u] - clo) >= span;
+            const float sig = __fdividef(1.0f, 1.0f + __expf(-eta));
+            const float r = train ? ys[u] - sig : 0.0f;
+            const float rh = tf32_hi(r);
+            e[j] = __float_as_uint(rh);
+            rlo[16 * h + j] = __float_as_uint(r - rh);
+            if (VALUE) {
+              if (train) ll += ys[u] * eta - (fmaxf(eta, 0.0f) + log1pf(__expf(-fabsf(eta))));
+              else if (real && !isfinite(eta)) ll += CUDART_NAN_F;  // 0 * non-finite test term
+            }
+          }
+        }
+        tmem_st16(ebuf + 16 * h, e);  // R_hi^T in place of eta^T
+      }
+      if (VALUE) llacc += static_cast<double>(ll);
+      if (t > 0) {  // G(g-1) has consumed R_lo(g-1); flush it if it closed a group
+        mbar_wait(&sm.g_bar, (g - 1) & 1u);
+        if (t % kFlush == 0) flush();
+      }
+      {
+        const uint32_t rl = sm.tmem_base + lane + kColRL + 32 * rb;
+        uint32_t a[16], b[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          a[j] = rlo[j];
+          b[j] = rlo[16 + j];
+        }
+        tmem_st16(rl, a);
+        tmem_st16(rl + 16, b);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       tmem_fence_before();
+      mbar_arrive(&sm.rdy);
     }
-    __syncthreads();  // eta / R buffers and the G accumulator are reused by the next tile
+    mbar_wait(&sm.g_bar, (g0 + ntiles - 1) & 1u);
+    flush();
+    if (VALUE) sm.llq[rb][c] = llacc;
   }
+  tmem_fence_before();
+  __syncthreads();  // G scratch / llq complete; every buffer of the pass is released
   P.g += ntiles;
 }
 
@@ -277,19 +353,25 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
   const size_t plane = static_cast<size_t>(dim) * nch;
   const int tile = blockIdx.x;
   const int ntiles = (M.n + kRows - 1) / kRows;
+  const bool owner = tid < kEpiThreads;
   const int oc = tid & (kC - 1), ok = tid / kC;
   const int ogc = tile * kC + oc;
-  const bool ovalid = ogc < nch;
+  const bool ovalid = owner && ogc < nch;
   const bool is_chain = tid < kC;
   const int gc = tile * kC + tid;
   const bool cvalid = is_chain && gc < nch;
-  double* gsc = gscratch + static_cast<size_t>(blockIdx.x) * (2 * kK) * kC;
+  double* gsc = gscratch + static_cast<size_t>(blockIdx.x) * kGN * kC;
 
-  if (tid == 0) mbar_init(&sm.full_a, 1);
-  if (tid == 1) mbar_init(&sm.full_b, 1);
-  if (tid == 2) mbar_init(&sm.mma_eta, 1);
-  if (tid == 3) mbar_init(&sm.mma_g, 1);
-  if (tid == 4 || tid == 5) mbar_init(&sm.full_y[tid - 4], 1);
+  if (tid == 0) {
+    mbar_init(&sm.full_a, 1);
+    mbar_init(&sm.full_b, 1);
+    mbar_init(&sm.full_y[0], 1);
+    mbar_init(&sm.full_y[1], 1);
+    mbar_init(&sm.eta_bar[0], 1);
+    mbar_init(&sm.eta_bar[1], 1);
+    mbar_init(&sm.g_bar, 1);
+    mbar_init(&sm.rdy, kEpiThreads);
+  }
   fence_mbar_init();
   if (tid < 32) {  // warp 0 allocates the tensor memory
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&sm.tmem_base)),
@@ -305,14 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
       fold = S.fold_override ? S.fold_override[gc] : S.fold0 + gc / S.L;
       sm.lo[tid] = M.fold_lo[fold];
       sm.hi[tid] = M.fold_hi[fold];
-      sm.ntr[tid] = M.n_train[fold];
       sm.cur[tid] = S.cur[gc];
       lp0 = S.lp0[gc];
       R.init(S.seed, S.rng_stream[gc], S.rng_pos[gc], S.rng_cached[gc], S.rng_has[gc] != 0);
     } else {
       sm.lo[tid] = 0;
       sm.hi[tid] = 0;
-      sm.ntr[tid] = M.n;
       sm.cur[tid] = 0;
     }
   }
@@ -323,18 +403,20 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
   Pipe32 P;
 
   double qown[kOwn];
-  // owners publish theta (hi / lo) into the B image of eta: element (n, k) at
-  // (k/4) * (2 kC 16) + n * 16 + (k%4) * 4, n = chain (hi) or kC + chain (lo)
+  // owners publish theta (hi / lo) into the A image of eta^T: element (chain, k) at
+  // (k/4) * kThChunk + chain * 16 + (k%4) * 4, lo chunks after the hi chunks
   auto put_theta = [&]() {
+    if (owner) {
 #pragma unroll
-    for (int j = 0; j < kOwn; ++j) {
-      const int k = ok + kOwners * j;
-      if (k < dim) {
-        const float v = static_cast<float>(qown[j]);
-        const float h = tf32_hi(v);
-        const uint32_t off = (k >> 2) * (2 * kC * 16) + (k & 3) * 4;
-        *reinterpret_cast<float*>(sm.th + off + oc * 16) = h;
-        *reinterpret_cast<float*>(sm.th + off + (kC + oc) * 16) = v - h;
+      for (int j = 0; j < kOwn; ++j) {
+        const int k = ok + kOwners * j;
+        if (k < dim) {
+          const float v = static_cast<float>(qown[j]);
+          const float h = tf32_hi(v);
+          const uint32_t off = (k >> 2) * kThChunk + oc * 16 + (k & 3) * 4;
+          *reinterpret_cast<float*>(sm.th + off) = h;
+          *reinterpret_cast<float*>(sm.th + kChunks * kThChunk + off) = v - h;
+        }
       }
     }
     fence_proxy_async();
@@ -349,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
   };
 
   if (A.mode == kModeEval) {
-    const int cu = sm.cur[oc];
+    const int cu = owner ? sm.cur[oc] : 0;
 #pragma unroll
     for (int j = 0; j < kOwn; ++j) {
       const int k = ok + kOwners * j;
@@ -358,16 +440,18 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
     put_theta();
     __syncthreads();
     grad_pass32<true>(sm, M, gsc, P, ntiles, false);
-    double pr = 0.0;
+    if (owner) {
+      double pr = 0.0;
 #pragma unroll
-    for (int j = 0; j < kOwn; ++j) {
-      const int k = ok + kOwners * j;
-      if (k < dim) {
-        if (ovalid) S.grad[cu * plane + static_cast<size_t>(k) * nch + ogc] = gk_of(k) - qown[j];
-        pr += -0.5 * (kLog2Pi + qown[j] * qown[j]);
+      for (int j = 0; j < kOwn; ++j) {
+        const int k = ok + kOwners * j;
+        if (k < dim) {
+          if (ovalid) S.grad[cu * plane + static_cast<size_t>(k) * nch + ogc] = gk_of(k) - qown[j];
+          pr += -0.5 * (kLog2Pi + qown[j] * qown[j]);
+        }
       }
+      sm.pri[ok][oc] = pr;
     }
-    sm.pri[ok][oc] = pr;
     __syncthreads();
     if (cvalid) {
       const double lp = lp_from_partials(tid);
@@ -379,9 +463,10 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
     const int n_lf = M.n_lf;
     for (int64_t it = 0; it < A.n_iters; ++it) {
       if (A.mode != kModePred) {
-        // momentum refresh (chain thread, reference draw order) -> staging in sm.red/pri? use R image
+        // momentum refresh (chain thread, reference draw order), staged [k][chain] in the Theta
+        // image (free between passes)
         double k0 = 0.0;
-        double* pstage = reinterpret_cast<double*>(sm.r[0]);  // [k][chain], free between passes
+        double* pstage = reinterpret_cast<double*>(sm.th);
         if (is_chain) {
           for (int k = 0; k < dim; ++k) {
             const double mk = __ldg(M.inv_mass + k);
@@ -395,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
         }
         __syncthreads();
         double pown[kOwn];
-        {
+        if (owner) {
           const int cu = sm.cur[oc];
           bool bad = false;
 #pragma unroll
@@ -413,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
           }
           if (bad) sm.bad[oc] = 1;
         }
-        __syncthreads();  // momentum staging read before the R images are overwritten
+        __syncthreads();  // momentum staging read before the Theta image is overwritten
         put_theta();
         __syncthreads();
         for (int s = 0; s < n_lf; ++s) {
@@ -421,38 +506,40 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
           const bool more = !last || it + 1 < A.n_iters;
           if (last) grad_pass32<true>(sm, M, gsc, P, ntiles, more);
           else grad_pass32<false>(sm, M, gsc, P, ntiles, more);
-          const double scale = last ? half : eps;
-          const int cu = sm.cur[oc];
-          bool bad = false;
-          double part = 0.0, part2 = 0.0;
+          if (owner) {
+            const double scale = last ? half : eps;
+            const int cu = sm.cur[oc];
+            bool bad = false;
+            double part = 0.0, part2 = 0.0;
 #pragma unroll
-          for (int j = 0; j < kOwn; ++j) {
-            const int k = ok + kOwners * j;
-            if (k < dim) {
-              const double g = gk_of(k) - qown[j];
-              bad |= !isfinite(g);
-              pown[j] += scale * g;
-              bad |= !isfinite(pown[j]);
-              if (last) {
-                part += __ldg(M.inv_mass + k) * pown[j] * pown[j];
-                part2 += -0.5 * (kLog2Pi + qown[j] * qown[j]);
-                if (ovalid) {
-                  const size_t gi = (cu ^ 1) * plane + static_cast<size_t>(k) * nch + ogc;
-                  S.pos[gi] = qown[j];
-                  S.grad[gi] = g;
-                  if (A.mode == kModeProbe && A.traj) A.traj[static_cast<size_t>(ogc) * dim + k] = pown[j];
+            for (int j = 0; j < kOwn; ++j) {
+              const int k = ok + kOwners * j;
+              if (k < dim) {
+                const double g = gk_of(k) - qown[j];
+                bad |= !isfinite(g);
+                pown[j] += scale * g;
+                bad |= !isfinite(pown[j]);
+                if (last) {
+                  part += __ldg(M.inv_mass + k) * pown[j] * pown[j];
+                  part2 += -0.5 * (kLog2Pi + qown[j] * qown[j]);
+                  if (ovalid) {
+                    const size_t gi = (cu ^ 1) * plane + static_cast<size_t>(k) * nch + ogc;
+                    S.pos[gi] = qown[j];
+                    S.grad[gi] = g;
+                    if (A.mode == kModeProbe && A.traj) A.traj[static_cast<size_t>(ogc) * dim + k] = pown[j];
+                  }
+                } else {
+                  qown[j] += eps * __ldg(M.inv_mass + k) * pown[j];
+                  bad |= !isfinite(qown[j]);
                 }
-              } else {
-                qown[j] += eps * __ldg(M.inv_mass + k) * pown[j];
-                bad |= !isfinite(qown[j]);
               }
             }
+            if (last) {
+              sm.red[ok][oc] = part;
+              sm.pri[ok][oc] = part2;
+            }
+            if (bad) sm.bad[oc] = 1;
           }
-          if (last) {
-            sm.red[ok][oc] = part;
-            sm.pri[ok][oc] = part2;
-          }
-          if (bad) sm.bad[oc] = 1;
           __syncthreads();  // G scratch read by every owner before the next pass rewrites it
           if (!last) {
             put_theta();
@@ -495,8 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
         __syncthreads();
         if (A.mode == kModeProbe) continue;
         if (A.mode == kModeChain) {
-          const int cu = sm.cur[oc];
           if (ovalid && A.traj) {
+            const int cu = sm.cur[oc];
 #pragma unroll
             for (int j = 0; j < kOwn; ++j) {
               const int k = ok + kOwners * j;
@@ -542,10 +629,10 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
       if (A.mode == kModeWarmup) S.warm_sum[gc] += warm;
     }
   }
-  if (tid == 0) {  // no bulk copy may still be landing in shared memory at exit
+  if (tid == kCtl) {  // no bulk copy may still be landing in shared memory at exit
     if (P.ia > P.g) {
       mbar_wait(&sm.full_a, P.g & 1u);
-      mbar_wait(&sm.full_y[P.g & 1], (P.g >> 1) & 1u);
+      mbar_wait(&sm.full_y[P.g & 1u], (P.g >> 1) & 1u);
     }
     if (P.ib > P.g) mbar_wait(&sm.full_b, P.g & 1u);
   }
@@ -561,8 +648,8 @@ size_t glm32_image_bytes(int64_t n) { return static_cast<size_t>((n + kRows - 1)
 
 // Host: the tile images of the augmented design xr ([n][KP] row-major, column 0 = intercept). Per
 // 128-row tile: the eta image [hi: 14 chunks][lo: 14 chunks] x [128 rows][4 columns], y (FP32), the
-// row key (int32, -1 on padding rows), then the G image [32 row chunks][128 stacked columns: hi 0..55,
-// lo 56..111, zero 112..127][4 rows].
+// row key (int32, -1 on padding rows), then the G image [32 row chunks][112 stacked columns: hi
+// 0..55, lo 56..111][4 rows].
 void glm32_tile_image(const double* xr, int kp, const double* y, const int* key, int64_t n, unsigned char* out) {
   const int64_t ntiles = (n + kRows - 1) / kRows;
   for (int64_t t = 0; t < ntiles; ++t) {
@@ -587,7 +674,7 @@ void glm32_tile_image(const double* xr, int kp, const double* y, const int* key,
         const size_t off = static_cast<size_t>(k / 4) * kRows * 4 + r * 4 + (k % 4);
         hi[off] = h;
         lo[off] = v - h;
-        const size_t go = static_cast<size_t>(r / 4) * 128 * 4 + (r % 4);
+        const size_t go = static_cast<size_t>(r / 4) * kGN * 4 + (r % 4);
         gi[go + static_cast<size_t>(k) * 4] = h;
         gi[go + static_cast<size_t>(kK + k) * 4] = v - h;
       }
@@ -612,7 +699,7 @@ cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A
   static int scratch_tiles = 0;
   if (tiles > scratch_tiles) {
     if (scratch) cudaFree(scratch);
-    cudaError_t e = cudaMalloc(&scratch, sizeof(double) * static_cast<size_t>(tiles) * 2 * kK * kC);
+    cudaError_t e = cudaMalloc(&scratch, sizeof(double) * static_cast<size_t>(tiles) * kGN * kC);
     if (e != cudaSuccess) return e;
     scratch_tiles = tiles;
   }
