@@ -38,7 +38,8 @@ def _compile(src, force):
     if not force and not _newer(obj, deps):
         return obj, None
     lang = [] if src.endswith(".cu") else ["-x", "cu"]
-    cmd = [NVCC] + ARCH + FLAGS + lang + ["-c", path, "-o", obj]
+    extra = os.environ.get("PCVG_NVCC_DEFS", "").split()  # tooling only (e.g. -DPCVG_GLM32_TRACE)
+    cmd = [NVCC] + ARCH + FLAGS + extra + lang + ["-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

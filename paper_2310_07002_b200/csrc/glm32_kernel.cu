@@ -29,6 +29,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 
 #include "device_common.cuh"
@@ -144,6 +145,15 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(r);
 }
 
+// 1 / (1 + 2^(-eta log2 e)) with one MUFU.EX2 and one MUFU.RCP (ftz forms: no range fix-ups);
+// relative error ~2^-21. eta -> -inf gives rcp(inf) = 0, eta -> +inf gives 1, NaN propagates.
+__device__ __forceinline__ float sigmoid_fast(float eta) {
+  float e, s;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(eta * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(1.0f + e));
+  return s;
+}
+
 __device__ __forceinline__ double bernoulli_logit32(double y, double x) {
   return y * x - (fmax(x, 0.0) + log1p(exp(-fabs(x))));
 }
@@ -173,16 +183,16 @@ __device__ __forceinline__ void load_g_image(Smem32& sm, const ModelDev& M, uint
   bulk_g2s(sm.xb, tile_src(M, j, ntiles) + kXImg + kYK, kGImg, &sm.full_b);
 }
 
-// eta^T(g) into buffer g & 1: 7 k-steps x {hi.hi, hi.lo, lo.hi}.
+// eta^T(g) into buffer g & 1: 7 k-steps x {hi.hi, hi.lo, lo.hi}. Descriptors advance by adding
+// (byte offset >> 4) to the start-address field (no carry: every image lies below 256 KB).
 __device__ __forceinline__ void issue_eta(Smem32& sm, uint32_t g) {
   constexpr uint32_t kId = idesc_tf32(128, kRows);
   const uint32_t d = sm.tmem_base + kColE0 + (g & 1u) * 128u;
-#pragma unroll 1
+  const uint64_t a0 = sdesc(sm.th, kThChunk, 128), b0 = sdesc(sm.xa, kChunkBytes, 128);
+#pragma unroll
   for (int ks = 0; ks < kChunks / 2; ++ks) {
-    const uint64_t ah = sdesc(sm.th + (2 * ks) * kThChunk, kThChunk, 128);
-    const uint64_t al = sdesc(sm.th + (kChunks + 2 * ks) * kThChunk, kThChunk, 128);
-    const uint64_t bh = sdesc(sm.xa + (2 * ks) * kChunkBytes, kChunkBytes, 128);
-    const uint64_t bl = sdesc(sm.xa + (kChunks + 2 * ks) * kChunkBytes, kChunkBytes, 128);
+    const uint64_t ah = a0 + ((2 * ks * kThChunk) >> 4), al = a0 + (((kChunks + 2 * ks) * kThChunk) >> 4);
+    const uint64_t bh = b0 + ((2 * ks * kChunkBytes) >> 4), bl = b0 + (((kChunks + 2 * ks) * kChunkBytes) >> 4);
     mma_ss(d, ah, bh, kId, ks > 0);
     mma_ss(d, ah, bl, kId, true);
     mma_ss(d, al, bh, kId, true);
@@ -190,20 +200,36 @@ __device__ __forceinline__ void issue_eta(Smem32& sm, uint32_t g) {
   mma_commit(&sm.eta_bar[g & 1]);
 }
 
-// G^T += R_hi^T(g) . [X_hi | X_lo] + R_lo^T . [X_hi | X_lo(0..7)]: 16 k-steps of 8 rows.
+// G^T += R_hi^T(g) . [X_hi | X_lo] + R_lo^T . [X_hi | X_lo(0..7)]: 16 k-steps of 8 rows
+// (measured 56 + 44 cycles per k-step: tools/probes/tf32_rate_probe.cu).
 __device__ __forceinline__ void issue_g(Smem32& sm, uint32_t g, bool fresh) {
   constexpr uint32_t kIdHi = idesc_tf32(128, kGN);
   constexpr uint32_t kIdLo = idesc_tf32(128, 64);
   const uint32_t d = sm.tmem_base + kColG;
   const uint32_t rh = sm.tmem_base + kColE0 + (g & 1u) * 128u, rl = sm.tmem_base + kColRL;
-#pragma unroll 1
+  const uint64_t b0 = sdesc(sm.xb, kGChunk, 128);
+#pragma unroll
   for (int ks = 0; ks < kRows / 8; ++ks) {
-    const uint64_t b = sdesc(sm.xb + (2 * ks) * kGChunk, kGChunk, 128);
+    const uint64_t b = b0 + ((2 * ks * kGChunk) >> 4);
     mma_ts(d, rh + 8 * ks, b, kIdHi, !(fresh && ks == 0));
     mma_ts(d, rl + 8 * ks, b, kIdLo, true);
   }
   mma_commit(&sm.g_bar);
 }
+
+#ifdef PCVG_GLM32_TRACE
+// Timeline probe (tools only): clock64 stamps of CTA 0 for pass 6, printed at its end.
+__device__ long long g_trace[64][10];
+__device__ int g_pass;
+#define TRACE(t, i)                                                         \
+  do {                                                                      \
+    if (blockIdx.x == 0 && g_pass == 6 && (t) < 64) g_trace[(t)][(i)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(t, i) \
+  do {              \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------ one gradient pass
 // Accumulates G (FP64, [stacked column][chain] in gsc) over all tiles for the CTA's 128 chains
@@ -232,20 +258,25 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
     for (int t = 0; t < ntiles; ++t) {
       const uint32_t g = g0 + t;
       mbar_wait(&sm.rdy, g & 1u);  // R^T(g) is in tensor memory
+      TRACE(t, 0);
       mbar_wait(&sm.full_b, g & 1u);
       tmem_fence_after();
       issue_g(sm, g, t % kFlush == 0);
+      TRACE(t, 1);
       if (t + 2 < ntiles || (t + 2 == ntiles && more)) {
         mbar_wait(&sm.eta_bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);  // eta(g+1) read the buffer
+        TRACE(t, 2);
         load_eta_image(sm, M, P.ia++, ntiles);  // y/key slot g & 1: epilogue(g) is done
         if (t + 2 < ntiles) {
           mbar_wait(&sm.full_a, (g + 2) & 1u);
+          TRACE(t, 3);
           tmem_fence_after();
           issue_eta(sm, g + 2);
         }
       }
       if (t + 1 < ntiles || more) {
         mbar_wait(&sm.g_bar, g & 1u);  // G(g) read the G image buffer
+        TRACE(t, 4);
         load_g_image(sm, M, P.ib++, ntiles);
       }
     }
@@ -278,8 +309,10 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
     };
     for (int t = 0; t < ntiles; ++t) {
       const uint32_t g = g0 + t;
+      if (tid == 0) TRACE(t, 5);
       mbar_wait(&sm.eta_bar[g & 1u], (g >> 1) & 1u);
       mbar_wait(&sm.full_y[g & 1u], (g >> 1) & 1u);
+      if (tid == 0) TRACE(t, 6);
       tmem_fence_after();
       const uint32_t ebuf = sm.tmem_base + lane + kColE0 + (g & 1u) * 128u + 32 * rb;
       const float4* yv4 = reinterpret_cast<const float4*>(sm.yk[g & 1u]) + 8 * rb;
@@ -300,15 +333,17 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * j4 + u;
             const float eta = __uint_as_float(e[j]);
-            const bool real = ks[u] >= 0;
-            const bool train = real && static_cast<unsigned>(ks[u] - clo) >= span;
-            const float sig = __fdividef(1.0f, 1.0f + __expf(-eta));
+            // padding rows (key -1) pass the fold test, but their G-image rows are zero
+            const bool train = static_cast<unsigned>(ks[u] - clo) >= span;
+            const float sig = sigmoid_fast(eta);
             const float r = train ? ys[u] - sig : 0.0f;
-            const float rh = tf32_hi(r);
-            e[j] = __float_as_uint(rh);
-            rlo[16 * h + j] = __float_as_uint(r - rh);
+            // hi = r truncated to TF32 (exact), lo = r - hi (exact in FP32)
+            const uint32_t rh = __float_as_uint(r) & 0xFFFFE000u;
+            e[j] = rh;
+            rlo[16 * h + j] = __float_as_uint(r - __uint_as_float(rh));
             if (VALUE) {
-              if (train) ll += ys[u] * eta - (fmaxf(eta, 0.0f) + log1pf(__expf(-fabsf(eta))));
+              const bool real = ks[u] >= 0;
+              if (real && train) ll += ys[u] * eta - (fmaxf(eta, 0.0f) + log1pf(__expf(-fabsf(eta))));
               else if (real && !isfinite(eta)) ll += CUDART_NAN_F;  // 0 * non-finite test term
             }
           }
@@ -316,8 +351,10 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
         tmem_st16(ebuf + 16 * h, e);  // R_hi^T in place of eta^T
       }
       if (VALUE) llacc += static_cast<double>(ll);
+      if (tid == 0) TRACE(t, 7);
       if (t > 0) {  // G(g-1) has consumed R_lo(g-1); flush it if it closed a group
         mbar_wait(&sm.g_bar, (g - 1) & 1u);
+        if (tid == 0) TRACE(t, 8);
         if (t % kFlush == 0) flush();
       }
       {
@@ -334,6 +371,7 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       tmem_fence_before();
       mbar_arrive(&sm.rdy);
+      if (tid == 0) TRACE(t, 9);
     }
     mbar_wait(&sm.g_bar, (g0 + ntiles - 1) & 1u);
     flush();
@@ -342,6 +380,19 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
   tmem_fence_before();
   __syncthreads();  // G scratch / llq complete; every buffer of the pass is released
   P.g += ntiles;
+#ifdef PCVG_GLM32_TRACE
+  if (blockIdx.x == 0 && tid == 0) {
+    if (g_pass == 6) {
+      const long long b = g_trace[0][5];
+      printf("tile: ctl rdy Gissued eta(g+1)done X(g+2)landed G(g)done | epi start etaready compdone G(g-1)done arrive\n");
+      for (int t = 0; t < 40 && t < ntiles; ++t)
+        printf("%2d: %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld\n", t, g_trace[t][0] - b, g_trace[t][1] - b,
+               g_trace[t][2] - b, g_trace[t][3] - b, g_trace[t][4] - b, g_trace[t][5] - b, g_trace[t][6] - b,
+               g_trace[t][7] - b, g_trace[t][8] - b, g_trace[t][9] - b);
+    }
+    ++g_pass;
+  }
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDev S, RunArgs A, double* gscratch) {
