@@ -215,14 +215,23 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
                            int32_t* slot);
 pcvg_status pcvg_model_dim(const pcvg_ctx* ctx, int32_t slot, int32_t* dim);
 
-/* Kernel selection. AUTO picks the FP64 tensor-core GLM kernel for predictors without group
- * effects when enough chains (or a row-split cluster) fill the GPU, else the generic lane-split
- * kernel; GENERIC / TENSOR force one (tests run both). Logistic always uses the tensor kernel,
- * hierarchical families (J > 1) always the generic one. */
-enum { PCVG_KERNEL_AUTO = 0, PCVG_KERNEL_GENERIC = 1, PCVG_KERNEL_TENSOR = 2, PCVG_KERNEL_TF32 = 3 };
+/* Kernel selection. AUTO runs the Gaussian linear families (grouped, radon-style, seasonal AR) on
+ * fold sufficient statistics (SUFFSTAT below) when their data are finite. Otherwise, and always
+ * under ROWS, the kernels stream the design matrix: the FP64 tensor-core GLM kernel for predictors
+ * without group effects when enough chains (or a row-split cluster) fill the GPU, the
+ * group-batched kernel for hierarchical models, else the generic lane-split kernel. GENERIC /
+ * TENSOR force one of the row kernels (tests run every kernel). Logistic always uses the tensor
+ * kernel. */
+enum { PCVG_KERNEL_AUTO = 0, PCVG_KERNEL_GENERIC = 1, PCVG_KERNEL_TENSOR = 2, PCVG_KERNEL_TF32 = 3,
+       PCVG_KERNEL_SUFFSTAT = 4, PCVG_KERNEL_ROWS = 5 };
 /* PCVG_KERNEL_TF32: the FP32 variant of the logistic family: both contractions on
  * tcgen05 kind::tf32 with hi/lo-split operands (FP32-class accuracy, per-step values within 1e-5
  * of the FP64 path); chain state, energies and accumulators stay FP64. Other families ignore it. */
+/* PCVG_KERNEL_SUFFSTAT: the Gaussian linear families (grouped, radon-style, seasonal AR) on fold
+ * sufficient statistics: the masked sums of every gradient pass come from each fold's training
+ * Gram matrix and group sums (built once on the host in double-double), O(d^2 + J d) per pass
+ * instead of O(n d); same values to rounding. Needs finite data; other families
+ * and non-finite datasets fall back to the ROWS choice. */
 pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy);
 pcvg_status pcvg_model_test_size(const pcvg_ctx* ctx, int32_t slot, int32_t fold, int64_t* n);
 

@@ -21,12 +21,14 @@
 #include "../../include/pcvg.h"
 #include "host_common.hpp"
 #include "score_extra.cuh"
+#include "suffstats.hpp"
 #include "types.cuh"
 
 namespace pcvg {
 
 // kernels (gauss_kernel.cu, glm_kernel.cu, chain_kernels.cu)
 int gauss_lanes_per_chain(const ModelDev& M, int nch);
+int suff_lanes_per_chain(const ModelDev& M, int nch);
 cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st);
 int glm_width(int family, int J, int nc);
 int glm_cluster_size(int n, int kp, int nch);
@@ -123,6 +125,8 @@ struct HostModel {
   DevBuf<double> yb, xb;         // group-batched layout (ModelDev::nb > 0)
   DevBuf<unsigned char> x32;     // logistic FP32 variant tile images
   DevBuf<int> keyb, bgroup, boff, tfirst, tr0, trows, bkey, bgrows, buni;
+  DevBuf<double> sA, sgn, sgs, sov_n, sov_s;  // fold sufficient statistics (suffstats.cpp)
+  DevBuf<int> sov_ptr, sov_g, sex_lo, sex_hi, sex_rows, sex_grp;
   int64_t bank_rows = 0;
   ModelDev md{};
 };
@@ -498,6 +502,26 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   m.hi.upload(hi);
   m.ntrain.upload(ntr);
 
+  // fold sufficient statistics for the Gaussian linear families (suffstats.cpp)
+  int suff = 0;
+  SuffStats ss;
+  if ((s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON || s->family == PCVG_FAMILY_SEASONAL_AR) &&
+      build_suffstats(n, m.nc, m.J, y.data(), xc.data(), key.data(), hier ? grp_ptr.data() : nullptr, m.K,
+                      lo.data(), hi.data(), ss)) {
+    suff = 1;
+    m.sA.upload(ss.A);
+    m.sgn.upload(ss.gn);
+    m.sgs.upload(ss.gs);
+    m.sov_ptr.upload(ss.ov_ptr);
+    m.sov_g.upload(ss.ov_g);
+    m.sov_n.upload(ss.ov_n);
+    m.sov_s.upload(ss.ov_s);
+    m.sex_lo.upload(ss.ex_lo);
+    m.sex_hi.upload(ss.ex_hi);
+    m.sex_rows.upload(ss.ex_rows);
+    m.sex_grp.upload(ss.ex_grp);
+  }
+
   // test segments (fold_meta_, grouped_regression.cpp:27-47): test rows grouped by group in
   // increasing group order, rows increasing within a group; unseen = no training row in group.
   const int Jg = hier ? m.J : 1;
@@ -634,6 +658,20 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.buniform = m.buni.p;
   md.ring = ring;
   md.x32 = m.x32.p;
+  md.suff = suff;
+  md.sd = ss.d;
+  md.sdp = ss.dp;
+  md.sA = m.sA.p;
+  md.sgn = m.sgn.p;
+  md.sgs = m.sgs.p;
+  md.sov_ptr = m.sov_ptr.p;
+  md.sov_g = m.sov_g.p;
+  md.sov_n = m.sov_n.p;
+  md.sov_s = m.sov_s.p;
+  md.sex_lo = m.sex_lo.p;
+  md.sex_hi = m.sex_hi.p;
+  md.sex_rows = m.sex_rows.p;
+  md.sex_grp = m.sex_grp.p;
   return hm;
 }
 
@@ -657,6 +695,8 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
   cudaError_t e;
   if (ctx->policy == PCVG_KERNEL_TF32 && md.family == kLogistic && md.x32) {
     e = launch_glm32(md, S, A, st);  // FP32 variant: tcgen05 kind::tf32, split operands
+  } else if ((ctx->policy == PCVG_KERNEL_SUFFSTAT || ctx->policy == PCVG_KERNEL_AUTO) && md.suff) {
+    e = launch_gauss(md, S, A, -suff_lanes_per_chain(md, S.nch), st);  // fold sufficient statistics
   } else if (use_glm(ctx, m, S.nch)) {
     e = launch_glm(md, S, A, st);
   } else if (md.nb > 0 && (ctx->policy != PCVG_KERNEL_GENERIC || md.family >= kRatB)) {
@@ -940,7 +980,7 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
 }
 
 pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy) {
-  if (!ctx || policy < PCVG_KERNEL_AUTO || policy > PCVG_KERNEL_TF32) return PCVG_INVALID_INPUT;
+  if (!ctx || policy < PCVG_KERNEL_AUTO || policy > PCVG_KERNEL_ROWS) return PCVG_INVALID_INPUT;
   ctx->policy = policy;
   return PCVG_OK;
 }

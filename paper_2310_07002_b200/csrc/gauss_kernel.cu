@@ -16,6 +16,8 @@
 // (accum.cpp:164-182). Chains are independent; a CTA holds 128/T chains.
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "score_extra.cuh"
 #include "tc_common.cuh"
@@ -395,6 +397,189 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
   global_grad<FAM, NCM, NGM>(M, P, qG, sxr, sr_tot, srr, G, n_train, gG, VALUE, lp);
   if (VALUE && poison) lp = CUDART_NAN;
   __syncwarp(mask);  // group-dim stores of lane 0 become visible to the chain's lanes
+}
+
+// grad_pass on the fold's sufficient statistics (suffstats.cpp; NB < 0): the same masked sums
+// S_r[g], S_xr, S_rr as the row loop, from the packed training Gram A_k and the group sums s_g, in
+// O(d^2 + J d) instead of O(n d) per pass. u = (y, x), om = (1, -w):
+//   S_r[g] = om.s_g - n_g off_g;  S_xr = (A om)[1..] - sum_g off_g s_g[1..];
+//   S_rr = om^T A om - sum_g off_g (om.s_g + S_r[g]).
+// T lanes per chain split the Gram entries and the groups (lane t owns groups t, t + T, ...) and
+// butterfly-reduce the partial sums, so every lane ends with identical bits. With `qs` (T = 32,
+// hierarchical), a lane keeps its groups' position / momentum in shared-memory slots across the
+// passes of a transition (slot j of group t + 32 j at qs[j * kBlock]); the planes are written in
+// the last pass only. The value pass also evaluates the fold's excluded rows for the reference's
+// poisoning of a non-finite masked term (grouped_regression.cpp:74-76).
+template <int FAM, int T, int NCM, int NGM, bool VALUE>
+__device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S, int c, int t, unsigned mask,
+                                          int fold, int n_train, const double* qG, int kind, bool last,
+                                          double scale, int cur, NormalCursor& nc, ChainRng& R,
+                                          const double* probe_p, double* gG, double& lp, double& k0g,
+                                          double& k1g, bool& bad, double* qs, double* ps) {
+  constexpr int D = NCM + 1;
+  Prep<NCM> P;
+  prepare<FAM, NCM, NGM>(M, qG, P);
+  const int nch = S.nch;
+  const int d = M.nc + 1;
+  const double eps = M.step, half = 0.5 * M.step;
+  const size_t plane = static_cast<size_t>(M.dim) * nch;
+  double om[D];
+  om[0] = 1.0;
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) om[1 + k] = -P.w[k];  // w = 0 past nc
+  // this lane's share of q = A om over the packed lower triangle (row i at i (i + 1) / 2)
+  const double* A = M.sA + static_cast<size_t>(fold) * M.sdp;
+  double q[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) q[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    if (i < d) {
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        const int e = i * (i + 1) / 2 + j;
+        if (T == 1 || e % T == t) {
+          const double a = __ldg(A + e);
+          q[i] = fma(a, om[j], q[i]);
+          if (j < i) q[j] = fma(a, om[i], q[j]);
+        }
+      }
+    }
+  }
+  double sv[D];  // this lane's sum_g off_g s_g
+#pragma unroll
+  for (int i = 0; i < D; ++i) sv[i] = 0.0;
+  double t2 = 0.0, sr_tot = 0.0, dk0 = 0.0, dk1 = 0.0;
+  GroupAcc G{0.0, 0.0, 0.0, 0.0};
+  const int ov0 = __ldg(M.sov_ptr + fold), ov_end = __ldg(M.sov_ptr + fold + 1);
+  int ov = ov0;
+  const int ngroups = M.J > 0 ? M.J : 1;
+  for (int g = t, jj = 0; g < ngroups; g += T, ++jj) {
+    double qg = 0.0, pg = 0.0;
+    const size_t gi = static_cast<size_t>(g) * nch + c;
+    if constexpr (FAM != kSeasonal) {
+      const double mg = __ldg(M.inv_mass + g);
+      if (kind == 0) {
+        qg = S.pos[cur * plane + gi];
+      } else if (kind == 1) {
+        const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + g] : nc.at(R, g) / sqrt(mg);
+        dk0 += mg * p0 * p0;
+        pg = p0 + half * S.grad[cur * plane + gi];
+        qg = S.pos[cur * plane + gi] + eps * mg * pg;
+      } else if (qs) {
+        pg = ps[jj * kBlock];
+        qg = qs[jj * kBlock] + eps * mg * pg;
+      } else {
+        pg = S.wp[gi];
+        qg = S.pos[(cur ^ 1) * plane + gi] + eps * mg * pg;
+      }
+      bad |= !isfinite(qg);
+    }
+    const double off = group_offset<FAM, NCM>(P, qg);
+    // this fold's statistics of group g: an override when the fold holds out some of its rows
+    while (ov < ov_end && __ldg(M.sov_g + ov) < g) ++ov;
+    double ng;
+    const double* sp;
+    if (ov < ov_end && __ldg(M.sov_g + ov) == g) {
+      ng = __ldg(M.sov_n + ov);
+      sp = M.sov_s + static_cast<size_t>(ov) * d;
+    } else {
+      ng = __ldg(M.sgn + g);
+      sp = M.sgs + static_cast<size_t>(g) * d;
+    }
+    double ws = 0.0;
+    double sg[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      sg[i] = i < d ? __ldg(sp + i) : 0.0;
+      ws = fma(om[i], sg[i], ws);
+    }
+    const double srg = fma(-ng, off, ws);
+#pragma unroll
+    for (int i = 1; i < D; ++i) sv[i] = fma(off, sg[i], sv[i]);
+    t2 = fma(off, ws + srg, t2);
+    if constexpr (FAM != kSeasonal) {
+      const double gg = group_grad<FAM, NCM, NGM>(P, qG, M, qg, srg, G);
+      bad |= !isfinite(gg);
+      if (kind == 0) {
+        S.grad[cur * plane + gi] = gg;
+      } else {
+        pg += scale * gg;
+        bad |= !isfinite(pg);
+        if (qs && !last) {
+          qs[jj * kBlock] = qg;
+          ps[jj * kBlock] = pg;
+        } else {
+          S.pos[(cur ^ 1) * plane + gi] = qg;
+          S.wp[gi] = pg;
+        }
+        if (last) {
+          S.grad[(cur ^ 1) * plane + gi] = gg;
+          dk1 += __ldg(M.inv_mass + g) * pg * pg;
+        }
+      }
+    } else {
+      sr_tot += srg;
+    }
+  }
+  // lane partials -> identical totals on every lane (xor butterfly)
+  double quad = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) quad = fma(om[i], q[i], quad);
+  double srr = quad - t2;
+  double sxr[NCM];
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) sxr[k] = q[1 + k] - sv[1 + k];
+  if constexpr (T > 1) {
+#pragma unroll
+    for (int k = 0; k < NCM; ++k)
+      if (k < M.nc) sxr[k] = lane_sum<T>(sxr[k], mask);
+    srr = lane_sum<T>(srr, mask);
+    if constexpr (FAM == kSeasonal) {
+      sr_tot = lane_sum<T>(sr_tot, mask);
+    } else {
+      G.a0 = lane_sum<T>(G.a0, mask);
+      G.a1 = lane_sum<T>(G.a1, mask);
+      if constexpr (FAM == kRadon) G.a2 = lane_sum<T>(G.a2, mask);
+      if (kind == 1) dk0 = lane_sum<T>(dk0, mask);
+      if (last) dk1 = lane_sum<T>(dk1, mask);
+    }
+  }
+  k0g += dk0;
+  k1g += dk1;
+  bool poison = false;
+  if (VALUE && fold < M.K) {
+    if constexpr (T > 1) __syncwarp(mask);  // group positions stored by their owning lanes
+    const int t0 = __ldg(M.sex_lo + fold), t1 = __ldg(M.sex_hi + fold);
+    for (int tt = t0 + t; tt < t1; tt += T) {
+      const int i = __ldg(M.sex_rows + tt);
+      double off = P.off0;
+      if constexpr (FAM != kSeasonal) {
+        const size_t gi = static_cast<size_t>(__ldg(M.sex_grp + tt)) * nch + c;
+        off = group_offset<FAM, NCM>(P, S.pos[(kind == 0 ? cur : cur ^ 1) * plane + gi]);
+      }
+      double m = off;
+#pragma unroll
+      for (int k = 0; k < NCM; ++k)
+        if (k < M.nc) m = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), m);
+      const double r = __ldg(M.y + i) - m;
+      poison |= !isfinite(P.logv + r * r * P.inv_v);
+    }
+    if constexpr (T > 1) poison = __ballot_sync(mask, poison) != 0;
+  }
+  bad = T > 1 ? __any_sync(mask, bad) : bad;
+  global_grad<FAM, NCM, NGM>(M, P, qG, sxr, sr_tot, srr, G, n_train, gG, VALUE, lp);
+  if (VALUE && poison) lp = CUDART_NAN;
+  if constexpr (T > 1) __syncwarp(mask);
+}
+
+// Shared-memory group slots of the sufficient-statistics kernel (position + momentum per owned
+// group, [slot][kBlock] doubles each): warp-per-chain launches of hierarchical models whose slots
+// fit; 0 = the group state goes through the HBM planes.
+__host__ __device__ inline int suff_slots(const ModelDev& M, int T) {
+  if (T != 32 || M.J < 2) return 0;
+  const int ns = (M.J + 31) / 32;
+  return 2 * ns * kBlock * 8 <= 96 * 1024 ? ns : 0;
 }
 
 // Row-tile ring of the group-batched kernel: the CTA's warps (one chain each) share one staged copy
@@ -919,6 +1104,17 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
   // group slots of each thread (NB > 0): [nb][kBlock] position / momentum after the ring
   double* qb = rg.qslots + threadIdx.x;
   double* pb = rg.qslots + static_cast<size_t>(M.nb) * kBlock + threadIdx.x;
+  // group slots of each thread (NB < 0, suff_slots): [ns][kBlock] position, then momentum
+  double* sq = nullptr;
+  double* sp = nullptr;
+  if constexpr (NB < 0) {
+    extern __shared__ __align__(16) double suff_raw[];
+    const int ns = suff_slots(M, T);
+    if (ns > 0) {
+      sq = suff_raw + threadIdx.x;
+      sp = suff_raw + static_cast<size_t>(ns) * kBlock + threadIdx.x;
+    }
+  }
 
   if (A.mode == kModeEval || A.mode == kModePred) {
     if (A.mode == kModeEval) {
@@ -927,6 +1123,9 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
       if constexpr (NB > 0)
         hgrad_pass<FAM, kNB, NCM, NGM, true, NCX>(M, S, c, t, lo, hi, n_train, qG, 0, false, 0.0, cur, nc,
                                              R, nullptr, gG, lp, k0, k1, bad, qb, pb, rg);
+      else if constexpr (NB < 0)
+        suff_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, fold, n_train, qG, 0, false, 0.0, cur, nc, R,
+                                          nullptr, gG, lp, k0, k1, bad, nullptr, nullptr);
       else
         grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, 0, false, 0.0,
                                           cur, nc, R, nullptr, gG, lp, k0, k1, bad);
@@ -986,6 +1185,13 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
         else
           hgrad_pass<FAM, kNB, NCM, NGM, false, NCX>(M, S, c, t, lo, hi, n_train, qG, first ? 1 : 2, false,
                                                 scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, qb, pb, rg);
+      } else if constexpr (NB < 0) {
+        if (last)
+          suff_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, fold, n_train, qG, first ? 1 : 2, true, scale,
+                                            cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, sq, sp);
+        else
+          suff_pass<FAM, T, NCM, NGM, false>(M, S, c, t, mask, fold, n_train, qG, first ? 1 : 2, false, scale,
+                                             cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad, sq, sp);
       } else if (last) {
         grad_pass<FAM, T, NCM, NGM, true>(M, S, c, t, mask, lo, hi, n_train, qG, first ? 1 : 2,
                                           true, scale, cur, nc, R, probe_p, gG, lp1, k0g, k1g, bad);
@@ -1042,7 +1248,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : 1) gauss_kernel(ModelDev 
 #pragma unroll
           for (int i = 0; i < NGM; ++i)
             if (i < ng) A.traj[static_cast<size_t>(c) * M.dim + M.goff + gidx<FAM>(M, i)] = pG[i];
-          if constexpr (NB == 0)
+          if constexpr (NB <= 0)
             for (int g = 0; g < J; ++g) A.traj[static_cast<size_t>(c) * M.dim + g] = S.wp[static_cast<size_t>(g) * nch + c];
         }
       }
@@ -1123,7 +1329,50 @@ cudaError_t launch_batched(const ModelDev& M, const ChainsDev& S, const RunArgs&
   return launch_nb<FAM, NCM, NGM, 1>(M, S, A, st, grid);
 }
 
+template <int FAM, int NCM, int NGM, int T>
+cudaError_t launch_suff_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
+  const int grid = (S.nch + kBlock / T - 1) / (kBlock / T);
+  if (grid == 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(suff_slots(M, T)) * 2 * kBlock * sizeof(double);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, T, NCM, NGM, -1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  gauss_kernel<FAM, T, NCM, NGM, -1><<<grid, kBlock, smem, st>>>(M, S, A);
+  return cudaGetLastError();
+}
+
+template <int FAM, int NCM, int NGM>
+cudaError_t launch_suff(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st) {
+  switch (T) {
+    case 1: return launch_suff_t<FAM, NCM, NGM, 1>(M, S, A, st);
+    case 4: return launch_suff_t<FAM, NCM, NGM, 4>(M, S, A, st);
+    case 8: return launch_suff_t<FAM, NCM, NGM, 8>(M, S, A, st);
+    case 32: return launch_suff_t<FAM, NCM, NGM, 32>(M, S, A, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace
+
+// Lanes per chain of the sufficient-statistics kernel: enough threads to fill the GPU, at most
+// what the Gram entries / groups can use.
+int suff_lanes_per_chain(const ModelDev& M, int nch) {
+  if (const char* env = std::getenv("PCVG_SUFF_LANES")) return std::atoi(env);  // tuning only
+  // Split lanes only pay for many groups: the per-pass partial sums cost (nc + 5) butterfly
+  // reductions, more than a lane saves on a d(d+1)/2 Gram product (measured: cfg1 / cfg4 are
+  // fastest at one lane, cfg3's 400 groups at 32, profiles/r01_suff_lanes.txt).
+  if (M.J < 64) return 1;
+  const long target_threads = 148L * 512;
+  int T = 1;
+  while (T < 32 && static_cast<long>(nch) * T < target_threads) T *= 2;
+  if (T == 2) T = 4;
+  if (T == 16) T = 32;
+  return T;
+}
 
 // Lanes per chain: enough threads to fill the GPU (>= ~64 resident warps worth of work per SM
 // is not reachable with few chains, so few chains get whole warps), capped by the rows a lane
@@ -1149,6 +1398,21 @@ cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A
     if (M.family == kRatB) return launch_batched<kRatB, 1, 4>(M, S, A, st);
     if (M.family == kRatA) return launch_batched<kRatA, 1, 5>(M, S, A, st);
     return cudaErrorInvalidValue;
+  }
+  if (T < 0) {  // fold sufficient statistics, -T lanes per chain
+    if (!M.suff) return cudaErrorInvalidValue;
+    switch (M.family) {
+      case kGrouped:
+        if (M.nc > 8) return cudaErrorInvalidValue;
+        return launch_suff<kGrouped, 8, 11>(M, S, A, -T, st);
+      case kRadon:
+        return launch_suff<kRadon, 1, 4>(M, S, A, -T, st);
+      case kSeasonal:
+        if (M.nc > 13) return cudaErrorInvalidValue;
+        return launch_suff<kSeasonal, 13, 15>(M, S, A, -T, st);
+      default:
+        return cudaErrorInvalidValue;
+    }
   }
   switch (M.family) {
     case kGrouped:

@@ -82,6 +82,23 @@ struct ModelDev {
   const int* buniform;    // [nb] 1 if every group of the batch has the batch's row count
   int ring;               // 1: row tiles staged through a shared-memory TMA ring; 0: read via L1
   const unsigned char* x32;  // logistic FP32 variant: TF32-split tile images (glm32_kernel.cu)
+  // fold sufficient statistics of the Gaussian families (suffstats.cpp, gauss_kernel NB < 0):
+  // u = (y, x_0..x_{nc-1}); sA[k] = packed lower sum of u u^T over fold k's training rows;
+  // sgn / sgs full-data group counts / sums of u; fold k overrides groups sov_g[sov_ptr[k] ..
+  // sov_ptr[k+1]) with (sov_n, sov_s); its excluded rows are sex_rows[sex_lo[k] .. sex_hi[k]).
+  int suff;  // 1 if the statistics exist
+  int sd, sdp;
+  const double* sA;
+  const double* sgn;
+  const double* sgs;
+  const int* sov_ptr;
+  const int* sov_g;
+  const double* sov_n;
+  const double* sov_s;
+  const int* sex_lo;
+  const int* sex_hi;
+  const int* sex_rows;
+  const int* sex_grp;
 };
 
 constexpr int kMaxBatches = 16;

@@ -402,7 +402,7 @@ class Context:
         self._keep.append((kern, bank))
         return slot.value
 
-    KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TENSOR, KERNEL_TF32 = 0, 1, 2, 3
+    KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TENSOR, KERNEL_TF32, KERNEL_SUFFSTAT, KERNEL_ROWS = 0, 1, 2, 3, 4, 5
 
     def set_kernel_policy(self, policy):
         self._chk(self.lib.pcvg_set_kernel_policy(self.h, policy))

@@ -22,10 +22,16 @@ BASES = ["cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timebloc
 
 
 @pytest.mark.parametrize("name", BASES)
-def test_short_adaptation_follows_reference(name):
+@pytest.mark.parametrize("policy", ["rows", "auto"])
+def test_short_adaptation_follows_reference(name, policy):
     case = Case(name)
     cfg = pcv.AdaptConfig(chains=4, warmup=30, draws=10, n_leapfrog=32)
+    # the row kernels sum in an order close to the reference's; the sufficient-statistics kernel
+    # (AUTO for the Gaussian families) differs by ~1e-12 from the first transitions on
+    first_tol = 1e-12 if policy == "rows" else 1e-11
     with pcv.Context(0) as ctx:
+        if policy == "rows":
+            ctx.set_kernel_policy(ctx.KERNEL_ROWS)
         for m, model in enumerate(case.models):
             fit = ctx.adapt_full_data(model, cfg, seed=3, model_id=m, trace=True)
             if m == 0:  # the per-iteration dual-averaging step sizes of the reference loop
@@ -36,7 +42,7 @@ def test_short_adaptation_follows_reference(name):
                 # chains' last-ulp differences (FMA contraction, CUDA libm) grow through the
                 # dual-averaging feedback; measured on B200: 0 for 5 iterations, ~1e-13 at 6-7,
                 # ~1e-9 at 8-9, then chaotic growth (percent level by iteration ~18).
-                assert rel[:5].max() <= 1e-12 and rel[:8].max() <= 1e-8, rel
+                assert rel[:5].max() <= first_tol and rel[:8].max() <= 1e-8, rel
             assert np.all(np.isfinite(fit.draws)) and fit.kparams.step_size > 0
 
 

@@ -30,9 +30,12 @@ def scale(th):
     return 1e4 * (1.0 + np.abs(th).max())
 
 
+@pytest.mark.parametrize("policy", [pcv.Context.KERNEL_ROWS, pcv.Context.KERNEL_SUFFSTAT])
 @pytest.mark.parametrize("scheme", ["logo", "kfold", "loo"])
 @pytest.mark.parametrize("family", [abi.FAMILY_GROUPED, abi.FAMILY_RADON, abi.FAMILY_RAT_GROWTH])
-def test_ragged_groups_and_row_keys(scheme, family):
+def test_ragged_groups_and_row_keys(scheme, family, policy):
+    if family == abi.FAMILY_RAT_GROWTH and policy == pcv.Context.KERNEL_SUFFSTAT:
+        pytest.skip("the growth model has no sufficient-statistics path")
     d = ragged_grouped()
     if family == abi.FAMILY_RADON:
         d = pcv.Dataset(d.y, (d.x[:, :1] > 0).astype(float), d.group_id)
@@ -48,6 +51,7 @@ def test_ragged_groups_and_row_keys(scheme, family):
     dim = model.dim()
     kp = pcv.KernelParams(0.01, 8, np.ones(dim))
     with pcv.Context(0) as ctx:
+        ctx.set_kernel_policy(policy)
         slot = ctx.add_model(model, kp, thetas(model, 2, 1))
         folds = sorted({0, 1, f.K // 2, f.K - 1, f.K})
         for fold in folds:
@@ -64,7 +68,8 @@ def test_ragged_groups_and_row_keys(scheme, family):
                 assert abs(pr[i] - ref) <= 1e-10 * (1.0 + abs(ref)), (fold, pr[i], ref)
 
 
-def test_poisoned_test_row():
+@pytest.mark.parametrize("policy", [pcv.Context.KERNEL_ROWS, pcv.Context.KERNEL_SUFFSTAT])
+def test_poisoned_test_row(policy):
     """A non-finite y in a test row: the reference's log_joint multiplies the test term by 0,
     which is NaN (grouped_regression.cpp:74-76); training folds stay finite."""
     d = ragged_grouped(seed=5, J=20)
@@ -76,6 +81,7 @@ def test_poisoned_test_row():
     model = pcv.GroupedRegressionModel("M", d, f)
     om = O.OModel(d, f.arrays(), model.spec)
     with pcv.Context(0) as ctx:
+        ctx.set_kernel_policy(policy)  # SUFFSTAT: non-finite data keeps the row kernels
         slot = ctx.add_model(model, pcv.KernelParams(0.01, 8, np.ones(model.dim())), thetas(model, 1, 1))
         th = thetas(model, 1, 4)
         for fold in (3, 4):

@@ -22,26 +22,30 @@ def ctx():
 
 
 _cases = {}
-# fixtures whose models have two device kernels: the tensor-core GLM kernel or the group-batched
-# hierarchical kernel (policy AUTO / TENSOR), and the generic row-split kernel (GENERIC)
+# fixtures whose models have two row-streaming kernels: the tensor-core GLM kernel or the
+# group-batched hierarchical kernel (policy ROWS / TENSOR), and the generic row-split kernel (GENERIC)
 BOTH_KERNELS = {"cfg1_linreg_loo": "tensor", "seasonal_timeblocks": "tensor", "seasonal_hvblock": "tensor",
                 "ex1_grouped_logo": "batched", "radon_logo": "batched"}
 
 
 def case_in(ctx, name):
     """(Case, slots) with the case's models registered in a fresh context. A name suffixed with
-    ':tensor' / ':batched' / ':generic' forces that kernel."""
+    ':tensor' / ':batched' / ':generic' / ':suffstat' forces that kernel."""
     name, _, kernel = name.partition(":")
     if name not in _cases:
         _cases[name] = Case(name)
     case = _cases[name]
     c = pcv.Context(0)
     if kernel:
-        c.set_kernel_policy({"tensor": c.KERNEL_TENSOR, "batched": c.KERNEL_AUTO,
-                             "generic": c.KERNEL_GENERIC}[kernel])
+        c.set_kernel_policy({"tensor": c.KERNEL_TENSOR, "batched": c.KERNEL_ROWS,
+                             "generic": c.KERNEL_GENERIC, "suffstat": c.KERNEL_SUFFSTAT}[kernel])
     slots = [c.add_model(m, kp, bank, model_id=i)
              for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
     return case, c, slots
+
+
+# Gaussian linear fixtures that also run on fold sufficient statistics (policy SUFFSTAT)
+SUFF_KERNEL = {"cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock"}
 
 
 def with_kernels(names):
@@ -51,6 +55,8 @@ def with_kernels(names):
             out += [n + ":" + BOTH_KERNELS[n], n + ":generic"]
         else:
             out.append(n)
+        if n in SUFF_KERNEL:
+            out.append(n + ":suffstat")
     return out
 
 

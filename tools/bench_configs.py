@@ -95,7 +95,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--policy", type=int, default=0, help="0 auto, 1 generic kernel, 2 tensor-core kernel")
+    ap.add_argument("--policy", type=int, default=0, help="0 auto, 1 generic kernel, 2 tensor-core kernel, 4 fold sufficient statistics, 5 row-streaming kernels")
     args = ap.parse_args()
     from parity_util import Case
     peak = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
