@@ -325,6 +325,13 @@ typedef struct {
 } pcvg_fit;                /* FullDataFit, adapt.hpp:56-62 */
 
 /* Model::initial_draw (model.hpp:44) on CounterRng(seed, stream): host, bit-exact. */
+/* Host-only probe of the sufficient-statistics kernel's fold statistics: for rows
+ * with y[n], x[nc][n] (column-major) and fold keys key[n], fold k (0..K-1) holding out rows with
+ * lo[k] <= key < hi[k], writes the packed lower triangle of sum u u^T over each fold's training
+ * rows, u = (y, x), to gram[(K+1) * (nc+1)(nc+2)/2] (index K = all rows). Returns
+ * PCVG_INVALID_INPUT when the data are not finite (the kernel then keeps the row kernels). */
+pcvg_status pcvg_fold_gram(int64_t n, int32_t nc, const double* y, const double* x, const int32_t* key,
+                           int32_t K, const int32_t* lo, const int32_t* hi, double* gram);
 pcvg_status pcvg_initial_draw(const pcvg_dataset* data, const pcvg_folds* folds,
                               const pcvg_model_spec* spec, uint64_t seed, uint64_t stream,
                               double* theta);

@@ -1759,6 +1759,23 @@ double param_ess(const std::vector<double>& bank, int L, int64_t n, int dim, int
 
 }  // namespace
 
+extern "C" pcvg_status pcvg_fold_gram(int64_t n, int32_t nc, const double* y, const double* x, const int32_t* key,
+                                      int32_t K, const int32_t* lo, const int32_t* hi, double* gram) {
+  return static_cast<pcvg_status>(guarded(nullptr, [&] {
+    if (n < 1 || nc < 0 || K < 0 || !y || (nc > 0 && !x) || !key || (K > 0 && (!lo || !hi)) || !gram)
+      throw Error(PCVG_INVALID_INPUT, "bad fold_gram arguments");
+    std::vector<int> lov(K + 1, 0), hiv(K + 1, 0);
+    for (int k = 0; k < K; ++k) {
+      lov[k] = lo[k];
+      hiv[k] = hi[k];
+    }
+    SuffStats ss;
+    if (!build_suffstats(n, nc, 0, y, x, key, nullptr, K, lov.data(), hiv.data(), ss))
+      throw Error(PCVG_INVALID_INPUT, "non-finite data or Gram entry");
+    std::copy(ss.A.begin(), ss.A.end(), gram);
+  }));
+}
+
 extern "C" pcvg_status pcvg_initial_draw(const pcvg_dataset* data, const pcvg_folds* folds,
                                          const pcvg_model_spec* spec, uint64_t seed, uint64_t stream,
                                          double* theta) {

@@ -1,0 +1,76 @@
+// Launchers of the sufficient-statistics kernel (gauss_impl.cuh, suff_pass).
+#include <cstdlib>
+
+#include "gauss_impl.cuh"
+
+namespace pcvg {
+
+namespace {
+
+// NB = -1: sufficient statistics at full registers; NB = -2 (one lane per chain, many chains):
+// capped at 128 registers for 4 CTAs/SM - its spills cost latency that only pays back when the
+// extra warps have chains to run (cfg5 +9%, cfg1 / cfg4 -20%).
+template <int FAM, int NCM, int NGM, int T, int NB = -1>
+cudaError_t launch_suff_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
+  const int grid = (S.nch + kBlock / T - 1) / (kBlock / T);
+  if (grid == 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(suff_slots(M, T)) * 2 * kBlock * sizeof(double);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, T, NCM, NGM, NB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  gauss_kernel<FAM, T, NCM, NGM, NB><<<grid, kBlock, smem, st>>>(M, S, A);
+  return cudaGetLastError();
+}
+
+template <int FAM, int NCM, int NGM>
+cudaError_t launch_suff(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st) {
+  switch (T) {
+    case 1:
+      if (S.nch >= 148 * 2 * kBlock * 2) return launch_suff_t<FAM, NCM, NGM, 1, -2>(M, S, A, st);
+      return launch_suff_t<FAM, NCM, NGM, 1>(M, S, A, st);
+    case 4: return launch_suff_t<FAM, NCM, NGM, 4>(M, S, A, st);
+    case 8: return launch_suff_t<FAM, NCM, NGM, 8>(M, S, A, st);
+    case 32: return launch_suff_t<FAM, NCM, NGM, 32>(M, S, A, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+// Lanes per chain of the sufficient-statistics kernel: enough threads to fill the GPU, at most
+// what the Gram entries / groups can use.
+int suff_lanes_per_chain(const ModelDev& M, int nch) {
+  if (const char* env = std::getenv("PCVG_SUFF_LANES")) return std::atoi(env);  // tuning only
+  // Split lanes only pay for many groups: the per-pass partial sums cost (nc + 5) butterfly
+  // reductions, more than a lane saves on a d(d+1)/2 Gram product (measured: cfg1 / cfg4 are
+  // fastest at one lane, cfg3's 400 groups at 32, profiles/r01_suff_lanes.txt).
+  if (M.J < 64) return 1;
+  const long target_threads = 148L * 512;
+  int T = 1;
+  while (T < 32 && static_cast<long>(nch) * T < target_threads) T *= 2;
+  if (T == 2) T = 4;
+  if (T == 16) T = 32;
+  return T;
+}
+
+cudaError_t launch_suff_family(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st) {
+  if (!M.suff) return cudaErrorInvalidValue;
+  switch (M.family) {
+    case kGrouped:
+      if (M.nc > 8) return cudaErrorInvalidValue;
+      return launch_suff<kGrouped, 8, 11>(M, S, A, T, st);
+    case kRadon:
+      return launch_suff<kRadon, 1, 4>(M, S, A, T, st);
+    case kSeasonal:
+      if (M.nc > 13) return cudaErrorInvalidValue;
+      return launch_suff<kSeasonal, 13, 15>(M, S, A, T, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pcvg

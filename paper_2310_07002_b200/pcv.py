@@ -119,6 +119,7 @@ def load():
     _sig(lib, "pcvg_adapt_full_data", i32, [vp, P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec),
                                             P(abi.AdaptConfig), u64, i32, P(abi.Fit)])
     _sig(lib, "pcvg_initial_draw", i32, [P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec), u64, u64, pf])
+    _sig(lib, "pcvg_fold_gram", i32, [i64, i32, pf, pf, pi32, i32, pi32, pi32, pf])
     if lib.pcvg_abi_version() != abi.ABI_VERSION:
         raise ImportError("libpcvg.so ABI version mismatch")
     _lib = lib
@@ -578,6 +579,24 @@ def merge_bench(n_models, K, cfg, iter_count, final, cols, bench_max):
     _check(lib.pcvg_merge_bench(n_models, K, C.byref(cfg), iter_count, int(final), C.byref(ft), _p(bm),
                                 C.byref(rep)))
     return abi.report_dict(rep, arrs, n_models)
+
+
+def fold_gram(y, x, key, lo, hi):
+    """pcvg_fold_gram (host): packed training Gram of u = (y, x) for every fold and the sentinel."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = y.size
+    x = np.asarray(x, dtype=np.float64).reshape(n, -1)
+    nc = x.shape[1]
+    xc = np.ascontiguousarray(x.T)
+    key = np.ascontiguousarray(key, dtype=np.int32)
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    hi = np.ascontiguousarray(hi, dtype=np.int32)
+    K = lo.size
+    dp = (nc + 1) * (nc + 2) // 2
+    out = np.zeros((K + 1) * dp)
+    _check(load().pcvg_fold_gram(n, nc, _p(y), _p(xc), _p(key, C.c_int32), K, _p(lo, C.c_int32), _p(hi, C.c_int32),
+                                 _p(out)))
+    return out.reshape(K + 1, dp)
 
 
 def initial_draw(model, seed, stream):

@@ -198,3 +198,44 @@ def test_merge_rejects_bad_arguments():
         pcv.merge(3, 2, cfg, 10, False, {k: np.zeros(6, dtype=dt) for k, dt in abi.FOLD_COLUMNS})
     with pytest.raises(pcv.InvalidInput):
         pcv.merge(1, 1, cfg, 10, False, cols)
+
+
+@pytest.mark.parametrize("scheme", ["loo", "kfold", "hv"])
+def test_fold_gram_is_the_rounded_exact_training_sum(scheme):
+    """Fold statistics of the sufficient-statistics kernel (suffstats.cpp): every
+    packed Gram entry of every fold is the training-row sum of u u^T (u = (y, x)) formed as
+    full - excluded in double-double, i.e. the exact rational sum rounded once (here: within
+    one ulp of it, also when cancellation makes the training sum tiny)."""
+    from fractions import Fraction
+    rng = np.random.default_rng(4)
+    n, nc = 40, 3
+    x = rng.standard_normal((n, nc)) * np.array([1.0, 1e3, 1e-3])
+    y = 1e4 + rng.standard_normal(n)  # large mean: sum y^2 cancels strongly in full - excluded
+    if scheme == "loo":
+        key = np.arange(n, dtype=np.int32)
+        lo, hi = np.arange(n), np.arange(n) + 1
+    elif scheme == "kfold":
+        key = rng.integers(0, 5, n).astype(np.int32)
+        lo, hi = np.arange(5), np.arange(5) + 1
+    else:  # hv-block: key = time rank, exclusion windows
+        key = rng.permutation(n).astype(np.int32)
+        lo = np.array([0, 5, 30, 35]); hi = np.array([12, 17, 40, 40])
+    g = pcv.fold_gram(y, x, key, lo, hi)
+    u = np.column_stack([y, x])
+    K = lo.size
+    fu = [[Fraction(float(v)) for v in row] for row in u]
+    for k in range(K + 1):
+        train = [i for i in range(n) if k == K or not (lo[k] <= key[i] < hi[k])]
+        e = 0
+        for a in range(nc + 1):
+            for b in range(a + 1):
+                exact = sum((fu[i][a] * fu[i][b] for i in train), Fraction(0))
+                got = g[k, e]
+                assert abs(Fraction(got) - exact) <= Fraction(np.spacing(abs(float(exact)))), (k, a, b, got, float(exact))
+                e += 1
+
+
+def test_fold_gram_rejects_non_finite_data():
+    y = np.array([1.0, np.inf, 2.0])
+    with pytest.raises(pcv.InvalidInput):
+        pcv.fold_gram(y, np.ones((3, 1)), np.arange(3), np.arange(3), np.arange(3) + 1)

@@ -111,11 +111,16 @@ def main():
         achieved = flops * value / 1e12
         is_logistic = name == "cfg2"
         pk = peak["dmma_tflops_bps8"] if is_logistic else peak["dfma_tflops_bps8"]
-        line = {"config": name, "policy": args.policy, "workload": desc, "chains": chains, "steps": steps,
+        # AUTO / SUFFSTAT run the Gaussian families on fold sufficient statistics: the
+        # row-streaming flop count is then a row-equivalent rate, not a roofline fraction
+        suff = not is_logistic and args.policy in (0, 4)
+        line = {"config": name, "policy": args.policy, "kernel": "suffstat" if suff else "rows",
+                "workload": desc, "chains": chains, "steps": steps,
                 "gpu_chain_steps_per_s": value, "gpu_ms_per_step": ms / steps,
-                "flop_per_chain_step": flops, "achieved_tflops": achieved,
+                "flop_per_chain_step": flops,
+                ("row_equivalent_tflops" if suff else "achieved_tflops"): achieved,
                 "peak_tflops": pk, "peak_kind": "FP64 DMMA" if is_logistic else "FP64 DFMA",
-                "frac": achieved / pk, "elpd_sum_model0": float(np.sum(cols["estimate"][:case.K]))}
+                "frac": None if suff else achieved / pk, "elpd_sum_model0": float(np.sum(cols["estimate"][:case.K]))}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             sample_folds = {"cfg1": 32, "cfg2": 32, "cfg3": 8, "cfg4": 8, "cfg5": 4}[name]
