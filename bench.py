@@ -249,7 +249,7 @@ def main():
     per_launch_ms = local_ms / args.steps
     achieved = FLOP_PER_CHAIN_STEP * (fe - fb) * L / (per_launch_ms * 1e-3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_glm.json")  # v5 capture
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_glm.json")  # v6 capture (current kernel)
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")

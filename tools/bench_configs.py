@@ -22,6 +22,7 @@ for p in (ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "tests", "golden
 CONFIGS = {
     "cfg1": ("cfg1_linreg_loo", 4, "linear regression N=100 P=5 (grouped, J=1), LOO 100 folds x 4 chains"),
     "cfg2": ("cfg2_logistic_bench", 8, "logistic N=10000 P=50, LOO 10000 folds x 8 chains"),
+    "cfg2k": ("cfg2_logistic_bench", 8, "logistic N=10000 P=50, K-fold K=10 (seed 1) x 8 chains"),
     "cfg3": ("cfg3_radon_bench", 8, "radon-style 12000 houses / 400 counties, LOGO, M_A+M_B x 8 chains"),
     "cfg4": ("cfg4_seasonal_bench", 4, "seasonal AR(2)+11 dummies T=5000, hv-block K=100 h=12, M_A+M_B x 4 chains"),
     "cfg5": ("cfg5_linreg_bench", 16, "linear regression N=100000 P=5, LOO 100000 folds x 16 chains"),
@@ -103,13 +104,18 @@ def main():
     for name in names:
         fixture, L, desc = CONFIGS[name]
         case = Case(fixture)
+        if name == "cfg2k":  # the K-fold scheme of BASELINE configs[1] on the same data and fit
+            from paper_2310_07002_b200 import pcv
+            case.folds = pcv.make_kfold_scheme(case.data, 10, 1)
+            case.models = [pcv.LogisticModel("M0", case.data, case.folds)]
+            case.fa = case.folds.arrays()
         steps = args.steps if name != "cfg5" else max(2, args.steps // 3)
         ms, cols = gpu_run(case, L, steps, args.warmup, args.policy)
         chains = case.K * L * len(case.models)
         value = chains * steps / (ms / 1e3)
         flops = sum(flops_per_chain_step(case, m) for m in range(len(case.models))) / len(case.models)
         achieved = flops * value / 1e12
-        is_logistic = name == "cfg2"
+        is_logistic = name.startswith("cfg2")
         pk = peak["dmma_tflops_bps8"] if is_logistic else peak["dfma_tflops_bps8"]
         # AUTO / SUFFSTAT run the Gaussian families on fold sufficient statistics: the
         # row-streaming flop count is then a row-equivalent rate, not a roofline fraction
@@ -123,7 +129,7 @@ def main():
                 "frac": None if suff else achieved / pk, "elpd_sum_model0": float(np.sum(cols["estimate"][:case.K]))}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
-            sample_folds = {"cfg1": 32, "cfg2": 32, "cfg3": 8, "cfg4": 8, "cfg5": 4}[name]
+            sample_folds = {"cfg1": 32, "cfg2": 32, "cfg2k": 2, "cfg3": 8, "cfg4": 8, "cfg5": 4}[name]
             cv, kind, sample = cpu_sample(case, L, sample_folds, 3, threads)
             line["cpu"] = {"chain_steps_per_s": cv, "kind": kind, "cores": threads, "sample": sample}
             line["speedup_vs_cpu"] = value / cv

@@ -27,6 +27,10 @@ def main():
     ap.add_argument("--every", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fit", action="store_true",
+                    help="also time one full-data fit per model (Step 1, adapt_full_data defaults: "
+                         "4 chains, 1000 warm-up + 2000 draws) on the same GPU, for the north star's "
+                         "'comparable to a single full-data fit'")
     args = ap.parse_args()
     from bench_configs import CONFIGS, cpu_sample
     from parity_util import Case
@@ -49,6 +53,16 @@ def main():
             "delta_hat": rep["delta_hat"], "mcse": rep["mcse"], "epistemic_se": rep["epistemic_se"],
             "rhat_max": rep["rhat_max"], "verdict_quantile_value": rep["verdict_quantile_value"],
             "verdict_pass": int(rep["verdict_pass"]), "chain_steps": chains * steps}
+    if args.fit:
+        fits = []
+        with pcv.Context(0) as ctx:
+            for i, m in enumerate(case.models):
+                t1 = time.perf_counter()
+                f = ctx.adapt_full_data(m, pcv.AdaptConfig(), seed=1, model_id=i)
+                fits.append({"wall_s": time.perf_counter() - t1, "device_s": f.device_ms / 1e3,
+                             "step_size": f.kparams.step_size})
+        line["full_data_fit"] = {"per_model": fits, "config": "4 chains, 1000 warm-up + 2000 draws, n_lf 32",
+                                 "note": "Step 1 on the same GPU (pcvg_adapt_full_data), warm context"}
     if not args.no_cpu:
         threads = os.cpu_count() or 1
         rate, kind, sample = cpu_sample(case, L, 8, 3, threads)
