@@ -89,3 +89,59 @@ def test_poisoned_test_row(policy):
             olp = om.log_joint(th[0], fold)
             assert (np.isnan(lp[0]) and np.isnan(olp)) or (not np.isfinite(olp) and lp[0] == olp) or \
                 abs(lp[0] - olp) <= 1e-10 * max(1.0, abs(olp)), (fold, lp[0], olp)
+
+
+def _many_groups_cases():
+    """Hierarchical models with J >= 64 groups: the sufficient-statistics kernel runs a warp per
+    chain there (lane-owned groups, shared-memory group slots, per-lane override walks)."""
+    import sys
+    from parity_util import Case
+    out = []
+    c = Case("cfg3_radon_bench")  # radon-style, 400 counties, LOGO; the fixture's kernel and bank
+    for m in range(len(c.models)):
+        kp = c.kparams[m]
+        out.append(("radon400_logo_m%d" % m, c.models[m], c.omodels[m],
+                    pcv.KernelParams(kp.step_size, 8, kp.inv_mass_diag),
+                    c.banks[m][np.linspace(0, len(c.banks[m]) - 1, 4).astype(int)], c.K))
+    d = ragged_grouped(seed=9, J=150)  # grouped, 150 ragged groups, K-fold: every fold touches many groups
+    f = pcv.make_kfold_scheme(d, 7, 3)
+    model = pcv.GroupedRegressionModel("M", d, f)
+    out.append(("grouped150_kfold", model, O.OModel(d, f.arrays(), model.spec),
+                pcv.KernelParams(0.01, 8, np.ones(model.dim())), thetas(model, 4, 5), f.K))
+    return out
+
+
+@pytest.mark.parametrize("policy", [pcv.Context.KERNEL_SUFFSTAT, pcv.Context.KERNEL_ROWS])
+def test_many_groups_warp_kernels(policy):
+    """J >= 64: log joint / gradient at the stored position, leapfrog end points (hmc.cpp:22-51)
+    and injected-momentum hmc_step (hmc.cpp:53-99) against the oracle."""
+    rng = np.random.default_rng(21)
+    for name, model, om, kp, th, K in _many_groups_cases():
+        step, im = kp.step_size, kp.inv_mass_diag
+        with pcv.Context(0) as ctx:
+            ctx.set_kernel_policy(policy)
+            slot = ctx.add_model(model, kp, th)
+            folds = np.array([0, 1, K // 2, K], dtype=np.int32)
+            lp, g = ctx.eval(slot, folds, th)
+            for i in range(4):
+                olp, og = om.log_joint(th[i], int(folds[i])), om.grad(th[i], int(folds[i]))
+                s = scale(th[i])
+                assert abs(lp[i] - olp) <= 1e-12 * s * max(1.0, abs(olp)), (name, i, lp[i], olp)
+                assert np.abs(g[i] - og).max() <= 1e-12 * s * max(1.0, np.abs(og).max()), (name, i)
+            mom = rng.standard_normal(th.shape) / np.sqrt(im)
+            q1, p1, ok = ctx.leapfrog(slot, folds, th, mom)
+            assert ok.all(), name
+            for i in range(4):
+                okr, oq, op = om.leapfrog(int(folds[i]), step, 8, im, th[i], mom[i])
+                assert okr, name
+                np.testing.assert_allclose(q1[i], oq, rtol=1e-8, atol=1e-9, err_msg=name)
+                np.testing.assert_allclose(p1[i], op, rtol=1e-8, atol=1e-8, err_msg=name)
+            u = rng.uniform(size=4)
+            out, h0, h1, acc, div = ctx.hmc_probe(slot, folds, th, mom, u)
+            for i in range(4):
+                oth, oh0, oh1, oacc, odiv = om.hmc_probe(int(folds[i]), step, 8, im, th[i], mom[i], u[i])
+                assert div[i] == odiv, name
+                assert abs(h0[i] - oh0) <= 1e-10 * (1 + abs(oh0)), (name, h0[i], oh0)
+                if not odiv:
+                    assert abs(h1[i] - oh1) <= 1e-8 * (1 + abs(oh1)), (name, h1[i], oh1)
+                    np.testing.assert_allclose(out[i], oth, rtol=1e-8, atol=1e-8, err_msg=name)
