@@ -19,7 +19,9 @@
 // thread-block cluster of CS CTAs that replicate one 64-chain tile: each CTA streams 1/CS of the
 // row tiles and the partial X^T R / residual sums are reduced through distributed shared memory in
 // fixed rank order, so every CTA of the cluster holds bit-identical state; rank 0 writes it back.
+#include <algorithm>
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 #include <math_constants.h>
 
@@ -729,6 +731,9 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     cudaError_t e = cudaFuncSetAttribute(glm_kernel<FAM, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sizeof(Smem<KP>)));
     if (e != cudaSuccess) return e;
+    // 16-CTA clusters (non-portable) for the fewest-chain configurations (cfg2 K-fold: 80 chains)
+    e = cudaFuncSetAttribute(glm_kernel<FAM, KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   auto launch = [&](int tile0, int ntiles, int cs) {
@@ -746,7 +751,36 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     cfg.numAttrs = cs > 1 ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs, tile0);
   };
-  const int cs = glm_cluster_size(M.n, KP, S.nch);
+  // Concurrently schedulable clusters of each size (a cluster must fit in one GPC): a 16-CTA cluster
+  // only pays while every tile's cluster runs at once, else halve it.
+  static int active[5] = {-1, -1, -1, -1, -1};  // index log2(cs)
+  auto fits = [&](int c) {
+    const int li = c == 1 ? 0 : (c == 2 ? 1 : (c == 4 ? 2 : (c == 8 ? 3 : 4)));
+    if (active[li] < 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(c);
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = sizeof(Smem<KP>);
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = c;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, glm_kernel<FAM, KP>, &q) != cudaSuccess) nclusters = 0;
+      cudaGetLastError();
+      active[li] = nclusters;
+    }
+    return active[li];
+  };
+  int cs = glm_cluster_size(M.n, KP, S.nch);
+  while (cs > 8 && fits(cs) < tiles) cs /= 2;
+  static const bool verbose = std::getenv("PCVG_VERBOSE") != nullptr;  // tuning only
+  if (verbose)
+    std::fprintf(stderr, "glm_kernel<%d,%d>: %d tiles, cluster %d (active clusters: 8 -> %d, 16 -> %d)\n", FAM, KP,
+                 tiles, cs, fits(8), fits(16));
   const int sms = glm_sm_count();
   static const bool no_split = std::getenv("PCVG_NO_TAIL_SPLIT") != nullptr;  // A/B tests only
   if (cs == 1 && tiles > sms && tiles % sms != 0 && !no_split) {
@@ -776,14 +810,14 @@ int glm_sm_count() {
   return sms;
 }
 
-// Cluster size: enough CTAs per 64-chain tile to cover the GPU, at most 8 (portable), and at least
-// two row tiles per CTA.
+// Cluster size: enough CTAs per 64-chain tile to cover the GPU, at most 16 (non-portable; the
+// launcher caps it at 8 where the device cannot schedule 16), and at least two row tiles per CTA.
 int glm_cluster_size(int n, int kp, int nch) {
   const int tm = kp <= 8 ? 256 : (kp <= 16 ? 128 : 64);
   const int tiles = (nch + kC - 1) / kC;
   const int ntiles = (n + tm - 1) / tm;
   int cs = 1;
-  while (cs < 8 && tiles * cs * 2 <= 148 && ntiles >= 4 * cs) cs *= 2;
+  while (cs < 16 && tiles * cs * 2 <= 148 && ntiles >= 4 * cs) cs *= 2;
   return cs;
 }
 
