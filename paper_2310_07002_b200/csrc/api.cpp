@@ -505,7 +505,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   // fold sufficient statistics for the Gaussian linear families (suffstats.cpp)
   int suff = 0;
   SuffStats ss;
-  if ((s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON || s->family == PCVG_FAMILY_SEASONAL_AR) &&
+  if ((s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON || s->family == PCVG_FAMILY_SEASONAL_AR ||
+       (s->family == PCVG_FAMILY_RAT_GROWTH && !s->per_subject_slope)) &&
       build_suffstats(n, m.nc, m.J, y.data(), xc.data(), key.data(), hier ? grp_ptr.data() : nullptr, m.K,
                       lo.data(), hi.data(), ss)) {
     suff = 1;

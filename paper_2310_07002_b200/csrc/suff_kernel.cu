@@ -65,6 +65,8 @@ cudaError_t launch_suff_family(const ModelDev& M, const ChainsDev& S, const RunA
       return launch_suff<kGrouped, 8, 11>(M, S, A, T, st);
     case kRadon:
       return launch_suff<kRadon, 1, 4>(M, S, A, T, st);
+    case kRatB:  // rat growth with a shared slope: m = alpha_g + beta t (rat_growth.cpp:148-172)
+      return launch_suff<kRatB, 1, 4>(M, S, A, T, st);
     case kSeasonal:
       if (M.nc > 13) return cudaErrorInvalidValue;
       return launch_suff<kSeasonal, 13, 15>(M, S, A, T, st);

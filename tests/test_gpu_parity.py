@@ -45,7 +45,8 @@ def case_in(ctx, name):
 
 
 # Gaussian linear fixtures that also run on fold sufficient statistics (policy SUFFSTAT)
-SUFF_KERNEL = {"cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock"}
+SUFF_KERNEL = {"cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock",
+               "rat_logo"}  # rat: the shared-slope model M_B (M_A keeps the batched kernel)
 
 
 def with_kernels(names):
