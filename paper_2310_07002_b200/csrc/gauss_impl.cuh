@@ -96,6 +96,7 @@ struct Prep {
   double off0;    // offset without the group term
   double v, inv_v, logv;
   double va, sa;  // group scale (grouped: va = sig_a^2; radon: va, sa = sqrt(va))
+  double inv_va;  // 1 / va (the sufficient-statistics passes multiply instead of dividing)
   double vb;      // rat M_A: slope scale s_b^2
 };
 
@@ -156,6 +157,7 @@ __device__ __forceinline__ void prepare(const ModelDev& M, const double* qG, Pre
     P.v = sigma * sigma;
   }
   P.inv_v = 1.0 / P.v;
+  if constexpr (FAM != kSeasonal) P.inv_va = 1.0 / P.va;  // used by the RCP passes only (else eliminated)
   P.logv = log(P.v);
 }
 
@@ -171,31 +173,38 @@ struct GroupAcc {
   double a0, a1, a2, a3;
 };
 
+// a / v, or a * (1 / v) in the sufficient-statistics passes (RCP: one rounding more, no division)
+template <bool RCP>
+__device__ __forceinline__ double dv(double a, double v, double inv) {
+  if constexpr (RCP) return a * inv;
+  else return a / v;
+}
+
 // d log p / d q_g given the lane-reduced residual sum of group g; updates replicated sums.
-template <int FAM, int NCM, int NGM>
+template <int FAM, int NCM, int NGM, bool RCP = false>
 __device__ __forceinline__ double group_grad(const Prep<NCM>& P, const double* qG,
                                             const ModelDev& M, double qg, double srg,
                                             GroupAcc& G) {
   if constexpr (FAM == kGrouped) {  // grouped_regression.cpp:100-116
     const double dev = qg - qG[0];
-    G.a0 += dev / P.va;  // -> d/d mu_alpha
+    G.a0 += dv<RCP>(dev, P.va, P.inv_va);  // -> d/d mu_alpha
     G.a1 += dev * dev;   // -> d/d log sigma_alpha, prior
-    return srg / P.v - dev / P.va;
+    return dv<RCP>(srg, P.v, P.inv_v) - dv<RCP>(dev, P.va, P.inv_va);
   } else if constexpr (FAM == kRatB || FAM == kRatA) {  // rat_growth.cpp:129-137, 159-164 (alpha_g)
     const double dev = qg - (FAM == kRatB ? qG[1] : qG[0]);
-    G.a0 += dev / P.va;  // -> d/d mu_a
+    G.a0 += dv<RCP>(dev, P.va, P.inv_va);  // -> d/d mu_a
     G.a1 += dev * dev;   // -> d/d log s_a, prior
-    return srg / P.v - dev / P.va;
+    return dv<RCP>(srg, P.v, P.inv_v) - dv<RCP>(dev, P.va, P.inv_va);
   } else {  // radon.cpp:93-105
     G.a0 += srg;       // sum r (-> d/d mu_alpha)
     G.a1 += srg * qg;  // sum r z (-> d/d log va)
     G.a2 += qg * qg;   // prior on z
-    return P.sa * srg / P.v - qg;
+    return dv<RCP>(P.sa * srg, P.v, P.inv_v) - qg;
   }
 }
 
 // Global gradient and (optionally) log joint from the reduced sums.
-template <int FAM, int NCM, int NGM>
+template <int FAM, int NCM, int NGM, bool RCP = false>
 __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& P,
                                             const double* qG, const double* sxr, double sr,
                                             double srr, const GroupAcc& G, int n_train,
@@ -204,10 +213,10 @@ __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& 
   if constexpr (FAM == kGrouped) {  // grouped_regression.cpp:109-121, 65-85
 #pragma unroll
     for (int c = 0; c < NCM; ++c)
-      if (c < M.nc) gG[3 + c] = M.cmask[c] * (sxr[c] / P.v) - qG[3 + c];
+      if (c < M.nc) gG[3 + c] = M.cmask[c] * dv<RCP>(sxr[c], P.v, P.inv_v) - qG[3 + c];
     gG[0] = G.a0 - qG[0];
-    gG[1] = G.a1 / P.va - M.J - P.va / 10.0 + 1.0;
-    gG[2] = srr / P.v - ntr - P.v / 10.0 + 1.0;
+    gG[1] = dv<RCP>(G.a1, P.va, P.inv_va) - M.J - P.va / 10.0 + 1.0;
+    gG[2] = dv<RCP>(srr, P.v, P.inv_v) - ntr - P.v / 10.0 + 1.0;
     if (value) {
       double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
       l += -0.5 * (M.J * (kLog2Pi + log(P.va)) + G.a1 / P.va);
@@ -221,10 +230,10 @@ __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& 
       lp = l;
     }
   } else if constexpr (FAM == kRadon) {  // radon.cpp:102-106, 50-74
-    gG[0] = (M.include_floor ? sxr[0] / P.v : 0.0) - qG[0];
-    gG[1] = G.a0 / P.v - qG[1] / 4.0;
-    gG[2] = 0.5 * P.sa * G.a1 / P.v + 6.0 - 9.0 * P.va;
-    gG[3] = 0.5 * (srr / P.v - ntr) + 10.0 - 10.0 * P.v;
+    gG[0] = (M.include_floor ? dv<RCP>(sxr[0], P.v, P.inv_v) : 0.0) - qG[0];
+    gG[1] = dv<RCP>(G.a0, P.v, P.inv_v) - qG[1] / 4.0;
+    gG[2] = dv<RCP>(0.5 * P.sa * G.a1, P.v, P.inv_v) + 6.0 - 9.0 * P.va;
+    gG[3] = 0.5 * (dv<RCP>(srr, P.v, P.inv_v) - ntr) + 10.0 - 10.0 * P.v;
     if (value) {
       double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
       l += -0.5 * (M.J * kLog2Pi + G.a2);
@@ -236,10 +245,10 @@ __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& 
     }
   } else if constexpr (FAM == kRatB) {  // rat_growth.cpp:148-172, 88-107
     const double s_a = exp(qG[2]), s_y = exp(qG[3]);
-    gG[0] = sxr[0] / P.v - (qG[0] - 6.0) / 2.0;
+    gG[0] = dv<RCP>(sxr[0], P.v, P.inv_v) - (qG[0] - 6.0) / 2.0;
     gG[1] = G.a0 - (qG[1] - 250.0) / 20.0;
-    gG[2] = G.a1 / P.va - M.J + 25.0 - 2.0 * s_a;
-    gG[3] = srr / P.v - ntr + 1.0 - 2.0 * s_y;
+    gG[2] = dv<RCP>(G.a1, P.va, P.inv_va) - M.J + 25.0 - 2.0 * s_a;
+    gG[3] = dv<RCP>(srr, P.v, P.inv_v) - ntr + 1.0 - 2.0 * s_y;
     if (value) {
       double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
       l += -0.5 * (M.J * (kLog2Pi + log(P.va)) + G.a1 / P.va);
@@ -277,15 +286,15 @@ __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& 
         const double w = logistic_fn(qG[2 + c]);
         const double dw = w * (1.0 - w);
         const double drho = M.rho_sym ? 2.0 * dw : 0.5 * dw;
-        gG[2 + c] = sxr[c] * drho / P.v + (4.0 * (1.0 - w) - 4.0 * w + 1.0 - 2.0 * w);
+        gG[2 + c] = dv<RCP>(sxr[c] * drho, P.v, P.inv_v) + (4.0 * (1.0 - w) - 4.0 * w + 1.0 - 2.0 * w);
         if (value) l += 4.0 * log(w) + 4.0 * log1p(-w) + M.c_lbeta55 + log(w) + log1p(-w);
       } else if (c < M.p + M.q) {
-        gG[2 + c] = sxr[c] / P.v - qG[2 + c];
+        gG[2 + c] = dv<RCP>(sxr[c], P.v, P.inv_v) - qG[2 + c];
         if (value) l += -0.5 * (kLog2Pi + qG[2 + c] * qG[2 + c]);
       }
     }
-    gG[0] = sr / P.v - qG[0];
-    gG[1] = srr / P.v - ntr - P.v + 1.0;
+    gG[0] = dv<RCP>(sr, P.v, P.inv_v) - qG[0];
+    gG[1] = dv<RCP>(srr, P.v, P.inv_v) - ntr - P.v + 1.0;
     if (value) {
       l += -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
       l += -0.5 * (kLog2Pi + qG[0] * qG[0]);
@@ -498,7 +507,7 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
     const double srg = fma(-ng, off, ws);
     t2 = fma(off, ws + srg, t2);
     if constexpr (FAM != kSeasonal) {
-      const double gg = group_grad<FAM, NCM, NGM>(P, qG, M, qg, srg, G);
+      const double gg = group_grad<FAM, NCM, NGM, true>(P, qG, M, qg, srg, G);
       bad |= !isfinite(gg);
       if (kind == 0) {
         S.grad[cur * plane + gi] = gg;
@@ -568,7 +577,7 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
     if constexpr (T > 1) poison = __ballot_sync(mask, poison) != 0;
   }
   bad = T > 1 ? __any_sync(mask, bad) : bad;
-  global_grad<FAM, NCM, NGM>(M, P, qG, sxr, sr_tot, srr, G, n_train, gG, VALUE, lp);
+  global_grad<FAM, NCM, NGM, true>(M, P, qG, sxr, sr_tot, srr, G, n_train, gG, VALUE, lp);
   if (VALUE && poison) lp = CUDART_NAN;
   if constexpr (T > 1) __syncwarp(mask);
 }

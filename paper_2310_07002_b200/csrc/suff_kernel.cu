@@ -39,6 +39,15 @@ cudaError_t launch_suff(const ModelDev& M, const ChainsDev& S, const RunArgs& A,
   }
 }
 
+// One lane per chain only (the many-chain throughput case, cfg1 / cfg5 linear regression with
+// P = 5): a narrower width class keeps the unrolled Gram product and parameter loops at the
+// model's size (21 instead of 45 Gram entries, 8 instead of 11 global parameters).
+template <int FAM, int NCM, int NGM>
+cudaError_t launch_suff1(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
+  if (S.nch >= 148 * 2 * kBlock * 2) return launch_suff_t<FAM, NCM, NGM, 1, -2>(M, S, A, st);
+  return launch_suff_t<FAM, NCM, NGM, 1>(M, S, A, st);
+}
+
 }  // namespace
 
 // Lanes per chain of the sufficient-statistics kernel: enough threads to fill the GPU, at most
@@ -62,6 +71,7 @@ cudaError_t launch_suff_family(const ModelDev& M, const ChainsDev& S, const RunA
   switch (M.family) {
     case kGrouped:
       if (M.nc > 8) return cudaErrorInvalidValue;
+      if (M.nc <= 5 && T == 1) return launch_suff1<kGrouped, 5, 8>(M, S, A, st);
       return launch_suff<kGrouped, 8, 11>(M, S, A, T, st);
     case kRadon:
       return launch_suff<kRadon, 1, 4>(M, S, A, T, st);
