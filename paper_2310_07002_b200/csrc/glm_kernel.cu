@@ -777,6 +777,7 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
   };
   int cs = glm_cluster_size(M.n, KP, S.nch);
   while (cs > 8 && fits(cs) < tiles) cs /= 2;
+  if (const char* e = std::getenv("PCVG_GLM_CS")) cs = std::atoi(e);  // tuning only
   static const bool verbose = std::getenv("PCVG_VERBOSE") != nullptr;  // tuning only
   if (verbose)
     std::fprintf(stderr, "glm_kernel<%d,%d>: %d tiles, cluster %d (active clusters: 8 -> %d, 16 -> %d)\n", FAM, KP,
