@@ -26,9 +26,12 @@
 // is checked by tools/probes/tf32_ts_probe.cu).
 // The chain state, integrator, energies, Metropolis test, RNG, log_pred and accumulators are FP64
 // and the same as glm_kernel.cu (hmc.cpp:22-99, engine.cpp:342-381).
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -164,23 +167,24 @@ __device__ __forceinline__ double bernoulli_logit32(double y, double x) {
 // is g & 1 (per-buffer barriers eta_bar[g & 1] and full_y[g & 1]: (g >> 1) & 1).
 struct Pipe32 {
   uint32_t g = 0, ia = 0, ib = 0;
+  int t0 = 0;  // first row tile of this CTA (row-split clusters: rank share [t0, t0 + ntiles))
 };
 
-__device__ __forceinline__ const unsigned char* tile_src(const ModelDev& M, uint32_t j, int ntiles) {
-  return M.x32 + static_cast<size_t>(j % static_cast<uint32_t>(ntiles)) * kTileBytes;
+__device__ __forceinline__ const unsigned char* tile_src(const ModelDev& M, uint32_t j, int ntiles, int t0) {
+  return M.x32 + static_cast<size_t>(t0 + static_cast<int>(j % static_cast<uint32_t>(ntiles))) * kTileBytes;
 }
-__device__ __forceinline__ void load_eta_image(Smem32& sm, const ModelDev& M, uint32_t j, int ntiles) {
-  const unsigned char* src = tile_src(M, j, ntiles);
+__device__ __forceinline__ void load_eta_image(Smem32& sm, const ModelDev& M, uint32_t j, int ntiles, int t0) {
+  const unsigned char* src = tile_src(M, j, ntiles, t0);
   fence_proxy_async();
   mbar_expect_tx(&sm.full_a, kXImg);
   bulk_g2s(sm.xa, src, kXImg, &sm.full_a);
   mbar_expect_tx(&sm.full_y[j & 1], kYK);
   bulk_g2s(sm.yk[j & 1], src + kXImg, kYK, &sm.full_y[j & 1]);
 }
-__device__ __forceinline__ void load_g_image(Smem32& sm, const ModelDev& M, uint32_t j, int ntiles) {
+__device__ __forceinline__ void load_g_image(Smem32& sm, const ModelDev& M, uint32_t j, int ntiles, int t0) {
   fence_proxy_async();
   mbar_expect_tx(&sm.full_b, kGImg);
-  bulk_g2s(sm.xb, tile_src(M, j, ntiles) + kXImg + kYK, kGImg, &sm.full_b);
+  bulk_g2s(sm.xb, tile_src(M, j, ntiles, t0) + kXImg + kYK, kGImg, &sm.full_b);
 }
 
 // eta^T(g) into buffer g & 1: 7 k-steps x {hi.hi, hi.lo, lo.hi}. Descriptors advance by adding
@@ -241,14 +245,14 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
   const uint32_t g0 = P.g;
   if (tid == kCtl) {
     // ---------------- control thread
-    if (P.ia == g0) load_eta_image(sm, M, P.ia++, ntiles);
-    if (P.ib == g0) load_g_image(sm, M, P.ib++, ntiles);
+    if (P.ia == g0) load_eta_image(sm, M, P.ia++, ntiles, P.t0);
+    if (P.ib == g0) load_g_image(sm, M, P.ib++, ntiles, P.t0);
     mbar_wait(&sm.full_a, g0 & 1u);
     tmem_fence_after();
     issue_eta(sm, g0);
     if (ntiles > 1 || more) {
       mbar_wait(&sm.eta_bar[g0 & 1u], (g0 >> 1) & 1u);  // the eta image buffer is free
-      load_eta_image(sm, M, P.ia++, ntiles);
+      load_eta_image(sm, M, P.ia++, ntiles, P.t0);
       if (ntiles > 1) {
         mbar_wait(&sm.full_a, (g0 + 1) & 1u);
         tmem_fence_after();
@@ -266,7 +270,7 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
       if (t + 2 < ntiles || (t + 2 == ntiles && more)) {
         mbar_wait(&sm.eta_bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);  // eta(g+1) read the buffer
         TRACE(t, 2);
-        load_eta_image(sm, M, P.ia++, ntiles);  // y/key slot g & 1: epilogue(g) is done
+        load_eta_image(sm, M, P.ia++, ntiles, P.t0);  // y/key slot g & 1: epilogue(g) is done
         if (t + 2 < ntiles) {
           mbar_wait(&sm.full_a, (g + 2) & 1u);
           TRACE(t, 3);
@@ -277,7 +281,7 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
       if (t + 1 < ntiles || more) {
         mbar_wait(&sm.g_bar, g & 1u);  // G(g) read the G image buffer
         TRACE(t, 4);
-        load_g_image(sm, M, P.ib++, ntiles);
+        load_g_image(sm, M, P.ib++, ntiles, P.t0);
       }
     }
   } else if (tid < kEpiThreads) {
@@ -395,15 +399,22 @@ __device__ void grad_pass32(Smem32& sm, const ModelDev& M, double* gsc, Pipe32& 
 #endif
 }
 
-__global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDev S, RunArgs A, double* gscratch) {
+// cs > 1: the CTAs of a cluster replicate one 128-chain tile and split its row tiles (the last
+// partial wave of a launch); per pass the FP64 G partials (global scratch) and log-likelihood
+// partials (DSMEM) are summed in rank order, so every rank holds identical chain state; rank 0
+// owns every global write (the glm_kernel cluster scheme, glm_kernel.cu).
+__global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDev S, RunArgs A, double* gscratch,
+                                                             int cs, int tile0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem32& sm = *reinterpret_cast<Smem32*>(smem_raw);
   const int tid = threadIdx.x;
   const int nch = S.nch;
   const int dim = M.dim;
   const size_t plane = static_cast<size_t>(dim) * nch;
-  const int tile = blockIdx.x;
-  const int ntiles = (M.n + kRows - 1) / kRows;
+  const int tile = tile0 + static_cast<int>(blockIdx.x) / cs, crank = static_cast<int>(blockIdx.x) % cs;
+  const bool writer = crank == 0;
+  const int ntiles_all = (M.n + kRows - 1) / kRows;
+  const int rt0 = crank * ntiles_all / cs, ntiles = (crank + 1) * ntiles_all / cs - rt0;
   const bool owner = tid < kEpiThreads;
   const int oc = tid & (kC - 1), ok = tid / kC;
   const int ogc = tile * kC + oc;
@@ -411,7 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
   const bool is_chain = tid < kC;
   const int gc = tile * kC + tid;
   const bool cvalid = is_chain && gc < nch;
+  const bool cwrite = cvalid && writer;
   double* gsc = gscratch + static_cast<size_t>(blockIdx.x) * kGN * kC;
+  double* gsc0 = gscratch + static_cast<size_t>(blockIdx.x - crank) * kGN * kC;  // rank 0 of the cluster
 
   if (tid == 0) {
     mbar_init(&sm.full_a, 1);
@@ -452,6 +465,11 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
   __syncthreads();
   tmem_fence_after();
   Pipe32 P;
+  P.t0 = rt0;
+  auto csync = [&]() {  // all of the cluster's G scratch / llq / chain-state writes visible
+    if (cs > 1) cooperative_groups::this_cluster().sync();
+    else __syncthreads();
+  };
 
   double qown[kOwn];
   // owners publish theta (hi / lo) into the A image of eta^T: element (chain, k) at
@@ -472,8 +490,22 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
     }
     fence_proxy_async();
   };
-  auto gk_of = [&](int k) { return gsc[static_cast<size_t>(k) * kC + oc] + gsc[static_cast<size_t>(kK + k) * kC + oc]; };
-  auto ll_of = [&](int c) { return (sm.llq[0][c] + sm.llq[1][c]) + (sm.llq[2][c] + sm.llq[3][c]); };
+  auto gk_of = [&](int k) {  // sum over the cluster's ranks in rank order (cs = 1: own scratch)
+    double s = 0.0;
+    for (int r = 0; r < cs; ++r) {
+      const double* gr = gsc0 + static_cast<size_t>(r) * kGN * kC;
+      s += gr[static_cast<size_t>(k) * kC + oc] + gr[static_cast<size_t>(kK + k) * kC + oc];
+    }
+    return s;
+  };
+  auto ll_of = [&](int c) {
+    double s = 0.0;
+    for (int r = 0; r < cs; ++r) {
+      const Smem32* rm = cs > 1 ? cooperative_groups::this_cluster().map_shared_rank(&sm, r) : &sm;
+      s += (rm->llq[0][c] + rm->llq[1][c]) + (rm->llq[2][c] + rm->llq[3][c]);
+    }
+    return s;
+  };
   auto lp_from_partials = [&](int c) {
     double pr = 0.0;
 #pragma unroll
@@ -491,24 +523,26 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
     put_theta();
     __syncthreads();
     grad_pass32<true>(sm, M, gsc, P, ntiles, false);
+    csync();
     if (owner) {
       double pr = 0.0;
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
         const int k = ok + kOwners * j;
         if (k < dim) {
-          if (ovalid) S.grad[cu * plane + static_cast<size_t>(k) * nch + ogc] = gk_of(k) - qown[j];
+          if (ovalid && writer) S.grad[cu * plane + static_cast<size_t>(k) * nch + ogc] = gk_of(k) - qown[j];
           pr += -0.5 * (kLog2Pi + qown[j] * qown[j]);
         }
       }
       sm.pri[ok][oc] = pr;
     }
     __syncthreads();
-    if (cvalid) {
+    if (cwrite) {
       const double lp = lp_from_partials(tid);
       S.lp0[gc] = lp;
       if (A.out_a) A.out_a[gc] = lp;
     }
+    csync();  // remote llq reads done before any rank exits
   } else {
     const double eps = M.step, half = 0.5 * M.step;
     const int n_lf = M.n_lf;
@@ -557,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
           const bool more = !last || it + 1 < A.n_iters;
           if (last) grad_pass32<true>(sm, M, gsc, P, ntiles, more);
           else grad_pass32<false>(sm, M, gsc, P, ntiles, more);
+          if (cs > 1) cooperative_groups::this_cluster().sync();  // every rank's G partials landed
           if (owner) {
             const double scale = last ? half : eps;
             const int cu = sm.cur[oc];
@@ -573,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
                 if (last) {
                   part += __ldg(M.inv_mass + k) * pown[j] * pown[j];
                   part2 += -0.5 * (kLog2Pi + qown[j] * qown[j]);
-                  if (ovalid) {
+                  if (ovalid && writer) {
                     const size_t gi = (cu ^ 1) * plane + static_cast<size_t>(k) * nch + ogc;
                     S.pos[gi] = qown[j];
                     S.grad[gi] = g;
@@ -591,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
             }
             if (bad) sm.bad[oc] = 1;
           }
-          __syncthreads();  // G scratch read by every owner before the next pass rewrites it
+          csync();  // G scratch read by every owner (every rank) before the next pass rewrites it
           if (!last) {
             put_theta();
             __syncthreads();
@@ -618,22 +653,22 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
               lp0 = lp1;
             }
           }
-          if (cvalid && A.mode == kModeProbe) {
+          if (cwrite && A.mode == kModeProbe) {
             A.out_a[gc] = h0;
             A.out_b[gc] = h1;
             A.out_flags[gc] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
           }
-          if (cvalid && A.mode == kModeChain) {
+          if (cwrite && A.mode == kModeChain) {
             const size_t row = static_cast<size_t>(it) * nch + gc;
             if (A.traj_div) A.traj_div[row] = (accepted ? 1 : 0) | (divergent ? 2 : 0);
             if (A.out_a) A.out_a[row] = h0;
             if (A.out_b) A.out_b[row] = h1;
           }
         }
-        __syncthreads();
+        csync();  // rank 0's proposal writes and every rank's llq reads before the next transition
         if (A.mode == kModeProbe) continue;
         if (A.mode == kModeChain) {
-          if (ovalid && A.traj) {
+          if (ovalid && writer && A.traj) {
             const int cu = sm.cur[oc];
 #pragma unroll
             for (int j = 0; j < kOwn; ++j) {
@@ -646,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
         }
       }
       // log_pred (FP64) at the current position + accumulators (engine.cpp:360-373)
-      if (cvalid) {
+      if (cwrite) {
         double sp = 0.0;
         if (fold < M.K) {
           const double* pos = S.pos + sm.cur[tid] * plane + gc;
@@ -670,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
       }
       if (A.mode == kModePred) break;
     }
-    if (cvalid && A.mode != kModePred) {
+    if (cwrite && A.mode != kModePred) {
       S.cur[gc] = static_cast<int8_t>(sm.cur[tid]);
       S.lp0[gc] = lp0;
       S.rng_pos[gc] = R.pos;
@@ -746,16 +781,56 @@ cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  static double* scratch = nullptr;
-  static int scratch_tiles = 0;
-  if (tiles > scratch_tiles) {
-    if (scratch) cudaFree(scratch);
-    cudaError_t e = cudaMalloc(&scratch, sizeof(double) * static_cast<size_t>(tiles) * kGN * kC);
-    if (e != cudaSuccess) return e;
-    scratch_tiles = tiles;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
   }
-  glm32_kernel<<<tiles, kThreads, sizeof(Smem32), st>>>(M, S, A, scratch);
-  return cudaGetLastError();
+  // Wave tail: one CTA per SM, so the last partial wave of r tiles would take a full wave time. It
+  // runs instead as row-split clusters of ct CTAs (same chains, summation split by rank).
+  const int ntiles_rows = (M.n + kRows - 1) / kRows;
+  static const bool no_split = std::getenv("PCVG_NO_TAIL_SPLIT") != nullptr;  // A/B tests only
+  int r = 0, ct = 1;
+  if (tiles > sms && tiles % sms != 0 && !no_split) {
+    r = tiles % sms;
+    while (ct < 8 && r * ct * 2 <= sms && ntiles_rows >= 4 * ct * 2) ct *= 2;
+    if (ct == 1) r = 0;
+  }
+  if (const char* e = std::getenv("PCVG_GLM32_CS")) {  // tests / tuning: every tile row-split
+    ct = std::max(1, std::atoi(e));
+    r = tiles;
+  }
+  const int grid_max = std::max(tiles - r, r * ct);
+  static double* scratch = nullptr;
+  static int scratch_ctas = 0;
+  if (grid_max > scratch_ctas) {  // one G scratch per CTA of a launch (launches are stream-ordered)
+    if (scratch) cudaFree(scratch);
+    cudaError_t e = cudaMalloc(&scratch, sizeof(double) * static_cast<size_t>(grid_max) * kGN * kC);
+    if (e != cudaSuccess) return e;
+    scratch_ctas = grid_max;
+  }
+  auto launch = [&](int tile0, int ntiles, int cs) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * cs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sizeof(Smem32);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = cs > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, glm32_kernel, M, S, A, scratch, cs, tile0);
+  };
+  if (tiles - r > 0) {
+    cudaError_t e = launch(0, tiles - r, 1);
+    if (e != cudaSuccess) return e;
+  }
+  if (r > 0) return launch(tiles - r, r, ct);
+  return cudaSuccess;
 }
 
 }  // namespace pcvg
