@@ -819,6 +819,9 @@ int glm_cluster_size(int n, int kp, int nch) {
   const int ntiles = (n + tm - 1) / tm;
   int cs = 1;
   while (cs < 16 && tiles * cs * 2 <= 148 && ntiles >= 4 * cs) cs *= 2;
+  // 16-CTA clusters only for the fewest tiles (cfg2 K-fold: 2, Step 1: 1): at most 7 fit at once,
+  // and two models' launches run concurrently (cfg4 under ROWS: 7 tiles stays at 8, 0.85M vs 0.61M)
+  if (cs == 16 && tiles * 16 > 64) cs = 8;
   return cs;
 }
 
