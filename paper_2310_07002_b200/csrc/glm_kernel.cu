@@ -352,31 +352,65 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
 }
 
 // Sums the staged partials (G in sm.rs, residual statistic in sm.llp) over the CS CTAs of the
-// cluster in rank order into sm.gt / sm.lt (CS = 1: a local copy, same bits).
+// cluster into sm.gt / sm.lt. CS = 1: a local copy (same bits). CS > 1: rank o reduces the o-th
+// slice of the KP x 64 + 64 elements - cs lanes load one element from the cs ranks at once and
+// xor-butterfly it (a fixed order) - then every rank copies the other slices from their owners, so
+// all ranks hold identical bits. Every remote load of a step is independent (a rank-ordered
+// dependent chain cost ~cs DSMEM latencies per element: ~40% of a pass at cs = 16, cfg2 K-fold).
 template <int KP>
 __device__ void reduce_pass(Smem<KP>& sm, int cs) {
   namespace cgr = cooperative_groups;
   const int tid = threadIdx.x;
-  if (cs > 1) cgr::this_cluster().sync();
-  for (int i = tid; i < KP * kC; i += kThreads) {
-    const int k = i / kC, c = i % kC;
-    double s = 0.0;
-    for (int r = 0; r < cs; ++r) {
-      const Smem<KP>* rem = cs > 1 ? cgr::this_cluster().map_shared_rank(&sm, r) : &sm;
-      s += rem->rs[k * kLdS + c];
+  constexpr int kE = KP * kC + kC;  // G elements, then the residual statistic per chain
+  if (cs == 1) {
+    for (int i = tid; i < KP * kC; i += kThreads) {
+      const int k = i / kC, c = i % kC;
+      sm.gt[k * kLdS + c] = sm.rs[k * kLdS + c];
     }
-    sm.gt[k * kLdS + c] = s;
+    if (tid < kC) sm.lt[tid] = (sm.llp[0][tid] + sm.llp[1][tid]) + (sm.llp[2][tid] + sm.llp[3][tid]);
+    __syncthreads();
+    return;
   }
-  if (tid < kC) {
-    double s = 0.0;
-    for (int r = 0; r < cs; ++r) {
-      const Smem<KP>* rem = cs > 1 ? cgr::this_cluster().map_shared_rank(&sm, r) : &sm;
-      s += (rem->llp[0][tid] + rem->llp[1][tid]) + (rem->llp[2][tid] + rem->llp[3][tid]);
+  cgr::cluster_group cl = cgr::this_cluster();
+  const int me = static_cast<int>(cl.block_rank());
+  const int slice = (kE + cs - 1) / cs;
+  cl.sync();  // every rank's partials staged
+  {
+    const int q = tid % cs;  // the rank this lane loads from
+    const Smem<KP>* rq = cl.map_shared_rank(&sm, q);
+    const int per = kThreads / cs;  // elements per sweep
+    for (int e0 = 0; e0 < slice; e0 += per) {
+      const int el = e0 + tid / cs, e = me * slice + el;
+      const bool ok = el < slice && e < kE;
+      double v = 0.0;
+      if (ok) {
+        if (e < KP * kC) {
+          v = rq->rs[(e / kC) * kLdS + e % kC];
+        } else {
+          const int c = e - KP * kC;
+          v = (rq->llp[0][c] + rq->llp[1][c]) + (rq->llp[2][c] + rq->llp[3][c]);
+        }
+      }
+      for (int off = cs / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (ok && q == 0) {
+        if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = v;
+        else sm.lt[e - KP * kC] = v;
+      }
     }
-    sm.lt[tid] = s;
   }
-  if (cs > 1) cgr::this_cluster().sync();  // remote reads done before rs / llp are reused
-  else __syncthreads();
+  cl.sync();  // every slice reduced (and every partial read: rs / llp may be reused)
+  for (int e = tid; e < kE; e += kThreads) {
+    const int o = e / slice;
+    if (o == me) continue;
+    const Smem<KP>* ro = cl.map_shared_rank(&sm, o);
+    if (e < KP * kC) {
+      const int i = (e / kC) * kLdS + e % kC;
+      sm.gt[i] = ro->gt[i];
+    } else {
+      sm.lt[e - KP * kC] = ro->lt[e - KP * kC];
+    }
+  }
+  __syncthreads();  // the copied slices are read by the owner threads next
 }
 
 __device__ __forceinline__ double bernoulli_logit(double y, double x) {
