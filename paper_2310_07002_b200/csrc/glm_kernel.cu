@@ -77,6 +77,7 @@ struct Smem {
   int lo[kC], hi[kC], ntr[kC];
   int bad[kC];
   int cur[kC];
+  int fold[kC];                           // the chain's fold (K for padding chains)
   unsigned long long full[kStages];
   unsigned int rel[kStages];  // warps done with each ring slot (monotonic; last arrival refills)
 };
@@ -197,6 +198,21 @@ __device__ __forceinline__ void issue_tile(Smem<KP>& sm, const ModelDev& M, int 
   bulk_g2s(sm.ks[slot], M.key + static_cast<size_t>(t) * G::TM, G::TM * 4, &sm.full[slot]);
 }
 
+#ifdef PCVG_GLM_TRACE
+// Timeline probe (tools only): clock64 stamps of CTA 0, thread 0 for the passes of its first
+// transition, printed at the end of the launch.
+__device__ long long g_gtrace[64][5];
+__device__ int g_gpass;
+#define GTRACE(i)                                                                          \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_gpass < 64) g_gtrace[g_gpass][(i)] = clock64(); \
+  } while (0)
+#else
+#define GTRACE(i) \
+  do {            \
+  } while (0)
+#endif
+
 // One pass over all observations for the 64 chains with weights sm.ws: G = X^T R into sm.rs as
 // [col][chain]; the per-chain residual statistic (logistic: log-likelihood when VALUE; Gaussian:
 // sum of squared training residuals, every pass) into sm.llp[quarter][chain].
@@ -313,6 +329,7 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
     }
   }
   gtile = g0 + ntiles;
+  GTRACE(1);
   __syncthreads();
   // Stage G [col][chain] into sm.rs: quarter 0 stores, quarters 1..3 add in order.
 #pragma unroll 1
@@ -496,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
       sm.hi[tid] = M.fold_hi[fold];
       sm.ntr[tid] = M.n_train[fold];
       sm.cur[tid] = S.cur[gc];
+      sm.fold[tid] = fold;
       lp0 = S.lp0[gc];
       R.init(S.seed, S.rng_stream[gc], S.rng_pos[gc], S.rng_cached[gc], S.rng_has[gc] != 0);
     } else {
@@ -503,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
       sm.hi[tid] = 0;
       sm.ntr[tid] = M.n;
       sm.cur[tid] = 0;
+      sm.fold[tid] = M.K;
     }
   }
   __syncthreads();
@@ -600,9 +619,12 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
       // -- leapfrog: n_lf gradient passes
       for (int s = 0; s < n_lf; ++s) {
         const bool last = s == n_lf - 1;
+        GTRACE(0);
         if (last) grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
         else grad_pass<FAM, KP, false>(sm, M, gtile, t0, t1);
+        GTRACE(2);
         reduce_pass(sm, cs);
+        GTRACE(3);
         const double scale = last ? half : eps;
         const int cu = sm.cur[oc];
         bool bad = false;
@@ -650,6 +672,10 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
         }
         if (bad) sm.bad[oc] = 1;
         __syncthreads();
+        GTRACE(4);
+#ifdef PCVG_GLM_TRACE
+        if (blockIdx.x == 0 && threadIdx.x == 0) ++g_gpass;
+#endif
       }
       // -- energies, Metropolis (chain thread)
       if (is_chain) {
@@ -702,34 +728,51 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
         continue;
       }
     }
-    // -- log_pred at the current position + accumulators (chain thread of rank 0)
-    if (cvalid && writer) {
-      double sp = 0.0;
-      if (fold < M.K) {
-        const int cu = sm.cur[tid];
-        const double* pos = S.pos + cu * plane + gc;
+    // -- log_pred at the current position (rank 0): the 8 owner threads of a chain split its fold's
+    //    test rows (K-fold: 1,000 rows at cfg2) with the position staged [k][chain] in sm.rs; the
+    //    chain thread adds the owner partials in owner order and updates the accumulators
+    if (writer) {
+      const int cu = sm.cur[oc];
+#pragma unroll
+      for (int j = 0; j < G::OWN; ++j) {
+        const int k = ok + kOwners * j;
+        if (k < dim) sm.rs[k * kLdS + oc] = ovalid ? S.pos[cu * plane + static_cast<size_t>(k) * nch + ogc] : 0.0;
+      }
+    }
+    __syncthreads();
+    {
+      double part = 0.0;
+      const int ofold = sm.fold[oc];
+      if (writer && ovalid && ofold < M.K) {
+        const double* th = sm.rs + oc;
         double v_pred = 1.0;
         if constexpr (FAM == kGrouped) {
-          const double sy = exp(pos[static_cast<size_t>(M.nc + 3) * nch]);
+          const double sy = exp(th[(M.nc + 3) * kLdS]);
           v_pred = sy * sy;  // grouped_regression.cpp:240-241
         } else if constexpr (FAM == kSeasonal) {
-          v_pred = exp(2.0 * pos[static_cast<size_t>(M.p + M.q + 1) * nch]);  // seasonal_ar.cpp:110
+          v_pred = exp(2.0 * th[(M.p + M.q + 1) * kLdS]);  // seasonal_ar.cpp:110
         }
-        const int s0 = M.fold_seg[fold], s1 = M.fold_seg[fold + 1];
-        for (int s = s0; s < s1; ++s) {
-          for (int tt = M.seg_row[s]; tt < M.seg_row[s + 1]; ++tt) {
-            const int i = M.seg_rows[tt];
-            const double* xrow = M.xr + static_cast<size_t>(i) * KP;
-            double eta = 0.0;
-            for (int k = 0; k < dim; ++k) {
-              const int col = col_of<FAM>(M, k);
-              if (col >= 0) eta = fma(xrow[col], w_of<FAM>(M, k, pos[static_cast<size_t>(k) * nch]), eta);
-            }
-            if constexpr (FAM == kLogistic) sp += bernoulli_logit(M.y[i], eta);
-            else sp += normal_logpdf(M.y[i], eta, v_pred);
+        const int s0 = M.fold_seg[ofold], s1 = M.fold_seg[ofold + 1];
+        const int r0 = M.seg_row[s0], r1 = M.seg_row[s1];  // the fold's test rows, contiguous
+        for (int tt = r0 + ok; tt < r1; tt += kOwners) {
+          const int i = M.seg_rows[tt];
+          const double* xrow = M.xr + static_cast<size_t>(i) * KP;
+          double eta = 0.0;
+          for (int k = 0; k < dim; ++k) {
+            const int col = col_of<FAM>(M, k);
+            if (col >= 0) eta = fma(xrow[col], w_of<FAM>(M, k, th[k * kLdS]), eta);
           }
+          if constexpr (FAM == kLogistic) part += bernoulli_logit(M.y[i], eta);
+          else part += normal_logpdf(M.y[i], eta, v_pred);
         }
       }
+      sm.red[ok][oc] = part;
+    }
+    __syncthreads();
+    if (cvalid && writer) {
+      double sp = 0.0;
+#pragma unroll
+      for (int o = 0; o < kOwners; ++o) sp += sm.red[o][tid];
       if (A.mode == kModePred) {
         if (A.out_a) A.out_a[gc] = sp;
       } else if (A.mode == kModeWarmup) {
@@ -745,6 +788,16 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
     }
     if (A.mode == kModePred) break;
   }
+#ifdef PCVG_GLM_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_gpass >= 32 && g_gpass < 96) {
+    printf("pass: start tiles_done staged reduced owners_done (cycles from pass start), cs=%d\n", cs);
+    for (int p = 0; p < 32 && p < 64; ++p)
+      printf("%2d: %lld %lld %lld %lld | next start +%lld\n", p, g_gtrace[p][1] - g_gtrace[p][0],
+             g_gtrace[p][2] - g_gtrace[p][0], g_gtrace[p][3] - g_gtrace[p][0], g_gtrace[p][4] - g_gtrace[p][0],
+             p + 1 < 32 ? g_gtrace[p + 1][0] - g_gtrace[p][0] : 0LL);
+    g_gpass = 1000;
+  }
+#endif
   if (cvalid && writer && A.mode != kModePred) {
     S.cur[gc] = static_cast<int8_t>(sm.cur[tid]);
     S.lp0[gc] = lp0;
