@@ -396,35 +396,52 @@ __device__ void reduce_pass(Smem<KP>& sm, int cs) {
     const int q = tid % cs;  // the rank this lane loads from
     const Smem<KP>* rq = cl.map_shared_rank(&sm, q);
     const int per = kThreads / cs;  // elements per sweep
-    for (int e0 = 0; e0 < slice; e0 += per) {
-      const int el = e0 + tid / cs, e = me * slice + el;
-      const bool ok = el < slice && e < kE;
-      double v = 0.0;
-      if (ok) {
-        if (e < KP * kC) {
-          v = rq->rs[(e / kC) * kLdS + e % kC];
-        } else {
-          const int c = e - KP * kC;
-          v = (rq->llp[0][c] + rq->llp[1][c]) + (rq->llp[2][c] + rq->llp[3][c]);
+    constexpr int kSw = 4;           // sweeps whose remote loads are in flight together
+    for (int e00 = 0; e00 < slice; e00 += kSw * per) {
+      double v[kSw];
+#pragma unroll
+      for (int w = 0; w < kSw; ++w) {
+        const int el = e00 + w * per + tid / cs, e = me * slice + el;
+        v[w] = 0.0;
+        if (el < slice && e < kE) {
+          if (e < KP * kC) {
+            v[w] = rq->rs[(e / kC) * kLdS + e % kC];
+          } else {
+            const int c = e - KP * kC;
+            v[w] = (rq->llp[0][c] + rq->llp[1][c]) + (rq->llp[2][c] + rq->llp[3][c]);
+          }
         }
       }
-      for (int off = cs / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (ok && q == 0) {
-        if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = v;
-        else sm.lt[e - KP * kC] = v;
+#pragma unroll
+      for (int w = 0; w < kSw; ++w) {
+        const int el = e00 + w * per + tid / cs, e = me * slice + el;
+        double x = v[w];
+        for (int off = cs / 2; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        if (el < slice && e < kE && q == 0) {
+          if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = x;
+          else sm.lt[e - KP * kC] = x;
+        }
       }
     }
   }
   cl.sync();  // every slice reduced (and every partial read: rs / llp may be reused)
-  for (int e = tid; e < kE; e += kThreads) {
-    const int o = e / slice;
-    if (o == me) continue;
-    const Smem<KP>* ro = cl.map_shared_rank(&sm, o);
-    if (e < KP * kC) {
-      const int i = (e / kC) * kLdS + e % kC;
-      sm.gt[i] = ro->gt[i];
-    } else {
-      sm.lt[e - KP * kC] = ro->lt[e - KP * kC];
+  constexpr int kPer = (kE + kThreads - 1) / kThreads;  // elements per thread, loads batched
+  double v[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = tid + j * kThreads;
+    v[j] = 0.0;
+    if (e < kE && e / slice != me) {
+      const Smem<KP>* ro = cl.map_shared_rank(&sm, e / slice);
+      v[j] = e < KP * kC ? ro->gt[(e / kC) * kLdS + e % kC] : ro->lt[e - KP * kC];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = tid + j * kThreads;
+    if (e < kE && e / slice != me) {
+      if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = v[j];
+      else sm.lt[e - KP * kC] = v[j];
     }
   }
   __syncthreads();  // the copied slices are read by the owner threads next
