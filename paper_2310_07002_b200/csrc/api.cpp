@@ -125,7 +125,7 @@ struct HostModel {
   DevBuf<double> yb, xb;         // group-batched layout (ModelDev::nb > 0)
   DevBuf<unsigned char> x32;     // logistic FP32 variant tile images
   DevBuf<int> keyb, bgroup, boff, tfirst, tr0, trows, bkey, bgrows, buni;
-  DevBuf<double> sA, sgn, sgs, sov_n, sov_s;  // fold sufficient statistics (suffstats.cpp)
+  DevBuf<double> sA, sgn, sgs, sov_n, sov_s, sgA, sov_A;  // fold sufficient statistics (suffstats.cpp)
   DevBuf<int> sov_ptr, sov_g, sex_lo, sex_hi, sex_rows, sex_grp;
   int64_t bank_rows = 0;
   ModelDev md{};
@@ -505,10 +505,11 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   // fold sufficient statistics for the Gaussian linear families (suffstats.cpp)
   int suff = 0;
   SuffStats ss;
+  const bool per_subject = s->family == PCVG_FAMILY_RAT_GROWTH && s->per_subject_slope;
   if ((s->family == PCVG_FAMILY_GROUPED || s->family == PCVG_FAMILY_RADON || s->family == PCVG_FAMILY_SEASONAL_AR ||
-       (s->family == PCVG_FAMILY_RAT_GROWTH && !s->per_subject_slope)) &&
+       s->family == PCVG_FAMILY_RAT_GROWTH) &&
       build_suffstats(n, m.nc, m.J, y.data(), xc.data(), key.data(), hier ? grp_ptr.data() : nullptr, m.K,
-                      lo.data(), hi.data(), ss)) {
+                      lo.data(), hi.data(), ss, per_subject)) {
     suff = 1;
     m.sA.upload(ss.A);
     m.sgn.upload(ss.gn);
@@ -521,6 +522,10 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
     m.sex_hi.upload(ss.ex_hi);
     m.sex_rows.upload(ss.ex_rows);
     m.sex_grp.upload(ss.ex_grp);
+    if (per_subject) {
+      m.sgA.upload(ss.gA);
+      m.sov_A.upload(ss.ov_A);
+    }
   }
 
   // test segments (fold_meta_, grouped_regression.cpp:27-47): test rows grouped by group in
@@ -673,6 +678,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.sex_hi = m.sex_hi.p;
   md.sex_rows = m.sex_rows.p;
   md.sex_grp = m.sex_grp.p;
+  md.sgA = m.sgA.p;
+  md.sov_A = m.sov_A.p;
   return hm;
 }
 

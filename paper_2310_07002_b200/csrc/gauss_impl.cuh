@@ -409,6 +409,18 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
   __syncwarp(mask);  // group-dim stores of lane 0 become visible to the chain's lanes
 }
 
+// Position + momentum slot arrays per group parameter kind (rat M_A: intercepts and slopes).
+__host__ __device__ inline int suff_slot_arrays(const ModelDev& M) { return M.family == kRatA ? 4 : 2; }
+
+// Shared-memory group slots of the sufficient-statistics kernel (position + momentum per owned
+// group, [slot][kBlock] doubles each): warp-per-chain launches of hierarchical models whose slots
+// fit; 0 = the group state goes through the HBM planes.
+__host__ __device__ inline int suff_slots(const ModelDev& M, int T) {
+  if (T != 32 || M.J < 2) return 0;
+  const int ns = (M.J + 31) / 32;
+  return suff_slot_arrays(M) * ns * kBlock * 8 <= 96 * 1024 ? ns : 0;
+}
+
 // grad_pass on the fold's sufficient statistics (suffstats.cpp; NB < 0): the same masked sums
 // S_r[g], S_xr, S_rr as the row loop, from the packed training Gram A_k and the group sums s_g, in
 // O(d^2 + J d) instead of O(n d) per pass. u = (y, x), om = (1, -w):
@@ -420,6 +432,10 @@ __device__ __forceinline__ void grad_pass(const ModelDev& M, const ChainsDev& S,
 // passes of a transition (slot j of group t + 32 j at qs[j * kBlock]); the planes are written in
 // the last pass only. The value pass also evaluates the fold's excluded rows for the reference's
 // poisoning of a non-finite masked term (grouped_regression.cpp:74-76).
+// Rat growth M_A (per-subject slope beta_g, rat_growth.cpp:117-147): every sum is per subject,
+// from the subject's (y, t) Gram (sgA / sov_A) and sums: om_g = (1, -beta_g),
+//   S_r[g] = om_g.s_g - n_g alpha_g, S_tr[g] = (A_g om_g)[1] - alpha_g s_g[1],
+//   S_rr = sum_g om_g^T A_g om_g - alpha_g (om_g.s_g + S_r[g]).
 template <int FAM, int T, int NCM, int NGM, bool VALUE>
 __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S, int c, int t, unsigned mask,
                                           int fold, int n_train, const double* qG, int kind, bool last,
@@ -442,7 +458,7 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
   for (int i = 0; i < D; ++i) q[i] = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
-    if (i < d) {
+    if (FAM != kRatA && i < d) {
 #pragma unroll
       for (int j = 0; j <= i; ++j) {
         const int e = i * (i + 1) / 2 + j;
@@ -457,8 +473,12 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
   double sv[D];  // this lane's sum_g off_g s_g
 #pragma unroll
   for (int i = 0; i < D; ++i) sv[i] = 0.0;
-  double t2 = 0.0, sr_tot = 0.0, dk0 = 0.0, dk1 = 0.0;
+  double t2 = 0.0, sr_tot = 0.0, dk0 = 0.0, dk1 = 0.0, srr_a = 0.0;
   GroupAcc G{0.0, 0.0, 0.0, 0.0};
+  // rat M_A: slope slots after the intercept slots
+  const int ns_a = FAM == kRatA && qs ? suff_slots(M, T) : 0;
+  double* qs2 = qs ? qs + 2 * static_cast<size_t>(ns_a) * kBlock : nullptr;
+  double* ps2 = qs ? qs + 3 * static_cast<size_t>(ns_a) * kBlock : nullptr;
   const int ov0 = __ldg(M.sov_ptr + fold), ov_end = __ldg(M.sov_ptr + fold + 1);
   int ov = ov0;
   const int ngroups = M.J > 0 ? M.J : 1;
@@ -488,12 +508,84 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
     while (ov < ov_end && __ldg(M.sov_g + ov) < g) ++ov;
     double ng;
     const double* sp;
+    const double* Ag = nullptr;  // rat M_A: the subject's (y, t) Gram
     if (ov < ov_end && __ldg(M.sov_g + ov) == g) {
       ng = __ldg(M.sov_n + ov);
       sp = M.sov_s + static_cast<size_t>(ov) * d;
+      if constexpr (FAM == kRatA) Ag = M.sov_A + static_cast<size_t>(ov) * 3;
     } else {
       ng = __ldg(M.sgn + g);
       sp = M.sgs + static_cast<size_t>(g) * d;
+      if constexpr (FAM == kRatA) Ag = M.sgA + static_cast<size_t>(g) * 3;
+    }
+    if constexpr (FAM == kRatA) {  // per-subject slope beta_g (dim J + g), its own slots
+      const int gs = M.J + g;
+      const size_t si = static_cast<size_t>(gs) * nch + c;
+      const double ms = __ldg(M.inv_mass + gs);
+      double qb = 0.0, pb = 0.0;
+      if (kind == 0) {
+        qb = S.pos[cur * plane + si];
+      } else if (kind == 1) {
+        const double p0 = probe_p ? probe_p[static_cast<size_t>(c) * M.dim + gs] : nc.at(R, gs) / sqrt(ms);
+        dk0 += ms * p0 * p0;
+        pb = p0 + half * S.grad[cur * plane + si];
+        qb = S.pos[cur * plane + si] + eps * ms * pb;
+      } else if (qs) {
+        pb = ps2[jj * kBlock];
+        qb = qs2[jj * kBlock] + eps * ms * pb;
+      } else {
+        pb = S.wp[si];
+        qb = S.pos[(cur ^ 1) * plane + si] + eps * ms * pb;
+      }
+      bad |= !isfinite(qb);
+      const double sy = __ldg(sp), st = __ldg(sp + 1);
+      const double ayy = __ldg(Ag), aty = __ldg(Ag + 1), att = __ldg(Ag + 2);
+      const double ws = fma(-qb, st, sy);
+      const double srg = fma(-ng, qg, ws);
+      const double str = fma(-qb, att, aty) - qg * st;  // sum t r
+      srr_a += (ayy - 2.0 * qb * aty + qb * qb * att) - qg * (ws + srg);
+      const double db = qb - qG[1];  // beta_g - mu_b
+      G.a2 += db / P.vb;
+      G.a3 += db * db;
+      const double gsl = dv<true>(str, P.v, P.inv_v) - db / P.vb;  // rat_growth.cpp:127-137
+      bad |= !isfinite(gsl);
+      if (kind == 0) {
+        S.grad[cur * plane + si] = gsl;
+      } else {
+        pb += scale * gsl;
+        bad |= !isfinite(pb);
+        if (qs && !last) {
+          qs2[jj * kBlock] = qb;
+          ps2[jj * kBlock] = pb;
+        } else {
+          S.pos[(cur ^ 1) * plane + si] = qb;
+          S.wp[si] = pb;
+        }
+        if (last) {
+          S.grad[(cur ^ 1) * plane + si] = gsl;
+          dk1 += ms * pb * pb;
+        }
+      }
+      const double gg = group_grad<FAM, NCM, NGM, true>(P, qG, M, qg, srg, G);  // alpha_g
+      bad |= !isfinite(gg);
+      if (kind == 0) {
+        S.grad[cur * plane + gi] = gg;
+      } else {
+        pg += scale * gg;
+        bad |= !isfinite(pg);
+        if (qs && !last) {
+          qs[jj * kBlock] = qg;
+          ps[jj * kBlock] = pg;
+        } else {
+          S.pos[(cur ^ 1) * plane + gi] = qg;
+          S.wp[gi] = pg;
+        }
+        if (last) {
+          S.grad[(cur ^ 1) * plane + gi] = gg;
+          dk1 += __ldg(M.inv_mass + g) * pg * pg;
+        }
+      }
+      continue;
     }
     double ws = 0.0;
 #pragma unroll
@@ -535,7 +627,7 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
 #pragma unroll
   for (int i = 0; i < D; ++i) quad = fma(PCVG_OM(i), q[i], quad);
 #undef PCVG_OM
-  double srr = quad - t2;
+  double srr = FAM == kRatA ? srr_a : quad - t2;
   double* sxr = q + 1;  // S_xr[k] = q[1 + k] - sv[1 + k], in place
 #pragma unroll
   for (int k = 0; k < NCM; ++k) sxr[k] -= sv[1 + k];
@@ -549,7 +641,8 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
     } else {
       G.a0 = lane_sum<T>(G.a0, mask);
       G.a1 = lane_sum<T>(G.a1, mask);
-      if constexpr (FAM == kRadon) G.a2 = lane_sum<T>(G.a2, mask);
+      if constexpr (FAM == kRadon || FAM == kRatA) G.a2 = lane_sum<T>(G.a2, mask);
+      if constexpr (FAM == kRatA) G.a3 = lane_sum<T>(G.a3, mask);
       if (kind == 1) dk0 = lane_sum<T>(dk0, mask);
       if (last) dk1 = lane_sum<T>(dk1, mask);
     }
@@ -568,9 +661,14 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
         off = group_offset<FAM, NCM>(P, S.pos[(kind == 0 ? cur : cur ^ 1) * plane + gi]);
       }
       double m = off;
+      if constexpr (FAM == kRatA) {  // the subject's own slope
+        const size_t si = static_cast<size_t>(M.J + __ldg(M.sex_grp + tt)) * nch + c;
+        m = fma(S.pos[(kind == 0 ? cur : cur ^ 1) * plane + si], __ldg(M.x + i), off);
+      } else {
 #pragma unroll
-      for (int k = 0; k < NCM; ++k)
-        if (k < M.nc) m = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), m);
+        for (int k = 0; k < NCM; ++k)
+          if (k < M.nc) m = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), m);
+      }
       const double r = __ldg(M.y + i) - m;
       poison |= !isfinite(P.logv + r * r * P.inv_v);
     }
@@ -582,14 +680,6 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
   if constexpr (T > 1) __syncwarp(mask);
 }
 
-// Shared-memory group slots of the sufficient-statistics kernel (position + momentum per owned
-// group, [slot][kBlock] doubles each): warp-per-chain launches of hierarchical models whose slots
-// fit; 0 = the group state goes through the HBM planes.
-__host__ __device__ inline int suff_slots(const ModelDev& M, int T) {
-  if (T != 32 || M.J < 2) return 0;
-  const int ns = (M.J + 31) / 32;
-  return 2 * ns * kBlock * 8 <= 96 * 1024 ? ns : 0;
-}
 
 // Row-tile ring of the group-batched kernel: the CTA's warps (one chain each) share one staged copy
 // of every batch row tile. Tile g of the launch's sequence (pass-major, M.ntile tiles per pass)
@@ -1259,7 +1349,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : (NB == -2 ? 4 : 1)) gauss
           for (int i = 0; i < NGM; ++i)
             if (i < ng) A.traj[static_cast<size_t>(c) * M.dim + M.goff + gidx<FAM>(M, i)] = pG[i];
           if constexpr (NB <= 0)
-            for (int g = 0; g < J; ++g) A.traj[static_cast<size_t>(c) * M.dim + g] = S.wp[static_cast<size_t>(g) * nch + c];
+            for (int g = 0; g < M.goff; ++g) A.traj[static_cast<size_t>(c) * M.dim + g] = S.wp[static_cast<size_t>(g) * nch + c];
         }
       }
       continue;

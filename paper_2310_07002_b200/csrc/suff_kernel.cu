@@ -14,7 +14,7 @@ template <int FAM, int NCM, int NGM, int T, int NB = -1>
 cudaError_t launch_suff_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
   const int grid = (S.nch + kBlock / T - 1) / (kBlock / T);
   if (grid == 0) return cudaSuccess;
-  const size_t smem = static_cast<size_t>(suff_slots(M, T)) * 2 * kBlock * sizeof(double);
+  const size_t smem = static_cast<size_t>(suff_slots(M, T)) * suff_slot_arrays(M) * kBlock * sizeof(double);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, T, NCM, NGM, NB>,
@@ -77,6 +77,8 @@ cudaError_t launch_suff_family(const ModelDev& M, const ChainsDev& S, const RunA
       return launch_suff<kRadon, 1, 4>(M, S, A, T, st);
     case kRatB:  // rat growth with a shared slope: m = alpha_g + beta t (rat_growth.cpp:148-172)
       return launch_suff<kRatB, 1, 4>(M, S, A, T, st);
+    case kRatA:  // per-subject slopes: per-subject (y, t) Gram (rat_growth.cpp:117-147)
+      return launch_suff<kRatA, 1, 5>(M, S, A, T, st);
     case kSeasonal:
       if (M.nc > 13) return cudaErrorInvalidValue;
       return launch_suff<kSeasonal, 13, 15>(M, S, A, T, st);

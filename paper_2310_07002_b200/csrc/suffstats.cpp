@@ -53,8 +53,11 @@ inline double dd_val(const DD& x) { return x.hi + x.lo; }
 // J = 0 (one pseudo-group holding every row); fold k holds out rows with lo[k] <= key < hi[k].
 // Returns false (no statistics) when a data value or a Gram entry is non-finite: full - excluded
 // would not give the reference's per-row masking then.
+// group_gram: also the per-group Gram of u (the per-subject-slope growth model, whose sums are all
+// per subject).
 bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc, const int* key,
-                     const int* grp_ptr, int K, const int* lo, const int* hi, SuffStats& S) {
+                     const int* grp_ptr, int K, const int* lo, const int* hi, SuffStats& S,
+                     bool group_gram) {
   const int d = nc + 1, dp = d * (d + 1) / 2, Jg = J > 0 ? J : 1;
   for (int64_t i = 0; i < n; ++i) {
     if (!std::isfinite(y[i])) return false;
@@ -70,12 +73,16 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
   auto u = [&](int64_t r, int i) { return i == 0 ? y[r] : xc[static_cast<size_t>(i - 1) * n + r]; };
 
   // full-data statistics
-  std::vector<DD> Af(dp), gsf(static_cast<size_t>(Jg) * d);
+  std::vector<DD> Af(dp), gsf(static_cast<size_t>(Jg) * d), gAf(group_gram ? static_cast<size_t>(Jg) * dp : 0);
   std::vector<int64_t> gnf(Jg, 0);
   for (int64_t r = 0; r < n; ++r) {
     for (int i = 0; i < d; ++i)
       for (int j = 0; j <= i; ++j) dd_add_prod(Af[i * (i + 1) / 2 + j], u(r, i), u(r, j), 1.0);
     const int g = grp[r];
+    if (group_gram)
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j <= i; ++j)
+          dd_add_prod(gAf[static_cast<size_t>(g) * dp + i * (i + 1) / 2 + j], u(r, i), u(r, j), 1.0);
     ++gnf[g];
     for (int i = 0; i < d; ++i) dd_add(gsf[static_cast<size_t>(g) * d + i], u(r, i), 0.0);
   }
@@ -87,6 +94,8 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
     S.gn[g] = static_cast<double>(gnf[g]);
     for (int i = 0; i < d; ++i) S.gs[static_cast<size_t>(g) * d + i] = dd_val(gsf[static_cast<size_t>(g) * d + i]);
   }
+  S.gA.resize(gAf.size());
+  for (size_t i = 0; i < gAf.size(); ++i) S.gA[i] = dd_val(gAf[i]);
 
   // rows in key order: a fold's excluded rows are one contiguous run
   S.ex_rows.resize(n);
@@ -102,7 +111,7 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
   S.ex_hi.assign(K + 1, 0);
   S.A.resize(static_cast<size_t>(K + 1) * dp);
   S.ov_ptr.assign(K + 2, 0);
-  std::vector<DD> Ak(dp), gsk(static_cast<size_t>(Jg) * d);
+  std::vector<DD> Ak(dp), gsk(static_cast<size_t>(Jg) * d), gAk(gAf.size());
   std::vector<int64_t> gnk(Jg, 0);
   std::vector<int> touched;
   for (int k = 0; k <= K; ++k) {
@@ -123,9 +132,15 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
       if (gnk[g] == 0) {
         touched.push_back(g);
         for (int i = 0; i < d; ++i) gsk[static_cast<size_t>(g) * d + i] = gsf[static_cast<size_t>(g) * d + i];
+        if (group_gram)
+          for (int e = 0; e < dp; ++e) gAk[static_cast<size_t>(g) * dp + e] = gAf[static_cast<size_t>(g) * dp + e];
       }
       ++gnk[g];
       for (int i = 0; i < d; ++i) dd_add(gsk[static_cast<size_t>(g) * d + i], -u(r, i), 0.0);
+      if (group_gram)
+        for (int i = 0; i < d; ++i)
+          for (int j = 0; j <= i; ++j)
+            dd_add_prod(gAk[static_cast<size_t>(g) * dp + i * (i + 1) / 2 + j], u(r, i), u(r, j), -1.0);
     }
     for (int i = 0; i < dp; ++i) S.A[static_cast<size_t>(k) * dp + i] = dd_val(Ak[i]);
     std::sort(touched.begin(), touched.end());
@@ -134,6 +149,8 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
       S.ov_g.push_back(g);
       S.ov_n.push_back(static_cast<double>(ntr));
       for (int i = 0; i < d; ++i) S.ov_s.push_back(ntr == 0 ? 0.0 : dd_val(gsk[static_cast<size_t>(g) * d + i]));
+      if (group_gram)
+        for (int e = 0; e < dp; ++e) S.ov_A.push_back(ntr == 0 ? 0.0 : dd_val(gAk[static_cast<size_t>(g) * dp + e]));
       gnk[g] = 0;
     }
   }
@@ -142,6 +159,7 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
     S.ov_g.push_back(-1);
     S.ov_n.push_back(0.0);
     S.ov_s.assign(d, 0.0);
+    if (group_gram) S.ov_A.assign(dp, 0.0);
   }
   return true;
 }

@@ -99,6 +99,8 @@ struct ModelDev {
   const int* sex_hi;
   const int* sex_rows;
   const int* sex_grp;
+  const double* sgA;    // rat M_A: [J][3] full-data per-group (y, t) Gram (yy, ty, tt)
+  const double* sov_A;  // rat M_A: [nov][3] the fold's override Grams
 };
 
 constexpr int kMaxBatches = 16;

@@ -34,8 +34,6 @@ def scale(th):
 @pytest.mark.parametrize("scheme", ["logo", "kfold", "loo"])
 @pytest.mark.parametrize("family", [abi.FAMILY_GROUPED, abi.FAMILY_RADON, abi.FAMILY_RAT_GROWTH])
 def test_ragged_groups_and_row_keys(scheme, family, policy):
-    if family == abi.FAMILY_RAT_GROWTH and policy == pcv.Context.KERNEL_SUFFSTAT:
-        pytest.skip("the growth model has no sufficient-statistics path")
     d = ragged_grouped()
     if family == abi.FAMILY_RADON:
         d = pcv.Dataset(d.y, (d.x[:, :1] > 0).astype(float), d.group_id)

@@ -46,7 +46,7 @@ def case_in(ctx, name):
 
 # Gaussian linear fixtures that also run on fold sufficient statistics (policy SUFFSTAT)
 SUFF_KERNEL = {"cfg1_linreg_loo", "ex1_grouped_logo", "radon_logo", "seasonal_timeblocks", "seasonal_hvblock",
-               "rat_logo"}  # rat: the shared-slope model M_B (M_A keeps the batched kernel)
+               "rat_logo"}  # rat: M_B (shared slope) and M_A (per-subject slopes, per-subject Grams)
 
 
 def with_kernels(names):
