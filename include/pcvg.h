@@ -216,7 +216,7 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
 pcvg_status pcvg_model_dim(const pcvg_ctx* ctx, int32_t slot, int32_t* dim);
 
 /* Kernel selection. AUTO runs the Gaussian linear families (grouped, radon-style, seasonal AR, rat
- * growth with a shared slope) on fold sufficient statistics (SUFFSTAT below) when their data are finite. Otherwise, and always
+ * growth) on fold sufficient statistics (SUFFSTAT below) when their data are finite. Otherwise, and always
  * under ROWS, the kernels stream the design matrix: the FP64 tensor-core GLM kernel for predictors
  * without group effects when enough chains (or a row-split cluster) fill the GPU, the
  * group-batched kernel for hierarchical models, else the generic lane-split kernel. GENERIC /
