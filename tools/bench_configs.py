@@ -23,6 +23,8 @@ CONFIGS = {
     "cfg1": ("cfg1_linreg_loo", 4, "linear regression N=100 P=5 (grouped, J=1), LOO 100 folds x 4 chains"),
     "cfg2": ("cfg2_logistic_bench", 8, "logistic N=10000 P=50, LOO 10000 folds x 8 chains"),
     "cfg2k": ("cfg2_logistic_bench", 8, "logistic N=10000 P=50, K-fold K=10 (seed 1) x 8 chains"),
+    "cfg4r": ("cfg4_seasonal_bench", 4, "seasonal AR(2)+11 dummies T=5000, hv-block Racine per-point folds "
+                                        "(K=4998, v=5, h=12), M_A+M_B x 4 chains"),
     "cfg3": ("cfg3_radon_bench", 8, "radon-style 12000 houses / 400 counties, LOGO, M_A+M_B x 8 chains"),
     "cfg4": ("cfg4_seasonal_bench", 4, "seasonal AR(2)+11 dummies T=5000, hv-block K=100 h=12, M_A+M_B x 4 chains"),
     "cfg5": ("cfg5_linreg_bench", 16, "linear regression N=100000 P=5, LOO 100000 folds x 16 chains"),
@@ -109,6 +111,12 @@ def main():
             case.folds = pcv.make_kfold_scheme(case.data, 10, 1)
             case.models = [pcv.LogisticModel("M0", case.data, case.folds)]
             case.fa = case.folds.arrays()
+        if name == "cfg4r":  # the Racine per-point hv variant on the same data and fits
+            from paper_2310_07002_b200 import pcv
+            case.folds = pcv.make_hv_racine_scheme(case.data, 5, 12)
+            case.models = [pcv.SeasonalARModel(f"M{m}", case.data, case.folds, kw["ar_order"], kw["dummies"],
+                                               kw["rho_transform"]) for m, kw in enumerate(case.kws)]
+            case.fa = case.folds.arrays()
         steps = args.steps if name != "cfg5" else max(2, args.steps // 3)
         ms, cols = gpu_run(case, L, steps, args.warmup, args.policy)
         chains = case.K * L * len(case.models)
@@ -129,7 +137,7 @@ def main():
                 "frac": None if suff else achieved / pk, "elpd_sum_model0": float(np.sum(cols["estimate"][:case.K]))}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
-            sample_folds = {"cfg1": 32, "cfg2": 32, "cfg2k": 2, "cfg3": 8, "cfg4": 8, "cfg5": 4}[name]
+            sample_folds = {"cfg1": 32, "cfg2": 32, "cfg2k": 2, "cfg3": 8, "cfg4": 8, "cfg4r": 8, "cfg5": 4}[name]
             cv, kind, sample = cpu_sample(case, L, sample_folds, 3, threads)
             line["cpu"] = {"chain_steps_per_s": cv, "kind": kind, "cores": threads, "sample": sample}
             line["speedup_vs_cpu"] = value / cv
