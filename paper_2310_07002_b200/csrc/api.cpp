@@ -34,6 +34,7 @@ int glm_width(int family, int J, int nc);
 int glm_cluster_size(int n, int kp, int nch);
 cudaError_t launch_glm(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
 cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+size_t glm32_scratch_doubles(int nch);
 size_t glm32_image_bytes(int64_t n);
 void glm32_tile_image(const double* xr, int kp, const double* y, const int* key, int64_t n, unsigned char* out);
 cudaError_t launch_init_chains(const ModelDev& M, const ChainsDev& S, const double* bank,
@@ -127,6 +128,7 @@ struct HostModel {
   DevBuf<int> keyb, bgroup, boff, tfirst, tr0, trows, bkey, bgrows, buni;
   DevBuf<double> sA, sgn, sgs, sov_n, sov_s, sgA, sov_A;  // fold sufficient statistics (suffstats.cpp)
   DevBuf<int> sov_ptr, sov_g, sex_lo, sex_hi, sex_rows, sex_grp;
+  mutable DevBuf<double> g32;  // FP32 variant G scratch (grown on first use, per model)
   int64_t bank_rows = 0;
   ModelDev md{};
 };
@@ -702,7 +704,11 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
   const ModelDev& md = md_override ? *md_override : m.md;
   cudaError_t e;
   if (ctx->policy == PCVG_KERNEL_TF32 && md.family == kLogistic && md.x32) {
-    e = launch_glm32(md, S, A, st);  // FP32 variant: tcgen05 kind::tf32, split operands
+    const size_t need = glm32_scratch_doubles(S.nch);
+    if (m.g32.n < need) m.g32.alloc(need);
+    ModelDev md32 = md;
+    md32.g32_scratch = m.g32.p;
+    e = launch_glm32(md32, S, A, st);  // FP32 variant: tcgen05 kind::tf32, split operands
   } else if ((ctx->policy == PCVG_KERNEL_SUFFSTAT || ctx->policy == PCVG_KERNEL_AUTO) && md.suff) {
     e = launch_gauss(md, S, A, -suff_lanes_per_chain(md, S.nch), st);  // fold sufficient statistics
   } else if (use_glm(ctx, m, S.nch)) {

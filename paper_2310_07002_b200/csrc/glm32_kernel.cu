@@ -770,6 +770,13 @@ void glm32_tile_image(const double* xr, int kp, const double* y, const int* key,
   }
 }
 
+// Doubles of G scratch a launch over nch chains needs at most: one [kGN][kC] block per CTA, and a
+// launch has at most max(tiles, SMs) CTAs (full waves, or a tail of row-split clusters <= SMs).
+size_t glm32_scratch_doubles(int nch) {
+  const int tiles = (nch + kC - 1) / kC;
+  return static_cast<size_t>(std::max(tiles, 256)) * kGN * kC;
+}
+
 cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
   const int tiles = (S.nch + kC - 1) / kC;
   if (tiles == 0) return cudaSuccess;
@@ -801,15 +808,11 @@ cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A
     ct = std::max(1, std::atoi(e));
     r = tiles;
   }
+  // one G scratch per CTA of a launch, owned by the model (its launches are stream-ordered)
   const int grid_max = std::max(tiles - r, r * ct);
-  static double* scratch = nullptr;
-  static int scratch_ctas = 0;
-  if (grid_max > scratch_ctas) {  // one G scratch per CTA of a launch (launches are stream-ordered)
-    if (scratch) cudaFree(scratch);
-    cudaError_t e = cudaMalloc(&scratch, sizeof(double) * static_cast<size_t>(grid_max) * kGN * kC);
-    if (e != cudaSuccess) return e;
-    scratch_ctas = grid_max;
-  }
+  double* scratch = M.g32_scratch;
+  if (scratch == nullptr || static_cast<size_t>(grid_max) * kGN * kC > glm32_scratch_doubles(S.nch))
+    return cudaErrorInvalidValue;
   auto launch = [&](int tile0, int ntiles, int cs) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ntiles * cs);
