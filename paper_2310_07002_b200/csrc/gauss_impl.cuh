@@ -1148,7 +1148,7 @@ __device__ void score_extra(const ModelDev& M, const ChainsDev& S, int c, int t,
 // NB = 0: row-split passes (grad_pass, T lanes per chain); NB > 0: group-batched passes
 // (hgrad_pass, T = 32, up to 32 * NB groups).
 template <int FAM, int T, int NCM, int NGM, int NB>
-__global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : (NB == -2 ? 4 : (NB < 0 && T > 1 ? 3 : 1))) gauss_kernel(ModelDev M, ChainsDev S, RunArgs A) {
+__global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : (NB == -2 ? 4 : (NB < 0 && T > 1 ? 4 : 1))) gauss_kernel(ModelDev M, ChainsDev S, RunArgs A) {
   constexpr int kChains = kBlock / T;
   const int t = threadIdx.x % T;
   const int local = threadIdx.x / T;
