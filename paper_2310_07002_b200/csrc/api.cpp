@@ -702,6 +702,7 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
                    cudaStream_t st = nullptr, const ModelDev* md_override = nullptr) {
   if (!st) st = ctx->stream;
   const ModelDev& md = md_override ? *md_override : m.md;
+  const int launches0 = sampler_launch_count();
   cudaError_t e;
   if (ctx->policy == PCVG_KERNEL_TF32 && md.family == kLogistic && md.x32) {
     const size_t need = glm32_scratch_doubles(S.nch);
@@ -719,7 +720,7 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
     const int T = gauss_lanes_per_chain(md, S.nch);
     e = launch_gauss(md, S, A, T, st);
   }
-  ++ctx->launches;
+  ctx->launches += sampler_launch_count() - launches0;  // two when a wave tail is split
   ck(e, "kernel launch");
 }
 

@@ -15,6 +15,7 @@ cudaError_t launch_family(const ModelDev& M, const ChainsDev& S, const RunArgs& 
   const int chains_per_block = kBlock / T;
   const int grid = (S.nch + chains_per_block - 1) / chains_per_block;
   if (grid == 0) return cudaSuccess;
+  ++sampler_launch_count();
   switch (T) {
     case 1: gauss_kernel<FAM, 1, NCM, NGM, 0><<<grid, kBlock, 0, st>>>(M, S, A); break;
     case 4: gauss_kernel<FAM, 4, NCM, NGM, 0><<<grid, kBlock, 0, st>>>(M, S, A); break;
@@ -37,6 +38,7 @@ cudaError_t launch_nb(const ModelDev& M, const ChainsDev& S, const RunArgs& A, c
     if (e != cudaSuccess) return e;
     attr = smem;
   }
+  ++sampler_launch_count();
   gauss_kernel<FAM, 32, NCM, NGM, NB><<<grid, kBlock, smem, st>>>(M, S, A);
   return cudaGetLastError();
 }

@@ -826,6 +826,7 @@ cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = cs > 1 ? 1 : 0;
+    ++sampler_launch_count();
     return cudaLaunchKernelEx(&cfg, glm32_kernel, M, S, A, scratch, cs, tile0);
   };
   if (tiles - r > 0) {

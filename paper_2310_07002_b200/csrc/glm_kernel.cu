@@ -853,6 +853,7 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = cs > 1 ? 1 : 0;
+    ++sampler_launch_count();
     return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs, tile0);
   };
   // Concurrently schedulable clusters of each size (a cluster must fit in one GPC): a 16-CTA cluster

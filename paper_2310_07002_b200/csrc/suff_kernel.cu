@@ -22,6 +22,7 @@ cudaError_t launch_suff_t(const ModelDev& M, const ChainsDev& S, const RunArgs& 
     if (e != cudaSuccess) return e;
     attr = smem;
   }
+  ++sampler_launch_count();
   gauss_kernel<FAM, T, NCM, NGM, NB><<<grid, kBlock, smem, st>>>(M, S, A);
   return cudaGetLastError();
 }

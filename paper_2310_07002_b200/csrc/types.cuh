@@ -106,6 +106,13 @@ struct ModelDev {
 
 constexpr int kMaxBatches = 16;
 
+// Kernel launches issued by the sampler launchers on this host thread (a wave-tail split issues
+// two); the driver adds the difference around each launch to its launch count.
+inline int& sampler_launch_count() {
+  static thread_local int n = 0;
+  return n;
+}
+
 // HS / DSS score state (ScoreKind::HS / DSS, engine.cpp:322-373; accum.cpp:10-99). Per local fold
 // kf with test size m = msize[kf], the L chains of the fold are interleaved entry-major: entry e of
 // chain cl sits at base[kf] + e * L + cl (one 8*L-byte segment per entry).
