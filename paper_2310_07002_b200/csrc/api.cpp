@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -969,9 +971,20 @@ pcvg_status pcvg_create(int32_t device, pcvg_ctx** out) {
 pcvg_status pcvg_destroy(pcvg_ctx* ctx) {
   if (!ctx) return PCVG_OK;
   cudaSetDevice(ctx->device);
+  static const bool verbose = std::getenv("PCVG_VERBOSE") != nullptr;  // tuning only
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
+  cudaDeviceSynchronize();
+  const auto t1 = now();
   ctx->chains.clear();
+  const auto t2 = now();
   ctx->centers.clear();
   ctx->models.clear();
+  const auto t3 = now();
+  if (verbose)
+    std::fprintf(stderr, "pcvg_destroy: sync %.3f s, chains %.3f s, models %.3f s\n",
+                 std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(t2 - t1).count(),
+                 std::chrono::duration<double>(t3 - t2).count());
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evj) cudaEventDestroy(ctx->evj);
