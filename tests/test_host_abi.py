@@ -239,3 +239,19 @@ def test_fold_gram_rejects_non_finite_data():
     y = np.array([1.0, np.inf, 2.0])
     with pytest.raises(pcv.InvalidInput):
         pcv.fold_gram(y, np.ones((3, 1)), np.arange(3), np.arange(3), np.arange(3) + 1)
+
+
+def test_bench_reference_arm_line():
+    """bench.py --impl reference (the driver's reference arm) prints one JSON line with the
+    contract keys; it runs the compiled reference engine (or the oracle port) on host cores only."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["metric"] == "chain-steps/sec" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
