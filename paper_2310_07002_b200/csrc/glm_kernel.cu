@@ -74,6 +74,7 @@ struct Smem {
   double red[kOwners][kC];                // owner partial sums (kinetic)
   double pri[kOwners][kC];                // owner partial sums (log joint)
   double exp_tab[16];                     // 2^(-j/16)
+  double exp_tab32[32];                   // 2^(-j/32) (gradient-only sigmoid)
   int lo[kC], hi[kC], ntr[kC];
   int bad[kC];
   int cur[kC];
@@ -285,15 +286,16 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
             const double x = eta[mt][j][e];
             const bool train = valid && static_cast<unsigned>(kv - lo[j][e]) >=
                                             static_cast<unsigned>(hi[j][e] - lo[j][e]);
-            if constexpr (!kGauss) {
-              const double ex = VALUE ? exp_neg(fabs(x), sm.exp_tab) : exp_neg_5(fabs(x), sm.exp_tab);
-              const double inv = VALUE ? rcp_1_2(1.0 + ex) : rcp_1_2_fast(1.0 + ex);
+            if constexpr (!kGauss && !VALUE) {
+              const double rr = logistic_resid_fast(x, yv, yv - 1.0, sm.exp_tab32);  // no branch
+              r2[e] = train ? rr : 0.0;
+            } else if constexpr (!kGauss) {
+              const double ex = exp_neg(fabs(x), sm.exp_tab);
+              const double inv = rcp_1_2(1.0 + ex);
               const double sig = x >= 0.0 ? inv : ex * inv;
               r2[e] = train ? yv - sig : 0.0;
-              if (VALUE) {
-                if (train) acc[j][e] += yv * x - (fmax(x, 0.0) + log1p(ex));
-                else if (valid && !isfinite(x)) acc[j][e] = CUDART_NAN;  // 0 * non-finite test term
-              }
+              if (train) acc[j][e] += yv * x - (fmax(x, 0.0) + log1p(ex));
+              else if (valid && !isfinite(x)) acc[j][e] = CUDART_NAN;  // 0 * non-finite test term
             } else {
               const double r = yv - x;
               r2[e] = train ? r : 0.0;
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
     sm.rel[tid] = 0u;
   }
   if (tid < 16) sm.exp_tab[tid] = exp2(-tid / 16.0);
+  if (tid < 32) sm.exp_tab32[tid] = exp2(-tid / 32.0);
   for (int i = tid; i < KP * kLdS; i += kThreads) sm.ws[i] = 0.0;
   fence_mbar_init();
   uint32_t gtile = 0;

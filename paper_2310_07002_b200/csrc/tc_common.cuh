@@ -118,6 +118,46 @@ __device__ __forceinline__ double rcp_1_2_fast(double d) {
   return fma(r, e, r);
 }
 
+// y - sigmoid(x) for the gradient-only passes in 11 FP64 operations (exp_neg_5 + rcp_1_2_fast +
+// select + subtract cost 18). DMMA and DFMA share one FP64 datapath, so every FP64 operation saved
+// here is returned to the GEMM:
+// * |x| <= 700 is clamped by an integer compare of the high word (|x| >= 0, so bit order is value
+//   order; NaN clamps to 700 exactly as fmin does);
+// * -|x| = -(n/32) ln2 + r with ONE reduction constant: ln2/32 is off by 7e-19 in double, so r is
+//   off by at most 2.3e-14 (at |x| = 700, where e^-|x| ~ 1e-304) and ~1e-16 where it matters;
+// * e^r on |r| <= ln2/64 by a degree-4 Chebyshev-interpolation polynomial (max relative error
+//   7.9e-14, tools/exp_poly.py), 2^(-j/32) from a 32-entry table;
+// * 2^(-j/32) * 2^(-m) subtracts m from the table entry's exponent (exact: the entry is in (0.5, 1]
+//   and m <= 1009, so the product stays normal);
+// * 1 + e^-|x| is one FMA, and both branches of the sigmoid share the reciprocal:
+//   x >= 0: y - 1/(1+e^-|x|);  x < 0: y - e^-|x|/(1+e^-|x|) = (y - 1) + 1/(1+e^-|x|),
+//   chosen on the sign bit (x = -0 gives y - 1/2 either way) with ym1 = y - 1 precomputed per row.
+//   Both branches carry the reciprocal's absolute error (~1e-14), symmetric in the sign of x.
+__device__ __forceinline__ double logistic_resid_fast(double x, double y, double ym1,
+                                                      const double* tab32) {
+  constexpr double kInvLn2x32 = 46.16624130844683;    // 32 / ln 2
+  constexpr double kLn2d32 = 0.02166084939249829;     // ln 2 / 32
+  constexpr double kShift = 6755399441055744.0;       // 1.5 * 2^52
+  constexpr double kC1 = 0.9999999999641696, kC2 = 0.4999999999940276;
+  constexpr double kC3 = 0.1666678885252701, kC4 = 0.04166687031843588;
+  const int xh = __double2hiint(x);
+  const int ah = xh & 0x7fffffff;
+  const double a = ah >= 0x4085E000 ? 700.0 : __hiloint2double(ah, __double2loint(x));
+  const double t = fma(a, kInvLn2x32, kShift);
+  const int n = __double2loint(t);
+  const double nd = t - kShift;
+  const double r = fma(nd, kLn2d32, -a);
+  double p = fma(r, kC4, kC3);
+  p = fma(p, r, kC2);
+  p = fma(p, r, kC1);
+  p = fma(p, r, 1.0);
+  const double tv = tab32[n & 31];
+  const double scaled = __hiloint2double(__double2hiint(tv) - ((n >> 5) << 20), __double2loint(tv));
+  const double inv = rcp_1_2_fast(fma(scaled, p, 1.0));
+  const bool pos = xh >= 0;
+  return fma(pos ? -1.0 : 1.0, inv, pos ? y : ym1);
+}
+
 // 1 / d for d in [1, 2]: hardware approximation + two Newton steps (no special cases needed).
 __device__ __forceinline__ double rcp_1_2(double d) {
   double r;
