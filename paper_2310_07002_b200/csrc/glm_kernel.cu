@@ -74,7 +74,7 @@ struct Smem {
   double red[kOwners][kC];                // owner partial sums (kinetic)
   double pri[kOwners][kC];                // owner partial sums (log joint)
   double exp_tab[16];                     // 2^(-j/16)
-  double exp_tab32[32];                   // 2^(-j/32) (gradient-only sigmoid)
+  int exp_hi32[32], exp_lo32[32];          // 2^(-j/32) as high / low words (gradient-only sigmoid)
   int lo[kC], hi[kC], ntr[kC];
   int bad[kC];
   int cur[kC];
@@ -287,7 +287,7 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
             const bool train = valid && static_cast<unsigned>(kv - lo[j][e]) >=
                                             static_cast<unsigned>(hi[j][e] - lo[j][e]);
             if constexpr (!kGauss && !VALUE) {
-              const double rr = logistic_resid_fast(x, yv, yv - 1.0, sm.exp_tab32);  // no branch
+              const double rr = logistic_resid_fast(x, yv, yv - 1.0, sm.exp_hi32, sm.exp_lo32);  // no branch
               r2[e] = train ? rr : 0.0;
             } else if constexpr (!kGauss) {
               const double ex = exp_neg(fabs(x), sm.exp_tab);
@@ -517,7 +517,11 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
     sm.rel[tid] = 0u;
   }
   if (tid < 16) sm.exp_tab[tid] = exp2(-tid / 16.0);
-  if (tid < 32) sm.exp_tab32[tid] = exp2(-tid / 32.0);
+  if (tid < 32) {
+    const double v = exp2(-tid / 32.0);
+    sm.exp_hi32[tid] = __double2hiint(v);
+    sm.exp_lo32[tid] = __double2loint(v);
+  }
   for (int i = tid; i < KP * kLdS; i += kThreads) sm.ws[i] = 0.0;
   fence_mbar_init();
   uint32_t gtile = 0;

@@ -126,7 +126,9 @@ __device__ __forceinline__ double rcp_1_2_fast(double d) {
 // * -|x| = -(n/32) ln2 + r with ONE reduction constant: ln2/32 is off by 7e-19 in double, so r is
 //   off by at most 2.3e-14 (at |x| = 700, where e^-|x| ~ 1e-304) and ~1e-16 where it matters;
 // * e^r on |r| <= ln2/64 by a degree-4 Chebyshev-interpolation polynomial (max relative error
-//   7.9e-14, tools/exp_poly.py), 2^(-j/32) from a 32-entry table;
+//   7.9e-14, tools/exp_poly.py), 2^(-j/32) from a 32-entry table split into high and low words
+//   (two 32-word arrays: any 32 indices hit 32 distinct banks, where a double table of 32
+//   entries would conflict 2-way);
 // * 2^(-j/32) * 2^(-m) subtracts m from the table entry's exponent (exact: the entry is in (0.5, 1]
 //   and m <= 1009, so the product stays normal);
 // * 1 + e^-|x| is one FMA, and both branches of the sigmoid share the reciprocal:
@@ -134,7 +136,7 @@ __device__ __forceinline__ double rcp_1_2_fast(double d) {
 //   chosen on the sign bit (x = -0 gives y - 1/2 either way) with ym1 = y - 1 precomputed per row.
 //   Both branches carry the reciprocal's absolute error (~1e-14), symmetric in the sign of x.
 __device__ __forceinline__ double logistic_resid_fast(double x, double y, double ym1,
-                                                      const double* tab32) {
+                                                      const int* tab_hi, const int* tab_lo) {
   constexpr double kInvLn2x32 = 46.16624130844683;    // 32 / ln 2
   constexpr double kLn2d32 = 0.02166084939249829;     // ln 2 / 32
   constexpr double kShift = 6755399441055744.0;       // 1.5 * 2^52
@@ -151,8 +153,7 @@ __device__ __forceinline__ double logistic_resid_fast(double x, double y, double
   p = fma(p, r, kC2);
   p = fma(p, r, kC1);
   p = fma(p, r, 1.0);
-  const double tv = tab32[n & 31];
-  const double scaled = __hiloint2double(__double2hiint(tv) - ((n >> 5) << 20), __double2loint(tv));
+  const double scaled = __hiloint2double(tab_hi[n & 31] - ((n >> 5) << 20), tab_lo[n & 31]);
   const double inv = rcp_1_2_fast(fma(scaled, p, 1.0));
   const bool pos = xh >= 0;
   return fma(pos ? -1.0 : 1.0, inv, pos ? y : ym1);
