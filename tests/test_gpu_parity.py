@@ -286,6 +286,42 @@ def test_leapfrog_endpoint_and_reversibility(ctx, name):
     c.close()
 
 
+@pytest.mark.parametrize("scale", [1.0, 30.0, 100.0, 1000.0])
+def test_logistic_leapfrog_wide_eta(ctx, scale):
+    """The gradient-only passes of the logistic kernel (tc_common.cuh::logistic_resid_fast: integer
+    clamp at |eta| = 700, exponent assembly, sign-folded reciprocal) against the oracle's std::exp
+    sigmoid on positions scaled so that eta = x . theta reaches |eta| ~ 360 (scale 100, still a
+    finite-energy trajectory) and ~3600 (scale 1000, past the clamp). The leapfrog probe runs
+    hmc_step with u = 0, so a trajectory the oracle calls divergent (|dH| > 1000, hmc.cpp:82-90)
+    must come back not-ok; every other end point matches at the posterior tolerance."""
+    case, c, slots = case_in(ctx, "logistic_loo")
+    rng = np.random.default_rng(21)
+    m, slot = 0, slots[0]
+    om, kp = case.omodels[m], case.kparams[m]
+    th = sample_thetas(case, m, 4, seed=4) * scale
+    mom = rng.standard_normal(th.shape) / np.sqrt(kp.inv_mass_diag)
+    folds = np.array([0, 1, case.K // 2, case.K], dtype=np.int32)
+    q1, p1, ok = c.leapfrog(slot, folds, th, mom)
+    for i in range(4):
+        _, oh0, oh1, _, odiv = om.hmc_probe(int(folds[i]), kp.step_size, kp.n_leapfrog, kp.inv_mass_diag,
+                                            th[i], mom[i], 0.0)
+        assert bool(ok[i]) == (not odiv), (scale, i, oh1 - oh0)
+        if odiv:
+            continue
+        okr, oq, op = om.leapfrog(int(folds[i]), kp.step_size, kp.n_leapfrog, kp.inv_mass_diag, th[i], mom[i])
+        np.testing.assert_allclose(q1[i], oq, rtol=1e-8, atol=1e-9 * (1 + np.abs(oq).max()))
+        np.testing.assert_allclose(p1[i], op, rtol=1e-8, atol=1e-8 * (1 + np.abs(op).max()))
+    _, h0, h1, _, div = c.hmc_probe(slot, folds, th, mom, np.zeros(4))
+    for i in range(4):
+        _, oh0, oh1, _, odiv = om.hmc_probe(int(folds[i]), kp.step_size, kp.n_leapfrog, kp.inv_mass_diag,
+                                            th[i], mom[i], 0.0)
+        assert div[i] == odiv
+        assert abs(h0[i] - oh0) <= 1e-10 * (1 + abs(oh0))
+        if not odiv:
+            assert abs(h1[i] - oh1) <= 1e-8 * (1 + abs(oh1))
+    c.close()
+
+
 def test_snapshots_prefix_stable(ctx):
     """test_engine.cpp:150-173: the first snapshot of a 200-iteration run equals the final
     statistics of a 100-iteration run (R-hat up to the block-boundary summation order)."""
