@@ -109,58 +109,55 @@ def load_inputs():
     return d, f, kp, bank
 
 
+def workload_config(folds, world):
+    """The `config` block shared by both arms (the reference arm times a fold sample of the same
+    workload; the sample is stated in its cpu_baseline)."""
+    return {"workload": WORKLOAD, "folds": folds, "chains_per_fold": L, "n_obs": N_OBS, "covariates": P,
+            "n_leapfrog": N_LF, "chains": folds * L,
+            "l2": "flushed between timed steps (256 MiB memset); X (4 MB) then re-read from HBM",
+            "parallelism": f"fold-sharded x{world}"}
+
+
 def cpu_sample(folds_total, steps, warmup, threads, prefer_ref=True):
-    """The reference's own Step 2-3 task loop on a bounded fold sample (oracle/_ref), or the C
-    port when the reference build is absent. Returns (chain-steps/s, kind, sample description)."""
-    import ctypes as C
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import _oracle as O
-    from paper_2310_07002_b200 import abi
-    d, f, kp, bank = load_inputs()
-    fa = f.arrays()
-    spec = abi.SpecArrays(abi.FAMILY_LOGISTIC)
-    kern = abi.KernelArrays(kp.step_size, kp.n_leapfrog, kp.inv_mass_diag)
-    rng = np.random.default_rng(0)
-    folds = np.sort(rng.choice(folds_total, CPU_SAMPLE_FOLDS, replace=False)).astype(np.int32)
-    bank = np.ascontiguousarray(bank)
-    s_s, w_s, cs = C.c_double(), C.c_double(), C.c_double()
-    if prefer_ref and O.have_ref():
-        lib = O.ref()
-        m = O.RModel(d, fa, spec)
-        rc = lib.pcvref_time_tasks(m.h, len(folds), abi.ptr(folds, C.c_int32), L, warmup, steps, 1, 0,
-                                   C.byref(kern.struct), abi.ptr(bank, C.c_double), bank.shape[0],
-                                   threads, C.byref(s_s), C.byref(w_s), C.byref(cs))
-        kind = "reference"
-    else:
-        lib = O.oracle()
-        m = O.OModel(d, fa, spec)
-        rc = lib.pcvo_time_tasks(m.h, len(folds), abi.ptr(folds, C.c_int32), L, warmup, steps, 1, 0,
-                                 C.byref(kern.struct), abi.ptr(bank, C.c_double), bank.shape[0],
-                                 threads, C.byref(s_s), C.byref(w_s), C.byref(cs))
-        kind = "port"
-    assert rc == 0, "cpu sample failed"
-    chain_steps = len(folds) * L * steps
-    sample = (f"{len(folds)} of {folds_total} LOO folds x {L} chains x {steps} sampling steps "
-              f"(after {warmup} warm-up steps) = {chain_steps} chain-steps, {threads} threads, "
-              f"{s_s.value:.2f} s")
-    return chain_steps / s_s.value, kind, sample
+    """The reference's own Step 2-3 task loop on a bounded fold sample (oracle/_ref, through
+    oracle/refarm.py, which never loads the product library), or the C port when the reference
+    build is absent. Returns (chain-steps/s, kind, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refarm
+    return refarm.cpu_sample(folds_total, CPU_SAMPLE_FOLDS, L, steps, warmup, threads, prefer_ref)
 
 
-def run_reference(args, rank):
+def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     value, kind, sample = cpu_sample(N_OBS, args.steps, args.warmup, threads)
     line = {"impl": "reference", "metric": "chain-steps/sec", "value": value, "unit": "chain-steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * CPU_SAMPLE_FOLDS * L / value, "higher_is_better": True,
+            "ms_per_step": 1e3 * N_OBS * L / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample": sample},
+            "config": workload_config(args.folds or N_OBS, args.gpus),
             "cpu_baseline": {"value": value, "unit": "chain-steps/s", "cores": threads, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": "chain-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch_ranks(n):
+    """`bench.py --gpus N` outside torchrun: start the N ranks (one per GPU) ourselves."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < n and "PCVG_FORCE_DEVICE" not in os.environ:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -182,7 +179,12 @@ def main():
     if "PCVG_FORCE_DEVICE" in os.environ:  # N ranks sharing one GPU (test of the multi-rank path)
         local = int(os.environ["PCVG_FORCE_DEVICE"])
     if args.impl == "reference":
-        return run_reference(args, rank)
+        return run_reference(args, rank, world)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_ranks(args.gpus)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
 
     import torch
     from paper_2310_07002_b200 import abi, pcv
@@ -260,10 +262,7 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32 (tf32 hi/lo split; chain state f64)" if args.fp32 else "f64",
                 "data": "synthetic",
-                "config": {"workload": WORKLOAD, "folds": K, "chains_per_fold": L, "n_obs": N_OBS,
-                           "covariates": P, "n_leapfrog": N_LF, "chains": chains_total,
-                           "l2": "flushed between timed steps (256 MiB memset); X (4 MB) then re-read from HBM",
-                           "parallelism": f"fold-sharded x{world}"},
+                "config": workload_config(K, world),
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "flop_per_chain_step": FLOP_PER_CHAIN_STEP, "peak_source": peak_src,

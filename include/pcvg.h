@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PCVG_ABI_VERSION 2
+#define PCVG_ABI_VERSION 3
 
 typedef enum {
   PCVG_OK = 0,
@@ -233,6 +233,10 @@ enum { PCVG_KERNEL_AUTO = 0, PCVG_KERNEL_GENERIC = 1, PCVG_KERNEL_TENSOR = 2, PC
  * instead of O(n d); same values to rounding. Needs finite data; other families
  * and non-finite datasets fall back to the ROWS choice. */
 pcvg_status pcvg_set_kernel_policy(pcvg_ctx* ctx, int32_t policy);
+/* Fault injection for tests (the reference's BrokenFoldModel, test_engine.cpp:57-90): every
+ * transition of every chain of `fold` (0..K-1; -1 clears) in model `slot` is divergent, as when the
+ * model's gradient is NaN on that fold. Exercises the failed-fold rule (engine.cpp:385-397). */
+pcvg_status pcvg_debug_break_fold(pcvg_ctx* ctx, int32_t slot, int32_t fold);
 pcvg_status pcvg_model_test_size(const pcvg_ctx* ctx, int32_t slot, int32_t fold, int64_t* n);
 
 /* Parity probes (device). n evaluation points: fold[n], theta[n*dim]. */
@@ -271,6 +275,15 @@ pcvg_status pcvg_score_streams(pcvg_ctx* ctx, int32_t L, int64_t n, const double
 int32_t pcvg_checkpoint_count(const pcvg_run_config* cfg);
 /* Full run_pcv on one device for the registered models. */
 pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* report);
+
+/* run_pcv's Steps 3-4 (checkpoints, per-fold statistics, shuffle benchmark, early-stop rule, report)
+ * on given log_pred streams instead of sampled ones: chain c of fold k observes
+ * s[(k*L + c)*iters + i] at iteration i through ScoreAccum::observe with centre centers[k]
+ * (accum.cpp:164-182). One model, K folds, LogS, on a context with no models registered. The
+ * harness of the reference's shuffle-benchmark acceptance criteria (acceptance.cpp:259-325, C6/C7)
+ * through the same device accumulators, kernels and stopping rule as pcvg_run. */
+pcvg_status pcvg_run_streams(pcvg_ctx* ctx, int32_t K, const double* s, const double* centers,
+                             const pcvg_run_config* cfg, pcvg_report* report);
 
 /* Stepwise API for fold-sharded multi-GPU runs (one process per GPU). */
 /* Step 2 for the shard: warm start, warm-up, centering constants. */
@@ -349,10 +362,11 @@ pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* data, const 
 pcvg_status pcvg_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_before,
                            int64_t nonfailed_total, int32_t blocks_used, double* rep_max,
                            int32_t* needs_host);
-/* The same positional benchmark on host block sums y_x/y_x2 [n_models][nfold][L][D_stride]
- * (multi-process CPU tests of the sharding arithmetic). */
+/* The same positional benchmark on host sub-block sums y_x/y_x2 [n_models][nfold][L][D_stride]
+ * (multi-process CPU tests of the sharding arithmetic): the first blocks_used sub-blocks regrouped
+ * into block_groups benchmark blocks (pcvg_benchmark uses min(RunConfig blocks, blocks_used)). */
 pcvg_status pcvg_benchmark_host(int32_t n_models, int32_t nfold, int32_t L, int32_t D_stride,
-                                int32_t blocks_used, int64_t iter_count, uint64_t seed,
+                                int32_t blocks_used, int32_t block_groups, int64_t iter_count, uint64_t seed,
                                 int32_t bench_draws, const double* y_x, const double* y_x2,
                                 const int32_t* failed, int64_t nonfailed_before,
                                 int64_t nonfailed_total, double* rep_max, int32_t* needs_host);

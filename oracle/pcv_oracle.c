@@ -190,6 +190,27 @@ int pcvo_make_kfold(int64_t n, int32_t K, uint64_t seed, int32_t* out) { /* fold
 }
 
 /* Stable argsort by time (std::stable_sort in folds.cpp:95-98), merge sort. */
+/* cfg2 logistic simulator (new family; same draw order as oracle/ref_shim.cpp
+ * pcvref_simulate_logistic on the reference CounterRng). */
+int pcvo_simulate_logistic(int64_t n, int32_t P, uint64_t seed, double* y, double* x) {
+  if (n < 2 || P < 1) return set_err(PCVG_INVALID_INPUT, "logistic simulator needs n >= 2, P >= 1");
+  pcvo_rng rng;
+  pcvo_rng_init(&rng, seed, pcvo_stream_key(PCVG_STREAM_SIMULATE, 5, 0, 0));
+  double* beta = (double*)malloc(sizeof(double) * (size_t)(P + 1));
+  for (int32_t j = 0; j <= P; ++j) beta[j] = pcvo_normal(&rng);
+  const double scale = 1.0 / sqrt((double)P);
+  for (int64_t i = 0; i < n; ++i) {
+    double eta = beta[0];
+    for (int32_t j = 0; j < P; ++j) {
+      x[i * P + j] = pcvo_normal(&rng) * scale;
+      eta += x[i * P + j] * beta[1 + j];
+    }
+    y[i] = pcvo_uniform(&rng) < 1.0 / (1.0 + exp(-eta)) ? 1.0 : 0.0;
+  }
+  free(beta);
+  return 0;
+}
+
 static void time_order(const int64_t* t, int64_t n, int64_t* order) {
   int64_t* tmp = malloc(sizeof(int64_t) * (n > 0 ? n : 1));
   for (int64_t i = 0; i < n; ++i) order[i] = i;
@@ -262,6 +283,7 @@ int pcvo_make_hv_racine(const pcvg_dataset* d, int64_t v, int64_t h, int64_t* iv
 /* ------------------------------------------------------------------ models */
 struct pcvo_model {
   int family;
+  int broken_fold; /* test_engine.cpp:57-90 BrokenFoldModel: gradient NaN on this fold (-1 = none) */
   int64_t n;
   int ncov;
   double *y, *x;
@@ -307,6 +329,7 @@ void pcvo_model_destroy(pcvo_model* m) {
 pcvo_model* pcvo_model_create(const pcvg_dataset* d, const pcvg_folds* f,
                               const pcvg_model_spec* s) {
   pcvo_model* m = calloc(1, sizeof *m);
+  m->broken_fold = -1;
   const int64_t n = d->n_obs;
   m->family = s->family;
   m->n = n;
@@ -634,7 +657,18 @@ double pcvo_log_joint(const pcvo_model* m, const double* th, int32_t fold) {
   return NAN;
 }
 
+/* Delegating fault injection of the reference's engine test (BrokenFoldModel, test_engine.cpp:57-90):
+ * every gradient on `fold` is NaN, so that fold's chains diverge on every step. */
+void pcvo_model_break_fold(pcvo_model* m, int32_t fold) { m->broken_fold = fold; }
+
+static void grad_impl(const pcvo_model* m, const double* th, int32_t fold, double* grad);
 void pcvo_grad(const pcvo_model* m, const double* th, int32_t fold, double* grad) {
+  grad_impl(m, th, fold, grad);
+  if (fold == m->broken_fold)
+    for (int i = 0; i < m->dim; ++i) grad[i] = NAN;
+}
+
+static void grad_impl(const pcvo_model* m, const double* th, int32_t fold, double* grad) {
   const int J = m->J;
   for (int i = 0; i < m->dim; ++i) grad[i] = 0.0;
   switch (m->family) {

@@ -50,6 +50,7 @@ int pcvo_make_hv_racine(const pcvg_dataset* d, int64_t v, int64_t h, int64_t* in
 
 /* Models (opaque). */
 typedef struct pcvo_model pcvo_model;
+void pcvo_model_break_fold(pcvo_model* m, int32_t fold);
 pcvo_model* pcvo_model_create(const pcvg_dataset* d, const pcvg_folds* f,
                               const pcvg_model_spec* s);
 void pcvo_model_destroy(pcvo_model* m);

@@ -19,6 +19,8 @@
 #include "pcv/models/registry.hpp"
 #include "pcv/report_io.hpp"
 #include "pcv/config.hpp"
+#include "pcv/diagnostics.hpp"
+#include "pcv/accum.hpp"
 #include "pcv/engine.hpp"
 #include "pcv/errors.hpp"
 #include "pcv/folds.hpp"
@@ -156,6 +158,27 @@ int pcvref_simulate_radon(int32_t houses, int32_t counties, uint64_t seed, doubl
     std::memcpy(y, r.data.y.data(), sizeof(double) * r.data.y.size());
     std::memcpy(x, r.data.x.data(), sizeof(double) * r.data.x.size());
     std::memcpy(g, r.data.group_id.data(), sizeof(int32_t) * r.data.group_id.size());
+  });
+}
+
+// cfg2 logistic simulator (the logistic family is a plugin, ref_plugins.hpp): the same draw order
+// as the product's pcvg_simulate_logistic on the reference's own CounterRng, so the reference arm
+// of bench.py builds its inputs without the product library.
+int pcvref_simulate_logistic(int64_t n, int32_t P, uint64_t seed, double* y, double* x) {
+  return guarded([&] {
+    if (n < 2 || P < 1) throw pcv::invalid_input("logistic simulator needs n >= 2, P >= 1");
+    pcv::CounterRng rng(seed, pcv::stream_key(pcv::StreamKind::Simulate, 5));
+    std::vector<double> beta(P + 1);
+    for (double& b : beta) b = rng.normal();
+    const double scale = 1.0 / std::sqrt(static_cast<double>(P));
+    for (int64_t i = 0; i < n; ++i) {
+      double eta = beta[0];
+      for (int32_t j = 0; j < P; ++j) {
+        x[i * P + j] = rng.normal() * scale;
+        eta += x[i * P + j] * beta[1 + j];
+      }
+      y[i] = rng.uniform() < 1.0 / (1.0 + std::exp(-eta)) ? 1.0 : 0.0;
+    }
   });
 }
 
@@ -559,6 +582,57 @@ int pcvref_run_pcv(int32_t n_models, void** models, const int32_t* model_ids,
     rep->verdict_quantile_value = r.verdict.quantile_value;
     rep->verdict_observed = r.verdict.observed;
     rep->iters_run = r.iters;
+  });
+}
+
+// The reference's shuffle-benchmark acceptance harness (acceptance.cpp:259-325, criteria C6/C7) run
+// on the reference library: K = 10 folds x L = 4 autocorrelated score chains of n = 1000 draws
+// (rho = 0.3, fold locations 2 N(0,1), overdispersed start), optionally one corrupted chain of
+// fold 2 (kind 1 = stuck at its start, kind 2 = shifted by +5), fed through ScoreAccum(b = 50,
+// D = 5, n, mu_k); returns the observed R-hat max, the 0.99 nearest-rank benchmark quantile of R
+// replicates and the verdict. tests/golden/make_acceptance.py stores them for the device runs.
+int pcvref_corrupted_run(int32_t seed, int32_t kind, int32_t bench_draws, double* observed,
+                         double* quantile_value, int32_t* pass) {
+  return guarded([&] {
+    const int k_folds = 10, l = 4, d_blocks = 5, b = 50;
+    const long n = 1000;
+    const int bad_fold = 2, bad_chain = 0;
+    const double rho = 0.3;
+    const std::uint64_t run_seed = 7000 + static_cast<std::uint64_t>(seed);
+    std::vector<std::vector<pcv::ScoreAccum>> acc(k_folds);
+    for (int k = 0; k < k_folds; ++k) {
+      pcv::CounterRng fold_rng(run_seed, pcv::stream_key(pcv::StreamKind::Simulate, static_cast<std::uint64_t>(k)));
+      const double mu_k = 2.0 * fold_rng.normal();
+      for (int c = 0; c < l; ++c) {
+        pcv::CounterRng rng(run_seed, pcv::stream_key(pcv::StreamKind::ChainSampling, 0, static_cast<std::uint64_t>(k),
+                                                      static_cast<std::uint64_t>(c)));
+        const bool corrupt = kind != 0 && k == bad_fold && c == bad_chain;
+        const double start = mu_k + 3.0;
+        double state = start - mu_k;
+        const double innov = std::sqrt(1.0 - rho * rho);
+        pcv::ScoreAccum a(b, d_blocks, n, mu_k);
+        for (long i = 0; i < n; ++i) {
+          state = rho * state + innov * rng.normal();
+          double v = (corrupt && kind == 1) ? start : mu_k + state;
+          if (corrupt && kind == 2) v += 5.0;
+          a.observe(v, i);
+        }
+        acc[k].push_back(std::move(a));
+      }
+    }
+    std::vector<double> rhats;
+    std::vector<pcv::FoldBlockSums> blocks;
+    for (int k = 0; k < k_folds; ++k) {
+      const auto st = pcv::rhat_from_blocks(acc[k], n);
+      rhats.push_back(st ? st->rhat : std::numeric_limits<double>::quiet_NaN());
+      blocks.push_back(pcv::gather_block_sums(acc[k], n));
+    }
+    const double obs = pcv::rhat_max(rhats);
+    const auto bench = pcv::shuffle_benchmark(blocks, bench_draws, run_seed);
+    const auto v = pcv::benchmark_verdict(obs, bench, 0.99);
+    *observed = v.observed;
+    *quantile_value = v.quantile_value;
+    *pass = v.pass ? 1 : 0;
   });
 }
 

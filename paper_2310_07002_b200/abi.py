@@ -10,7 +10,7 @@ import os
 
 import numpy as np
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 OK, INVALID_INPUT, NUMERIC_FAULT, ADAPTATION_FAILURE, UNDEFINED_DIAGNOSTIC, \
     UNSUPPORTED_SCORE, CUDA_ERROR, COMM_ERROR = range(8)

@@ -20,7 +20,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr"]
 SOURCES = ["gauss_kernel.cu", "suff_kernel.cu", "glm_kernel.cu", "glm32_kernel.cu", "chain_kernels.cu", "api.cpp", "stats.cpp",
            "host_folds.cpp", "suffstats.cpp"]
-HEADERS = ["device_common.cuh", "types.cuh", "host_common.hpp", "tc_common.cuh", "score_extra.cuh", "suffstats.hpp", "gauss_impl.cuh"]
+HEADERS = ["device_cache.hpp", "device_common.cuh", "types.cuh", "host_common.hpp", "tc_common.cuh", "score_extra.cuh", "suffstats.hpp", "gauss_impl.cuh"]
 
 
 def _newer(target, deps):

@@ -47,12 +47,13 @@ cudaError_t launch_fold_stats(const ChainsDev& S, int nfold, int64_t n, int b, i
                               double* estimate, double* log_f_hat, double* mc, double* naive,
                               double* ess, double* rhat, int64_t* batches, int32_t* fault,
                               cudaStream_t st);
-cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, int D, int b,
+cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t stride, int64_t i0, int64_t i1,
+                                int64_t planned_n, int D, int b,
                                 cudaStream_t st);
 cudaError_t launch_extra_centers(const ChainsDev& S, int nfold, int64_t warmup, cudaStream_t st);
 cudaError_t launch_extra_merge(const ChainsDev& S, int nfold, double* merged, cudaStream_t st);
-cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int D_used,
-                         int D_stride, int64_t n, unsigned long long* rep_max, int* reject,
+cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int sub_used,
+                         int groups, int64_t n, unsigned long long* rep_max, int* reject,
                          cudaStream_t st);
 // host_folds.cpp
 void rng_sequence(uint64_t, uint64_t, int32_t, uint64_t, const char*, const uint64_t*, int64_t, double*);
@@ -67,8 +68,8 @@ void simulate_logistic(int64_t, int32_t, uint64_t, double*, double*);
 // stats.cpp
 void merge_stats(int32_t n_models, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
                  int32_t final_checkpoint, const pcvg_fold_table* folds, const double* y_x,
-                 const double* y_x2, int D_used, pcvg_report* rep, const double* bench_max);
-void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t D_used, int64_t n,
+                 const double* y_x2, int sub_used, pcvg_report* rep, const double* bench_max);
+void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t sub_used, int32_t groups, int64_t n,
                  uint64_t seed, int32_t R, const double* y_x, const double* y_x2,
                  const int32_t* failed, int64_t nonfailed_before, int64_t nonfailed_total,
                  double* rep_max, int32_t* needs_host);
@@ -230,6 +231,9 @@ struct pcvg_ctx {
   double last_ms = 0.0, warm_ms = 0.0, sample_ms = 0.0;
   int64_t launches = 0;
   int policy = PCVG_KERNEL_AUTO;
+  // score-stream runs (pcvg_run_streams): chains observe given log_pred streams instead of sampling
+  bool stream_mode = false;
+  DevBuf<double> stream_scores;  // [K*L][iters]
 };
 
 namespace {
@@ -609,6 +613,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.ng = m.ng;
   md.dim = m.dim;
   md.K = m.K;
+  md.broken_fold = -1;
   md.y = m.y.p;
   md.x = m.x.p;
   md.xr = m.xr.p;
@@ -738,6 +743,18 @@ int effective_batch(const pcvg_run_config* c) {  // engine.cpp:5-9
   return std::max(1, static_cast<int>(std::sqrt(static_cast<double>(c->iters) * c->chains)));
 }
 
+// Shuffle sub-blocks stored per chain: RunConfig::blocks, or one per check interval under early
+// stop (regrouped into `blocks` benchmark blocks at each checkpoint).
+int sub_block_count(const pcvg_run_config* c) {
+  return c->early_stop ? static_cast<int>(c->iters / c->checkpoint_every) : c->blocks;
+}
+
+// Sub-blocks completed after iter_count sampling iterations (a checkpoint).
+int completed_sub_blocks(const pcvg_run_config* c, int64_t iter_count) {
+  if (!c->early_stop) return c->blocks;
+  return static_cast<int>(std::clamp<int64_t>(iter_count / c->checkpoint_every, 1, c->iters / c->checkpoint_every));
+}
+
 void validate_run(const pcvg_ctx* ctx, const pcvg_run_config* c) {
   if (!c) throw Error(PCVG_INVALID_INPUT, "null run config");
   // RunConfig::validate, engine.cpp:21-30
@@ -769,6 +786,9 @@ void validate_run(const pcvg_ctx* ctx, const pcvg_run_config* c) {
   if (c->early_stop) {
     if (c->checkpoint_every <= 0 || c->iters % c->checkpoint_every != 0)
       throw Error(PCVG_INVALID_INPUT, "early_stop needs checkpoint_every dividing iters");
+    // the rule needs at least `blocks` completed check intervals to form the benchmark's blocks
+    if (c->iters / c->checkpoint_every < c->blocks)
+      throw Error(PCVG_INVALID_INPUT, "early_stop needs iters / checkpoint_every >= blocks");
   }
 }
 
@@ -846,7 +866,7 @@ void extra_estimates(pcvg_ctx* ctx, const HostModel& m, const ChainSet& cs, int 
 
 // Shuffle benchmark of the shard on device (bench_kernel): replicate maxima + rejection flags.
 void device_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_before,
-                      int64_t nonfailed_total, int D_used, double* rep_max, int32_t* needs_host) {
+                      int64_t nonfailed_total, int sub_used, double* rep_max, int32_t* needs_host) {
   const pcvg_run_config& cfg = ctx->cfg;
   const int nfold = ctx->fe - ctx->fb, L = cfg.chains, R = cfg.bench_draws;
   DevBuf<unsigned long long> mx;
@@ -863,8 +883,8 @@ void device_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_be
     DevBuf<int64_t> it;
     it.upload(item);
     const ChainSet& cs = *ctx->chains[mi];
-    ck(launch_bench(cs.view(L, ctx->fb, cfg.seed, 0), nfold, it.p, R, D_used, cs.D, ctx->iters_done,
-                    mx.p, rj.p, ctx->stream), "benchmark");
+    ck(launch_bench(cs.view(L, ctx->fb, cfg.seed, 0), nfold, it.p, R, sub_used, std::min(cfg.blocks, sub_used),
+                    ctx->iters_done, mx.p, rj.p, ctx->stream), "benchmark");
     ++ctx->launches;
     ck(cudaStreamSynchronize(ctx->stream), "benchmark");  // `it` is freed at scope exit
   }
@@ -1004,6 +1024,14 @@ pcvg_status pcvg_add_model(pcvg_ctx* ctx, const pcvg_dataset* data, const pcvg_f
     ctx->models.push_back(build_model(data, folds, spec, kernel, bank, bank_rows, model_id));
     ctx->begun = false;
     if (slot) *slot = static_cast<int32_t>(ctx->models.size() - 1);
+  }));
+}
+
+pcvg_status pcvg_debug_break_fold(pcvg_ctx* ctx, int32_t slot, int32_t fold) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= static_cast<int>(ctx->models.size())) throw Error(PCVG_INVALID_INPUT, "bad slot");
+    if (fold < -1 || fold >= ctx->models[slot]->K) throw Error(PCVG_INVALID_INPUT, "fold out of range");
+    ctx->models[slot]->md.broken_fold = fold;
   }));
 }
 
@@ -1235,7 +1263,7 @@ pcvg_status pcvg_score_streams(pcvg_ctx* ctx, int32_t L, int64_t n, const double
     ChainsDev S = cs.view(L, 0, 0, 0);
     ck(cudaMemset(cs.warm.p, 0, sizeof(double) * L), "memset");
     ck(launch_centers(S, 0, 0, centers.p, D, ctx->stream), "reset");  // nfold 0: no centre recompute
-    ck(launch_feed_streams(S, streams.p, n, D, b, ctx->stream), "feed");
+    ck(launch_feed_streams(S, streams.p, n, 0, n, n, D, b, ctx->stream), "feed");
     DevBuf<double> o;
     o.alloc(6);
     DevBuf<int64_t> bt;
@@ -1274,10 +1302,12 @@ pcvg_status pcvg_begin(pcvg_ctx* ctx, const pcvg_run_config* cfg) {
     ctx->fe = (cfg->fold_begin == 0 && cfg->fold_end == 0) ? K : cfg->fold_end;
     const int nfold = ctx->fe - ctx->fb;
     const int L = cfg->chains;
-    const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
+    const int D = sub_block_count(cfg);
     ctx->chains.clear();
     ctx->centers.clear();
     ctx->div_base.clear();
+    ctx->stream_mode = false;
+    ctx->stream_scores.alloc(0);
     ctx->iters_done = 0;
     ctx->sample_ms = 0.0;
     ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
@@ -1329,7 +1359,13 @@ pcvg_status pcvg_advance(pcvg_ctx* ctx, int64_t n_iters) {
     const pcvg_run_config& cfg = ctx->cfg;
     ck(cudaEventRecord(ctx->ev0, ctx->stream), "event");
     ck(cudaStreamWaitEvent(ctx->stream2, ctx->ev0, 0), "wait");
-    for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+    if (ctx->stream_mode && n_iters > 0) {
+      const ChainSet& cs = *ctx->chains[0];
+      ck(launch_feed_streams(cs.view(cfg.chains, 0, cfg.seed, 0), ctx->stream_scores.p, cfg.iters, ctx->iters_done,
+                             ctx->iters_done + n_iters, cfg.iters, cs.D, ctx->b, ctx->stream), "feed");
+      ++ctx->launches;
+    }
+    for (size_t mi = 0; mi < ctx->models.size() && !ctx->stream_mode; ++mi) {
       const HostModel& m = *ctx->models[mi];
       const uint64_t sm = cfg.shared_streams ? 0u : static_cast<uint64_t>(m.model_id);
       const ChainsDev S = ctx->chains[mi]->view(cfg.chains, ctx->fb, cfg.seed, sm);
@@ -1360,7 +1396,7 @@ pcvg_status pcvg_fold_stats(pcvg_ctx* ctx, pcvg_fold_table* out, int64_t* diverg
     require_device(ctx);
     const pcvg_run_config& cfg = ctx->cfg;
     const int nfold = ctx->fe - ctx->fb, L = cfg.chains;
-    const int nm = static_cast<int>(ctx->models.size());
+    const int nm = static_cast<int>(ctx->chains.size());
     std::vector<std::vector<int64_t>> sdiv(nm);
     int64_t drop = 0;
     for (int mi = 0; mi < nm; ++mi) {
@@ -1452,8 +1488,8 @@ pcvg_status pcvg_merge(int32_t n_models, int32_t K, const pcvg_run_config* cfg, 
   return static_cast<pcvg_status>(guarded(nullptr, [&] {
     if (!cfg || !folds || !report || n_models < 1 || n_models > 2 || K < 2)
       throw Error(PCVG_INVALID_INPUT, "bad merge arguments");
-    const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
-    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, y_x, y_x2, D, report, nullptr);
+    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, y_x, y_x2, completed_sub_blocks(cfg, iter_count),
+                report, nullptr);
   }));
 }
 
@@ -1472,15 +1508,15 @@ pcvg_status pcvg_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfail
 }
 
 pcvg_status pcvg_benchmark_host(int32_t n_models, int32_t nfold, int32_t L, int32_t D_stride,
-                                int32_t blocks_used, int64_t iter_count, uint64_t seed,
+                                int32_t blocks_used, int32_t block_groups, int64_t iter_count, uint64_t seed,
                                 int32_t bench_draws, const double* y_x, const double* y_x2,
                                 const int32_t* failed, int64_t nonfailed_before,
                                 int64_t nonfailed_total, double* rep_max, int32_t* needs_host) {
   return static_cast<pcvg_status>(guarded(nullptr, [&] {
     if (n_models < 1 || n_models > 2 || nfold < 0 || L < 2 || blocks_used < 1 || blocks_used > D_stride ||
-        bench_draws < 0 || !y_x || !y_x2 || !rep_max || !needs_host)
+        block_groups < 1 || block_groups > blocks_used || bench_draws < 0 || !y_x || !y_x2 || !rep_max || !needs_host)
       throw Error(PCVG_INVALID_INPUT, "bad benchmark arguments");
-    bench_shard(n_models, nfold, L, D_stride, blocks_used, iter_count, seed, bench_draws, y_x, y_x2,
+    bench_shard(n_models, nfold, L, D_stride, blocks_used, block_groups, iter_count, seed, bench_draws, y_x, y_x2,
                 failed, nonfailed_before, nonfailed_total, rep_max, needs_host);
   }));
 }
@@ -1492,10 +1528,124 @@ pcvg_status pcvg_merge_bench(int32_t n_models, int32_t K, const pcvg_run_config*
   return static_cast<pcvg_status>(guarded(nullptr, [&] {
     if (!cfg || !folds || !report || !bench_max || n_models < 1 || n_models > 2 || K < 2)
       throw Error(PCVG_INVALID_INPUT, "bad merge arguments");
-    const int D = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
-    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, nullptr, nullptr, D, report, bench_max);
+    merge_stats(n_models, K, cfg, iter_count, final_checkpoint, folds, nullptr, nullptr,
+                completed_sub_blocks(cfg, iter_count), report, bench_max);
   }));
 }
+
+}  // extern "C"
+
+namespace {
+
+// Steps 3-4 of run_pcv (engine.cpp:342-483) on a begun context that owns every fold: advance to each
+// checkpoint, per-fold statistics, snapshot merge; at the last checkpoint (or when the early-stop rule
+// fires) the shuffle benchmark, exclusions and the final report.
+void run_checkpoints(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep) {
+  int32_t st = PCVG_OK;
+  const int K = ctx->fe - ctx->fb, L = cfg->chains;
+  const int nm = static_cast<int>(ctx->chains.size());
+  const int D = ctx->chains[0]->D;
+  std::vector<int64_t> cks;
+  if (cfg->checkpoint_every > 0)
+    for (int64_t t = cfg->checkpoint_every; t < cfg->iters; t += cfg->checkpoint_every) cks.push_back(t);
+  cks.push_back(cfg->iters);
+  // per-fold scratch table
+  const size_t rows = static_cast<size_t>(nm) * K;
+  std::vector<double> est(rows), lf(rows), mc(rows), nv(rows), ess(rows), rh(rows);
+  std::vector<int64_t> bt(rows);
+  std::vector<int32_t> ft(rows), fl(rows), rg(rows);
+  pcvg_fold_table tab{est.data(), lf.data(), mc.data(), nv.data(), ess.data(), rh.data(), bt.data(), ft.data(), fl.data(), rg.data()};
+  std::vector<double> yx(rows * L * D), yx2(rows * L * D);
+  int64_t dropped = 0, done = 0;
+  std::vector<int64_t> divs(rows * L);
+  rep->n_checkpoints = 0;
+  bool stopped = false;
+  for (size_t ci = 0; ci < cks.size() && !stopped; ++ci) {
+    st = pcvg_advance(ctx, cks[ci] - ctx->iters_done);
+    if (st != PCVG_OK) throw Error(st, ctx->err);
+    st = pcvg_fold_stats(ctx, &tab, divs.data(), &dropped, &done);
+    if (st != PCVG_OK) throw Error(st, ctx->err);
+    const bool last = ci + 1 == cks.size();
+    bool final_ck = last;
+    if (cfg->early_stop && !last && static_cast<int>(ci + 1) >= cfg->blocks) {
+      // Early-stop rule: the completed check intervals (sub-blocks) are regrouped into
+      // `blocks` benchmark blocks, so the rule only looks once there are at least that many.
+      pcvg_report probe = *rep;
+      std::vector<double> bench(cfg->bench_draws);
+      probe.benchmark = bench.data();
+      probe.snapshots = nullptr;
+      probe.delta_k = nullptr;
+      pcvg_fold_table t2 = tab;
+      t2.failed = nullptr;
+      std::vector<double> bmax(cfg->bench_draws);
+      std::vector<int32_t> bhost(cfg->bench_draws);
+      device_benchmark(ctx, nullptr, 0, K, completed_sub_blocks(cfg, done), bmax.data(), bhost.data());
+      const bool host_path = std::any_of(bhost.begin(), bhost.end(), [](int32_t v) { return v != 0; });
+      if (host_path) {
+        st = pcvg_block_sums(ctx, yx.data(), yx2.data());
+        if (st != PCVG_OK) throw Error(st, ctx->err);
+      }
+      merge_stats(nm, K, cfg, done, 2, &t2, yx.data(), yx2.data(), completed_sub_blocks(cfg, done), &probe,
+                  host_path ? nullptr : bmax.data());
+      if (probe.verdict_pass && std::isfinite(probe.rhat_max) && probe.mcse < probe.epistemic_se) final_ck = true;
+    }
+    if (final_ck) {
+      // shuffle benchmark on device over the non-failed folds (failed flags from fold_stats)
+      const int D_used = completed_sub_blocks(cfg, done);
+      int64_t nonfailed = 0;
+      for (int k = 0; k < K; ++k) nonfailed += fl[k] ? 0 : 1;
+      std::vector<double> bmax(cfg->bench_draws);
+      std::vector<int32_t> bhost(cfg->bench_draws);
+      device_benchmark(ctx, fl.data(), 0, nonfailed, D_used, bmax.data(), bhost.data());
+      const bool host_path = std::any_of(bhost.begin(), bhost.end(), [](int32_t v) { return v != 0; });
+      if (host_path) {  // a below() rejection: the reference's sequential stream on the host
+        st = pcvg_block_sums(ctx, yx.data(), yx2.data());
+        if (st != PCVG_OK) throw Error(st, ctx->err);
+      }
+      merge_stats(nm, K, cfg, done, 1, &tab, yx.data(), yx2.data(), D_used, rep,
+                  host_path ? nullptr : bmax.data());
+      stopped = true;
+    } else {
+      pcvg_fold_table t2 = tab;
+      t2.failed = nullptr;
+      merge_stats(nm, K, cfg, done, 0, &t2, nullptr, nullptr, D, rep, nullptr);
+    }
+    if (rep->snapshots) {
+      double* o = rep->snapshots + 7 * ci;
+      o[0] = static_cast<double>(done);
+      o[1] = rep->delta_hat;
+      o[2] = rep->mcse;
+      o[3] = rep->epistemic_se;
+      o[4] = rep->prob_a_better;
+      o[5] = rep->ess_overall;
+      o[6] = rep->rhat_max;
+    }
+    rep->n_checkpoints = static_cast<int32_t>(ci + 1);
+  }
+  // final tables
+  for (size_t i = 0; i < rows; ++i) {
+    rep->folds.estimate[i] = est[i];
+    rep->folds.log_f_hat[i] = lf[i];
+    rep->folds.mc_contribution[i] = mc[i];
+    if (rep->folds.naive_contribution) rep->folds.naive_contribution[i] = nv[i];
+    rep->folds.ess[i] = ess[i];
+    rep->folds.rhat[i] = rh[i];
+    rep->folds.batches[i] = bt[i];
+    rep->folds.fault[i] = ft[i];
+    if (rep->folds.dss_ridged) rep->folds.dss_ridged[i] = rg[i];
+  }
+  // failed flags after exclusions are written by merge_stats into rep->folds.failed
+  std::copy(divs.begin(), divs.end(), rep->divergences);
+  rep->dropped_batch_draws = dropped;
+  rep->iters_run = done;
+  rep->warmup_ms = ctx->warm_ms;
+  rep->sampling_ms = ctx->sample_ms;
+  rep->gpu_launches = ctx->launches;
+}
+
+}  // namespace
+
+extern "C" {
 
 pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep) {
   return static_cast<pcvg_status>(guarded(ctx, [&] {
@@ -1505,104 +1655,51 @@ pcvg_status pcvg_run(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
       throw Error(PCVG_INVALID_INPUT, "pcvg_run runs every fold; shard with the stepwise API");
     int32_t st = pcvg_begin(ctx, cfg);
     if (st != PCVG_OK) throw Error(st, ctx->err);
-    const int K = ctx->models[0]->K, L = cfg->chains;
-    const int nm = static_cast<int>(ctx->models.size());
-    const int D = ctx->chains[0]->D;
-    std::vector<int64_t> cks;
-    if (cfg->checkpoint_every > 0)
-      for (int64_t t = cfg->checkpoint_every; t < cfg->iters; t += cfg->checkpoint_every) cks.push_back(t);
-    cks.push_back(cfg->iters);
-    // per-fold scratch table
-    const size_t rows = static_cast<size_t>(nm) * K;
-    std::vector<double> est(rows), lf(rows), mc(rows), nv(rows), ess(rows), rh(rows);
-    std::vector<int64_t> bt(rows);
-    std::vector<int32_t> ft(rows), fl(rows), rg(rows);
-    pcvg_fold_table tab{est.data(), lf.data(), mc.data(), nv.data(), ess.data(), rh.data(), bt.data(), ft.data(), fl.data(), rg.data()};
-    std::vector<double> yx(rows * L * D), yx2(rows * L * D);
-    int64_t dropped = 0, done = 0;
-    std::vector<int64_t> divs(rows * L);
-    rep->n_checkpoints = 0;
-    bool stopped = false;
-    for (size_t ci = 0; ci < cks.size() && !stopped; ++ci) {
-      st = pcvg_advance(ctx, cks[ci] - ctx->iters_done);
-      if (st != PCVG_OK) throw Error(st, ctx->err);
-      st = pcvg_fold_stats(ctx, &tab, divs.data(), &dropped, &done);
-      if (st != PCVG_OK) throw Error(st, ctx->err);
-      const bool last = ci + 1 == cks.size();
-      bool final_ck = last;
-      if (cfg->early_stop && !last) {
-        // Early-stop rule: blocks are the completed check intervals.
-        pcvg_report probe = *rep;
-        std::vector<double> bench(cfg->bench_draws);
-        probe.benchmark = bench.data();
-        probe.snapshots = nullptr;
-        probe.delta_k = nullptr;
-        pcvg_fold_table t2 = tab;
-        t2.failed = nullptr;
-        std::vector<double> bmax(cfg->bench_draws);
-        std::vector<int32_t> bhost(cfg->bench_draws);
-        device_benchmark(ctx, nullptr, 0, K, static_cast<int>(ci + 1), bmax.data(), bhost.data());
-        const bool host_path = std::any_of(bhost.begin(), bhost.end(), [](int32_t v) { return v != 0; });
-        if (host_path) {
-          st = pcvg_block_sums(ctx, yx.data(), yx2.data());
-          if (st != PCVG_OK) throw Error(st, ctx->err);
-        }
-        merge_stats(nm, K, cfg, done, 2, &t2, yx.data(), yx2.data(), static_cast<int>(ci + 1), &probe,
-                    host_path ? nullptr : bmax.data());
-        if (probe.verdict_pass && std::isfinite(probe.rhat_max) && probe.mcse < probe.epistemic_se) final_ck = true;
-      }
-      if (final_ck) {
-        // shuffle benchmark on device over the non-failed folds (failed flags from fold_stats)
-        const int D_used = last ? D : static_cast<int>(ci + 1);
-        int64_t nonfailed = 0;
-        for (int k = 0; k < K; ++k) nonfailed += fl[k] ? 0 : 1;
-        std::vector<double> bmax(cfg->bench_draws);
-        std::vector<int32_t> bhost(cfg->bench_draws);
-        device_benchmark(ctx, fl.data(), 0, nonfailed, D_used, bmax.data(), bhost.data());
-        const bool host_path = std::any_of(bhost.begin(), bhost.end(), [](int32_t v) { return v != 0; });
-        if (host_path) {  // a below() rejection: the reference's sequential stream on the host
-          st = pcvg_block_sums(ctx, yx.data(), yx2.data());
-          if (st != PCVG_OK) throw Error(st, ctx->err);
-        }
-        merge_stats(nm, K, cfg, done, 1, &tab, yx.data(), yx2.data(), D_used, rep,
-                    host_path ? nullptr : bmax.data());
-        stopped = true;
-      } else {
-        pcvg_fold_table t2 = tab;
-        t2.failed = nullptr;
-        merge_stats(nm, K, cfg, done, 0, &t2, nullptr, nullptr, D, rep, nullptr);
-      }
-      if (rep->snapshots) {
-        double* o = rep->snapshots + 7 * ci;
-        o[0] = static_cast<double>(done);
-        o[1] = rep->delta_hat;
-        o[2] = rep->mcse;
-        o[3] = rep->epistemic_se;
-        o[4] = rep->prob_a_better;
-        o[5] = rep->ess_overall;
-        o[6] = rep->rhat_max;
-      }
-      rep->n_checkpoints = static_cast<int32_t>(ci + 1);
-    }
-    // final tables
-    for (size_t i = 0; i < rows; ++i) {
-      rep->folds.estimate[i] = est[i];
-      rep->folds.log_f_hat[i] = lf[i];
-      rep->folds.mc_contribution[i] = mc[i];
-      if (rep->folds.naive_contribution) rep->folds.naive_contribution[i] = nv[i];
-      rep->folds.ess[i] = ess[i];
-      rep->folds.rhat[i] = rh[i];
-      rep->folds.batches[i] = bt[i];
-      rep->folds.fault[i] = ft[i];
-      if (rep->folds.dss_ridged) rep->folds.dss_ridged[i] = rg[i];
-    }
-    // failed flags after exclusions are written by merge_stats into rep->folds.failed
-    std::copy(divs.begin(), divs.end(), rep->divergences);
-    rep->dropped_batch_draws = dropped;
-    rep->iters_run = done;
-    rep->warmup_ms = ctx->warm_ms;
-    rep->sampling_ms = ctx->sample_ms;
-    rep->gpu_launches = ctx->launches;
+    run_checkpoints(ctx, cfg, rep);
+  }));
+}
+
+pcvg_status pcvg_run_streams(pcvg_ctx* ctx, int32_t K, const double* s, const double* centers,
+                             const pcvg_run_config* cfg, pcvg_report* rep) {
+  return static_cast<pcvg_status>(guarded(ctx, [&] {
+    if (!ctx || !s || !centers || !cfg || !rep) throw Error(PCVG_INVALID_INPUT, "null argument");
+    if (!ctx->models.empty()) throw Error(PCVG_INVALID_INPUT, "score-stream runs need a context without models");
+    const pcvg_run_config* c = cfg;
+    if (c->chains < 2 || c->chains > 64) throw Error(PCVG_INVALID_INPUT, "need 2..64 chains per fold");
+    if (c->iters < 1 || c->iters < effective_batch(c)) throw Error(PCVG_INVALID_INPUT, "chain length must cover a batch");
+    if (c->blocks < 1 || c->bench_draws < 1 || c->checkpoint_every < 0 || K < 2)
+      throw Error(PCVG_INVALID_INPUT, "bad run configuration");
+    if (c->score != PCVG_SCORE_LOGS) throw Error(PCVG_UNSUPPORTED_SCORE, "score streams carry LogS only");
+    if (c->fold_begin != 0 || c->fold_end != 0) throw Error(PCVG_INVALID_INPUT, "score-stream runs are unsharded");
+    if (c->early_stop && (c->checkpoint_every <= 0 || c->iters % c->checkpoint_every != 0 ||
+                          c->iters / c->checkpoint_every < c->blocks))
+      throw Error(PCVG_INVALID_INPUT, "early_stop needs checkpoint_every dividing iters into >= blocks intervals");
+    require_device(ctx);
+    ctx->cfg = *cfg;
+    ctx->b = effective_batch(cfg);
+    ctx->fb = 0;
+    ctx->fe = K;
+    const int L = cfg->chains, D = sub_block_count(cfg);
+    ctx->chains.clear();
+    ctx->centers.clear();
+    ctx->div_base.clear();
+    ctx->iters_done = 0;
+    ctx->sample_ms = ctx->warm_ms = 0.0;
+    auto cs = std::make_unique<ChainSet>();
+    cs->alloc(K * L, 1, D);
+    ck(cudaMemset(cs->div.p, 0, sizeof(int64_t) * cs->div.n), "memset");
+    ck(cudaMemset(cs->pending.p, 0, sizeof(int32_t) * cs->pending.n), "memset");
+    auto cb = std::make_unique<DevBuf<double>>();
+    cb->upload(std::vector<double>(centers, centers + K));
+    ck(launch_centers(cs->view(L, 0, cfg->seed, 0), 0, 0, cb->p, D, ctx->stream), "reset");  // given centres
+    ++ctx->launches;
+    ctx->stream_scores.upload(std::vector<double>(s, s + static_cast<size_t>(K) * L * cfg->iters));
+    ctx->div_base.push_back(std::vector<int64_t>(static_cast<size_t>(K) * L, 0));
+    ctx->chains.push_back(std::move(cs));
+    ctx->centers.push_back(std::move(cb));
+    ctx->stream_mode = true;
+    ctx->begun = true;
+    run_checkpoints(ctx, cfg, rep);
   }));
 }
 

@@ -177,11 +177,13 @@ __global__ void fold_stats_kernel(ChainsDev S, int nfold, int64_t n, int b, int 
   out.fault[k] = fault ? 1 : 0;
 }
 
-// Probe: chain c feeds its explicit score stream through accum_observe (accum.cpp:164-182).
-__global__ void feed_streams_kernel(ChainsDev S, const double* s, int64_t n, int D, int b) {
+// Score streams: chain c feeds iterations [i0, i1) of its explicit stream s[c * stride + i] through
+// accum_observe (accum.cpp:164-182) of a planned_n-iteration run.
+__global__ void feed_streams_kernel(ChainsDev S, const double* s, int64_t stride, int64_t i0, int64_t i1,
+                                    int64_t planned_n, int D, int b) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= S.nch) return;
-  for (int64_t i = 0; i < n; ++i) accum_observe(S.acc, c, S.nch, s[c * n + i], i, n, D, b);
+  for (int64_t i = i0; i < i1; ++i) accum_observe(S.acc, c, S.nch, s[c * stride + i], i, planned_n, D, b);
 }
 
 __global__ void extra_centers_kernel(ExtraDev X, int L, int nfold, int64_t warmup) {
@@ -219,8 +221,8 @@ __global__ void extra_merge_kernel(ExtraDev X, int L, int nfold, double* merged)
 // words 2j, 2j+1: every item computes its draws at its global position and flags a rejection
 // (the caller then runs the sequential host path for that replicate). R-hat > 0 always, so the
 // maximum is kept as the bit pattern of a non-negative double (0 = no item) via atomicMax.
-__global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R, int D_used,
-                             int D_stride, int64_t n, unsigned long long* rep_max, int* reject) {
+__global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R, int sub_used,
+                             int groups, int64_t n, unsigned long long* rep_max, int* reject) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int k = static_cast<int>(idx % nfold);
   const int r = static_cast<int>(idx / nfold);
@@ -230,7 +232,7 @@ __global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R,
   const uint64_t bound = L64 * ((~0ull) / L64);
   const uint64_t stream = stream_key(6 /*Benchmark*/, static_cast<uint64_t>(r), 0, 0);
   const uint32_t k0 = static_cast<uint32_t>(S.seed), k1 = static_cast<uint32_t>(S.seed >> 32);
-  uint64_t word = 2ull * static_cast<uint64_t>(item[k]) * L64 * static_cast<uint64_t>(D_used);
+  uint64_t word = 2ull * static_cast<uint64_t>(item[k]) * L64 * static_cast<uint64_t>(groups);
   uint64_t blk_cached = ~0ull;
   uint4 buf = make_uint4(0, 0, 0, 0);
   bool rej = false;
@@ -238,7 +240,7 @@ __global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R,
   const size_t c0 = static_cast<size_t>(k) * l;
   for (int c = 0; c < l; ++c) {
     double a = 0.0, b = 0.0;
-    for (int d = 0; d < D_used; ++d, word += 2) {
+    for (int g = 0; g < groups; ++g, word += 2) {
       const uint64_t blk = word >> 2;
       if (blk != blk_cached) {
         buf = philox_block(blk, stream, k0, k1);
@@ -248,13 +250,18 @@ __global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R,
                                     : (static_cast<uint64_t>(buf.x) | (static_cast<uint64_t>(buf.y) << 32));
       rej |= v >= bound;
       const size_t src = c0 + static_cast<size_t>(v % L64);
-      a += S.acc.y_x[static_cast<size_t>(d) * S.nch + src];
-      b += S.acc.y_x2[static_cast<size_t>(d) * S.nch + src];
+      // block g = sub-blocks [g*sub_used/groups, (g+1)*sub_used/groups) (one sub-block when equal)
+      double ga = 0.0, gb = 0.0;
+      for (int d = block_group_begin(g, sub_used, groups); d < block_group_begin(g + 1, sub_used, groups); ++d) {
+        ga += S.acc.y_x[static_cast<size_t>(d) * S.nch + src];
+        gb += S.acc.y_x2[static_cast<size_t>(d) * S.nch + src];
+      }
+      a += ga;
+      b += gb;
     }
     sx[c] = a;
     sxx[c] = b;
   }
-  (void)D_stride;
   if (rej) reject[r] = 1;
   double rh;
   if (!rhat_from_sums_dev(sx, sxx, l, n, &rh)) return;
@@ -263,14 +270,14 @@ __global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R,
 
 }  // namespace
 
-cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int D_used,
-                         int D_stride, int64_t n, unsigned long long* rep_max, int* reject,
+cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int sub_used,
+                         int groups, int64_t n, unsigned long long* rep_max, int* reject,
                          cudaStream_t st) {
   if (nfold == 0 || R == 0) return cudaSuccess;
   if (S.L > 64) return cudaErrorInvalidValue;
   const int64_t total = static_cast<int64_t>(nfold) * R;
-  bench_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, st>>>(S, nfold, item, R, D_used,
-                                                                         D_stride, n, rep_max, reject);
+  bench_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, st>>>(S, nfold, item, R, sub_used,
+                                                                         groups, n, rep_max, reject);
   return cudaGetLastError();
 }
 
@@ -286,9 +293,9 @@ cudaError_t launch_extra_merge(const ChainsDev& S, int nfold, double* merged, cu
   return cudaGetLastError();
 }
 
-cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t n, int D, int b,
-                                cudaStream_t st) {
-  feed_streams_kernel<<<(S.nch + 127) / 128, 128, 0, st>>>(S, s, n, D, b);
+cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t stride, int64_t i0, int64_t i1,
+                                int64_t planned_n, int D, int b, cudaStream_t st) {
+  feed_streams_kernel<<<(S.nch + 127) / 128, 128, 0, st>>>(S, s, stride, i0, i1, planned_n, D, b);
   return cudaGetLastError();
 }
 

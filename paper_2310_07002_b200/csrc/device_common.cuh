@@ -13,6 +13,14 @@
 namespace pcvg {
 
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;
+
+// Shuffle-benchmark blocks over stored sub-blocks: with `sub` completed sub-blocks
+// regrouped into `groups` blocks, block g covers sub-blocks [begin(g), begin(g + 1)). Without early
+// stop sub == groups == RunConfig::blocks and every block is one sub-block (the reference layout,
+// accum.cpp:129-156).
+__host__ __device__ inline int block_group_begin(int g, int sub, int groups) {
+  return static_cast<int>(static_cast<int64_t>(g) * sub / groups);
+}
 constexpr double kTwoPi = 6.283185307179586476925286766559;
 
 __host__ __device__ inline uint64_t mix64(uint64_t z) {  // rng.hpp:18-23

@@ -19,6 +19,7 @@
 
 #include <cstdlib>
 
+#include "device_cache.hpp"
 #include "device_common.cuh"
 #include "score_extra.cuh"
 #include "tc_common.cuh"
@@ -1323,6 +1324,7 @@ __global__ void __launch_bounds__(kBlock, NB > 0 ? 3 : (NB == -2 ? 4 : (NB < 0 &
         }
       }
     }
+    bad |= fold == M.broken_fold;
     const double h0 = -lp0 + 0.5 * (k0g + k0G);
     const double h1 = bad ? CUDART_NAN : -lp1 + 0.5 * (k1g + k1G);
     const double dh = h1 - h0;

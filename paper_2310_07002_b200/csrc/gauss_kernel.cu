@@ -31,12 +31,9 @@ template <int FAM, int NCM, int NGM, int NB>
 cudaError_t launch_nb(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st, int grid) {
   const size_t smem = kRing * ring_slot_bytes(M) + 16 * kRing +
                       (FAM == kRatA ? 4 : 2) * static_cast<size_t>(M.nb) * kBlock * sizeof(double);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, 32, NCM, NGM, NB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  {
+    cudaError_t e = ensure_kernel_smem(reinterpret_cast<const void*>(gauss_kernel<FAM, 32, NCM, NGM, NB>), smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   ++sampler_launch_count();
   gauss_kernel<FAM, 32, NCM, NGM, NB><<<grid, kBlock, smem, st>>>(M, S, A);
@@ -58,7 +55,7 @@ cudaError_t launch_batched(const ModelDev& M, const ChainsDev& S, const RunArgs&
 // is not reachable with few chains, so few chains get whole warps), capped by the rows a lane
 // would own in the smallest segment.
 int gauss_lanes_per_chain(const ModelDev& M, int nch) {
-  const long target_threads = 148L * 512;
+  const long target_threads = static_cast<long>(device_sm_count()) * 512;
   int T = 1;
   while (T < 32 && static_cast<long>(nch) * T < target_threads) T *= 2;
   if (T == 2) T = 4;

@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstring>
 
+#include "device_cache.hpp"
 #include "device_common.cuh"
 #include "tc_common.cuh"
 #include "types.cuh"
@@ -637,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm32_kernel(ModelDev M, ChainsDe
 #pragma unroll
           for (int o = 0; o < kOwners; ++o) k1 += sm.red[o][tid];
           const double lp1 = lp_from_partials(tid);
-          const bool bad = sm.bad[tid] != 0;
+          const bool bad = sm.bad[tid] != 0 || fold == M.broken_fold;
           const double h0 = -lp0 + 0.5 * k0;
           const double h1 = bad ? CUDART_NAN : -lp1 + 0.5 * k1;
           const double dh = h1 - h0;
@@ -781,19 +782,11 @@ cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A
   const int tiles = (S.nch + kC - 1) / kC;
   if (tiles == 0) return cudaSuccess;
   if (M.family != kLogistic || M.x32 == nullptr || M.dim > kK) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(glm32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sizeof(Smem32)));
+  {
+    cudaError_t e = ensure_kernel_smem(reinterpret_cast<const void*>(glm32_kernel), sizeof(Smem32));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-  }
+  const int sms = device_sm_count();
   // Wave tail: one CTA per SM, so the last partial wave of r tiles would take a full wave time. It
   // runs instead as row-split clusters of ct CTAs (same chains, summation split by rank).
   const int ntiles_rows = (M.n + kRows - 1) / kRows;

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <math_constants.h>
 
+#include "device_cache.hpp"
 #include "device_common.cuh"
 #include "score_extra.cuh"
 #include "tc_common.cuh"
@@ -596,6 +597,9 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
       S.lp0[gc] = lp;
       if (A.out_a) A.out_a[gc] = lp;
     }
+    // rank 0 may still be reading the other ranks' reduced slices (reduce_pass copy phase): no
+    // rank may exit (releasing its shared memory) before every rank is past that point
+    if (cs > 1) cooperative_groups::this_cluster().sync();
     return;
   }
 
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev 
 #pragma unroll
         for (int o = 0; o < kOwners; ++o) k1 += sm.red[o][tid];
         const double lp1 = lp_from_partials(tid);
-        const bool bad = sm.bad[tid] != 0;
+        const bool bad = sm.bad[tid] != 0 || sm.fold[tid] == M.broken_fold;
         const double h0 = -lp0 + 0.5 * k0;
         const double h1 = bad ? CUDART_NAN : -lp1 + 0.5 * k1;
         const double dh = h1 - h0;
@@ -837,15 +841,10 @@ template <int FAM, int KP>
 cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
   const int tiles = (S.nch + kC - 1) / kC;
   if (tiles == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(glm_kernel<FAM, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sizeof(Smem<KP>)));
-    if (e != cudaSuccess) return e;
+  {
     // 16-CTA clusters (non-portable) for the fewest-chain configurations (cfg2 K-fold: 80 chains)
-    e = cudaFuncSetAttribute(glm_kernel<FAM, KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = ensure_kernel_smem(reinterpret_cast<const void*>(glm_kernel<FAM, KP>), sizeof(Smem<KP>), true);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   auto launch = [&](int tile0, int ntiles, int cs) {
     cudaLaunchConfig_t cfg = {};
@@ -865,10 +864,8 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
   };
   // Concurrently schedulable clusters of each size (a cluster must fit in one GPC): a 16-CTA cluster
   // only pays while every tile's cluster runs at once, else halve it.
-  static int active[5] = {-1, -1, -1, -1, -1};  // index log2(cs)
   auto fits = [&](int c) {
-    const int li = c == 1 ? 0 : (c == 2 ? 1 : (c == 4 ? 2 : (c == 8 ? 3 : 4)));
-    if (active[li] < 0) {
+    return cached_launch_fact(reinterpret_cast<const void*>(glm_kernel<FAM, KP>), c, [&] {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(c);
       q.blockDim = dim3(kThreads);
@@ -883,9 +880,8 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
       int nclusters = 0;
       if (cudaOccupancyMaxActiveClusters(&nclusters, glm_kernel<FAM, KP>, &q) != cudaSuccess) nclusters = 0;
       cudaGetLastError();
-      active[li] = nclusters;
-    }
-    return active[li];
+      return nclusters;
+    });
   };
   int cs = glm_cluster_size(M.n, KP, S.nch);
   while (cs > 8 && fits(cs) < tiles) cs /= 2;
@@ -899,7 +895,9 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
   if (cs == 1 && tiles > sms && tiles % sms != 0 && !no_split) {
     // Wave tail: one CTA per SM per wave, so the last partial wave of r tiles would take as long
     // as a full one. Its tiles run instead as row-split clusters of up to 8 CTAs (the cluster
-    // path of the few-chain configurations), same results bit for bit.
+    // path of the few-chain configurations). Their X^T R sums are split by rank and combined in a
+    // different order than the unsplit quarter sums, so tail chains agree with an unsplit launch to
+    // rounding only (test_wave_tail_split_matches_unsplit); full-wave chains are bit-identical.
     const int r = tiles % sms, ntiles_rows = (M.n + Geom<KP>::TM - 1) / Geom<KP>::TM;
     int ct = 1;
     while (ct < 8 && r * ct * 2 <= sms && ntiles_rows >= 4 * ct * 2) ct *= 2;
@@ -913,15 +911,7 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
 
 }  // namespace
 
-int glm_sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-  }
-  return sms;
-}
+int glm_sm_count() { return device_sm_count(); }
 
 // Cluster size: enough CTAs per 64-chain tile to cover the GPU, at most 16 (non-portable; the
 // launcher caps it at 8 where the device cannot schedule 16), and at least two row tiles per CTA.
@@ -929,8 +919,9 @@ int glm_cluster_size(int n, int kp, int nch) {
   const int tm = kp <= 8 ? 256 : (kp <= 16 ? 128 : 64);
   const int tiles = (nch + kC - 1) / kC;
   const int ntiles = (n + tm - 1) / tm;
+  const int sms = device_sm_count();
   int cs = 1;
-  while (cs < 16 && tiles * cs * 2 <= 148 && ntiles >= 4 * cs) cs *= 2;
+  while (cs < 16 && tiles * cs * 2 <= sms && ntiles >= 4 * cs) cs *= 2;
   // 16-CTA clusters only for the fewest tiles (cfg2 K-fold: 2, Step 1: 1): at most 7 fit at once,
   // and two models' launches run concurrently (cfg4 under ROWS: 7 tiles stays at 8, 0.85M vs 0.61M)
   if (cs == 16 && tiles * 16 > 64) cs = 8;

@@ -113,15 +113,13 @@ bool dss_fold_estimate(const double* merged, const double* center, const double*
   return true;
 }
 
-// final_checkpoint: 0 = intermediate snapshot (no exclusions), 1 = final (exclusions, per-model
-// report, benchmark + verdict), 2 = early-stop probe (no exclusions, benchmark + verdict on the
-// first D_used blocks).
 // Positional shuffle benchmark of one shard (the host restatement of bench_kernel,
-// chain_kernels.cu): y_x / y_x2 are the shard's block sums [m][k][c][D_stride]; item index of
+// chain_kernels.cu): y_x / y_x2 are the shard's sub-block sums [m][k][c][D_stride], of which the
+// first sub_used are regrouped into `groups` benchmark blocks (block_group_begin); item index of
 // (m, local non-failed fold j) = m * nonfailed_total + nonfailed_before + j. rep_max[r] is the max
 // R-hat over the shard's items (0 = none); needs_host[r] = 1 on a below() rejection.
-void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t D_used, int64_t n,
-                 uint64_t seed, int32_t R, const double* y_x, const double* y_x2,
+void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t sub_used, int32_t groups,
+                 int64_t n, uint64_t seed, int32_t R, const double* y_x, const double* y_x2,
                  const int32_t* failed, int64_t nonfailed_before, int64_t nonfailed_total,
                  double* rep_max, int32_t* needs_host) {
   const uint64_t L64 = static_cast<uint64_t>(l);
@@ -136,13 +134,13 @@ void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t
       for (int k = 0; k < nfold; ++k) {
         if (failed && failed[k]) continue;
         const int64_t item = m * nonfailed_total + nonfailed_before + j++;
-        uint64_t word = 2ull * static_cast<uint64_t>(item) * L64 * static_cast<uint64_t>(D_used);
+        uint64_t word = 2ull * static_cast<uint64_t>(item) * L64 * static_cast<uint64_t>(groups);
         HostRng rng(seed, stream);
         const size_t base = (static_cast<size_t>(m) * nfold + k) * l * D_stride;
         for (int c = 0; c < l; ++c) {
           sx[c] = 0.0;
           sxx[c] = 0.0;
-          for (int blk = 0; blk < D_used; ++blk, word += 2) {
+          for (int g = 0; g < groups; ++g, word += 2) {
             rng.skip_to(word >> 2);
             if (word & 2) {
               rng.next_u32();
@@ -151,8 +149,13 @@ void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t
             const uint64_t v = rng.next_u64();
             if (v >= bound) needs_host[r] = 1;
             const size_t src = static_cast<size_t>(v % L64);
-            sx[c] += y_x[base + src * D_stride + blk];
-            sxx[c] += y_x2[base + src * D_stride + blk];
+            double ga = 0.0, gb = 0.0;
+            for (int d = block_group_begin(g, sub_used, groups); d < block_group_begin(g + 1, sub_used, groups); ++d) {
+              ga += y_x[base + src * D_stride + d];
+              gb += y_x2[base + src * D_stride + d];
+            }
+            sx[c] += ga;
+            sxx[c] += gb;
           }
         }
         double rr;
@@ -162,9 +165,13 @@ void bench_shard(int32_t nm, int32_t nfold, int32_t l, int32_t D_stride, int32_t
   }
 }
 
+// final_checkpoint: 0 = intermediate snapshot (no exclusions), 1 = final (exclusions, per-model
+// report, benchmark + verdict), 2 = early-stop probe (no exclusions, benchmark + verdict on the
+// first sub_used sub-blocks, regrouped into min(blocks, sub_used) blocks).
 void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter_count,
                  int32_t final_checkpoint, const pcvg_fold_table* ft, const double* y_x,
-                 const double* y_x2, int D_used, pcvg_report* rep, const double* bench_max) {
+                 const double* y_x2, int sub_used, pcvg_report* rep, const double* bench_max) {
+  const int groups = std::min(cfg->blocks, sub_used);
   const int l = cfg->chains;
   const bool final = final_checkpoint == 1;
   const int D_stride = cfg->early_stop ? static_cast<int>(cfg->iters / cfg->checkpoint_every) : cfg->blocks;
@@ -256,10 +263,15 @@ void merge_stats(int32_t nm, int32_t K, const pcvg_run_config* cfg, int64_t iter
           for (int c = 0; c < l; ++c) {
             sx[c] = 0.0;
             sxx[c] = 0.0;
-            for (int blk = 0; blk < D_used; ++blk) {
+            for (int g = 0; g < groups; ++g) {
               const int src = static_cast<int>(rng.below(static_cast<uint64_t>(l)));
-              sx[c] += y_x[base + static_cast<size_t>(src) * D_stride + blk];
-              sxx[c] += y_x2[base + static_cast<size_t>(src) * D_stride + blk];
+              double ga = 0.0, gb = 0.0;
+              for (int d = block_group_begin(g, sub_used, groups); d < block_group_begin(g + 1, sub_used, groups); ++d) {
+                ga += y_x[base + static_cast<size_t>(src) * D_stride + d];
+                gb += y_x2[base + static_cast<size_t>(src) * D_stride + d];
+              }
+              sx[c] += ga;
+              sxx[c] += gb;
             }
           }
           double rr;

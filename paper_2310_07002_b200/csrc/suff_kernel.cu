@@ -15,12 +15,9 @@ cudaError_t launch_suff_t(const ModelDev& M, const ChainsDev& S, const RunArgs& 
   const int grid = (S.nch + kBlock / T - 1) / (kBlock / T);
   if (grid == 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(suff_slots(M, T)) * suff_slot_arrays(M) * kBlock * sizeof(double);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(gauss_kernel<FAM, T, NCM, NGM, NB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  {
+    cudaError_t e = ensure_kernel_smem(reinterpret_cast<const void*>(gauss_kernel<FAM, T, NCM, NGM, NB>), smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   ++sampler_launch_count();
   gauss_kernel<FAM, T, NCM, NGM, NB><<<grid, kBlock, smem, st>>>(M, S, A);
@@ -31,7 +28,7 @@ template <int FAM, int NCM, int NGM>
 cudaError_t launch_suff(const ModelDev& M, const ChainsDev& S, const RunArgs& A, int T, cudaStream_t st) {
   switch (T) {
     case 1:
-      if (S.nch >= 148 * 2 * kBlock * 2) return launch_suff_t<FAM, NCM, NGM, 1, -2>(M, S, A, st);
+      if (S.nch >= device_sm_count() * 2 * kBlock * 2) return launch_suff_t<FAM, NCM, NGM, 1, -2>(M, S, A, st);
       return launch_suff_t<FAM, NCM, NGM, 1>(M, S, A, st);
     case 4: return launch_suff_t<FAM, NCM, NGM, 4>(M, S, A, st);
     case 8: return launch_suff_t<FAM, NCM, NGM, 8>(M, S, A, st);
@@ -45,7 +42,7 @@ cudaError_t launch_suff(const ModelDev& M, const ChainsDev& S, const RunArgs& A,
 // model's size (21 instead of 45 Gram entries, 8 instead of 11 global parameters).
 template <int FAM, int NCM, int NGM>
 cudaError_t launch_suff1(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st) {
-  if (S.nch >= 148 * 2 * kBlock * 2) return launch_suff_t<FAM, NCM, NGM, 1, -2>(M, S, A, st);
+  if (S.nch >= device_sm_count() * 2 * kBlock * 2) return launch_suff_t<FAM, NCM, NGM, 1, -2>(M, S, A, st);
   return launch_suff_t<FAM, NCM, NGM, 1>(M, S, A, st);
 }
 
@@ -59,7 +56,7 @@ int suff_lanes_per_chain(const ModelDev& M, int nch) {
   // reductions, more than a lane saves on a d(d+1)/2 Gram product (measured: cfg1 / cfg4 are
   // fastest at one lane, cfg3's 400 groups at 32, profiles/r01_suff_lanes.txt).
   if (M.J < 64) return 1;
-  const long target_threads = 148L * 512;
+  const long target_threads = static_cast<long>(device_sm_count()) * 512;
   int T = 1;
   while (T < 32 && static_cast<long>(nch) * T < target_threads) T *= 2;
   if (T == 2) T = 4;

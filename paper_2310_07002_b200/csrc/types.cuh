@@ -102,6 +102,10 @@ struct ModelDev {
   double* g32_scratch;  // logistic FP32 variant: per-CTA FP64 G partials (the model's own buffer)
   const double* sgA;    // rat M_A: [J][3] full-data per-group (y, t) Gram (yy, ty, tt)
   const double* sov_A;  // rat M_A: [nov][3] the fold's override Grams
+  // fault injection (tests only, pcvg_debug_break_fold): every transition of a chain of this fold is
+  // divergent, as with the reference's BrokenFoldModel whose gradient is NaN on one fold
+  // (test_engine.cpp:57-90); -1 = none
+  int broken_fold;
 };
 
 constexpr int kMaxBatches = 16;

@@ -3,9 +3,16 @@
 SURVEY.md 8(e): each rank owns a contiguous fold range with all L chains of a fold, so per-fold
 R-hat/ESS/LogS need no communication. The only exchange is at check intervals: the per-fold
 tables (a few doubles per fold) are all-gathered in rank order = reference fold order, and every
-rank merges them with pcvg_merge (engine.cpp:117-253). Because the merge sums in fold order, the
-headline statistics are bit-identical for any GPU count (the reference's thread-count invariance,
-test_engine.cpp:135-147, becomes GPU-count invariance).
+rank merges them with pcvg_merge (engine.cpp:117-253) in fold order, so the merge itself is
+independent of the GPU count (the reference's thread-count invariance, test_engine.cpp:135-147).
+The per-fold inputs are bit-identical for any GPU count wherever a chain's arithmetic does not
+depend on the launch geometry: the sufficient-statistics, group-batched and row-split Gaussian
+kernels (one chain per thread / lane group). The tensor-core GLM kernels (logistic; Gaussian models
+under the ROWS policy) run a shard's last partial wave of 64-chain tiles as row-split clusters whose
+partial sums are combined in a different order, and which tiles form that tail depends on the shard
+size: those chains agree with a single-GPU run to rounding (~1e-14 relative per gradient), then
+diverge chaotically as any two MCMC runs with last-ulp differences do; the estimates agree within
+Monte Carlo error (tests/test_gpu_dist.py).
 """
 from __future__ import annotations
 
@@ -110,14 +117,14 @@ def run_pcv_sharded(inputs, cfg, device=0, group=None):
     K = inputs[0].model.K
     nm = len(inputs)
     fb, fe = shard_range(K, rank, world)
-    if cfg.early_stop:
-        raise pcv.InvalidInput("early stop is not available in the sharded driver")
     cfg_s = copy.copy(cfg)
     cfg_s.fold_begin, cfg_s.fold_end = fb, fe
     if fe == fb:
         raise pcv.InvalidInput("more ranks than folds")
     checkpoints = list(range(cfg.checkpoint_every, cfg.iters, cfg.checkpoint_every)) if cfg.checkpoint_every > 0 else []
     checkpoints.append(cfg.iters)
+    # shuffle sub-blocks stored per chain (one per check interval under early stop)
+    d_stride = cfg.iters // cfg.checkpoint_every if cfg.early_stop else cfg.blocks
     snaps = []
     dev = None
     try:
@@ -126,6 +133,14 @@ def run_pcv_sharded(inputs, cfg, device=0, group=None):
             dev = torch.device("cuda", device)
     except Exception:
         dev = None
+
+    def shard_benchmark(failed_local, sub_used):
+        if failed_local is None:
+            failed_local = np.zeros(fe - fb, dtype=np.int32)
+        before, total = shard_benchmark_offsets(failed_local, group)
+        mx, nh = ctx.benchmark(failed_local, before, total, sub_used)
+        return reduce_benchmark(mx, nh, dev, group)
+
     with pcv.Context(device) as ctx:
         for mi in inputs:
             ctx.add_model(mi.model, mi.fit.kparams, mi.fit.draws, mi.model_id)
@@ -136,18 +151,31 @@ def run_pcv_sharded(inputs, cfg, device=0, group=None):
             done = t
             cols, div, dropped, iters = ctx.fold_stats(fe - fb)
             full = gather_fold_tables(cols, nm, group)
+            sub_used = iters // cfg.checkpoint_every if cfg.early_stop else cfg.blocks
             last = ci + 1 == len(checkpoints)
-            if not last:
+            final = last
+            if cfg.early_stop and not last and sub_used >= cfg.blocks:
+                # the early-stop probe of pcvg_run: no exclusions, benchmark over every fold
+                part = dict(full)
+                part["failed"] = np.zeros_like(part["failed"])
+                mx, nh = shard_benchmark(None, sub_used)
+                if nh.max() > 0:
+                    yx, yx2 = ctx.block_sums(fe - fb, d_stride)
+                    probe = pcv.merge(nm, K, cfg, iters, 2, part, gather_rows(yx, nm, group),
+                                      gather_rows(yx2, nm, group))
+                else:
+                    probe = pcv.merge_bench(nm, K, cfg, iters, 2, part, mx)
+                final = bool(probe["verdict_pass"]) and np.isfinite(probe["rhat_max"]) and \
+                    probe["mcse"] < probe["epistemic_se"]
+            if not final:
                 part = dict(full)
                 part["failed"] = np.zeros_like(part["failed"])
                 rep = pcv.merge(nm, K, cfg, iters, False, part)
             else:
                 failed_local = cols["failed"][: fe - fb]
-                before, total = shard_benchmark_offsets(failed_local, group)
-                mx, nh = ctx.benchmark(failed_local, before, total, cfg.blocks)
-                mx, nh = reduce_benchmark(mx, nh, dev, group)
+                mx, nh = shard_benchmark(failed_local, sub_used)
                 if nh.max() > 0:  # a below() rejection: the sequential stream needs all block sums
-                    yx, yx2 = ctx.block_sums(fe - fb, cfg.blocks)
+                    yx, yx2 = ctx.block_sums(fe - fb, d_stride)
                     rep = pcv.merge(nm, K, cfg, iters, True, full, gather_rows(yx, nm, group),
                                     gather_rows(yx2, nm, group))
                 else:
@@ -162,6 +190,8 @@ def run_pcv_sharded(inputs, cfg, device=0, group=None):
                 rep["iters_run"] = iters
             snaps.append([iters, rep["delta_hat"], rep["mcse"], rep["epistemic_se"], rep["prob_a_better"],
                           rep["ess_overall"], rep["rhat_max"]])
+            if final:
+                break
     rep["snapshots"] = np.array(snaps)
     rep["n_checkpoints"] = len(snaps)
     return rep

@@ -112,7 +112,9 @@ def load():
     _sig(lib, "pcvg_merge", i32, [i32, i32, P(abi.RunConfig), i64, i32, P(abi.FoldTable), pf, pf,
                                   P(abi.Report)])
     _sig(lib, "pcvg_benchmark", i32, [vp, pi32, i64, i64, i32, pf, pi32])
-    _sig(lib, "pcvg_benchmark_host", i32, [i32, i32, i32, i32, i32, i64, u64, i32, pf, pf, pi32, i64,
+    _sig(lib, "pcvg_run_streams", i32, [vp, i32, pf, pf, P(abi.RunConfig), P(abi.Report)])
+    _sig(lib, "pcvg_debug_break_fold", i32, [vp, i32, i32])
+    _sig(lib, "pcvg_benchmark_host", i32, [i32, i32, i32, i32, i32, i32, i64, u64, i32, pf, pf, pi32, i64,
                                            i64, pf, pi32])
     _sig(lib, "pcvg_merge_bench", i32, [i32, i32, P(abi.RunConfig), i64, i32, P(abi.FoldTable), pf,
                                         P(abi.Report)])
@@ -405,6 +407,10 @@ class Context:
 
     KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TENSOR, KERNEL_TF32, KERNEL_SUFFSTAT, KERNEL_ROWS = 0, 1, 2, 3, 4, 5
 
+    def debug_break_fold(self, slot, fold):
+        """Tests only: every transition of fold `fold`'s chains diverges (BrokenFoldModel)."""
+        self._chk(self.lib.pcvg_debug_break_fold(self.h, slot, fold))
+
     def set_kernel_policy(self, policy):
         self._chk(self.lib.pcvg_set_kernel_policy(self.h, policy))
 
@@ -501,6 +507,20 @@ class Context:
         self._chk(self.lib.pcvg_run(self.h, C.byref(cfg), C.byref(rep)))
         return abi.report_dict(rep, arrs, len(self.models))
 
+    def run_streams(self, scores, centers, cfg):
+        """pcvg_run_streams: run_pcv's checkpoints, per-fold statistics, shuffle benchmark and early-stop
+        rule on explicit log_pred streams scores[K][L][iters] (fold centres centers[K]) instead of
+        sampled ones; needs a context without models."""
+        s = np.ascontiguousarray(scores, dtype=np.float64)
+        K, L, n = s.shape
+        if L != cfg.chains or n != cfg.iters:
+            raise InvalidInput("scores must be [K][chains][iters]")
+        c = np.ascontiguousarray(centers, dtype=np.float64)
+        nck = self.lib.pcvg_checkpoint_count(C.byref(cfg))
+        rep, arrs = abi.new_report(1, K, L, nck, cfg.bench_draws)
+        self._chk(self.lib.pcvg_run_streams(self.h, K, _p(s), _p(c), C.byref(cfg), C.byref(rep)))
+        return abi.report_dict(rep, arrs, 1)
+
     # stepwise API (sharded runs)
     def begin(self, cfg):
         self._cfg = cfg
@@ -556,13 +576,15 @@ def merge(n_models, K, cfg, iter_count, final, cols, y_x=None, y_x2=None):
 
 
 def benchmark_host(n_models, nfold, L, D_stride, blocks_used, iter_count, seed, bench_draws, y_x, y_x2,
-                   failed=None, nonfailed_before=0, nonfailed_total=None):
-    """pcvg_benchmark_host: positional shuffle benchmark of one shard from host block sums."""
+                   failed=None, nonfailed_before=0, nonfailed_total=None, block_groups=None):
+    """pcvg_benchmark_host: positional shuffle benchmark of one shard from host sub-block sums (the
+    first blocks_used sub-blocks regrouped into block_groups blocks; default: one each)."""
     if nonfailed_total is None:
         nonfailed_total = nfold if failed is None else int(np.sum(np.asarray(failed) == 0))
     fl = None if failed is None else np.ascontiguousarray(failed, dtype=np.int32)
     mx, nh = np.zeros(bench_draws), np.zeros(bench_draws, dtype=np.int32)
-    _check(load().pcvg_benchmark_host(n_models, nfold, L, D_stride, blocks_used, iter_count, seed, bench_draws,
+    _check(load().pcvg_benchmark_host(n_models, nfold, L, D_stride, blocks_used, block_groups or blocks_used,
+                                      iter_count, seed, bench_draws,
                                       _p(np.ascontiguousarray(y_x)), _p(np.ascontiguousarray(y_x2)),
                                       _p(fl, C.c_int32), nonfailed_before, nonfailed_total, _p(mx),
                                       _p(nh, C.c_int32)))

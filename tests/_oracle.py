@@ -43,6 +43,7 @@ def oracle():
         _sig(lib, "pcvo_make_hv_racine", C.c_int, [P(abi.Dataset), i64, i64, pi64])
         _sig(lib, "pcvo_model_create", vp, [P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec)])
         _sig(lib, "pcvo_model_destroy", None, [vp])
+        _sig(lib, "pcvo_model_break_fold", None, [vp, i32])
         _sig(lib, "pcvo_model_dim", i32, [vp])
         _sig(lib, "pcvo_test_size", i64, [vp, i32])
         _sig(lib, "pcvo_log_joint", f64, [vp, pf64, i32])
@@ -131,6 +132,10 @@ class OModel:
     def __del__(self):
         if getattr(self, "h", None):
             self.lib.pcvo_model_destroy(self.h)
+
+    def break_fold(self, fold):
+        """BrokenFoldModel (test_engine.cpp:57-90): NaN gradient on `fold` (-1 clears)."""
+        self.lib.pcvo_model_break_fold(self.h, fold)
 
     def log_joint(self, th, fold):
         th = np.ascontiguousarray(th, dtype=np.float64)

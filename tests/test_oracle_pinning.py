@@ -390,3 +390,31 @@ def test_adapt_trace_oracle_matches_reference():
         tr = rm.adapt_trace(chains=4, warmup=30, seed=3, model_id=0)
         assert np.array_equal(tr["inv_mass"], z[f"{name}:0:inv_mass"])
         assert np.array_equal(tr["step_trace"], z[f"{name}:0:step_trace"])
+
+
+# ---------------------------------------------------------------- bench.py CPU arms
+def test_refarm_builds_cfg2_without_the_product_library():
+    """bench.py's reference arm (oracle/refarm.py) simulates the cfg2 dataset inside the CPU library
+    (the reference plugin's simulator, or the oracle port's); both must equal the product simulator
+    bit for bit, and the arm must not load libpcvg.so."""
+    import os
+    import subprocess
+    import sys
+    from paper_2310_07002_b200 import pcv
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import refarm
+    d = pcv.simulate_logistic(2000, 50, seed=1)
+    for prefer_ref in ([True, False] if O.have_ref() else [False]):
+        w = refarm.Workload(prefer_ref)
+        y, x = np.zeros(2000), np.zeros(2000 * 50)
+        sim = w.lib.pcvref_simulate_logistic if w.kind == "reference" else w.lib.pcvo_simulate_logistic
+        sim.argtypes = [C.c_int64, C.c_int32, C.c_uint64, refarm.PF64, refarm.PF64]
+        assert sim(2000, 50, 1, refarm._ptr(y, C.c_double), refarm._ptr(x, C.c_double)) == 0
+        assert np.array_equal(y, d.y) and np.array_equal(x.reshape(d.x.shape), d.x), w.kind
+        w.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, 'oracle'); import refarm; w = refarm.Workload(); "
+            "maps = open('/proc/self/maps').read(); print('libpcvg' in maps, 'paper_2310_07002_b200' in sys.modules)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.split() == ["False", "False"]
