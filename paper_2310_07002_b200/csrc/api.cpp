@@ -875,7 +875,7 @@ void device_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_be
   rj.alloc(std::max(R, 1));
   ck(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long) * mx.n, ctx->stream), "memset");
   ck(cudaMemsetAsync(rj.p, 0, sizeof(int) * rj.n, ctx->stream), "memset");
-  for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+  for (size_t mi = 0; mi < ctx->chains.size(); ++mi) {  // one chain set per model (or score-stream run)
     std::vector<int64_t> item(nfold, -1);
     int64_t j = 0;
     for (int k = 0; k < nfold; ++k)
@@ -1587,7 +1587,9 @@ void run_checkpoints(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
       }
       merge_stats(nm, K, cfg, done, 2, &t2, yx.data(), yx2.data(), completed_sub_blocks(cfg, done), &probe,
                   host_path ? nullptr : bmax.data());
-      if (probe.verdict_pass && std::isfinite(probe.rhat_max) && probe.mcse < probe.epistemic_se) final_ck = true;
+      if (probe.verdict_pass && probe.benchmark_count > 0 && std::isfinite(probe.rhat_max) &&
+          probe.mcse < probe.epistemic_se)
+        final_ck = true;
     }
     if (final_ck) {
       // shuffle benchmark on device over the non-failed folds (failed flags from fold_stats)

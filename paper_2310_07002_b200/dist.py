@@ -165,8 +165,8 @@ def run_pcv_sharded(inputs, cfg, device=0, group=None):
                                       gather_rows(yx2, nm, group))
                 else:
                     probe = pcv.merge_bench(nm, K, cfg, iters, 2, part, mx)
-                final = bool(probe["verdict_pass"]) and np.isfinite(probe["rhat_max"]) and \
-                    probe["mcse"] < probe["epistemic_se"]
+                final = bool(probe["verdict_pass"]) and probe["benchmark_count"] > 0 and \
+                    np.isfinite(probe["rhat_max"]) and probe["mcse"] < probe["epistemic_se"]
             if not final:
                 part = dict(full)
                 part["failed"] = np.zeros_like(part["failed"])
