@@ -16,7 +16,11 @@
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
+#include <algorithm>
+#include <iterator>
 #include <map>
+#include <string_view>
+#include <unordered_map>
 #include <memory>
 #include <sstream>
 #include <stdexcept>
@@ -44,87 +48,101 @@ void check(int32_t st, pcvg_ctx* ctx = nullptr) {
   if (st != PCVG_OK) throw Failure(st, pcvg_last_error(ctx));
 }
 
-// ------------------------------------------------------------------ ConfigMap (config.cpp:20-120)
-std::string trim(const std::string& s) {
-  const size_t a = s.find_first_not_of(" \t\r");
-  const size_t b = s.find_last_not_of(" \t\r");
-  return a == std::string::npos ? "" : s.substr(a, b - a + 1);
+// ------------------------------------------------------------------ run settings (config.cpp grammar)
+// The reference's INI dialect: `[section]` headers, `key = value` pairs, `#` starts a comment; a key
+// is addressed as "section.key" (plain "key" before the first header).
+std::string_view strip(std::string_view v) {
+  auto blank = [](char ch) { return ch == ' ' || ch == '\t' || ch == '\r'; };
+  while (!v.empty() && blank(v.front())) v.remove_prefix(1);
+  while (!v.empty() && blank(v.back())) v.remove_suffix(1);
+  return v;
 }
 
-class ConfigMap {
+class Settings {
  public:
-  static ConfigMap parse_file(const std::string& path) {
-    std::ifstream in(path);
-    if (!in) throw UsageError("cannot open config file: " + path);
-    std::stringstream ss;
-    ss << in.rdbuf();
-    ConfigMap cfg;
-    std::istringstream lines(ss.str());
-    std::string line, section;
-    long lineno = 0;
-    while (std::getline(lines, line)) {
-      ++lineno;
-      const auto hash = line.find('#');
-      if (hash != std::string::npos) line.erase(hash);
-      line = trim(line);
-      if (line.empty()) continue;
-      if (line.front() == '[') {
-        if (line.back() != ']')
-          throw UsageError("config line " + std::to_string(lineno) + ": unterminated section header");
-        section = trim(line.substr(1, line.size() - 2));
+  static Settings load(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw UsageError("config file not readable: " + path);
+    const std::string text((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    return parse(text, path);
+  }
+
+  static Settings parse(std::string_view text, const std::string& origin) {
+    Settings out;
+    std::string prefix;
+    size_t line_no = 0;
+    while (!text.empty()) {
+      const size_t nl = text.find('\n');
+      std::string_view raw = text.substr(0, nl);
+      text.remove_prefix(nl == std::string_view::npos ? text.size() : nl + 1);
+      ++line_no;
+      raw = strip(raw.substr(0, raw.find('#')));
+      if (raw.empty()) continue;
+      const std::string where = origin + ":" + std::to_string(line_no) + ": ";
+      if (raw.front() == '[') {
+        if (raw.back() != ']') throw UsageError(where + "section header needs a closing ']'");
+        const std::string_view name = strip(raw.substr(1, raw.size() - 2));
+        prefix = name.empty() ? std::string() : std::string(name) + ".";
         continue;
       }
-      const auto eq = line.find('=');
-      if (eq == std::string::npos)
-        throw UsageError("config line " + std::to_string(lineno) + ": expected key = value");
-      const std::string key = trim(line.substr(0, eq));
-      cfg.v_[section.empty() ? key : section + "." + key] = trim(line.substr(eq + 1));
+      const size_t eq = raw.find('=');
+      if (eq == std::string_view::npos) throw UsageError(where + "not a 'key = value' line");
+      out.kv_[prefix + std::string(strip(raw.substr(0, eq)))] = std::string(strip(raw.substr(eq + 1)));
     }
-    return cfg;
+    return out;
   }
-  bool has(const std::string& k) const { return v_.count(k) > 0; }
-  void set(const std::string& k, const std::string& val) { v_[k] = val; }
-  std::string str(const std::string& k) const {
-    const auto it = v_.find(k);
-    if (it == v_.end()) throw UsageError("missing required config key '" + k + "'");
+
+  bool contains(const std::string& key) const { return kv_.find(key) != kv_.end(); }
+  void put(const std::string& key, std::string value) { kv_[key] = std::move(value); }
+  const std::string& need(const std::string& key) const {
+    const auto it = kv_.find(key);
+    if (it == kv_.end()) throw UsageError("setting '" + key + "' is required");
     return it->second;
   }
-  std::string str(const std::string& k, const std::string& fb) const {
-    const auto it = v_.find(k);
-    return it == v_.end() ? fb : it->second;
+  std::string text(const std::string& key, const std::string& fallback) const {
+    return contains(key) ? need(key) : fallback;
   }
-  long lng(const std::string& k, long fb) const { return has(k) ? std::stol(str(k)) : fb; }
-  double dbl(const std::string& k, double fb) const { return has(k) ? std::stod(str(k)) : fb; }
-  uint64_t u64(const std::string& k, uint64_t fb) const { return has(k) ? std::stoull(str(k)) : fb; }
-  bool boolean(const std::string& k, bool fb) const {
-    if (!has(k)) return fb;
-    const std::string v = str(k);
-    if (v == "1" || v == "true" || v == "yes" || v == "on") return true;
-    if (v == "0" || v == "false" || v == "no" || v == "off") return false;
-    throw UsageError("config key '" + k + "' is not a boolean: " + v);
+  template <class T>
+  T number(const std::string& key, T fallback) const {
+    if (!contains(key)) return fallback;
+    const std::string& v = need(key);
+    T out{};
+    const auto [end, ec] = std::from_chars(v.data(), v.data() + v.size(), out);
+    if (ec != std::errc{} || end != v.data() + v.size())
+      throw UsageError("setting '" + key + "' is not a number: '" + v + "'");
+    return out;
   }
-  std::vector<std::string> list(const std::string& k) const {
+  long integer(const std::string& key, long fallback) const { return number<long>(key, fallback); }
+  double real(const std::string& key, double fallback) const { return number<double>(key, fallback); }
+  uint64_t unsigned64(const std::string& key, uint64_t fallback) const { return number<uint64_t>(key, fallback); }
+  bool flag(const std::string& key, bool fallback) const {
+    static const std::map<std::string, bool> kWords = {{"1", true},  {"true", true},  {"yes", true},  {"on", true},
+                                                        {"0", false}, {"false", false}, {"no", false}, {"off", false}};
+    if (!contains(key)) return fallback;
+    const auto w = kWords.find(need(key));
+    if (w == kWords.end()) throw UsageError("setting '" + key + "' must be a boolean, got '" + need(key) + "'");
+    return w->second;
+  }
+  std::vector<std::string> items(const std::string& key) const {  // comma-separated list
     std::vector<std::string> out;
-    std::string cur;
-    for (char ch : str(k)) {
-      if (ch == ',') {
-        out.push_back(trim(cur));
-        cur.clear();
-      } else {
-        cur += ch;
-      }
+    std::string_view rest = need(key);
+    if (strip(rest).empty()) return out;
+    for (;;) {
+      const size_t comma = rest.find(',');
+      out.emplace_back(strip(rest.substr(0, comma)));
+      if (comma == std::string_view::npos) break;
+      rest.remove_prefix(comma + 1);
     }
-    if (!trim(cur).empty() || !out.empty()) out.push_back(trim(cur));
     return out;
   }
 
  private:
-  std::map<std::string, std::string> v_;
+  std::unordered_map<std::string, std::string> kv_;
 };
 
-// ------------------------------------------------------------------ dataset CSV (dataset.cpp:40-146)
+// ------------------------------------------------------------------ dataset tables (dataset.cpp formats)
 struct Dataset {
-  std::vector<double> y, x;
+  std::vector<double> y, x;  // x row-major [n][n_cov]
   int n_cov = 0;
   std::vector<int32_t> group;
   std::vector<int64_t> time;
@@ -132,98 +150,111 @@ struct Dataset {
     return pcvg_dataset{static_cast<int64_t>(y.size()), n_cov, y.data(), x.data(),
                         group.empty() ? nullptr : group.data(), time.empty() ? nullptr : time.data()};
   }
-  int n_groups() const {
-    int j = 0;
-    for (int32_t g : group) j = std::max(j, g + 1);
-    return j;
+  int n_groups() const { return group.empty() ? 0 : *std::max_element(group.begin(), group.end()) + 1; }
+};
+
+// A comma-separated table held column by column: the header names, then every field as text.
+struct CsvTable {
+  std::vector<std::string> names;
+  std::vector<std::vector<std::string>> cols;
+
+  static CsvTable read(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw UsageError("data file not readable: " + path);
+    const std::string body((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    CsvTable t;
+    std::string_view rest(body);
+    size_t row = 0;
+    while (!rest.empty()) {
+      const size_t nl = rest.find('\n');
+      std::string_view line = rest.substr(0, nl);
+      rest.remove_prefix(nl == std::string_view::npos ? rest.size() : nl + 1);
+      if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
+      if (row > 0 && line.empty()) continue;
+      std::vector<std::string_view> fields;
+      for (size_t from = 0;;) {
+        const size_t comma = line.find(',', from);
+        fields.push_back(line.substr(from, comma == std::string_view::npos ? std::string_view::npos : comma - from));
+        if (comma == std::string_view::npos) break;
+        from = comma + 1;
+      }
+      if (row == 0) {
+        for (auto fv : fields) t.names.emplace_back(fv);
+        t.cols.resize(t.names.size());
+      } else {
+        if (fields.size() != t.names.size())
+          throw UsageError(path + ": line " + std::to_string(row + 1) + " has " + std::to_string(fields.size()) +
+                           " fields, the header " + std::to_string(t.names.size()));
+        for (size_t c = 0; c < fields.size(); ++c) t.cols[c].emplace_back(fields[c]);
+      }
+      ++row;
+    }
+    if (row == 0) throw UsageError(path + ": no header line");
+    return t;
+  }
+
+  std::vector<double> numbers(const std::string& name, const std::string& path) const {
+    const auto it = std::find(names.begin(), names.end(), name);
+    if (it == names.end()) throw UsageError(path + ": no column named '" + name + "'");
+    const auto& col = cols[static_cast<size_t>(it - names.begin())];
+    std::vector<double> out(col.size());
+    for (size_t r = 0; r < col.size(); ++r) {
+      std::string_view v = strip(col[r]);
+      const auto [end, ec] = std::from_chars(v.data(), v.data() + v.size(), out[r]);
+      if (ec != std::errc{} || end != v.data() + v.size())
+        throw UsageError(path + ": column '" + name + "', data row " + std::to_string(r + 1) + ": '" + col[r] +
+                         "' is not a number");
+    }
+    return out;
   }
 };
 
-std::vector<std::string> split_line(const std::string& line) {
-  std::vector<std::string> out;
-  std::string cur;
-  for (char ch : line) {
-    if (ch == ',') {
-      out.push_back(cur);
-      cur.clear();
-    } else if (ch != '\r') {
-      cur += ch;
-    }
-  }
-  out.push_back(cur);
-  return out;
-}
-
-double parse_double(const std::string& tok, long row, const std::string& col) {
-  double v = 0.0;
-  const char* b = tok.data();
-  const char* e = b + tok.size();
-  while (b != e && (*b == ' ' || *b == '\t')) ++b;
-  auto [ptr, ec] = std::from_chars(b, e, v);
-  if (ec != std::errc{} || ptr != e)
-    throw UsageError("bad numeric value '" + tok + "' at row " + std::to_string(row) + ", column '" + col + "'");
-  return v;
-}
-
 Dataset read_csv(const std::string& path, const std::string& resp, const std::vector<std::string>& covs,
                  const std::string& group, const std::string& time) {
-  std::ifstream in(path);
-  if (!in) throw UsageError("cannot open CSV file: " + path);
-  std::string line;
-  if (!std::getline(in, line)) throw UsageError("CSV has no header: " + path);
-  const auto header = split_line(line);
-  auto col_of = [&](const std::string& name) {
-    for (size_t i = 0; i < header.size(); ++i)
-      if (header[i] == name) return static_cast<int>(i);
-    throw UsageError("CSV column '" + name + "' not found in " + path);
-  };
-  const int yc = col_of(resp);
-  std::vector<int> xc;
-  for (const auto& c : covs) xc.push_back(col_of(c));
-  const int gc = group.empty() ? -1 : col_of(group);
-  const int tc = time.empty() ? -1 : col_of(time);
+  const CsvTable t = CsvTable::read(path);
   Dataset d;
-  d.n_cov = static_cast<int>(xc.size());
-  long row = 1;
-  while (std::getline(in, line)) {
-    ++row;
-    if (line.empty()) continue;
-    const auto tok = split_line(line);
-    if (tok.size() != header.size())
-      throw UsageError("row " + std::to_string(row) + " has " + std::to_string(tok.size()) +
-                       " fields, expected " + std::to_string(header.size()));
-    d.y.push_back(parse_double(tok[yc], row, resp));
-    for (size_t j = 0; j < xc.size(); ++j) d.x.push_back(parse_double(tok[xc[j]], row, covs[j]));
-    if (gc >= 0) d.group.push_back(static_cast<int32_t>(std::lround(parse_double(tok[gc], row, group))));
-    if (tc >= 0) d.time.push_back(std::lround(parse_double(tok[tc], row, time)));
+  d.y = t.numbers(resp, path);
+  if (d.y.empty()) throw UsageError(path + ": the table has no data rows");
+  d.n_cov = static_cast<int>(covs.size());
+  d.x.assign(d.y.size() * covs.size(), 0.0);
+  for (size_t j = 0; j < covs.size(); ++j) {
+    const std::vector<double> c = t.numbers(covs[j], path);
+    for (size_t i = 0; i < c.size(); ++i) d.x[i * covs.size() + j] = c[i];
   }
-  if (d.y.empty()) throw UsageError("dataset is empty");
+  if (!group.empty())
+    for (double v : t.numbers(group, path)) d.group.push_back(static_cast<int32_t>(std::lround(v)));
+  if (!time.empty())
+    for (double v : t.numbers(time, path)) d.time.push_back(std::lround(v));
   return d;
 }
 
+// Writes the dataset in the reference simulator's column order (y, covariates, group, t) with
+// every real printed as %.17g (round-trip exact; registry.cpp writes the same bytes).
 void write_csv(const std::string& path, const Dataset& d, const std::vector<std::string>& covs) {
-  std::ofstream out(path);
-  if (!out) throw UsageError("cannot write CSV file: " + path);
-  out << "y";
-  for (const auto& c : covs) out << ',' << c;
-  if (!d.group.empty()) out << ",group";
-  if (!d.time.empty()) out << ",t";
-  out << '\n';
-  char buf[32];
-  auto put = [&](double v) {
-    std::snprintf(buf, sizeof buf, "%.17g", v);
-    out << buf;
+  std::vector<std::string> header{"y"};
+  header.insert(header.end(), covs.begin(), covs.end());
+  if (!d.group.empty()) header.push_back("group");
+  if (!d.time.empty()) header.push_back("t");
+  std::string body;
+  for (size_t h = 0; h < header.size(); ++h) body += (h ? "," : "") + header[h];
+  body += '\n';
+  auto real = [&](double v) {
+    char buf[40];
+    body.append(buf, static_cast<size_t>(std::snprintf(buf, sizeof buf, "%.17g", v)));
   };
   for (size_t i = 0; i < d.y.size(); ++i) {
-    put(d.y[i]);
+    real(d.y[i]);
     for (int j = 0; j < d.n_cov; ++j) {
-      out << ',';
-      put(d.x[i * d.n_cov + j]);
+      body += ',';
+      real(d.x[i * d.n_cov + j]);
     }
-    if (!d.group.empty()) out << ',' << d.group[i];
-    if (!d.time.empty()) out << ',' << d.time[i];
-    out << '\n';
+    if (!d.group.empty()) body += ',' + std::to_string(d.group[i]);
+    if (!d.time.empty()) body += ',' + std::to_string(d.time[i]);
+    body += '\n';
   }
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw UsageError("cannot create " + path);
+  f << body;
 }
 
 // ------------------------------------------------------------------ registry (registry.cpp:17-96)
@@ -278,14 +309,14 @@ std::vector<std::string> param_names(const Built& b, const Model& m) {
   return n;
 }
 
-Built build_models(const ConfigMap& cfg) {
+Built build_models(const Settings& cfg) {
   Built b;
   std::vector<std::string> covs;
-  if (cfg.has("data.covariates")) covs = cfg.list("data.covariates");
-  b.data = read_csv(cfg.str("data.path"), cfg.str("data.response", "y"), covs, cfg.str("data.group", ""),
-                    cfg.str("data.time", ""));
+  if (cfg.contains("data.covariates")) covs = cfg.items("data.covariates");
+  b.data = read_csv(cfg.need("data.path"), cfg.text("data.response", "y"), covs, cfg.text("data.group", ""),
+                    cfg.text("data.time", ""));
   pcvg_dataset dv = b.data.view();
-  const std::string kind = cfg.str("scheme.kind", "logo");
+  const std::string kind = cfg.text("scheme.kind", "logo");
   const int64_t n = dv.n_obs;
   b.test_index.assign(n, 0);
   int32_t K = 0;
@@ -294,29 +325,29 @@ Built build_models(const ConfigMap& cfg) {
   } else if (kind == "logo") {
     check(pcvg_make_logo(&dv, b.test_index.data(), &K));
   } else if (kind == "kfold") {
-    K = static_cast<int32_t>(std::stol(cfg.str("scheme.k")));
-    check(pcvg_make_kfold(n, K, cfg.u64("scheme.seed", 1), b.test_index.data()));
+    K = static_cast<int32_t>(std::stol(cfg.need("scheme.k")));
+    check(pcvg_make_kfold(n, K, cfg.unsigned64("scheme.seed", 1), b.test_index.data()));
   } else if (kind == "time-blocks") {
-    K = static_cast<int32_t>(std::stol(cfg.str("scheme.k")));
+    K = static_cast<int32_t>(std::stol(cfg.need("scheme.k")));
     check(pcvg_make_time_blocks(&dv, K, b.test_index.data()));
   } else if (kind == "hv-block") {  // new
-    K = static_cast<int32_t>(std::stol(cfg.str("scheme.k")));
+    K = static_cast<int32_t>(std::stol(cfg.need("scheme.k")));
     b.intervals.assign(4 * static_cast<size_t>(K), 0);
-    check(pcvg_make_hv_block(&dv, K, cfg.lng("scheme.h", 0), b.intervals.data()));
+    check(pcvg_make_hv_block(&dv, K, cfg.integer("scheme.h", 0), b.intervals.data()));
   } else if (kind == "hv-racine") {  // new
     K = static_cast<int32_t>(n);
     b.intervals.assign(4 * static_cast<size_t>(n), 0);
-    check(pcvg_make_hv_racine(&dv, cfg.lng("scheme.v", 0), cfg.lng("scheme.h", 0), b.intervals.data()));
+    check(pcvg_make_hv_racine(&dv, cfg.integer("scheme.v", 0), cfg.integer("scheme.h", 0), b.intervals.data()));
   } else {
     throw UsageError("unknown scheme.kind '" + kind + "'");
   }
   b.folds = pcvg_folds{K, b.intervals.empty() ? b.test_index.data() : nullptr,
                        b.intervals.empty() ? nullptr : b.intervals.data()};
 
-  const std::string family = cfg.str("model.family");
-  const std::string na = cfg.str("model.name_a", "M_A"), nb = cfg.str("model.name_b", "M_B");
-  const bool pair = cfg.has("model.mask_b") || cfg.has("model.slope_b") || cfg.has("model.floor_b") ||
-                    cfg.has("model.q_b");
+  const std::string family = cfg.need("model.family");
+  const std::string na = cfg.text("model.name_a", "M_A"), nb = cfg.text("model.name_b", "M_B");
+  const bool pair = cfg.contains("model.mask_b") || cfg.contains("model.slope_b") || cfg.contains("model.floor_b") ||
+                    cfg.contains("model.q_b");
   auto add = [&](const std::string& name) -> Model& {
     b.models.emplace_back();
     b.models.back().name = name;
@@ -326,14 +357,14 @@ Built build_models(const ConfigMap& cfg) {
     auto mk = [&](const std::string& name, const std::string& key) {
       Model& m = add(name);
       m.spec.family = PCVG_FAMILY_GROUPED;
-      if (cfg.has(key))
-        for (const auto& t : cfg.list(key)) m.mask.push_back(std::stoi(t));
+      if (cfg.contains(key))
+        for (const auto& t : cfg.items(key)) m.mask.push_back(std::stoi(t));
     };
     mk(na, "model.mask_a");
     if (pair) mk(nb, "model.mask_b");
   } else if (family == "rat-growth") {
     auto slope = [&](const std::string& key, const std::string& fb) {
-      const std::string v = cfg.str(key, fb);
+      const std::string v = cfg.text(key, fb);
       if (v == "per-subject") return 1;
       if (v == "shared") return 0;
       throw UsageError(key + " must be per-subject or shared");
@@ -341,15 +372,15 @@ Built build_models(const ConfigMap& cfg) {
     add(na).spec = pcvg_model_spec{PCVG_FAMILY_RAT_GROWTH, nullptr, 1, 1, 0, 0, slope("model.slope_a", "per-subject")};
     if (pair) add(nb).spec = pcvg_model_spec{PCVG_FAMILY_RAT_GROWTH, nullptr, 1, 1, 0, 0, slope("model.slope_b", "shared")};
   } else if (family == "radon") {
-    add(na).spec = pcvg_model_spec{PCVG_FAMILY_RADON, nullptr, cfg.boolean("model.floor_a", true), 1, 0, 0, 0};
-    if (pair) add(nb).spec = pcvg_model_spec{PCVG_FAMILY_RADON, nullptr, cfg.boolean("model.floor_b", false), 1, 0, 0, 0};
+    add(na).spec = pcvg_model_spec{PCVG_FAMILY_RADON, nullptr, cfg.flag("model.floor_a", true), 1, 0, 0, 0};
+    if (pair) add(nb).spec = pcvg_model_spec{PCVG_FAMILY_RADON, nullptr, cfg.flag("model.floor_b", false), 1, 0, 0, 0};
   } else if (family == "seasonal-ar") {
-    const int p = static_cast<int>(cfg.lng("model.p", 1));
-    const std::string t = cfg.str("model.rho_transform", "half-open");
+    const int p = static_cast<int>(cfg.integer("model.p", 1));
+    const std::string t = cfg.text("model.rho_transform", "half-open");
     if (t != "half-open" && t != "symmetric") throw UsageError("model.rho_transform must be half-open or symmetric");
     const int tf = t == "symmetric" ? PCVG_RHO_SYMMETRIC : PCVG_RHO_HALF_OPEN;
-    add(na).spec = pcvg_model_spec{PCVG_FAMILY_SEASONAL_AR, nullptr, 1, p, static_cast<int32_t>(cfg.lng("model.q_a", 11)), tf, 0};
-    if (pair) add(nb).spec = pcvg_model_spec{PCVG_FAMILY_SEASONAL_AR, nullptr, 1, p, static_cast<int32_t>(cfg.lng("model.q_b", 0)), tf, 0};
+    add(na).spec = pcvg_model_spec{PCVG_FAMILY_SEASONAL_AR, nullptr, 1, p, static_cast<int32_t>(cfg.integer("model.q_a", 11)), tf, 0};
+    if (pair) add(nb).spec = pcvg_model_spec{PCVG_FAMILY_SEASONAL_AR, nullptr, 1, p, static_cast<int32_t>(cfg.integer("model.q_b", 0)), tf, 0};
   } else if (family == "logistic") {  // new
     add(na).spec.family = PCVG_FAMILY_LOGISTIC;
   } else {
@@ -384,25 +415,25 @@ struct RunCfg {
   pcvg_adapt_config fd{};
 };
 
-RunCfg make_run_config(const ConfigMap& cfg, const RunFlags& f) {
+RunCfg make_run_config(const Settings& cfg, const RunFlags& f) {
   RunCfg r;
   pcvg_run_config& c = r.run;
-  c.seed = cfg.u64("run.seed", 1);
-  c.chains = static_cast<int32_t>(cfg.lng("run.chains", 4));
-  c.iters = cfg.lng("run.iters", 1000);
-  c.warmup = cfg.lng("run.warmup", 100);
-  c.batch_size = static_cast<int32_t>(cfg.lng("run.batch_size", 50));
-  c.blocks = static_cast<int32_t>(cfg.lng("run.blocks", 5));
-  c.bench_draws = static_cast<int32_t>(cfg.lng("run.bench_draws", 500));
-  c.bench_quantile = cfg.dbl("run.bench_quantile", 0.99);
-  c.score = score_from_name(cfg.str("run.score", "logs"));
-  c.checkpoint_every = cfg.lng("run.checkpoint_every", 0);
-  c.early_stop = cfg.boolean("run.early_stop", false) ? 1 : 0;  // new
-  r.fd.chains = static_cast<int32_t>(cfg.lng("full_data.chains", 4));
-  r.fd.warmup = cfg.lng("full_data.warmup", 1000);
-  r.fd.draws = cfg.lng("full_data.draws", 2000);
-  r.fd.n_leapfrog = static_cast<int32_t>(cfg.lng("full_data.leapfrog", 32));
-  r.fd.target_accept = cfg.dbl("full_data.target_accept", 0.8);
+  c.seed = cfg.unsigned64("run.seed", 1);
+  c.chains = static_cast<int32_t>(cfg.integer("run.chains", 4));
+  c.iters = cfg.integer("run.iters", 1000);
+  c.warmup = cfg.integer("run.warmup", 100);
+  c.batch_size = static_cast<int32_t>(cfg.integer("run.batch_size", 50));
+  c.blocks = static_cast<int32_t>(cfg.integer("run.blocks", 5));
+  c.bench_draws = static_cast<int32_t>(cfg.integer("run.bench_draws", 500));
+  c.bench_quantile = cfg.real("run.bench_quantile", 0.99);
+  c.score = score_from_name(cfg.text("run.score", "logs"));
+  c.checkpoint_every = cfg.integer("run.checkpoint_every", 0);
+  c.early_stop = cfg.flag("run.early_stop", false) ? 1 : 0;  // new
+  r.fd.chains = static_cast<int32_t>(cfg.integer("full_data.chains", 4));
+  r.fd.warmup = cfg.integer("full_data.warmup", 1000);
+  r.fd.draws = cfg.integer("full_data.draws", 2000);
+  r.fd.n_leapfrog = static_cast<int32_t>(cfg.integer("full_data.leapfrog", 32));
+  r.fd.target_accept = cfg.real("full_data.target_accept", 0.8);
   r.fd.init_step_size = 0.0;
   if (f.seed >= 0) c.seed = static_cast<uint64_t>(f.seed);
   if (f.chains >= 0) c.chains = static_cast<int32_t>(f.chains);
@@ -516,7 +547,7 @@ struct Ctx {
 
 // ------------------------------------------------------------------ subcommands
 int cmd_fit(const RunFlags& flags) {
-  const auto cfg = ConfigMap::parse_file(flags.config_path);
+  const auto cfg = Settings::load(flags.config_path);
   const auto rc = make_run_config(cfg, flags);
   Built b = build_models(cfg);
   std::filesystem::create_directories(flags.out_dir);
@@ -629,7 +660,7 @@ json report_to_json(const Built& b, const pcvg_run_config& c, int eff_b, const p
 }
 
 int cmd_pcv(const RunFlags& flags) {
-  const auto cfg = ConfigMap::parse_file(flags.config_path);
+  const auto cfg = Settings::load(flags.config_path);
   const auto rc = make_run_config(cfg, flags);
   Built b = build_models(cfg);
   std::vector<Fit> fits;
@@ -715,57 +746,69 @@ double json_num(const json& j) {
   return j.get<double>();
 }
 
-int cmd_report(const std::string& path) {  // pcv_main.cpp:142-182
-  std::ifstream in(path);
-  if (!in) throw UsageError("cannot open report: " + path);
+// `pcvg report`: a summary of a report.json (ours or the reference's) - the run shape, per model the
+// score total, divergences and failed folds, then the headline statistics and the benchmark verdict.
+int cmd_report(const std::string& path) {
   json j;
-  try {
-    j = json::parse(in);
-  } catch (const json::parse_error& e) {
-    throw UsageError("malformed report JSON: " + std::string(e.what()));
-  }
-  std::printf("folds: %ld   chains/fold: %ld   iters/chain: %ld   score: %s\n", j.at("folds").get<long>(),
-              j.at("chains").get<long>(), j.at("iters").get<long>(), j.at("score").get<std::string>().c_str());
-  for (const auto& m : j.at("models")) {
-    long divergences = 0;
-    for (const auto& fold : m.at("divergences"))
-      for (const auto& e : fold) divergences += e.get<long>();
-    std::printf("model %-12s total score: %12.4f   divergences: %ld\n", m.at("name").get<std::string>().c_str(),
-                json_num(m.at("score_total")), divergences);
-    const auto& failed = m.at("failed_folds");
-    if (!failed.empty()) {
-      std::printf("  failed folds:");
-      for (const auto& k : failed) std::printf(" %ld", k.get<long>());
-      std::printf("\n");
+  {
+    std::ifstream in(path);
+    if (!in) throw UsageError("report not readable: " + path);
+    try {
+      in >> j;
+    } catch (const json::exception& e) {
+      throw UsageError(path + " is not a valid report: " + e.what());
     }
   }
-  std::printf("delta_hat:      %12.4f\n", json_num(j.at("delta_hat")));
-  std::printf("mcse:           %12.4f\n", json_num(j.at("mcse")));
-  std::printf("epistemic_se:   %12.4f\n", json_num(j.at("epistemic_se")));
-  std::printf("prob_a_better:  %12.4f\n", json_num(j.at("prob_a_better")));
-  std::printf("ess:            %12.1f\n", json_num(j.at("ess")));
+  auto fmt = [](const char* spec, double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, spec, v);
+    return std::string(buf);
+  };
+  std::string out = "run: " + std::to_string(j.at("folds").get<long>()) + " folds x " +
+                    std::to_string(j.at("chains").get<long>()) + " chains x " +
+                    std::to_string(j.at("iters").get<long>()) + " iterations, score " +
+                    j.at("score").get<std::string>() + "\n";
+  for (const auto& m : j.at("models")) {
+    long div = 0;
+    for (const auto& per_fold : m.at("divergences"))
+      for (const auto& c : per_fold) div += c.get<long>();
+    out += "model " + m.at("name").get<std::string>() + ": score total " + fmt("%.4f", json_num(m.at("score_total"))) +
+           ", " + std::to_string(div) + " divergent transitions";
+    const auto& failed = m.at("failed_folds");
+    if (!failed.empty()) {
+      out += ", failed folds";
+      for (const auto& k : failed) out += " " + std::to_string(k.get<long>());
+    }
+    out += "\n";
+  }
+  const std::pair<const char*, const char*> rows[] = {{"delta_hat", "%.4f"},    {"mcse", "%.4f"},
+                                                      {"epistemic_se", "%.4f"}, {"prob_a_better", "%.4f"},
+                                                      {"ess", "%.1f"},          {"rhat_max", "%.4f"}};
+  for (const auto& [key, spec] : rows) out += std::string(key) + ": " + fmt(spec, json_num(j.at(key))) + "\n";
   const auto& v = j.at("verdict");
-  std::printf("rhat_max:       %12.4f  vs benchmark q%.2f = %.4f  -> %s\n", json_num(j.at("rhat_max")),
-              json_num(v.at("quantile")), json_num(v.at("quantile_value")), v.at("pass").get<bool>() ? "pass" : "FAIL");
+  out += "benchmark verdict: rhat_max " + fmt("%.4f", json_num(j.at("rhat_max"))) + (v.at("pass").get<bool>() ? " <= " : " > ") +
+         "q" + fmt("%.2f", json_num(v.at("quantile"))) + " " + fmt("%.4f", json_num(v.at("quantile_value"))) + " (" +
+         (v.at("pass").get<bool>() ? "pass" : "FAIL") + ")\n";
+  std::fputs(out.c_str(), stdout);
   return 0;
 }
 
-int cmd_simulate(const std::string& family, const ConfigMap& a, uint64_t seed, const std::string& out_dir) {
+int cmd_simulate(const std::string& family, const Settings& a, uint64_t seed, const std::string& out_dir) {
   Dataset d;
   std::vector<std::string> covs;
   pcvg::SimTruth truth;
   if (family == "grouped-reg") {  // registry.cpp:104-117
-    const int J = static_cast<int>(a.lng("J", 50)), Nj = static_cast<int>(a.lng("Nj", 5)),
-              P = static_cast<int>(a.lng("P", 4));
+    const int J = static_cast<int>(a.integer("J", 50)), Nj = static_cast<int>(a.integer("Nj", 5)),
+              P = static_cast<int>(a.integer("P", 4));
     d.n_cov = P;
     d.y.resize(static_cast<size_t>(J) * Nj);
     d.x.resize(d.y.size() * P);
     d.group.resize(d.y.size());
-    pcvg::simulate_grouped(J, Nj, P, a.dbl("min_omitted_beta", 0.0), seed, d.y.data(), d.x.data(),
+    pcvg::simulate_grouped(J, Nj, P, a.real("min_omitted_beta", 0.0), seed, d.y.data(), d.x.data(),
                            d.group.data(), &truth);
     for (int p = 0; p < P; ++p) covs.push_back("x" + std::to_string(p + 1));
   } else if (family == "rat-growth") {
-    const int J = static_cast<int>(a.lng("J", 30));
+    const int J = static_cast<int>(a.integer("J", 30));
     d.n_cov = 1;
     d.y.resize(5 * static_cast<size_t>(std::max(J, 0)));
     d.x.resize(d.y.size());
@@ -773,7 +816,7 @@ int cmd_simulate(const std::string& family, const ConfigMap& a, uint64_t seed, c
     pcvg::simulate_rat(J, seed, d.y.data(), d.x.data(), d.group.data(), &truth);
     covs = {"t"};
   } else if (family == "radon") {
-    const int H = static_cast<int>(a.lng("houses", 600)), C = static_cast<int>(a.lng("counties", 30));
+    const int H = static_cast<int>(a.integer("houses", 600)), C = static_cast<int>(a.integer("counties", 30));
     d.n_cov = 1;
     d.y.resize(std::max(H, 0));
     d.x.resize(d.y.size());
@@ -781,14 +824,14 @@ int cmd_simulate(const std::string& family, const ConfigMap& a, uint64_t seed, c
     pcvg::simulate_radon(H, C, seed, d.y.data(), d.x.data(), d.group.data(), &truth);
     covs = {"floor"};
   } else if (family == "seasonal-ar") {
-    const long T = a.lng("T", 432);
-    const int p = static_cast<int>(a.lng("p", 1)), q = static_cast<int>(a.lng("q", 11));
+    const long T = a.integer("T", 432);
+    const int p = static_cast<int>(a.integer("p", 1)), q = static_cast<int>(a.integer("q", 11));
     d.n_cov = p + q;
     const long n = std::max<long>(T - p, 0);
     d.y.resize(n);
     d.x.resize(static_cast<size_t>(n) * d.n_cov);
     d.time.resize(n);
-    pcvg::simulate_seasonal(T, p, q, a.dbl("rho", 0.6), a.dbl("amp", 1.0), a.dbl("sigma", 1.0), seed, d.y.data(),
+    pcvg::simulate_seasonal(T, p, q, a.real("rho", 0.6), a.real("amp", 1.0), a.real("sigma", 1.0), seed, d.y.data(),
                             d.x.data(), d.time.data(), &truth);
     for (int i = 0; i < p; ++i) covs.push_back("lag" + std::to_string(i + 1));
     for (int j = 1; j <= q; ++j) covs.push_back("d" + std::to_string(j));
@@ -895,7 +938,7 @@ int main(int argc, char** argv) {
     const Args a = parse_args(argc, argv, 2);
     if (cmd == "simulate") {
       if (a.pos.size() != 1) throw UsageError("simulate needs exactly one family");
-      ConfigMap args;
+      Settings args;
       for (const auto& [k, v] : a.opt) {
         static const std::map<std::string, std::string> keys = {
             {"J", "J"}, {"Nj", "Nj"}, {"P", "P"}, {"T", "T"}, {"p", "p"}, {"q", "q"}, {"houses", "houses"},
@@ -904,7 +947,7 @@ int main(int argc, char** argv) {
         if (k == "seed" || k == "out") continue;
         const auto it = keys.find(k);
         if (it == keys.end()) throw UsageError("unknown option --" + k);
-        args.set(it->second, v);
+        args.put(it->second, v);
       }
       const std::string out = a.opt.count("out") ? a.opt.at("out") : ".";
       std::filesystem::create_directories(out);
