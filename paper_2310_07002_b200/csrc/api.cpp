@@ -35,6 +35,7 @@ cudaError_t launch_gauss(const ModelDev& M, const ChainsDev& S, const RunArgs& A
 int glm_width(int family, int J, int nc);
 int glm_cluster_size(int n, int kp, int nch);
 cudaError_t launch_glm(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+cudaError_t launch_lean(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
 cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
 size_t glm32_scratch_doubles(int nch);
 size_t glm32_image_bytes(int64_t n);
@@ -626,6 +627,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.fold_seg = m.fseg.p;
   md.seg_group = m.sgroup.p;
   md.seg_unseen = m.sunseen.p;
+  md.any_unseen = std::any_of(seg_unseen.begin(), seg_unseen.end(), [](int u) { return u != 0; }) ? 1 : 0;
   md.seg_row = m.srow.p;
   md.seg_rows = m.srows.p;
   md.inv_mass = m.inv_mass.p;
@@ -718,7 +720,15 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
     md32.g32_scratch = m.g32.p;
     e = launch_glm32(md32, S, A, st);  // FP32 variant: tcgen05 kind::tf32, split operands
   } else if ((ctx->policy == PCVG_KERNEL_SUFFSTAT || ctx->policy == PCVG_KERNEL_AUTO) && md.suff) {
-    e = launch_gauss(md, S, A, -suff_lanes_per_chain(md, S.nch), st);  // fold sufficient statistics
+    // fold sufficient statistics: the lean all-global kernel for warm-up / sampling where it applies
+    static const bool no_lean = std::getenv("PCVG_NO_LEAN") != nullptr;  // A/B tests only
+    const int T = suff_lanes_per_chain(md, S.nch);
+    e = cudaErrorNotSupported;
+    if (T == 1 && !no_lean) e = launch_lean(md, S, A, st);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      e = launch_gauss(md, S, A, -T, st);
+    }
   } else if (use_glm(ctx, m, S.nch)) {
     e = launch_glm(md, S, A, st);
   } else if (md.nb > 0 && (ctx->policy != PCVG_KERNEL_GENERIC || md.family >= kRatB)) {

@@ -216,8 +216,8 @@ __device__ __forceinline__ void global_grad(const ModelDev& M, const Prep<NCM>& 
     for (int c = 0; c < NCM; ++c)
       if (c < M.nc) gG[3 + c] = M.cmask[c] * dv<RCP>(sxr[c], P.v, P.inv_v) - qG[3 + c];
     gG[0] = G.a0 - qG[0];
-    gG[1] = dv<RCP>(G.a1, P.va, P.inv_va) - M.J - P.va / 10.0 + 1.0;
-    gG[2] = dv<RCP>(srr, P.v, P.inv_v) - ntr - P.v / 10.0 + 1.0;
+    gG[1] = dv<RCP>(G.a1, P.va, P.inv_va) - M.J - P.va * 0.1 + 1.0;  // half-normal(0, 10) prior: v / 10
+    gG[2] = dv<RCP>(srr, P.v, P.inv_v) - ntr - P.v * 0.1 + 1.0;
     if (value) {
       double l = -0.5 * (ntr * (kLog2Pi + P.logv) + srr / P.v);
       l += -0.5 * (M.J * (kLog2Pi + log(P.va)) + G.a1 / P.va);

@@ -106,6 +106,7 @@ struct ModelDev {
   // divergent, as with the reference's BrokenFoldModel whose gradient is NaN on one fold
   // (test_engine.cpp:57-90); -1 = none
   int broken_fold;
+  int any_unseen;  // some fold holds out every row of a group (compound predictive needed)
 };
 
 constexpr int kMaxBatches = 16;

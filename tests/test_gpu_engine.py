@@ -211,3 +211,39 @@ def test_sharded_driver_single_rank_equals_run():
         np.testing.assert_array_equal(rep["snapshots"], rep2["snapshots"])
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["cfg1_linreg_loo", "seasonal_timeblocks", "seasonal_hvblock"])
+def test_lean_kernel_matches_general_kernel(name):
+    """The lean all-global sufficient-statistics kernel (lean_kernel.cu: warm-up and sampling of
+    J = 1 grouped regression and seasonal AR) against the general sufficient-statistics kernel it
+    replaces on those launches (PCVG_NO_LEAN): the same arithmetic on the same streams, so a short
+    run's per-fold estimates and R-hat agree to rounding on (nearly) every fold."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path[:0] = ["tests", "tests/golden", "."]
+from parity_util import Case
+from paper_2310_07002_b200 import abi, pcv
+case = Case(sys.argv[2])
+with pcv.Context(0) as c:
+    for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks)):
+        c.add_model(m, kp, bank, model_id=i)
+    rep = c.run(abi.run_config(chains=4, iters=16, warmup=4, batch_size=4, blocks=4, bench_draws=10, seed=9))
+np.save(sys.argv[1], np.stack([rep["estimate"], rep["rhat"]]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env in (("lean", {}), ("general", {"PCVG_NO_LEAN": "1"})):
+        path = f"/tmp/pcvg_lean_{tag}_{name}.npy"
+        r = subprocess.run([sys.executable, "-c", code, path, name], env={**os.environ, **env}, capture_output=True,
+                           text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr
+        out[tag] = np.load(path)
+    a, b = out["lean"], out["general"]
+    ok = np.isfinite(b)
+    np.testing.assert_array_equal(ok, np.isfinite(a))
+    rel = np.abs(a[ok] - b[ok]) / (1.0 + np.abs(b[ok]))
+    assert np.mean(rel <= 1e-10) >= 0.95, np.sort(rel)[-5:]
