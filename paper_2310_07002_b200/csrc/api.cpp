@@ -16,6 +16,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -53,6 +54,7 @@ cudaError_t launch_feed_streams(const ChainsDev& S, const double* s, int64_t str
                                 cudaStream_t st);
 cudaError_t launch_extra_centers(const ChainsDev& S, int nfold, int64_t warmup, cudaStream_t st);
 cudaError_t launch_extra_merge(const ChainsDev& S, int nfold, double* merged, cudaStream_t st);
+cudaError_t launch_regroup(const ChainsDev& S, int sub_used, int groups, double* g_x, double* g_x2, cudaStream_t st);
 cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int sub_used,
                          int groups, int64_t n, unsigned long long* rep_max, int* reject,
                          cudaStream_t st);
@@ -85,31 +87,57 @@ void ck(cudaError_t e, const char* what) {
     throw Error(PCVG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Device buffers come from the device's stream-ordered memory pool (cudaMallocAsync / cudaFreeAsync on
+// the owning context's stream), which keeps its memory mapped between uses: a context teardown returns
+// ~300 MB of chain state to the pool in milliseconds, where cudaFree unmapped it in 2 s
+// (profiles/r02_teardown.log), and the next context on the device reuses it.
+thread_local cudaStream_t g_alloc_stream = nullptr;  // the calling context's stream (set by guarded())
+
+void retain_pool_memory() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.push_back(dev);
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;  // stream the buffer was allocated on; freed in its order
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
   }
   void alloc(size_t count) {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     n = count;
-    if (count) ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    st = g_alloc_stream;
+    if (count) {
+      ck(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, st), "cudaMallocAsync");
+      ck(cudaStreamSynchronize(st), "alloc");  // usable from any stream (synchronous copies) from here
+    }
   }
   void upload(const std::vector<T>& v) {
     alloc(v.size());
     if (!v.empty()) ck(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
   }
-  std::vector<T> download(cudaStream_t st) const {
+  std::vector<T> download(cudaStream_t s) const {
     std::vector<T> v(n);
     if (n) {
-      ck(cudaMemcpyAsync(v.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost, st), "download");
-      ck(cudaStreamSynchronize(st), "sync");
+      ck(cudaMemcpyAsync(v.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost, s), "download");
+      ck(cudaStreamSynchronize(s), "sync");
     }
     return v;
   }
@@ -243,6 +271,11 @@ thread_local std::string g_last_error;
 
 template <class F>
 int32_t guarded(pcvg_ctx* ctx, F&& f) {
+  struct StreamScope {  // device buffers allocated by this call belong to the context's stream
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~StreamScope() { g_alloc_stream = prev; }
+  } scope(ctx ? ctx->stream : nullptr);
   try {
     f();
     return PCVG_OK;
@@ -676,6 +709,7 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.ring = ring;
   md.x32 = m.x32.p;
   md.suff = suff;
+  for (int i = 0; i <= kMaxCov; ++i) md.su[i] = suff && i < static_cast<int>(ss.ubar.size()) ? ss.ubar[i] : 0.0;
   md.sd = ss.d;
   md.sdp = ss.dp;
   md.sA = m.sA.p;
@@ -893,8 +927,18 @@ void device_benchmark(pcvg_ctx* ctx, const int32_t* failed, int64_t nonfailed_be
     DevBuf<int64_t> it;
     it.upload(item);
     const ChainSet& cs = *ctx->chains[mi];
-    ck(launch_bench(cs.view(L, ctx->fb, cfg.seed, 0), nfold, it.p, R, sub_used, std::min(cfg.blocks, sub_used),
-                    ctx->iters_done, mx.p, rj.p, ctx->stream), "benchmark");
+    ChainsDev S = cs.view(L, ctx->fb, cfg.seed, 0);
+    const int groups = std::min(cfg.blocks, sub_used);
+    DevBuf<double> gx, gx2;
+    if (groups != sub_used) {  // early stop: regroup the completed check intervals once
+      gx.alloc(static_cast<size_t>(groups) * cs.nch);
+      gx2.alloc(static_cast<size_t>(groups) * cs.nch);
+      ck(launch_regroup(S, sub_used, groups, gx.p, gx2.p, ctx->stream), "regroup");
+      ++ctx->launches;
+      S.acc.y_x = gx.p;
+      S.acc.y_x2 = gx2.p;
+    }
+    ck(launch_bench(S, nfold, it.p, R, groups, groups, ctx->iters_done, mx.p, rj.p, ctx->stream), "benchmark");
     ++ctx->launches;
     ck(cudaStreamSynchronize(ctx->stream), "benchmark");  // `it` is freed at scope exit
   }
@@ -994,6 +1038,7 @@ pcvg_status pcvg_create(int32_t device, pcvg_ctx** out) {
     ck(cudaEventCreateWithFlags(&ctx->evj, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreate(&ctx->ev0), "cudaEventCreate");
     ck(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
+    retain_pool_memory();
     *out = ctx.release();
   }));
 }
@@ -1010,6 +1055,7 @@ pcvg_status pcvg_destroy(pcvg_ctx* ctx) {
   const auto t2 = now();
   ctx->centers.clear();
   ctx->models.clear();
+  ctx->stream_scores.alloc(0);  // every device buffer is freed in its stream's order before the streams go
   const auto t3 = now();
   if (verbose)
     std::fprintf(stderr, "pcvg_destroy: sync %.3f s, chains %.3f s, models %.3f s\n",
@@ -1570,11 +1616,17 @@ void run_checkpoints(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
   std::vector<int64_t> divs(rows * L);
   rep->n_checkpoints = 0;
   bool stopped = false;
+  static const bool verbose = std::getenv("PCVG_VERBOSE") != nullptr;  // tuning only
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
   for (size_t ci = 0; ci < cks.size() && !stopped; ++ci) {
+    const auto t0 = now();
     st = pcvg_advance(ctx, cks[ci] - ctx->iters_done);
     if (st != PCVG_OK) throw Error(st, ctx->err);
+    const auto t1 = now();
     st = pcvg_fold_stats(ctx, &tab, divs.data(), &dropped, &done);
     if (st != PCVG_OK) throw Error(st, ctx->err);
+    const auto t2 = now();
     const bool last = ci + 1 == cks.size();
     bool final_ck = last;
     if (cfg->early_stop && !last && static_cast<int>(ci + 1) >= cfg->blocks) {
@@ -1622,6 +1674,9 @@ void run_checkpoints(pcvg_ctx* ctx, const pcvg_run_config* cfg, pcvg_report* rep
       t2.failed = nullptr;
       merge_stats(nm, K, cfg, done, 0, &t2, nullptr, nullptr, D, rep, nullptr);
     }
+    if (verbose)
+      std::fprintf(stderr, "checkpoint %zu (iteration %lld): advance %.3f s, fold_stats %.3f s, rule + merge %.3f s\n", ci,
+                   static_cast<long long>(done), secs(t0, t1), secs(t1, t2), secs(t2, now()));
     if (rep->snapshots) {
       double* o = rep->snapshots + 7 * ci;
       o[0] = static_cast<double>(done);
@@ -1907,7 +1962,7 @@ extern "C" pcvg_status pcvg_fold_gram(int64_t n, int32_t nc, const double* y, co
       hiv[k] = hi[k];
     }
     SuffStats ss;
-    if (!build_suffstats(n, nc, 0, y, x, key, nullptr, K, lov.data(), hiv.data(), ss))
+    if (!build_suffstats(n, nc, 0, y, x, key, nullptr, K, lov.data(), hiv.data(), ss, false, false))
       throw Error(PCVG_INVALID_INPUT, "non-finite data or Gram entry");
     std::copy(ss.A.begin(), ss.A.end(), gram);
   }));

@@ -268,7 +268,32 @@ __global__ void bench_kernel(ChainsDev S, int nfold, const int64_t* item, int R,
   atomicMax(rep_max + r, static_cast<unsigned long long>(__double_as_longlong(rh)));
 }
 
+// Regrouped benchmark blocks: block g of chain c = sum of its sub-blocks [begin(g), begin(g + 1)) in
+// order (the sums bench_kernel forms on the fly), written once so the R replicates each read
+// `groups` values per chain instead of `sub_used`.
+__global__ void regroup_kernel(const double* y_x, const double* y_x2, int nch, int sub_used, int groups,
+                               double* g_x, double* g_x2) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nch) return;
+  for (int g = 0; g < groups; ++g) {
+    double a = 0.0, b = 0.0;
+    for (int d = block_group_begin(g, sub_used, groups); d < block_group_begin(g + 1, sub_used, groups); ++d) {
+      a += y_x[static_cast<size_t>(d) * nch + c];
+      b += y_x2[static_cast<size_t>(d) * nch + c];
+    }
+    g_x[static_cast<size_t>(g) * nch + c] = a;
+    g_x2[static_cast<size_t>(g) * nch + c] = b;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_regroup(const ChainsDev& S, int sub_used, int groups, double* g_x, double* g_x2,
+                           cudaStream_t st) {
+  if (S.nch == 0) return cudaSuccess;
+  regroup_kernel<<<(S.nch + 255) / 256, 256, 0, st>>>(S.acc.y_x, S.acc.y_x2, S.nch, sub_used, groups, g_x, g_x2);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_bench(const ChainsDev& S, int nfold, const int64_t* item, int R, int sub_used,
                          int groups, int64_t n, unsigned long long* rep_max, int* reject,

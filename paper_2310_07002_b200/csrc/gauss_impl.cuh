@@ -474,7 +474,12 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
   double sv[D];  // this lane's sum_g off_g s_g
 #pragma unroll
   for (int i = 0; i < D; ++i) sv[i] = 0.0;
-  double t2 = 0.0, sr_tot = 0.0, dk0 = 0.0, dk1 = 0.0, srr_a = 0.0;
+  // centred statistics (suffstats.cpp): offsets shift by om.ubar, S_xr gains ubar_x * sum_g S_r[g]
+  double om_u = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+    if (i < d) om_u = fma(PCVG_OM(i), M.su[i], om_u);
+  double t2 = 0.0, sr_tot = 0.0, sr_all = 0.0, dk0 = 0.0, dk1 = 0.0, srr_a = 0.0;
   GroupAcc G{0.0, 0.0, 0.0, 0.0};
   // rat M_A: slope slots after the intercept slots
   const int ns_a = FAM == kRatA && qs ? suff_slots(M, T) : 0;
@@ -504,7 +509,7 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
       }
       bad |= !isfinite(qg);
     }
-    const double off = group_offset<FAM, NCM>(P, qg);
+    const double off = group_offset<FAM, NCM>(P, qg) - om_u;
     // this fold's statistics of group g: an override when the fold holds out some of its rows
     while (ov < ov_end && __ldg(M.sov_g + ov) < g) ++ov;
     double ng;
@@ -599,6 +604,7 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
     }
     const double srg = fma(-ng, off, ws);
     t2 = fma(off, ws + srg, t2);
+    sr_all += srg;
     if constexpr (FAM != kSeasonal) {
       const double gg = group_grad<FAM, NCM, NGM, true>(P, qG, M, qg, srg, G);
       bad |= !isfinite(gg);
@@ -647,6 +653,11 @@ __device__ __forceinline__ void suff_pass(const ModelDev& M, const ChainsDev& S,
       if (kind == 1) dk0 = lane_sum<T>(dk0, mask);
       if (last) dk1 = lane_sum<T>(dk1, mask);
     }
+    if constexpr (FAM != kRatA) sr_all = lane_sum<T>(sr_all, mask);
+  }
+  if constexpr (FAM != kRatA) {
+#pragma unroll
+    for (int k = 0; k < NCM; ++k) sxr[k] += M.su[1 + k] * sr_all;  // sum x r = sum x' r + xbar sum r
   }
   k0g += dk0;
   k1g += dk1;

@@ -41,24 +41,40 @@ namespace {
 using namespace tc;
 
 constexpr int kC = 64;          // chains per CTA
-constexpr int kThreads = 512;
-constexpr int kWarps = kThreads / 32;
 constexpr int kLdS = 68;        // leading dim of [k][chain] / [row][chain] shared arrays
-constexpr int kOwners = kThreads / kC;  // owner threads per chain (8)
+constexpr int kMaxOwners = 8;   // owner threads per chain at 512 threads
 constexpr int kStages = 3;      // TMA ring depth
 
-template <int KP>
+// Warp layout: 4 chain groups (16 chains each) x RQ row groups. WREG (tested for KP = 52 with 8 warps
+// of 250 registers holding each warp's GEMM-weight fragments for the whole pass) ran 3% slower than
+// 16 warps of 128 registers: with two warps per scheduler the sigmoid phases no longer hide behind
+// other warps' DMMA (profiles/r02_glm_layout.log; ncu's "shared pipe" is the FP64 datapath that
+// DMMA and DFMA share, not shared memory). So every design runs 16 warps.
+template <int KP, int THREADS_ = 512>
 struct Geom {
+  static constexpr int THREADS = THREADS_;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int RQ = WARPS / 4;                    // row groups
+  static constexpr int OWNERS = THREADS / kC;             // owner threads per chain
+  static constexpr bool WREG = THREADS_ < 512;            // weight fragments in registers
   static constexpr int KS = KP / 4;                       // k-steps of X . W
   static constexpr int PT = (KP + 7) / 8;                 // 8-row tiles of X^T . R
   static constexpr int TM = KP <= 8 ? 256 : (KP <= 16 ? 128 : 64);  // rows per TMA tile
-  static constexpr int ROWS_W = TM / 4;                   // rows per warp (row quarter)
+  static constexpr int ROWS_W = TM / RQ;                  // rows per warp per tile
   static constexpr int CHUNKS = ROWS_W / 16;              // 16-row chunks per warp per tile
   static constexpr int XPAD = PT * 8 - KP + 4;            // X^T p-tile overread
   static constexpr int DIMP = KP + 4;                     // max parameters (incl. specials)
-  static constexpr int OWN = (DIMP + kOwners - 1) / kOwners;
+  static constexpr int OWN = (DIMP + OWNERS - 1) / OWNERS;
   static constexpr int TILE_BYTES = TM * KP * 8 + TM * 8 + TM * 4;
 };
+
+// Residual statistic of chain c summed over the row groups in a fixed tree order.
+template <int RQ>
+__device__ __forceinline__ double rq_sum(const double (*llp)[kC], int c) {
+  if constexpr (RQ == 4) return (llp[0][c] + llp[1][c]) + (llp[2][c] + llp[3][c]);
+  else if constexpr (RQ == 2) return llp[0][c] + llp[1][c];
+  else return llp[0][c];
+}
 
 template <int KP>
 struct Smem {
@@ -69,11 +85,11 @@ struct Smem {
   double rs[(KP > 64 ? KP : 64) * kLdS];  // per-warp R blocks; reused as G and momentum staging
   double qs[G::DIMP * kLdS];              // parameters, [k][chain]
   double ws[KP * kLdS];                   // GEMM weights, [col][chain]
-  double llp[4][kC];                      // per row quarter: log-lik (logistic) / sum r^2 (gaussian)
+  double llp[4][kC];                      // per row group: log-lik (logistic) / sum r^2 (gaussian)
   double gt[KP * kLdS];                   // cluster-reduced G, [col][chain]
   double lt[kC];                          // cluster-reduced residual statistic
-  double red[kOwners][kC];                // owner partial sums (kinetic)
-  double pri[kOwners][kC];                // owner partial sums (log joint)
+  double red[kMaxOwners][kC];             // owner partial sums (kinetic)
+  double pri[kMaxOwners][kC];             // owner partial sums (log joint)
   double exp_tab[16];                     // 2^(-j/16)
   int exp_hi32[32], exp_lo32[32];          // 2^(-j/32) as high / low words (gradient-only sigmoid)
   int lo[kC], hi[kC], ntr[kC];
@@ -239,6 +255,14 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
       hi[j][e] = sm.hi[ch];
     }
   const double* wcol = sm.ws + 16 * cg + (l >> 2);
+  // B fragments of X . W for this warp's 16 chains, held across the pass (WREG) or read per chunk
+  double wf[G::WREG ? G::KS : 1][2];
+  if constexpr (G::WREG) {
+#pragma unroll
+    for (int ks = 0; ks < G::KS; ++ks)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) wf[ks][j] = wcol[(4 * ks + (l & 3)) * kLdS + 8 * j];
+  }
   double gacc[G::PT][2][2];
 #pragma unroll
   for (int pt = 0; pt < G::PT; ++pt)
@@ -265,7 +289,7 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
       for (int ks = 0; ks < G::KS; ++ks) {
         double b[2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) b[j] = wcol[(4 * ks + (l & 3)) * kLdS + 8 * j];
+        for (int j = 0; j < 2; ++j) b[j] = G::WREG ? wf[G::WREG ? ks : 0][j] : wcol[(4 * ks + (l & 3)) * kLdS + 8 * j];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           const double a = xs[(row0 + 8 * mt + (l >> 2)) * KP + 4 * ks + (l & 3)];
@@ -326,7 +350,7 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
     }
     if (l == 0 && tl + kStages < ntiles) {
       const unsigned int old = atomicAdd(&sm.rel[slot], 1u);
-      if ((old + 1u) % kWarps == 0u) issue_tile(sm, M, t + kStages, g + kStages);
+      if ((old + 1u) % G::WARPS == 0u) issue_tile(sm, M, t + kStages, g + kStages);
     } else if (l == 0) {
       atomicAdd(&sm.rel[slot], 1u);
     }
@@ -334,9 +358,9 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
   gtile = g0 + ntiles;
   GTRACE(1);
   __syncthreads();
-  // Stage G [col][chain] into sm.rs: quarter 0 stores, quarters 1..3 add in order.
+  // Stage G [col][chain] into sm.rs: row group 0 stores, the others add in order.
 #pragma unroll 1
-  for (int qq = 0; qq < 4; ++qq) {
+  for (int qq = 0; qq < G::RQ; ++qq) {
     if (rq == qq) {
 #pragma unroll
       for (int pt = 0; pt < G::PT; ++pt) {
@@ -380,6 +404,8 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
 template <int KP>
 __device__ void reduce_pass(Smem<KP>& sm, int cs) {
   namespace cgr = cooperative_groups;
+  using G = Geom<KP>;
+  constexpr int kThreads = G::THREADS;
   const int tid = threadIdx.x;
   constexpr int kE = KP * kC + kC;  // G elements, then the residual statistic per chain
   if (cs == 1) {
@@ -387,7 +413,7 @@ __device__ void reduce_pass(Smem<KP>& sm, int cs) {
       const int k = i / kC, c = i % kC;
       sm.gt[k * kLdS + c] = sm.rs[k * kLdS + c];
     }
-    if (tid < kC) sm.lt[tid] = (sm.llp[0][tid] + sm.llp[1][tid]) + (sm.llp[2][tid] + sm.llp[3][tid]);
+    if (tid < kC) sm.lt[tid] = rq_sum<G::RQ>(sm.llp, tid);
     __syncthreads();
     return;
   }
@@ -411,7 +437,7 @@ __device__ void reduce_pass(Smem<KP>& sm, int cs) {
             v[w] = rq->rs[(e / kC) * kLdS + e % kC];
           } else {
             const int c = e - KP * kC;
-            v[w] = (rq->llp[0][c] + rq->llp[1][c]) + (rq->llp[2][c] + rq->llp[3][c]);
+            v[w] = rq_sum<G::RQ>(rq->llp, c);
           }
         }
       }
@@ -493,9 +519,10 @@ __device__ void glm_score_extra(const ModelDev& M, const ChainsDev& S, int gc, i
 }
 
 template <int FAM, int KP>
-__global__ void __launch_bounds__(kThreads, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs,
+__global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs,
                                                            int tile0) {
   using G = Geom<KP>;
+  constexpr int kThreads = G::THREADS, kOwners = G::OWNERS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem<KP>& sm = *reinterpret_cast<Smem<KP>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -849,7 +876,7 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
   auto launch = [&](int tile0, int ntiles, int cs) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ntiles * cs);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(Geom<KP>::THREADS);
     cfg.dynamicSmemBytes = sizeof(Smem<KP>);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -868,7 +895,7 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     return cached_launch_fact(reinterpret_cast<const void*>(glm_kernel<FAM, KP>), c, [&] {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(c);
-      q.blockDim = dim3(kThreads);
+      q.blockDim = dim3(Geom<KP>::THREADS);
       q.dynamicSmemBytes = sizeof(Smem<KP>);
       cudaLaunchAttribute qa[1];
       qa[0].id = cudaLaunchAttributeClusterDimension;

@@ -115,7 +115,11 @@ __device__ __forceinline__ void lean_pass(const ModelDev& M, const GR& A, const 
     }
   }
   GroupAcc G{0.0, 0.0, 0.0, 0.0};
-  const double off = group_offset<FAM, NCM>(P, qa);
+  double om_u = 0.0;  // centred statistics: the offset shifts by om.ubar (suffstats.cpp)
+#pragma unroll
+  for (int i = 0; i < D; ++i) om_u = fma(PCVG_OM(i), M.su[i], om_u);
+  const double off_raw = group_offset<FAM, NCM>(P, qa);
+  const double off = off_raw - om_u;
   double ws = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) ws = fma(PCVG_OM(i), s[i], ws);
@@ -132,11 +136,14 @@ __device__ __forceinline__ void lean_pass(const ModelDev& M, const GR& A, const 
   double* sxr = q + 1;
 #pragma unroll
   for (int k = 0; k < NCM; ++k) sxr[k] -= __dmul_rn(off, s[1 + k]);  // sum_g off_g s_g (one group)
+  const double sr_all = 0.0 + srg;
+#pragma unroll
+  for (int k = 0; k < NCM; ++k) sxr[k] += M.su[1 + k] * sr_all;  // sum x r = sum x' r + xbar sum r
   if constexpr (VALUE) {
     bool poison = false;  // 0 * non-finite held-out term = NaN (grouped_regression.cpp:74-76)
     for (int tt = ex0; tt < ex1; ++tt) {
       const int i = __ldg(M.sex_rows + tt);
-      double m = off;
+      double m = off_raw;
 #pragma unroll
       for (int k = 0; k < NCM; ++k) m = fma(P.w[k], __ldg(M.x + static_cast<size_t>(k) * M.n + i), m);
       const double r = __ldg(M.y + i) - m;

@@ -13,6 +13,12 @@
 // training-row sum to ~1 ulp whatever the excluded set; a group with no training row gets exact
 // zeros. The excluded rows of each fold (key-sorted) are kept so the value pass can reproduce the
 // reference's poisoning by a non-finite masked row (grouped_regression.cpp:74-76).
+// Centring: the statistics are of u' = u - ubar (ubar the full-data column means), formed from the
+// double-double sums as A' = A - ubar s^T - s ubar^T + n ubar ubar^T and s'_g = s_g - n_g ubar before
+// the single rounding. With r_i = om.u'_i - (off_g - om.ubar) the kernel's S_rr = om^T A' om - ...
+// then cancels only ~eps * sum (u - ubar)^2 / sum r^2 instead of ~eps * sum y^2 / sum r^2, which for
+// data with a large level (y ~ 1e4 +- 1) is the difference between 1e-16 and 1e-8 relative error.
+// The per-subject Grams of the growth model M_A stay uncentred (ubar = 0).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -57,7 +63,7 @@ inline double dd_val(const DD& x) { return x.hi + x.lo; }
 // per subject).
 bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc, const int* key,
                      const int* grp_ptr, int K, const int* lo, const int* hi, SuffStats& S,
-                     bool group_gram) {
+                     bool group_gram, bool center) {
   const int d = nc + 1, dp = d * (d + 1) / 2, Jg = J > 0 ? J : 1;
   for (int64_t i = 0; i < n; ++i) {
     if (!std::isfinite(y[i])) return false;
@@ -88,11 +94,29 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
   }
   for (const DD& a : Af)
     if (!std::isfinite(a.hi) || !std::isfinite(a.lo)) return false;  // overflowing products
+  // the centre and the full-data sum of u (over all groups)
+  std::vector<DD> sf(d);
+  for (int g = 0; g < Jg; ++g)
+    for (int i = 0; i < d; ++i) {
+      const DD& v = gsf[static_cast<size_t>(g) * d + i];
+      dd_add(sf[i], v.hi, v.lo);
+    }
+  S.ubar.assign(d, 0.0);
+  if (center && !group_gram && n > 0)
+    for (int i = 0; i < d; ++i) S.ubar[i] = dd_val(sf[i]) / static_cast<double>(n);
+  const std::vector<double>& ub = S.ubar;
+  // s' = s - cnt ubar, rounded once
+  auto centred_sum = [&](const DD& v, double cnt, int i) {
+    DD x = v;
+    dd_add_prod(x, cnt, ub[i], -1.0);
+    return dd_val(x);
+  };
   S.gn.resize(Jg);
   S.gs.resize(static_cast<size_t>(Jg) * d);
   for (int g = 0; g < Jg; ++g) {
     S.gn[g] = static_cast<double>(gnf[g]);
-    for (int i = 0; i < d; ++i) S.gs[static_cast<size_t>(g) * d + i] = dd_val(gsf[static_cast<size_t>(g) * d + i]);
+    for (int i = 0; i < d; ++i)
+      S.gs[static_cast<size_t>(g) * d + i] = centred_sum(gsf[static_cast<size_t>(g) * d + i], static_cast<double>(gnf[g]), i);
   }
   S.gA.resize(gAf.size());
   for (size_t i = 0; i < gAf.size(); ++i) S.gA[i] = dd_val(gAf[i]);
@@ -124,11 +148,14 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
     S.ex_lo[k] = t0;
     S.ex_hi[k] = t1;
     std::copy(Af.begin(), Af.end(), Ak.begin());
+    std::vector<DD> sk(sf);  // the fold's training sum of u
     touched.clear();
     for (int t = t0; t < t1; ++t) {
       const int r = S.ex_rows[t], g = S.ex_grp[t];
-      for (int i = 0; i < d; ++i)
+      for (int i = 0; i < d; ++i) {
+        dd_add(sk[i], -u(r, i), 0.0);
         for (int j = 0; j <= i; ++j) dd_add_prod(Ak[i * (i + 1) / 2 + j], u(r, i), u(r, j), -1.0);
+      }
       if (gnk[g] == 0) {
         touched.push_back(g);
         for (int i = 0; i < d; ++i) gsk[static_cast<size_t>(g) * d + i] = gsf[static_cast<size_t>(g) * d + i];
@@ -142,13 +169,29 @@ bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc
           for (int j = 0; j <= i; ++j)
             dd_add_prod(gAk[static_cast<size_t>(g) * dp + i * (i + 1) / 2 + j], u(r, i), u(r, j), -1.0);
     }
+    // A' = A - ubar s^T - s ubar^T + n ubar ubar^T (training rows of fold k)
+    const double nk = static_cast<double>(n - (t1 - t0));
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j <= i; ++j) {
+        DD& a = Ak[i * (i + 1) / 2 + j];
+        if (ub[i] != 0.0 || ub[j] != 0.0) {
+          dd_add_prod(a, ub[i], sk[j].hi, -1.0);
+          dd_add(a, -ub[i] * sk[j].lo, 0.0);
+          dd_add_prod(a, ub[j], sk[i].hi, -1.0);
+          dd_add(a, -ub[j] * sk[i].lo, 0.0);
+          const double uu = ub[i] * ub[j], uue = std::fma(ub[i], ub[j], -uu);
+          dd_add_prod(a, nk, uu, 1.0);
+          dd_add(a, nk * uue, 0.0);
+        }
+      }
     for (int i = 0; i < dp; ++i) S.A[static_cast<size_t>(k) * dp + i] = dd_val(Ak[i]);
     std::sort(touched.begin(), touched.end());
     for (int g : touched) {
       const int64_t ntr = gnf[g] - gnk[g];
       S.ov_g.push_back(g);
       S.ov_n.push_back(static_cast<double>(ntr));
-      for (int i = 0; i < d; ++i) S.ov_s.push_back(ntr == 0 ? 0.0 : dd_val(gsk[static_cast<size_t>(g) * d + i]));
+      for (int i = 0; i < d; ++i)
+        S.ov_s.push_back(ntr == 0 ? 0.0 : centred_sum(gsk[static_cast<size_t>(g) * d + i], static_cast<double>(ntr), i));
       if (group_gram)
         for (int e = 0; e < dp; ++e) S.ov_A.push_back(ntr == 0 ? 0.0 : dd_val(gAk[static_cast<size_t>(g) * dp + e]));
       gnk[g] = 0;

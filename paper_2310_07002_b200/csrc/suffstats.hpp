@@ -14,10 +14,11 @@ struct SuffStats {
   std::vector<int> ex_lo, ex_hi;     // [K+1]: fold k's excluded rows are ex_rows[ex_lo..ex_hi)
   std::vector<int> ex_rows, ex_grp;  // [n] device rows sorted by key (stable), their group
   std::vector<double> gA, ov_A;      // group_gram: [Jg][dp], [nov][dp] per-group Grams of u
+  std::vector<double> ubar;          // [d] centre: A and the group sums are of u - ubar (zeros: uncentred)
 };
 
 bool build_suffstats(int64_t n, int nc, int J, const double* y, const double* xc, const int* key,
                      const int* grp_ptr, int K, const int* lo, const int* hi, SuffStats& S,
-                     bool group_gram = false);
+                     bool group_gram = false, bool center = true);
 
 }  // namespace pcvg

@@ -100,6 +100,7 @@ struct ModelDev {
   const int* sex_rows;
   const int* sex_grp;
   double* g32_scratch;  // logistic FP32 variant: per-CTA FP64 G partials (the model's own buffer)
+  double su[kMaxCov + 1];  // centre ubar of u = (y, x): sA / sgs / sov_s are statistics of u - ubar
   const double* sgA;    // rat M_A: [J][3] full-data per-group (y, t) Gram (yy, ty, tt)
   const double* sov_A;  // rat M_A: [nov][3] the fold's override Grams
   // fault injection (tests only, pcvg_debug_break_fold): every transition of a chain of this fold is

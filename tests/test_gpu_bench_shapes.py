@@ -232,3 +232,46 @@ def test_logs_short_horizon_per_fold_matches_oracle(name):
         rel = np.abs(a[ok] - b[ok]) / (1.0 + np.abs(b[ok]))
         assert np.mean(rel <= 1e-8) >= 0.9, (name, key, np.sort(rel)[-5:])
     np.testing.assert_array_equal(rep["fault"], orep["fault"])
+
+
+# ------------------------------------------------------------------------------ uncentred data
+@pytest.mark.parametrize("policy", list(POLICIES))
+def test_gram_statistics_on_uncentred_data(policy):
+    """Fold sufficient statistics on data with a large level (cfg1 with y + 1e6, x + 1e3): the masked
+    residual sums come from Gram matrices of u - ubar (suffstats.cpp). The row form of S_rr = sum r^2
+    has the terms r^2 and, inside each r = y - alpha - x.beta, the products 2|r| (|y| + |alpha| +
+    sum|x beta|) (~4e8 here); the raw Gram's om^T A om cancels sum y^2 (~1e14) and would miss that by
+    ~1e-2 (25x the 1e-12 budget), the centred one by nothing measurable. The log sigma_y and beta
+    gradient components match the oracle at 1e-12 of those term sums on both kernels, at positions
+    equivalent to the posterior (the intercept shifted so residuals stay O(1))."""
+    base = case("cfg1_linreg_loo")
+    cy, cx = 1.0e6, 1.0e3
+    d = pcv.Dataset(base.data.y + cy, base.data.x + cx, base.data.group_id, base.data.time_index)
+    f = pcv.make_loo_scheme(d)
+    m = pcv.GroupedRegressionModel("shifted", d, f)
+    om = O.OModel(d, f.arrays(), abi.SpecArrays(family=abi.FAMILY_GROUPED))
+    kp = base.kparams[0]
+    P = d.x.shape[1]
+    th = sample_thetas(base, 0, 12, seed=5)
+    th[:, 0] += cy - cx * th[:, 1:1 + P].sum(axis=1)  # alpha_0: identical residuals
+    th[:, 1 + P] = th[:, 0]  # mu_alpha next to alpha_0 keeps the hierarchical prior O(1)
+    folds = np.array([0, 1, 17, 50, 98, 99, 100, 3, 4, 5, 6, 7], dtype=np.int32)
+    c = pcv.Context(0)
+    c.set_kernel_policy(POLICIES[policy])
+    slot = c.add_model(m, kp, base.banks[0] + 0.0, model_id=0)
+    _, g = c.eval(slot, folds, th)
+    c.close()
+    for i, fk in enumerate(folds):
+        fk = int(fk)
+        og = om.grad(th[i], fk)
+        train = np.ones(d.n_obs, bool)
+        if fk < f.K:
+            train[f.test_index == fk] = False
+        r = d.y - th[i, 0] - d.x @ th[i, 1:1 + P]
+        v = np.exp(th[i, P + 3]) ** 2
+        terms = np.abs(d.y) + abs(th[i, 0]) + np.abs(d.x * th[i, 1:1 + P]).sum(axis=1)  # inside each r
+        s_rr = np.sum((r ** 2 + 2 * np.abs(r) * terms)[train]) / v + train.sum() + v / 10 + 1
+        assert abs(g[i, P + 3] - og[P + 3]) <= RTOL * s_rr, (policy, fk, g[i, P + 3], og[P + 3], s_rr)
+        for cc in range(P):
+            s_x = np.sum(np.abs(d.x[train, cc]) * terms[train]) / v + abs(th[i, 1 + cc])
+            assert abs(g[i, 1 + cc] - og[1 + cc]) <= RTOL * s_x, (policy, fk, cc, g[i, 1 + cc], og[1 + cc])
