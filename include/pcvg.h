@@ -299,6 +299,8 @@ pcvg_status pcvg_fold_stats(pcvg_ctx* ctx, pcvg_fold_table* out, int64_t* diverg
 pcvg_status pcvg_block_sums(pcvg_ctx* ctx, double* y_x, double* y_x2);
 /* Device event time of the last pcvg_advance call (ms) and kernel count so far. */
 pcvg_status pcvg_timing(const pcvg_ctx* ctx, double* last_advance_ms, int64_t* launches);
+/* Device time of the current run's Step 2 (pcvg_begin) and of its Step-3 advances so far (ms). */
+pcvg_status pcvg_phase_times(const pcvg_ctx* ctx, double* warmup_ms, double* sampling_ms);
 
 /* Host merge (Step 4, engine.cpp:117-253 + 385-480): from the full (all-shard, fold-order)
  * per-fold tables produce the global statistics. `final_checkpoint` applies the failed-fold
@@ -375,6 +377,23 @@ pcvg_status pcvg_merge_bench(int32_t n_models, int32_t K, const pcvg_run_config*
                              int64_t iter_count, int32_t final_checkpoint,
                              const pcvg_fold_table* folds, const double* bench_max,
                              pcvg_report* report);
+
+/* ---------------------------------------------------------------- multi-GPU (one process)
+ * run_pcv with the folds sharded across devices: one context per device, device i
+ * owning folds [i K / n, (i + 1) K / n) with all L chains of each fold; each device advances on its own
+ * host thread, the per-fold tables are merged in fold order at every check interval and the shuffle
+ * benchmark runs on each device's block sums at its global stream offset (replicate maxima combined
+ * by MAX), so the statistics do not depend on the device count. Implemented above this ABI with the
+ * stepwise calls (csrc/multi_device.cpp). A device id may repeat (several shards on one GPU). */
+typedef struct pcvg_multi pcvg_multi;
+pcvg_status pcvg_multi_create(int32_t n_devices, const int32_t* devices, pcvg_multi** out);
+pcvg_status pcvg_multi_destroy(pcvg_multi* mc);
+const char* pcvg_multi_last_error(const pcvg_multi* mc);
+pcvg_status pcvg_multi_add_model(pcvg_multi* mc, const pcvg_dataset* data, const pcvg_folds* folds,
+                                 const pcvg_model_spec* spec, const pcvg_kernel* kernel, const double* bank,
+                                 int64_t bank_rows, int32_t model_id, int32_t* slot);
+pcvg_status pcvg_multi_set_kernel_policy(pcvg_multi* mc, int32_t policy);
+pcvg_status pcvg_multi_run(pcvg_multi* mc, const pcvg_run_config* cfg, pcvg_report* report);
 
 #ifdef __cplusplus
 }

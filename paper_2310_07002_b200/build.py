@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr"]
-SOURCES = ["gauss_kernel.cu", "suff_kernel.cu", "lean_kernel.cu", "glm_kernel.cu", "glm32_kernel.cu", "chain_kernels.cu", "api.cpp", "stats.cpp",
+SOURCES = ["gauss_kernel.cu", "suff_kernel.cu", "lean_kernel.cu", "glm_kernel.cu", "glm32_kernel.cu", "chain_kernels.cu", "api.cpp", "multi_device.cpp", "stats.cpp",
            "host_folds.cpp", "suffstats.cpp"]
 HEADERS = ["device_cache.hpp", "device_common.cuh", "types.cuh", "host_common.hpp", "tc_common.cuh", "score_extra.cuh", "suffstats.hpp", "gauss_impl.cuh"]
 

@@ -1531,6 +1531,13 @@ pcvg_status pcvg_block_sums(pcvg_ctx* ctx, double* y_x, double* y_x2) {
   }));
 }
 
+pcvg_status pcvg_phase_times(const pcvg_ctx* ctx, double* warmup_ms, double* sampling_ms) {
+  if (!ctx) return PCVG_INVALID_INPUT;
+  if (warmup_ms) *warmup_ms = ctx->warm_ms;
+  if (sampling_ms) *sampling_ms = ctx->sample_ms;
+  return PCVG_OK;
+}
+
 pcvg_status pcvg_timing(const pcvg_ctx* ctx, double* last_ms, int64_t* launches) {
   if (!ctx) return PCVG_INVALID_INPUT;
   if (last_ms) *last_ms = ctx->last_ms;

@@ -114,6 +114,14 @@ def load():
     _sig(lib, "pcvg_benchmark", i32, [vp, pi32, i64, i64, i32, pf, pi32])
     _sig(lib, "pcvg_run_streams", i32, [vp, i32, pf, pf, P(abi.RunConfig), P(abi.Report)])
     _sig(lib, "pcvg_debug_break_fold", i32, [vp, i32, i32])
+    _sig(lib, "pcvg_phase_times", i32, [vp, pf, pf])
+    _sig(lib, "pcvg_multi_create", i32, [i32, pi32, P(vp)])
+    _sig(lib, "pcvg_multi_destroy", i32, [vp])
+    _sig(lib, "pcvg_multi_last_error", C.c_char_p, [vp])
+    _sig(lib, "pcvg_multi_add_model", i32, [vp, P(abi.Dataset), P(abi.Folds), P(abi.ModelSpec), P(abi.Kernel),
+                                            pf, i64, i32, pi32])
+    _sig(lib, "pcvg_multi_set_kernel_policy", i32, [vp, i32])
+    _sig(lib, "pcvg_multi_run", i32, [vp, P(abi.RunConfig), P(abi.Report)])
     _sig(lib, "pcvg_benchmark_host", i32, [i32, i32, i32, i32, i32, i32, i64, u64, i32, pf, pf, pi32, i64,
                                            i64, pf, pi32])
     _sig(lib, "pcvg_merge_bench", i32, [i32, i32, P(abi.RunConfig), i64, i32, P(abi.FoldTable), pf,
@@ -561,6 +569,64 @@ class Context:
         a, b = np.zeros(n), np.zeros(n)
         self._chk(self.lib.pcvg_block_sums(self.h, _p(a), _p(b)))
         return a, b
+
+
+class MultiContext:
+    """run_pcv across several devices in one process (pcvg_multi_*): folds sharded in contiguous
+    ranges, one host thread per device, per-fold tables merged in fold order. Device ids may repeat
+    (several shards on one GPU)."""
+
+    def __init__(self, devices):
+        self.lib = load()
+        ids = np.ascontiguousarray(devices, dtype=np.int32)
+        self.h = C.c_void_p()
+        rc = self.lib.pcvg_multi_create(len(ids), _p(ids, C.c_int32), C.byref(self.h))
+        if rc != 0:
+            _check(rc)
+        self.models = []
+        self._keep = []
+
+    def close(self):
+        if self.h:
+            self.lib.pcvg_multi_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, rc):
+        if rc != 0:
+            raise _EXC.get(rc, PcvError)(self.lib.pcvg_multi_last_error(self.h).decode())
+
+    def set_kernel_policy(self, policy):
+        self._chk(self.lib.pcvg_multi_set_kernel_policy(self.h, policy))
+
+    def add_model(self, model, kparams, bank, model_id=0):
+        kern = abi.KernelArrays(kparams.step_size, kparams.n_leapfrog, kparams.inv_mass_diag)
+        bank = np.ascontiguousarray(bank, dtype=np.float64)
+        slot = C.c_int32()
+        self._chk(self.lib.pcvg_multi_add_model(self.h, C.byref(model.data.struct), C.byref(model.fold_arrays.struct),
+                                                C.byref(model.spec.struct), C.byref(kern.struct), _p(bank),
+                                                bank.shape[0], model_id, C.byref(slot)))
+        self.models.append(model)
+        self._keep.append((kern, bank))
+        return slot.value
+
+    def run(self, cfg):
+        K, L = self.models[0].K, cfg.chains
+        nck = self.lib.pcvg_checkpoint_count(C.byref(cfg))
+        rep, arrs = abi.new_report(len(self.models), K, L, nck, cfg.bench_draws)
+        self._chk(self.lib.pcvg_multi_run(self.h, C.byref(cfg), C.byref(rep)))
+        return abi.report_dict(rep, arrs, len(self.models))
 
 
 def merge(n_models, K, cfg, iter_count, final, cols, y_x=None, y_x2=None):

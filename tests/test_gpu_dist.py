@@ -98,3 +98,37 @@ def test_sharded_logistic_within_rounding_then_mc_error():
     full = dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50, seed=5)
     a, b = run_sharded("logistic_loo", full), run_single("logistic_loo", full)
     assert abs(a["delta_hat"] - b["delta_hat"]) <= 4 * np.hypot(a["mcse"], b["mcse"])
+
+
+# ------------------------------------------------------------------------------ in-process multi-device
+def run_multi(name, cfgkw, devices):
+    from paper_2310_07002_b200 import abi, pcv
+    from parity_util import Case
+    case = Case(name)
+    with pcv.MultiContext(devices) as c:
+        for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks)):
+            c.add_model(m, kp, bank, model_id=i)
+        return c.run(abi.run_config(**cfgkw))
+
+
+@pytest.mark.parametrize("name,cfgkw,devices", [
+    ("cfg1_linreg_loo", dict(chains=4, iters=200, warmup=50, batch_size=20, bench_draws=50, checkpoint_every=100, seed=1), [0, 0]),
+    ("ex1_grouped_logo", dict(chains=4, iters=200, warmup=50, batch_size=20, bench_draws=50, seed=2), [0, 0, 0]),
+    ("seasonal_hvblock", dict(chains=4, iters=200, warmup=30, batch_size=20, bench_draws=50, checkpoint_every=20,
+                              early_stop=1, seed=3), [0, 0]),
+    ("radon_logo", dict(chains=4, iters=100, warmup=20, batch_size=10, bench_draws=50, seed=4), [0, 0, 0, 0]),
+])
+def test_multi_device_bit_identical_to_single(name, cfgkw, devices):
+    """pcvg_multi_run (csrc/multi_device.cpp: one context per shard, one host thread each, fold-order
+    merge) with the shards on cuda:0: every per-fold column, divergence count, benchmark replicate and
+    headline statistic equals the single-context pcvg_run bit for bit."""
+    a = run_multi(name, cfgkw, devices)
+    b = run_single(name, cfgkw)
+    for k in COLUMNS:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    np.testing.assert_array_equal(a["divergences"], b["divergences"])
+    for k in HEADLINE:
+        assert a[k] == b[k] or (np.isnan(a[k]) and np.isnan(b[k])), (k, a[k], b[k])
+    np.testing.assert_array_equal(a["benchmark"], b["benchmark"])
+    np.testing.assert_array_equal(a["snapshots"], b["snapshots"])
+    assert a["gpu_launches"] > 0
