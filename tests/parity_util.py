@@ -64,7 +64,7 @@ def term_scales(case, m, theta, fold):
     train = ~case.excluded(fold)
     fam = kw["family"]
     th = np.asarray(theta)
-    big = 10.0 + d.n_obs * 0 + np.abs(th).max() * th.size * 4
+    big = 1.0 + np.abs(th).max()  # the largest plain prior term of one component (-theta_j and its log)
     if fam == abi.FAMILY_LOGISTIC:
         eta = th[0] + x @ th[1:]
         r = y - 1 / (1 + np.exp(-eta))
@@ -116,3 +116,30 @@ def sample_thetas(case, m, n, seed=0):
 def probe_folds(case):
     K = case.K
     return sorted({0, 1, K // 2, K - 1, K})
+
+
+def leapfrog_scales(case, m, theta, momentum, fold, kp, n_lf=None, theta_end=None):
+    """Sums of absolute terms of the leapfrog end point (hmc.cpp:22-51): p' = p + eps/2 g(q0) + eps
+    g(q1) + ... + eps/2 g(qn) and q' = q + eps M^-1 (p + ...), bounded per component by
+    S_p = |p| + eps n_lf S_g and S_q = |q| + eps n_lf m S_p with S_g the gradient term sum at the
+    start (and at theta_end when given)."""
+    n_lf = kp.n_leapfrog if n_lf is None else n_lf
+    _, s_g = term_scales(case, m, theta, fold)
+    if theta_end is not None:
+        s_g = max(s_g, term_scales(case, m, theta_end, fold)[1])
+    s_p = np.abs(momentum) + kp.step_size * n_lf * s_g
+    s_q = np.abs(theta) + kp.step_size * n_lf * np.asarray(kp.inv_mass_diag) * s_p
+    return s_q, s_p
+
+
+class DataCase:
+    """The pieces of Case that term_scales / leapfrog_scales read, for a dataset built in a test."""
+
+    def __init__(self, data, folds, kw):
+        self.data, self.folds, self.kws = data, folds, [kw]
+
+    @property
+    def K(self):
+        return self.folds.K
+
+    excluded = Case.excluded

@@ -7,6 +7,9 @@ import pytest
 
 from paper_2310_07002_b200 import abi, pcv
 import _oracle as O
+from parity_util import DataCase, leapfrog_scales, term_scales
+
+RTOL = 1e-12
 
 pytestmark = pytest.mark.gpu
 
@@ -26,8 +29,9 @@ def thetas(model, n, seed):
     return np.array([pcv.initial_draw(model, seed, 100 + i) for i in range(n)]) * 0.5
 
 
-def scale(th):
-    return 1e4 * (1.0 + np.abs(th).max())
+FAMILY_KW = {abi.FAMILY_GROUPED: {"family": abi.FAMILY_GROUPED},
+             abi.FAMILY_RADON: {"family": abi.FAMILY_RADON, "include_floor": 1},
+             abi.FAMILY_RAT_GROWTH: {"family": abi.FAMILY_RAT_GROWTH, "per_subject_slope": 1}}
 
 
 @pytest.mark.parametrize("policy", [pcv.Context.KERNEL_ROWS, pcv.Context.KERNEL_SUFFSTAT])
@@ -48,6 +52,7 @@ def test_ragged_groups_and_row_keys(scheme, family, policy):
     om = O.OModel(d, f.arrays(), model.spec)
     dim = model.dim()
     kp = pcv.KernelParams(0.01, 8, np.ones(dim))
+    dc = DataCase(d, f, FAMILY_KW[family])
     with pcv.Context(0) as ctx:
         ctx.set_kernel_policy(policy)
         slot = ctx.add_model(model, kp, thetas(model, 2, 1))
@@ -57,9 +62,9 @@ def test_ragged_groups_and_row_keys(scheme, family, policy):
             lp, g = ctx.eval(slot, np.full(3, fold), th)
             for i in range(3):
                 olp, og = om.log_joint(th[i], fold), om.grad(th[i], fold)
-                s = scale(th[i])
-                assert abs(lp[i] - olp) <= 1e-12 * s * max(1.0, abs(olp)), (fold, lp[i], olp)
-                assert np.abs(g[i] - og).max() <= 1e-12 * s * max(1.0, np.abs(og).max()), fold
+                s_lp, s_g = term_scales(dc, 0, th[i], fold)
+                assert abs(lp[i] - olp) <= RTOL * s_lp, (fold, lp[i], olp, s_lp)
+                assert np.abs(g[i] - og).max() <= RTOL * s_g, (fold, np.abs(g[i] - og).max(), s_g)
             pr = ctx.eval_pred(slot, np.full(3, fold), th)
             for i in range(3):
                 ref = om.log_pred(th[i], fold)
@@ -100,12 +105,14 @@ def _many_groups_cases():
         kp = c.kparams[m]
         out.append(("radon400_logo_m%d" % m, c.models[m], c.omodels[m],
                     pcv.KernelParams(kp.step_size, 8, kp.inv_mass_diag),
-                    c.banks[m][np.linspace(0, len(c.banks[m]) - 1, 4).astype(int)], c.K))
+                    c.banks[m][np.linspace(0, len(c.banks[m]) - 1, 4).astype(int)], c.K,
+                    DataCase(c.data, c.folds, c.kws[m])))
     d = ragged_grouped(seed=9, J=150)  # grouped, 150 ragged groups, K-fold: every fold touches many groups
     f = pcv.make_kfold_scheme(d, 7, 3)
     model = pcv.GroupedRegressionModel("M", d, f)
     out.append(("grouped150_kfold", model, O.OModel(d, f.arrays(), model.spec),
-                pcv.KernelParams(0.01, 8, np.ones(model.dim())), thetas(model, 4, 5), f.K))
+                pcv.KernelParams(0.01, 8, np.ones(model.dim())), thetas(model, 4, 5), f.K,
+                DataCase(d, f, FAMILY_KW[abi.FAMILY_GROUPED])))
     # growth model with per-subject slopes, 120 ragged subjects: two slot arrays per lane
     d0 = ragged_grouped(seed=13, J=120)
     dr = pcv.Dataset(d0.y + 250.0, np.abs(d0.x[:, :1]) * 10.0, d0.group_id)
@@ -116,7 +123,8 @@ def _many_groups_cases():
     base = np.concatenate([gm, np.zeros(J), [250.0, 0.0, 0.0, -1.0, -0.3]])
     th_r = base + 0.01 * np.random.default_rng(6).standard_normal((4, base.size))
     out.append(("rat120_kfold", rm, O.OModel(dr, fr.arrays(), rm.spec),
-                pcv.KernelParams(0.005, 8, np.ones(rm.dim())), th_r, fr.K))
+                pcv.KernelParams(0.005, 8, np.ones(rm.dim())), th_r, fr.K,
+                DataCase(dr, fr, FAMILY_KW[abi.FAMILY_RAT_GROWTH])))
     return out
 
 
@@ -125,7 +133,7 @@ def test_many_groups_warp_kernels(policy):
     """J >= 64: log joint / gradient at the stored position, leapfrog end points (hmc.cpp:22-51)
     and injected-momentum hmc_step (hmc.cpp:53-99) against the oracle."""
     rng = np.random.default_rng(21)
-    for name, model, om, kp, th, K in _many_groups_cases():
+    for name, model, om, kp, th, K, dc in _many_groups_cases():
         step, im = kp.step_size, kp.inv_mass_diag
         with pcv.Context(0) as ctx:
             ctx.set_kernel_policy(policy)
@@ -134,23 +142,29 @@ def test_many_groups_warp_kernels(policy):
             lp, g = ctx.eval(slot, folds, th)
             for i in range(4):
                 olp, og = om.log_joint(th[i], int(folds[i])), om.grad(th[i], int(folds[i]))
-                s = scale(th[i])
-                assert abs(lp[i] - olp) <= 1e-12 * s * max(1.0, abs(olp)), (name, i, lp[i], olp)
-                assert np.abs(g[i] - og).max() <= 1e-12 * s * max(1.0, np.abs(og).max()), (name, i)
+                s_lp, s_g = term_scales(dc, 0, th[i], int(folds[i]))
+                assert abs(lp[i] - olp) <= RTOL * s_lp, (name, i, lp[i], olp, s_lp)
+                assert np.abs(g[i] - og).max() <= RTOL * s_g, (name, i, np.abs(g[i] - og).max(), s_g)
             mom = rng.standard_normal(th.shape) / np.sqrt(im)
             q1, p1, ok = ctx.leapfrog(slot, folds, th, mom)
             assert ok.sum() >= 2, (name, ok)
             for i in range(4):
                 okr, oq, op = om.leapfrog(int(folds[i]), step, 8, im, th[i], mom[i])
                 assert bool(okr) == bool(ok[i]), (name, i)
-                np.testing.assert_allclose(q1[i], oq, rtol=1e-8, atol=1e-9, err_msg=name)
-                np.testing.assert_allclose(p1[i], op, rtol=1e-8, atol=1e-8, err_msg=name)
+                if not okr:
+                    continue
+                s_q, s_p = leapfrog_scales(dc, 0, th[i], mom[i], int(folds[i]), kp, theta_end=oq)
+                assert np.all(np.abs(q1[i] - oq) <= RTOL * s_q), (name, i, np.max(np.abs(q1[i] - oq) / s_q))
+                assert np.all(np.abs(p1[i] - op) <= RTOL * s_p), (name, i, np.max(np.abs(p1[i] - op) / s_p))
             u = rng.uniform(size=4)
             out, h0, h1, acc, div = ctx.hmc_probe(slot, folds, th, mom, u)
             for i in range(4):
                 oth, oh0, oh1, oacc, odiv = om.hmc_probe(int(folds[i]), step, 8, im, th[i], mom[i], u[i])
                 assert div[i] == odiv, name
-                assert abs(h0[i] - oh0) <= 1e-10 * (1 + abs(oh0)), (name, h0[i], oh0)
+                s_lp, _ = term_scales(dc, 0, th[i], int(folds[i]))
+                assert abs(h0[i] - oh0) <= RTOL * s_lp, (name, h0[i], oh0)
                 if not odiv:
-                    assert abs(h1[i] - oh1) <= 1e-8 * (1 + abs(oh1)), (name, h1[i], oh1)
-                    np.testing.assert_allclose(out[i], oth, rtol=1e-8, atol=1e-8, err_msg=name)
+                    s_lp1, _ = term_scales(dc, 0, oth, int(folds[i]))
+                    assert abs(h1[i] - oh1) <= RTOL * max(s_lp, s_lp1), (name, h1[i], oh1)
+                    s_q, _ = leapfrog_scales(dc, 0, th[i], mom[i], int(folds[i]), kp, theta_end=oth)
+                    assert np.all(np.abs(out[i] - oth) <= RTOL * s_q), name

@@ -7,7 +7,7 @@ import pytest
 
 from paper_2310_07002_b200 import abi, pcv
 import _oracle as O
-from parity_util import ALL_FIXTURES, Case, sample_thetas, term_scales, probe_folds
+from parity_util import ALL_FIXTURES, Case, leapfrog_scales, sample_thetas, term_scales, probe_folds
 
 pytestmark = pytest.mark.gpu
 
@@ -117,11 +117,13 @@ def test_hmc_step_injected(ctx, name):
             s_lp, _ = term_scales(case, m, th[i], int(folds[i]))
             assert abs(h0[i] - oh0) <= RTOL * s_lp
             if not odiv:
-                # trajectory of n_lf=32 steps: allow error growth along the integrator
-                assert abs(h1[i] - oh1) <= 1e-9 * s_lp, (name, i, h1[i], oh1)
-                if abs((-oh1 + oh0)) > 1e-6 or True:
-                    assert acc[i] == oacc or abs(np.log(u[i]) + (oh1 - oh0)) < 1e-8
-                np.testing.assert_allclose(out[i], oth, rtol=1e-8, atol=1e-8)
+                # H1 after n_lf = 32 leapfrog steps: 1e-12 of the log joint's terms at either end
+                s_lp1, _ = term_scales(case, m, oth, int(folds[i]))
+                assert abs(h1[i] - oh1) <= RTOL * max(s_lp, s_lp1), (name, i, h1[i], oh1)
+                if abs(np.log(u[i]) + (oh1 - oh0)) > 1e-8:
+                    assert acc[i] == oacc
+                s_q, _ = leapfrog_scales(case, m, th[i], mom[i], int(folds[i]), kp, theta_end=oth)
+                assert np.all(np.abs(out[i] - oth) <= RTOL * s_q), (name, i, np.max(np.abs(out[i] - oth) / s_q))
     c.close()
 
 
@@ -133,13 +135,22 @@ def test_chain_trajectory_reference_stream(ctx, name):
     case, c, slots = case_in(ctx, name)
     m, slot = 0, slots[0]
     om, kp = case.omodels[m], case.kparams[m]
-    fold, chain, seed, steps = min(3, case.K - 1), 1, 17, 30
+    fold, chain, seed, steps = min(3, case.K - 1), 1, 17, 120
     th0 = case.banks[m][7]
     traj, div = c.hmc_chain(slot, fold, chain, seed, th0, steps)
     stream = pcv.stream_key(abi.STREAM_CHAIN_SAMPLING, m, fold, chain)
     otraj, odiv = om.hmc_chain(fold, kp.step_size, kp.n_leapfrog, kp.inv_mass_diag, seed, stream, th0, steps)
-    np.testing.assert_array_equal(div[:10], odiv[:10])
-    np.testing.assert_allclose(traj[:10], otraj[:10], rtol=1e-7, atol=1e-7)
+    # identical streams: the same divergence / acceptance sequence and positions equal to rounding
+    # until the first last-ulp difference is amplified by the chaotic dynamics
+    rel = np.abs(traj - otraj).max(axis=1) / (1.0 + np.abs(otraj).max(axis=1))
+    onset = int(np.argmax(rel > 1e-6)) if np.any(rel > 1e-6) else steps
+    print(f"{name}: trajectories agree to 1e-6 for {onset} of {steps} transitions (1e-12 for "
+          f"{int(np.argmax(rel > 1e-12)) if np.any(rel > 1e-12) else steps})")
+    # rounding-level at first, then exponential growth (J = 1 grouped regression: ~1.35x per transition
+    # from 1e-15, crossing 1e-6 after ~74 transitions; every other fixture stays below 1e-6 for 120)
+    assert np.all(rel[:10] < 1e-13), (name, rel[:10])
+    assert onset >= min(steps, 60), (name, onset, rel[:onset + 3])
+    np.testing.assert_array_equal(div[:onset], odiv[:onset])
     c.close()
 
 
@@ -277,8 +288,9 @@ def test_leapfrog_endpoint_and_reversibility(ctx, name):
     assert ok.all()
     for i in range(4):
         okr, oq, op = om.leapfrog(int(folds[i]), kp.step_size, kp.n_leapfrog, kp.inv_mass_diag, th[i], mom[i])
-        np.testing.assert_allclose(q1[i], oq, rtol=1e-8, atol=1e-9)
-        np.testing.assert_allclose(p1[i], op, rtol=1e-8, atol=1e-8)
+        s_q, s_p = leapfrog_scales(case, m, th[i], mom[i], int(folds[i]), kp, theta_end=oq)
+        assert np.all(np.abs(q1[i] - oq) <= RTOL * s_q), (name, i, np.max(np.abs(q1[i] - oq) / s_q))
+        assert np.all(np.abs(p1[i] - op) <= RTOL * s_p), (name, i, np.max(np.abs(p1[i] - op) / s_p))
     q2, p2, ok2 = c.leapfrog(slot, folds, q1, -p1)
     assert ok2.all()
     np.testing.assert_allclose(q2, th, rtol=0, atol=1e-10 * (1 + np.abs(th).max()))
