@@ -251,10 +251,11 @@ def main():
     per_launch_ms = local_ms / args.steps
     achieved = FLOP_PER_CHAIN_STEP * (fe - fb) * L / (per_launch_ms * 1e-3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_glm.json")  # v6 capture (current kernel)
+    prof = os.path.join(ROOT, "profiles", "r02_ncu_glm_base.json")  # ncu --set full of the current kernel
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            pj = json.load(fh)
+            traffic = pj.get("dram_bytes_per_launch") or pj.get("launches", [{}])[0].get("dram_bytes_per_launch")
     line = None
     if rank == 0:
         line = {"metric": "chain-steps/sec", "value": value, "unit": "chain-steps/s", "n_gpus": world,
@@ -267,7 +268,8 @@ def main():
                              "frac": achieved / peak, "traffic": traffic,
                              "flop_per_chain_step": FLOP_PER_CHAIN_STEP, "peak_source": peak_src,
                              "kernel": "glm32_kernel (tcgen05 kind::tf32)" if args.fp32 else "glm_kernel<logistic,52> (FP64 DMMA)",
-                             "traffic_source": "profiles/r01_ncu_glm.json (ncu --set full, dram read+write per launch)"},
+                             "traffic_source": "profiles/r02_ncu_glm_base.json (ncu --set full of the full-wave "
+                                               "sampling launch, dram read+write)"},
                 "clocks": clk.summary(), "gpu_launches": int(launches1 - launches0), "result": result}
     # e2e: the public API call with host buffers (pcvg_run: H2D of data/bank, Step 2 + Step 3,
     # per-fold + Step-4 statistics, D2H of the report), wall-clock, max over ranks.
