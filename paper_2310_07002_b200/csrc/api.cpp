@@ -37,6 +37,7 @@ int glm_width(int family, int J, int nc);
 int glm_cluster_size(int n, int kp, int nch);
 cudaError_t launch_glm(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
 cudaError_t launch_lean(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
+void glm_multicluster_scratch(int kp, int nch, size_t* part_doubles, size_t* counters);
 cudaError_t launch_glm32(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cudaStream_t st);
 size_t glm32_scratch_doubles(int nch);
 size_t glm32_image_bytes(int64_t n);
@@ -161,6 +162,8 @@ struct HostModel {
   DevBuf<double> sA, sgn, sgs, sov_n, sov_s, sgA, sov_A;  // fold sufficient statistics (suffstats.cpp)
   DevBuf<int> sov_ptr, sov_g, sex_lo, sex_hi, sex_rows, sex_grp;
   mutable DevBuf<double> g32;  // FP32 variant G scratch (grown on first use, per model)
+  mutable DevBuf<double> glm_part;      // few-chain multi-cluster GLM launches: cluster partials
+  mutable DevBuf<unsigned int> glm_cnt;  // and per-tile arrival counters
   int64_t bank_rows = 0;
   ModelDev md{};
 };
@@ -648,6 +651,8 @@ std::unique_ptr<HostModel> build_model(const pcvg_dataset* d, const pcvg_folds* 
   md.dim = m.dim;
   md.K = m.K;
   md.broken_fold = -1;
+  md.glm_part = nullptr;
+  md.glm_cnt = nullptr;
   md.y = m.y.p;
   md.x = m.x.p;
   md.xr = m.xr.p;
@@ -764,7 +769,20 @@ void launch_family(pcvg_ctx* ctx, const HostModel& m, const ChainsDev& S, const 
       e = launch_gauss(md, S, A, -T, st);
     }
   } else if (use_glm(ctx, m, S.nch)) {
-    e = launch_glm(md, S, A, st);
+    ModelDev mdg = md;
+    if ((S.nch + 63) / 64 <= 8) {
+      // few chain tiles: the launcher may split each tile over several clusters (a cooperative
+      // launch with a second reduction level in global memory); it runs on the context's first
+      // stream, ordered with the other model's launches
+      size_t pd = 0, nct = 0;
+      glm_multicluster_scratch(md.nc_pad, S.nch, &pd, &nct);
+      if (m.glm_part.n < pd) m.glm_part.alloc(pd);
+      if (m.glm_cnt.n < nct) m.glm_cnt.alloc(nct);
+      mdg.glm_part = m.glm_part.p;
+      mdg.glm_cnt = m.glm_cnt.p;
+      st = ctx->stream;
+    }
+    e = launch_glm(mdg, S, A, st);
   } else if (md.nb > 0 && (ctx->policy != PCVG_KERNEL_GENERIC || md.family >= kRatB)) {
     e = launch_gauss(md, S, A, 0, st);  // group-batched hierarchical kernel
   } else {

@@ -21,6 +21,7 @@
 // fixed rank order, so every CTA of the cluster holds bit-identical state; rank 0 writes it back.
 #include <algorithm>
 #include <cooperative_groups.h>
+#include <cuda/atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <math_constants.h>
@@ -35,6 +36,7 @@ namespace pcvg {
 
 int glm_cluster_size(int n, int kp, int nch);
 int glm_sm_count();
+int glm_clusters_per_tile(int n, int kp, int nch, int cs, bool have_scratch);
 
 namespace {
 
@@ -401,8 +403,45 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
 // xor-butterfly it (a fixed order) - then every rank copies the other slices from their owners, so
 // all ranks hold identical bits. Every remote load of a step is independent (a rank-ordered
 // dependent chain cost ~cs DSMEM latencies per element: ~40% of a pass at cs = 16, cfg2 K-fold).
+// Second level for a tile split over nc clusters (few chains on many SMs): each cluster's rank 0
+// publishes its cluster sum to global memory (double-buffered by pass parity), arrives on the
+// tile's counter, and every CTA of the tile waits for all nc arrivals and sums the nc partials in
+// cluster order, so all CTAs again hold identical bits. The launch is cooperative: all CTAs of the
+// grid are co-resident, so the wait cannot deadlock.
 template <int KP>
-__device__ void reduce_pass(Smem<KP>& sm, int cs) {
+__device__ void reduce_clusters(Smem<KP>& sm, const ModelDev& M, int tile, int nc, int clus, int crank,
+                                uint32_t& gpass) {
+  using G = Geom<KP>;
+  constexpr int kThreads = G::THREADS;
+  constexpr int kE = KP * kC + kC;
+  const int tid = threadIdx.x;
+  double* base = M.glm_part + (static_cast<size_t>(tile) * 2 + (gpass & 1u)) * nc * kE;
+  if (crank == 0) {
+    for (int e = tid; e < kE; e += kThreads)
+      __stcg(base + static_cast<size_t>(clus) * kE + e, e < KP * kC ? sm.gt[(e / kC) * kLdS + e % kC] : sm.lt[e - KP * kC]);
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> cnt(M.glm_cnt[tile]);
+    if (crank == 0) cnt.fetch_add(1u, cuda::memory_order_release);
+    const unsigned int target = (gpass + 1u) * static_cast<unsigned int>(nc);
+    while (cnt.load(cuda::memory_order_acquire) < target) __nanosleep(40);
+  }
+  __syncthreads();
+  for (int e = tid; e < kE; e += kThreads) {
+    double x = __ldcg(base + e);
+    for (int c = 1; c < nc; ++c) x += __ldcg(base + static_cast<size_t>(c) * kE + e);
+    if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = x;
+    else sm.lt[e - KP * kC] = x;
+  }
+  __syncthreads();
+  ++gpass;
+}
+
+template <int KP>
+__device__ void reduce_pass(Smem<KP>& sm, int cs, const ModelDev& M, int tile, int nc, int clus, int crank,
+                            uint32_t& gpass) {
   namespace cgr = cooperative_groups;
   using G = Geom<KP>;
   constexpr int kThreads = G::THREADS;
@@ -415,6 +454,7 @@ __device__ void reduce_pass(Smem<KP>& sm, int cs) {
     }
     if (tid < kC) sm.lt[tid] = rq_sum<G::RQ>(sm.llp, tid);
     __syncthreads();
+    if (nc > 1) reduce_clusters(sm, M, tile, nc, clus, crank, gpass);
     return;
   }
   cgr::cluster_group cl = cgr::this_cluster();
@@ -474,6 +514,10 @@ __device__ void reduce_pass(Smem<KP>& sm, int cs) {
     }
   }
   __syncthreads();  // the copied slices are read by the owner threads next
+  if (nc > 1) {
+    cl.sync();  // every rank done copying the others' slices before gt is overwritten
+    reduce_clusters(sm, M, tile, nc, clus, crank, gpass);
+  }
 }
 
 __device__ __forceinline__ double bernoulli_logit(double y, double x) {
@@ -520,7 +564,7 @@ __device__ void glm_score_extra(const ModelDev& M, const ChainsDev& S, int gc, i
 
 template <int FAM, int KP>
 __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, ChainsDev S, RunArgs A, int cs,
-                                                           int tile0) {
+                                                           int tile0, int nc) {
   using G = Geom<KP>;
   constexpr int kThreads = G::THREADS, kOwners = G::OWNERS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -529,10 +573,13 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
   const int nch = S.nch;
   const int dim = M.dim;
   const size_t plane = static_cast<size_t>(dim) * nch;
-  const int tile = tile0 + blockIdx.x / cs, crank = blockIdx.x % cs;  // chain tile, rank in the cluster
-  const bool writer = crank == 0;                              // rank 0 owns all global writes
+  const int span = cs * nc;                                     // CTAs per chain tile
+  const int tile = tile0 + blockIdx.x / span, gr = blockIdx.x % span;  // chain tile, rank in the tile
+  const int clus = gr / cs, crank = gr % cs;                   // cluster of the tile, rank in the cluster
+  const bool writer = gr == 0;                                 // rank 0 owns the final global writes
   const int ntiles_all = (M.n + G::TM - 1) / G::TM;
-  const int t0 = crank * ntiles_all / cs, t1 = (crank + 1) * ntiles_all / cs;
+  const int t0 = gr * ntiles_all / span, t1 = (gr + 1) * ntiles_all / span;
+  uint32_t gpass = 0;                                          // second-level reductions done
   const int oc = tid & (kC - 1), ok = tid / kC;  // owner: chain oc, params ok + 8j
   const int ogc = tile * kC + oc;
   const bool ovalid = ogc < nch;
@@ -603,7 +650,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
     }
     __syncthreads();
     grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
-    reduce_pass(sm, cs);
+    reduce_pass(sm, cs, M, tile, nc, clus, crank, gpass);
     double pr = 0.0;
     const int cu = sm.cur[oc];
 #pragma unroll
@@ -678,7 +725,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         if (last) grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
         else grad_pass<FAM, KP, false>(sm, M, gtile, t0, t1);
         GTRACE(2);
-        reduce_pass(sm, cs);
+        reduce_pass(sm, cs, M, tile, nc, clus, crank, gpass);
         GTRACE(3);
         const double scale = last ? half : eps;
         const int cu = sm.cur[oc];
@@ -700,12 +747,14 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
             if (last) {
               part += __ldg(M.inv_mass + k) * pown[j] * pown[j];
               part2 += logp_of<FAM, KP>(M, sm, k, oc, q);
-              if (ovalid && writer) {
+              // the proposal plane: rank 0 of a cluster (its ranks sync on the cluster barrier); over
+              // several clusters every CTA stores the same bits and reads back its own stores
+              if (ovalid && (writer || nc > 1)) {
                 const size_t gi = (cu ^ 1) * plane + static_cast<size_t>(k) * nch + ogc;
                 S.pos[gi] = q;
                 S.grad[gi] = g;
-                if (A.mode == kModeProbe && A.traj) A.traj[static_cast<size_t>(ogc) * dim + k] = pown[j];
               }
+              if (ovalid && writer && A.mode == kModeProbe && A.traj) A.traj[static_cast<size_t>(ogc) * dim + k] = pown[j];
             }
           }
         }
@@ -873,21 +922,30 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     cudaError_t e = ensure_kernel_smem(reinterpret_cast<const void*>(glm_kernel<FAM, KP>), sizeof(Smem<KP>), true);
     if (e != cudaSuccess) return e;
   }
-  auto launch = [&](int tile0, int ntiles, int cs) {
+  auto launch = [&](int tile0, int ntiles, int cs, int nc) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * cs);
+    cfg.gridDim = dim3(ntiles * cs * nc);
     cfg.blockDim = dim3(Geom<KP>::THREADS);
     cfg.dynamicSmemBytes = sizeof(Smem<KP>);
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (cs > 1) {
+      at[na].id = cudaLaunchAttributeClusterDimension;
+      at[na].val.clusterDim.x = cs;
+      at[na].val.clusterDim.y = 1;
+      at[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    if (nc > 1) {  // co-residency of every CTA: the second-level reduction waits on the others
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na].val.cooperative = 1;
+      ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = cs > 1 ? 1 : 0;
+    cfg.numAttrs = na;
     ++sampler_launch_count();
-    return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs, tile0);
+    return cudaLaunchKernelEx(&cfg, glm_kernel<FAM, KP>, M, S, A, cs, tile0, nc);
   };
   // Concurrently schedulable clusters of each size (a cluster must fit in one GPC): a 16-CTA cluster
   // only pays while every tile's cluster runs at once, else halve it.
@@ -913,7 +971,32 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
   int cs = glm_cluster_size(M.n, KP, S.nch);
   while (cs > 8 && fits(cs) < tiles) cs /= 2;
   if (const char* e = std::getenv("PCVG_GLM_CS")) cs = std::atoi(e);  // tuning only
+  // several clusters per tile: as many as the device can keep resident at once (the cooperative
+  // launch requires it), for the cluster size that puts the most CTAs on each tile
+  int nc = 1;
+  const int cs_single = cs;
+  const bool scratch = M.glm_part != nullptr && M.glm_cnt != nullptr;
+  for (int c = cs; c >= 8 && cs >= 8; c /= 2) {
+    const int k = std::min(glm_clusters_per_tile(M.n, KP, S.nch, c, scratch), fits(c) / tiles);
+    if (k > 1 && c * k > cs * nc) {
+      cs = c;
+      nc = k;
+    }
+  }
   static const bool verbose = std::getenv("PCVG_VERBOSE") != nullptr;  // tuning only
+  if (nc > 1) {
+    cudaError_t e = cudaMemsetAsync(M.glm_cnt, 0, sizeof(unsigned int) * tiles, st);
+    if (e != cudaSuccess) return e;
+    e = launch(0, tiles, cs, nc);
+    if (verbose)
+      std::fprintf(stderr, "glm_kernel<%d,%d>: %d tiles x %d clusters of %d CTAs: %s\n", FAM, KP, tiles, nc, cs,
+                   cudaGetErrorString(e));
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();  // not co-residentable as one cooperative grid: one cluster per tile
+    --sampler_launch_count();
+    nc = 1;
+    cs = cs_single;
+  }
   if (verbose)
     std::fprintf(stderr, "glm_kernel<%d,%d>: %d tiles, cluster %d (active clusters: 8 -> %d, 16 -> %d)\n", FAM, KP,
                  tiles, cs, fits(8), fits(16));
@@ -928,11 +1011,11 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     const int r = tiles % sms, ntiles_rows = (M.n + Geom<KP>::TM - 1) / Geom<KP>::TM;
     int ct = 1;
     while (ct < 8 && r * ct * 2 <= sms && ntiles_rows >= 4 * ct * 2) ct *= 2;
-    cudaError_t e = launch(0, tiles - r, 1);
+    cudaError_t e = launch(0, tiles - r, 1, 1);
     if (e != cudaSuccess) return e;
-    return launch(tiles - r, r, ct);
+    return launch(tiles - r, r, ct, 1);
   }
-  return launch(0, tiles, cs);
+  return launch(0, tiles, cs, 1);
 }
 
 
@@ -953,6 +1036,27 @@ int glm_cluster_size(int n, int kp, int nch) {
   // and two models' launches run concurrently (cfg4 under ROWS: 7 tiles stays at 8, 0.85M vs 0.61M)
   if (cs == 16 && tiles * 16 > 64) cs = 8;
   return cs;
+}
+
+// Clusters per chain tile for the few-chain launches: when 16-CTA clusters still leave most SMs
+// idle (cfg2 K-fold: two tiles on 32 of 148 SMs; Step 1: one tile), each tile is split over nc
+// clusters whose sums meet in global memory (reduce_clusters), keeping >= 2 row tiles per CTA.
+int glm_clusters_per_tile(int n, int kp, int nch, int cs, bool have_scratch) {
+  static const bool off = std::getenv("PCVG_NO_MULTICLUSTER") != nullptr;  // A/B tests only
+  if (off || !have_scratch || cs < 8) return 1;
+  const int tm = kp <= 8 ? 256 : (kp <= 16 ? 128 : 64);
+  const int tiles = (nch + kC - 1) / kC;
+  const int ntiles = (n + tm - 1) / tm;
+  int nc = std::min(8, device_sm_count() / (tiles * cs));
+  while (nc > 1 && ntiles < 2 * cs * nc) --nc;
+  return std::max(nc, 1);
+}
+
+// Scratch of the multi-cluster launches of a model with nch chains: partial doubles and counters.
+void glm_multicluster_scratch(int kp, int nch, size_t* part_doubles, size_t* counters) {
+  const int tiles = (nch + kC - 1) / kC;
+  *part_doubles = static_cast<size_t>(tiles) * 2 * 8 * (static_cast<size_t>(kp) * kC + kC);
+  *counters = static_cast<size_t>(tiles);
 }
 
 // Padded design width for a model on the tensor-core path, or 0 if it does not qualify

@@ -107,7 +107,11 @@ struct ModelDev {
   // divergent, as with the reference's BrokenFoldModel whose gradient is NaN on one fold
   // (test_engine.cpp:57-90); -1 = none
   int broken_fold;
-  int any_unseen;  // some fold holds out every row of a group (compound predictive needed)
+  int any_unseen;
+  // few-chain GLM launches split over several clusters per chain tile (glm_kernel.cu): cluster
+  // partials [tile][parity][cluster][KP*64 + 64] and per-tile arrival counters (the model's buffers)
+  double* glm_part;
+  unsigned int* glm_cnt;  // some fold holds out every row of a group (compound predictive needed)
 };
 
 constexpr int kMaxBatches = 16;

