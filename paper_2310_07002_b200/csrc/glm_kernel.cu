@@ -20,6 +20,7 @@
 // row tiles and the partial X^T R / residual sums are reduced through distributed shared memory in
 // fixed rank order, so every CTA of the cluster holds bit-identical state; rank 0 writes it back.
 #include <algorithm>
+#include <mutex>
 #include <cooperative_groups.h>
 #include <cuda/atomic>
 #include <cstdio>
@@ -985,9 +986,14 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
   }
   static const bool verbose = std::getenv("PCVG_VERBOSE") != nullptr;  // tuning only
   if (nc > 1) {
+    // Two cooperative grids waiting on their own clusters must not share the device at once (each
+    // could hold SMs the other needs): within the process they run one at a time per device.
+    static std::mutex coop_mu[64];
+    std::lock_guard<std::mutex> guard(coop_mu[current_device() & 63]);
     cudaError_t e = cudaMemsetAsync(M.glm_cnt, 0, sizeof(unsigned int) * tiles, st);
     if (e != cudaSuccess) return e;
     e = launch(0, tiles, cs, nc);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (verbose)
       std::fprintf(stderr, "glm_kernel<%d,%d>: %d tiles x %d clusters of %d CTAs: %s\n", FAM, KP, tiles, nc, cs,
                    cudaGetErrorString(e));

@@ -255,3 +255,26 @@ def test_bench_reference_arm_line():
     assert line["impl"] == "reference" and line["metric"] == "chain-steps/sec" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_benchmark_regroups_sub_blocks_like_presummed_blocks():
+    """Early stop keeps one shuffle sub-block per check interval and regroups the completed ones
+    into `blocks` benchmark blocks (block g = sub-blocks [g c / B, (g + 1) c / B)). The
+    positional host benchmark on c sub-blocks regrouped into B must equal the benchmark on the
+    B presummed blocks bit for bit (same summation order), including uneven groups."""
+    rng = np.random.default_rng(8)
+    nm, nfold, L, stride = 2, 9, 4, 12
+    y = rng.standard_normal((nm, nfold, L, stride))
+    y2 = y ** 2 + rng.uniform(size=y.shape)
+    for sub, B in ((10, 5), (7, 5), (12, 3), (5, 5)):
+        starts = [g * sub // B for g in range(B + 1)]
+        gy = np.zeros((nm, nfold, L, B))
+        gy2 = np.zeros_like(gy)
+        for g in range(B):
+            for d in range(starts[g], starts[g + 1]):
+                gy[..., g] += y[..., d]
+                gy2[..., g] += y2[..., d]
+        a, ah = pcv.benchmark_host(nm, nfold, L, stride, sub, 200, 7, 50, y.ravel(), y2.ravel(), block_groups=B)
+        b, bh = pcv.benchmark_host(nm, nfold, L, B, B, 200, 7, 50, gy.ravel(), gy2.ravel())
+        np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(ah, bh)

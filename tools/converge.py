@@ -27,6 +27,10 @@ def main():
     ap.add_argument("--every", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--device-fit", action="store_true",
+                    help="run the PCV on the kernel and bank of a device Step 1 with the reference defaults "
+                         "(4 chains, 1000 warm-up + 2000 draws; run_pcv_with_fits, engine.cpp:493-503) instead of "
+                         "the fixture's reference-adapted kernel")
     ap.add_argument("--fit", action="store_true",
                     help="also time one full-data fit per model (Step 1, adapt_full_data defaults: "
                          "4 chains, 1000 warm-up + 2000 draws) on the same GPU, for the north star's "
@@ -39,9 +43,15 @@ def main():
     case = Case(fixture)
     cfg = abi.run_config(chains=L, iters=args.iters, warmup=args.warmup, batch_size=args.every, blocks=5,
                          bench_draws=500, seed=1, checkpoint_every=args.every, early_stop=1)
-    inputs = [pcv.ModelInput(m, pcv.FullDataFit(kp, bank), i)
-              for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
     t0 = time.perf_counter()
+    fit_s = 0.0
+    if args.device_fit:
+        fits = [pcv.adapt_full_data(m, pcv.AdaptConfig(), seed=1, model_id=i) for i, m in enumerate(case.models)]
+        inputs = [pcv.ModelInput(m, f, i) for i, (m, f) in enumerate(zip(case.models, fits))]
+        fit_s = time.perf_counter() - t0
+    else:
+        inputs = [pcv.ModelInput(m, pcv.FullDataFit(kp, bank), i)
+                  for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
     rep = pcv.run_pcv(inputs, cfg)
     wall = time.perf_counter() - t0
     chains = case.K * L * len(case.models)
@@ -49,6 +59,8 @@ def main():
     line = {"config": args.config, "workload": desc, "chains": chains, "iters_run": int(rep["iters_run"]),
             "warmup": args.warmup, "check_every": args.every, "max_iters": args.iters,
             "stopped_early": bool(rep["iters_run"] < args.iters), "wall_s": wall,
+            "kernel": "device Step 1 (1000 + 2000, wall %.1f s incl. in wall_s)" % fit_s if args.device_fit
+            else "fixture (reference adapt_full_data)",
             "device_s": (rep["warmup_ms"] + rep["sampling_ms"]) / 1e3,
             "delta_hat": rep["delta_hat"], "mcse": rep["mcse"], "epistemic_se": rep["epistemic_se"],
             "rhat_max": rep["rhat_max"], "verdict_quantile_value": rep["verdict_quantile_value"],
