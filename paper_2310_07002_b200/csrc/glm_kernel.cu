@@ -993,11 +993,10 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     cudaError_t e = cudaMemsetAsync(M.glm_cnt, 0, sizeof(unsigned int) * tiles, st);
     if (e != cudaSuccess) return e;
     e = launch(0, tiles, cs, nc);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (verbose)
       std::fprintf(stderr, "glm_kernel<%d,%d>: %d tiles x %d clusters of %d CTAs: %s\n", FAM, KP, tiles, nc, cs,
                    cudaGetErrorString(e));
-    if (e == cudaSuccess) return e;
+    if (e == cudaSuccess) return cudaStreamSynchronize(st);  // a kernel fault is returned, not retried
     cudaGetLastError();  // not co-residentable as one cooperative grid: one cluster per tile
     --sampler_launch_count();
     nc = 1;
