@@ -8,7 +8,8 @@ chain + its log_pred + the online accumulator update (engine.cpp:360-373). Kerne
 the warm-start draw bank are the reference's own adapt_full_data output on this dataset
 (tests/golden/cfg2_logistic_bench.npz). Multi-GPU: folds are sharded across ranks (strong
 scaling, total work fixed); no collective on the data path, the per-fold statistics are gathered
-once after the timed region.
+once after the timed region. The line also carries `time_to_converged`: the wall-clock of one
+run_pcv call with the early-stop rule on cfg4 (BASELINE configs[3], the early-stopping config).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -144,6 +145,45 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+CONVERGE_WORKLOAD = ("cfg4: seasonal AR(2)+11 dummies T=5000, hv-block K=100 h=12 (BASELINE configs[3], the "
+                     "early-stopping configuration), M_A + M_B x 4 chains, check every 50 iterations, at most 2000")
+
+
+def time_to_converged(world, local, dist):
+    """Wall-clock to R-hat-converged elpd (the second half of BASELINE.json's metric) through the
+    public API with host inputs: run_pcv with the early-stop rule on cfg4, one call
+    (one GPU) or the fold-sharded driver (N ranks), max over ranks."""
+    from make_golden import load
+    from paper_2310_07002_b200 import pcv
+    d, f, models, _ = load("cfg4_seasonal_bench")
+    inputs = [pcv.ModelInput(pcv.SeasonalARModel(f"M{i}", d, f, kw["ar_order"], kw["dummies"], kw["rho_transform"]),
+                             pcv.FullDataFit(kp, bank), i) for i, (kw, kp, bank) in enumerate(models)]
+    cfg = pcv.RunConfig(chains=4, iters=2000, warmup=100, batch_size=50, blocks=5, bench_draws=500, seed=1,
+                        checkpoint_every=50, early_stop=1)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    if dist:
+        from paper_2310_07002_b200 import dist as pdist
+        rep = pdist.run_pcv_sharded(inputs, cfg, device=local)
+    else:
+        rep = pcv.run_pcv(inputs, cfg, device=local)
+    wall = time.perf_counter() - t0
+    if dist:
+        import torch
+        t = torch.tensor([wall], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    return {"workload": CONVERGE_WORKLOAD, "iters_run": int(rep["iters_run"]),
+            "stopped_early": bool(rep["iters_run"] < cfg.iters), "wall_s": wall,
+            "device_s": (rep["warmup_ms"] + rep["sampling_ms"]) / 1e3 if not dist else None,
+            "rhat_max": rep["rhat_max"], "verdict_quantile_value": rep["verdict_quantile_value"],
+            "delta_hat": rep["delta_hat"], "mcse": rep["mcse"], "epistemic_se": rep["epistemic_se"],
+            "chain_steps": 800 * (int(rep["iters_run"]) + cfg.warmup),
+            "note": "one pcv.run_pcv call with host inputs (upload, warm start, warm-up, sampling with the rule "
+                    "at every check interval, report); the wall-clock includes the context's creation"}
+
+
 def relaunch_ranks(n):
     """`bench.py --gpus N` outside torchrun: start the N ranks (one per GPU) ourselves."""
     import socket
@@ -168,6 +208,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-converge", action="store_true", help="skip the time-to-R-hat-converged leg (cfg4)")
     ap.add_argument("--folds", type=int, default=0, help="debug: limit the fold count")
     ap.add_argument("--fp32", action="store_true",
                     help="the separately reported FP32 variant (glm32_kernel: tcgen05 kind::tf32, "
@@ -209,7 +250,7 @@ def main():
     ctx = pcv.Context(local)
     if args.fp32:
         ctx.set_kernel_policy(ctx.KERNEL_TF32)
-        args.no_e2e = args.no_cpu = True
+        args.no_e2e = args.no_cpu = args.no_converge = True
     ctx.add_model(model, kp, bank, model_id=0)
     ctx.begin(cfg)  # Step 2: warm start + args.warmup untimed warm-up transitions
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -315,6 +356,10 @@ def main():
                                    "with host inputs: upload, warm start, warm-up + sampling, per-fold stats, "
                                    "shuffle benchmark (R=100, on device), report download and context "
                                    "teardown"}
+    if not args.no_converge:
+        conv = time_to_converged(world, local, dist)
+        if line is not None:
+            line["time_to_converged"] = conv
     if line is not None and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         cv, kind, sample = cpu_sample(K, 12, 1, threads)
