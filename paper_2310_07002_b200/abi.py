@@ -219,4 +219,4 @@ def run_config(chains=4, iters=1000, warmup=100, batch_size=50, blocks=5, bench_
 
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libpcvg.so")
+LIB_PATH = os.environ.get("PCVG_LIB_PATH") or os.path.join(PKG_DIR, "lib", "libpcvg.so")  # override: tooling builds

@@ -69,6 +69,19 @@ struct Geom {
   static constexpr int DIMP = KP + 4;                     // max parameters (incl. specials)
   static constexpr int OWN = (DIMP + OWNERS - 1) / OWNERS;
   static constexpr int TILE_BYTES = TM * KP * 8 + TM * 8 + TM * 4;
+  // reduced rows: G [col][chain] rows 0..KP-1 and the residual statistic as row KP, in sm.rs
+  static constexpr int RROWS = KP + 1;
+  // receive scratch rows of a cluster reduction: (cs - 1) partials of ceil(RROWS / cs) rows, any cs <= 16
+  static constexpr int scr_rows() {
+    int m = 0;
+    for (int c = 2; c <= 16; ++c) {
+      const int v = (c - 1) * ((RROWS + c - 1) / c);
+      m = v > m ? v : m;
+    }
+    return m;
+  }
+  static constexpr int SCR = scr_rows();
+  static_assert(RROWS <= 64, "the reduced rows live in sm.rs (64 rows)");
 };
 
 // Residual statistic of chain c summed over the row groups in a fixed tree order.
@@ -89,8 +102,7 @@ struct Smem {
   double qs[G::DIMP * kLdS];              // parameters, [k][chain]
   double ws[KP * kLdS];                   // GEMM weights, [col][chain]
   double llp[4][kC];                      // per row group: log-lik (logistic) / sum r^2 (gaussian)
-  double gt[KP * kLdS];                   // cluster-reduced G, [col][chain]
-  double lt[kC];                          // cluster-reduced residual statistic
+  double gt[G::SCR * kLdS];               // cluster reduction: partial rows received from the other ranks
   double red[kMaxOwners][kC];             // owner partial sums (kinetic)
   double pri[kMaxOwners][kC];             // owner partial sums (log joint)
   double exp_tab[16];                     // 2^(-j/16)
@@ -100,8 +112,10 @@ struct Smem {
   int cur[kC];
   int fold[kC];                           // the chain's fold (K for padding chains)
   unsigned long long full[kStages];
+  unsigned long long rbar[2];  // cluster reduction: partials received (0), reduced rows gathered (1)
   unsigned int rel[kStages];  // warps done with each ring slot (monotonic; last arrival refills)
 };
+static_assert(sizeof(Smem<52>) <= 227 * 1024, "one CTA per SM: at most 227 KB of shared memory");
 
 // ------------------------------------------------------------------ family hooks
 __device__ __forceinline__ double logistic_fn(double u) { return 1.0 / (1.0 + exp(-u)); }
@@ -129,7 +143,7 @@ __device__ __forceinline__ double w_of(const ModelDev& M, int k, double qk) {
 
 template <int KP>
 __device__ __forceinline__ double quarter_sum(const Smem<KP>& sm, int c) {
-  return sm.lt[c];  // reduced over row quarters and cluster ranks (reduce_pass)
+  return sm.rs[KP * kLdS + c];  // reduced over row quarters and cluster ranks (reduce_pass)
 }
 
 // d log p / d q_k from the reduced G column, the parameters and the residual sum of squares.
@@ -222,11 +236,20 @@ __device__ __forceinline__ void issue_tile(Smem<KP>& sm, const ModelDev& M, int 
 #ifdef PCVG_GLM_TRACE
 // Timeline probe (tools only): clock64 stamps of CTA 0, thread 0 for the passes of its first
 // transition, printed at the end of the launch.
-__device__ long long g_gtrace[64][5];
+__device__ long long g_gtrace[64][12];
 __device__ int g_gpass;
+__device__ unsigned long long g_rtrace[16][8][12];  // CTAs 0..15, passes 32..39, globaltimer ns
+__device__ int g_bpass[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define GTRACE(i)                                                                          \
   do {                                                                                     \
     if (blockIdx.x == 0 && threadIdx.x == 0 && g_gpass < 64) g_gtrace[g_gpass][(i)] = clock64(); \
+    if (blockIdx.x < 16 && threadIdx.x == 0 && g_bpass[blockIdx.x] >= 8 && g_bpass[blockIdx.x] < 16) \
+      g_rtrace[blockIdx.x][g_bpass[blockIdx.x] - 8][(i)] = gtimer();                      \
   } while (0)
 #else
 #define GTRACE(i) \
@@ -398,127 +421,133 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
   }
 }
 
-// Sums the staged partials (G in sm.rs, residual statistic in sm.llp) over the CS CTAs of the
-// cluster into sm.gt / sm.lt. CS = 1: a local copy (same bits). CS > 1: rank o reduces the o-th
-// slice of the KP x 64 + 64 elements - cs lanes load one element from the cs ranks at once and
-// xor-butterfly it (a fixed order) - then every rank copies the other slices from their owners, so
-// all ranks hold identical bits. Every remote load of a step is independent (a rank-ordered
-// dependent chain cost ~cs DSMEM latencies per element: ~40% of a pass at cs = 16, cfg2 K-fold).
-// Second level for a tile split over nc clusters (few chains on many SMs): each cluster's rank 0
-// publishes its cluster sum to global memory (double-buffered by pass parity), arrives on the
-// tile's counter, and every CTA of the tile waits for all nc arrivals and sums the nc partials in
-// cluster order, so all CTAs again hold identical bits. The launch is cooperative: all CTAs of the
-// grid are co-resident, so the wait cannot deadlock.
+// Sums the staged partials (G in sm.rs rows 0..KP-1, residual statistic in sm.llp) over the CS CTAs
+// of the cluster and the NC clusters of the chain tile, in place: afterwards sm.rs rows 0..KP hold
+// the reduced G and (row KP) the residual statistic, identical bits in every CTA of the tile.
+//  * CS = 1: the staged rows already are the sums (row KP = the row-group sum).
+//  * CS > 1, push-based over DSMEM: rank o owns rows [o*per, (o+1)*per). Every rank bulk-copies
+//    (cp.async.bulk shared::cta -> shared::cluster, SASS UBLKCP) each owner's rows of its partial
+//    into the owner's receive slot (sm.gt) completing on the owner's mbarrier; the owner adds the
+//    CS partials in rank order, then bulk-copies its reduced rows into every other rank's sm.rs.
+//    Two mbarrier waits per pass and no cluster barrier (round 1 pulled the partials with DSMEM
+//    loads between three cluster.sync: ~6 us of a ~31 us cfg2 K-fold pass, ~2 us now).
+//  * NC > 1 (reduce_clusters): between the two steps, each owner's rows meet the same rows of the
+//    other clusters in global memory (published by pass parity, one arrival counter per tile and
+//    rank) and are added in cluster order.
+// Hazards are ordered by the data flow: a rank's partial rows are overwritten (gather) only after
+// their owner received them; an owner's receive slot is rewritten (next pass) only after its
+// gather reached the sender; the mbarriers are armed (expect_tx) once per pass by thread 0 and
+// may see bytes before they are armed (the transaction count goes negative, the phase waits for
+// the local arrival). The launch syncs the cluster once after the barriers are initialised.
 template <int KP>
-__device__ void reduce_clusters(Smem<KP>& sm, const ModelDev& M, int tile, int nc, int clus, int crank,
-                                uint32_t& gpass) {
+__device__ void reduce_clusters(Smem<KP>& sm, const ModelDev& M, int tile, int nc, int clus, int crank, int r0,
+                                int r1, uint32_t& gpass) {
   using G = Geom<KP>;
   constexpr int kThreads = G::THREADS;
-  constexpr int kE = KP * kC + kC;
+  constexpr int kE = G::RROWS * kC;
   const int tid = threadIdx.x;
-  double* base = M.glm_part + (static_cast<size_t>(tile) * 2 + (gpass & 1u)) * nc * kE;
-  if (crank == 0) {
-    for (int e = tid; e < kE; e += kThreads)
-      __stcg(base + static_cast<size_t>(clus) * kE + e, e < KP * kC ? sm.gt[(e / kC) * kLdS + e % kC] : sm.lt[e - KP * kC]);
-    __threadfence();
+  const uint32_t par = gpass & 1u;
+  ++gpass;
+  if (r1 <= r0) return;  // no rows: neither does this rank in any other cluster
+  double* base = M.glm_part + (static_cast<size_t>(tile) * 2 + par) * nc * kE;
+  const int n = (r1 - r0) * kC;
+  GTRACE(5);
+  for (int i = tid; i < n; i += kThreads) {
+    const int row = r0 + i / kC, c = i % kC;
+    __stcg(base + static_cast<size_t>(clus) * kE + row * kC + c, sm.rs[row * kLdS + c]);
   }
+  __threadfence();
   __syncthreads();
   if (tid == 0) {
-    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> cnt(M.glm_cnt[tile]);
-    if (crank == 0) cnt.fetch_add(1u, cuda::memory_order_release);
-    const unsigned int target = (gpass + 1u) * static_cast<unsigned int>(nc);
-    while (cnt.load(cuda::memory_order_acquire) < target) __nanosleep(40);
+    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> cnt(M.glm_cnt[tile * 16 + crank]);
+    cnt.fetch_add(1u, cuda::memory_order_release);
+    const unsigned int target = (gpass) * static_cast<unsigned int>(nc);
+    while (cnt.load(cuda::memory_order_acquire) < target) __nanosleep(32);
   }
   __syncthreads();
-  for (int e = tid; e < kE; e += kThreads) {
-    double x = __ldcg(base + e);
-    for (int c = 1; c < nc; ++c) x += __ldcg(base + static_cast<size_t>(c) * kE + e);
-    if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = x;
-    else sm.lt[e - KP * kC] = x;
+  GTRACE(6);
+  // every partial of an element loaded before any is added, then summed in cluster order
+  constexpr int kMaxNc = 8;
+  for (int i = tid; i < n; i += kThreads) {
+    const int row = r0 + i / kC, c = i % kC;
+    double v[kMaxNc];
+#pragma unroll
+    for (int q = 0; q < kMaxNc; ++q)
+      v[q] = q < nc ? __ldcg(base + static_cast<size_t>(q) * kE + row * kC + c) : 0.0;
+    double x = v[0];
+#pragma unroll
+    for (int q = 1; q < kMaxNc; ++q)
+      if (q < nc) x += v[q];
+    sm.rs[row * kLdS + c] = x;
   }
-  __syncthreads();
-  ++gpass;
 }
 
 template <int KP>
 __device__ void reduce_pass(Smem<KP>& sm, int cs, const ModelDev& M, int tile, int nc, int clus, int crank,
-                            uint32_t& gpass) {
-  namespace cgr = cooperative_groups;
+                            uint32_t& gpass, uint32_t& cpass) {
   using G = Geom<KP>;
   constexpr int kThreads = G::THREADS;
+  constexpr int R = G::RROWS;
+  constexpr uint32_t kRowBytes = kLdS * sizeof(double);
   const int tid = threadIdx.x;
-  constexpr int kE = KP * kC + kC;  // G elements, then the residual statistic per chain
+  if (tid < kC) sm.rs[KP * kLdS + tid] = rq_sum<G::RQ>(sm.llp, tid);
   if (cs == 1) {
-    for (int i = tid; i < KP * kC; i += kThreads) {
-      const int k = i / kC, c = i % kC;
-      sm.gt[k * kLdS + c] = sm.rs[k * kLdS + c];
-    }
-    if (tid < kC) sm.lt[tid] = rq_sum<G::RQ>(sm.llp, tid);
     __syncthreads();
-    if (nc > 1) reduce_clusters(sm, M, tile, nc, clus, crank, gpass);
+    if (nc > 1) {
+      reduce_clusters(sm, M, tile, nc, clus, 0, 0, R, gpass);
+      __syncthreads();
+    }
     return;
   }
-  cgr::cluster_group cl = cgr::this_cluster();
-  const int me = static_cast<int>(cl.block_rank());
-  const int slice = (kE + cs - 1) / cs;
-  cl.sync();  // every rank's partials staged
-  {
-    const int q = tid % cs;  // the rank this lane loads from
-    const Smem<KP>* rq = cl.map_shared_rank(&sm, q);
-    const int per = kThreads / cs;  // elements per sweep
-    constexpr int kSw = 4;           // sweeps whose remote loads are in flight together
-    for (int e00 = 0; e00 < slice; e00 += kSw * per) {
-      double v[kSw];
-#pragma unroll
-      for (int w = 0; w < kSw; ++w) {
-        const int el = e00 + w * per + tid / cs, e = me * slice + el;
-        v[w] = 0.0;
-        if (el < slice && e < kE) {
-          if (e < KP * kC) {
-            v[w] = rq->rs[(e / kC) * kLdS + e % kC];
-          } else {
-            const int c = e - KP * kC;
-            v[w] = rq_sum<G::RQ>(rq->llp, c);
-          }
-        }
+  const int me = crank;
+  const int per = (R + cs - 1) / cs;
+  const int r0 = min(R, me * per), r1 = min(R, r0 + per);
+  const uint32_t ph = cpass & 1u;
+  ++cpass;
+  tc::fence_proxy_async();  // the staged rows are read by the bulk copies
+  __syncthreads();
+  GTRACE(7);
+  if (tid == 0) {
+    tc::mbar_expect_tx(&sm.rbar[0], static_cast<uint32_t>(cs - 1) * (r1 - r0) * kRowBytes);
+    tc::mbar_expect_tx(&sm.rbar[1], static_cast<uint32_t>(R - (r1 - r0)) * kRowBytes);
+    for (int j = 1; j < cs; ++j) {
+      const int o = (me + j) % cs;  // owners in a rotated order: not every rank hits rank 0 first
+      const int a = min(R, o * per), b = min(R, a + per);
+      if (b <= a) continue;
+      const int slot = me < o ? me : me - 1;
+      tc::bulk_s2c(tc::cluster_addr(&sm.gt[slot * per * kLdS], o), &sm.rs[a * kLdS],
+                   static_cast<uint32_t>(b - a) * kRowBytes, tc::cluster_addr(&sm.rbar[0], o));
+    }
+  }
+  if (r1 > r0) {
+    tc::mbar_wait(&sm.rbar[0], ph);
+    for (int i = tid; i < (r1 - r0) * kC; i += kThreads) {
+      const int rr = i / kC, c = i % kC, row = r0 + rr;
+      double x = 0.0;
+      for (int q = 0; q < cs; ++q) {
+        const double v = q == me ? sm.rs[row * kLdS + c] : sm.gt[((q < me ? q : q - 1) * per + rr) * kLdS + c];
+        x = q == 0 ? v : x + v;
       }
-#pragma unroll
-      for (int w = 0; w < kSw; ++w) {
-        const int el = e00 + w * per + tid / cs, e = me * slice + el;
-        double x = v[w];
-        for (int off = cs / 2; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-        if (el < slice && e < kE && q == 0) {
-          if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = x;
-          else sm.lt[e - KP * kC] = x;
-        }
-      }
+      sm.rs[row * kLdS + c] = x;
     }
   }
-  cl.sync();  // every slice reduced (and every partial read: rs / llp may be reused)
-  constexpr int kPer = (kE + kThreads - 1) / kThreads;  // elements per thread, loads batched
-  double v[kPer];
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = tid + j * kThreads;
-    v[j] = 0.0;
-    if (e < kE && e / slice != me) {
-      const Smem<KP>* ro = cl.map_shared_rank(&sm, e / slice);
-      v[j] = e < KP * kC ? ro->gt[(e / kC) * kLdS + e % kC] : ro->lt[e - KP * kC];
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = tid + j * kThreads;
-    if (e < kE && e / slice != me) {
-      if (e < KP * kC) sm.gt[(e / kC) * kLdS + e % kC] = v[j];
-      else sm.lt[e - KP * kC] = v[j];
-    }
-  }
-  __syncthreads();  // the copied slices are read by the owner threads next
+  GTRACE(8);
   if (nc > 1) {
-    cl.sync();  // every rank done copying the others' slices before gt is overwritten
-    reduce_clusters(sm, M, tile, nc, clus, crank, gpass);
+    __syncthreads();
+    reduce_clusters(sm, M, tile, nc, clus, crank, r0, r1, gpass);
   }
+  tc::fence_proxy_async();  // the reduced rows are read by the bulk copies
+  __syncthreads();
+  GTRACE(9);
+  if (tid == 0 && r1 > r0) {
+    for (int j = 1; j < cs; ++j) {
+      const int o = (me + j) % cs;
+      tc::bulk_s2c(tc::cluster_addr(&sm.rs[r0 * kLdS], o), &sm.rs[r0 * kLdS],
+                   static_cast<uint32_t>(r1 - r0) * kRowBytes, tc::cluster_addr(&sm.rbar[1], o));
+    }
+  }
+  tc::mbar_wait(&sm.rbar[1], ph);
+  GTRACE(10);
 }
 
 __device__ __forceinline__ double bernoulli_logit(double y, double x) {
@@ -581,6 +610,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
   const int ntiles_all = (M.n + G::TM - 1) / G::TM;
   const int t0 = gr * ntiles_all / span, t1 = (gr + 1) * ntiles_all / span;
   uint32_t gpass = 0;                                          // second-level reductions done
+  uint32_t cpass = 0;                                          // cluster reductions done
   const int oc = tid & (kC - 1), ok = tid / kC;  // owner: chain oc, params ok + 8j
   const int ogc = tile * kC + oc;
   const bool ovalid = ogc < nch;
@@ -592,6 +622,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
     mbar_init(&sm.full[tid], 1);
     sm.rel[tid] = 0u;
   }
+  if (tid < 2) mbar_init(&sm.rbar[tid], 1);
   if (tid < 16) sm.exp_tab[tid] = exp2(-tid / 16.0);
   if (tid < 32) {
     const double v = exp2(-tid / 32.0);
@@ -625,6 +656,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
     }
   }
   __syncthreads();
+  if (cs > 1) cooperative_groups::this_cluster().sync();  // reduction barriers initialised cluster-wide
 
   // owners: publish parameters + GEMM weights of their slots
   auto put_q = [&](int k, double q) {
@@ -651,7 +683,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
     }
     __syncthreads();
     grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
-    reduce_pass(sm, cs, M, tile, nc, clus, crank, gpass);
+    reduce_pass(sm, cs, M, tile, nc, clus, crank, gpass, cpass);
     double pr = 0.0;
     const int cu = sm.cur[oc];
 #pragma unroll
@@ -660,7 +692,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
       if (k < dim) {
         const double q = sm.qs[k * kLdS + oc];
         const int col = col_of<FAM>(M, k);
-        const double gk = col >= 0 ? sm.gt[col * kLdS + oc] : 0.0;
+        const double gk = col >= 0 ? sm.rs[col * kLdS + oc] : 0.0;
         if (ovalid && writer) S.grad[cu * plane + static_cast<size_t>(k) * nch + ogc] = grad_of<FAM, KP>(M, sm, k, oc, gk, q);
         pr += logp_of<FAM, KP>(M, sm, k, oc, q);
       }
@@ -726,7 +758,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         if (last) grad_pass<FAM, KP, true>(sm, M, gtile, t0, t1);
         else grad_pass<FAM, KP, false>(sm, M, gtile, t0, t1);
         GTRACE(2);
-        reduce_pass(sm, cs, M, tile, nc, clus, crank, gpass);
+        reduce_pass(sm, cs, M, tile, nc, clus, crank, gpass, cpass);
         GTRACE(3);
         const double scale = last ? half : eps;
         const int cu = sm.cur[oc];
@@ -740,7 +772,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
           if (k < dim) {
             const double q = sm.qs[k * kLdS + oc];
             const int col = col_of<FAM>(M, k);
-            const double g = grad_of<FAM, KP>(M, sm, k, oc, col >= 0 ? sm.gt[col * kLdS + oc] : 0.0, q);
+            const double g = grad_of<FAM, KP>(M, sm, k, oc, col >= 0 ? sm.rs[col * kLdS + oc] : 0.0, q);
             gk_new[j] = g;
             bad |= !isfinite(g);
             pown[j] += scale * g;
@@ -780,6 +812,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         GTRACE(4);
 #ifdef PCVG_GLM_TRACE
         if (blockIdx.x == 0 && threadIdx.x == 0) ++g_gpass;
+        if (blockIdx.x < 16 && threadIdx.x == 0) ++g_bpass[blockIdx.x];
 #endif
       }
       // -- energies, Metropolis (chain thread)
@@ -895,12 +928,23 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
   }
 #ifdef PCVG_GLM_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0 && g_gpass >= 32 && g_gpass < 96) {
-    printf("pass: start tiles_done staged reduced owners_done (cycles from pass start), cs=%d\n", cs);
+    printf("pass: start tiles_done staged reduced owners_done | cluster-level-done arrived (cycles), cs=%d nc=%d\n",
+           cs, nc);
     for (int p = 0; p < 32 && p < 64; ++p)
-      printf("%2d: %lld %lld %lld %lld | next start +%lld\n", p, g_gtrace[p][1] - g_gtrace[p][0],
+      printf("%2d: %lld %lld %lld %lld | %lld %lld | next start +%lld\n", p, g_gtrace[p][1] - g_gtrace[p][0],
              g_gtrace[p][2] - g_gtrace[p][0], g_gtrace[p][3] - g_gtrace[p][0], g_gtrace[p][4] - g_gtrace[p][0],
+             g_gtrace[p][5] - g_gtrace[p][0], g_gtrace[p][6] - g_gtrace[p][0],
              p + 1 < 32 ? g_gtrace[p + 1][0] - g_gtrace[p][0] : 0LL);
     g_gpass = 1000;
+    printf("per-CTA (ns from CTA0 pass start): cta pass | tiles staged red-start rows-reduced pre-gather gathered glob-publish glob-arrived reduced owners\n");
+    for (int p = 0; p < 3; ++p) {
+      const unsigned long long z = g_rtrace[0][p][0];
+      for (int b = 0; b < 16; ++b)
+        printf("%2d %d | %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld (start %lld)\n", b, p, (long long)(g_rtrace[b][p][1] - z),
+               (long long)(g_rtrace[b][p][2] - z), (long long)(g_rtrace[b][p][7] - z), (long long)(g_rtrace[b][p][8] - z),
+               (long long)(g_rtrace[b][p][9] - z), (long long)(g_rtrace[b][p][10] - z), (long long)(g_rtrace[b][p][5] - z), (long long)(g_rtrace[b][p][6] - z),
+               (long long)(g_rtrace[b][p][3] - z), (long long)(g_rtrace[b][p][4] - z), (long long)(g_rtrace[b][p][0] - z));
+    }
   }
 #endif
   if (cvalid && writer && A.mode != kModePred) {
@@ -990,7 +1034,7 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     // could hold SMs the other needs): within the process they run one at a time per device.
     static std::mutex coop_mu[64];
     std::lock_guard<std::mutex> guard(coop_mu[current_device() & 63]);
-    cudaError_t e = cudaMemsetAsync(M.glm_cnt, 0, sizeof(unsigned int) * tiles, st);
+    cudaError_t e = cudaMemsetAsync(M.glm_cnt, 0, sizeof(unsigned int) * tiles * 16, st);
     if (e != cudaSuccess) return e;
     e = launch(0, tiles, cs, nc);
     if (verbose)
@@ -1061,7 +1105,7 @@ int glm_clusters_per_tile(int n, int kp, int nch, int cs, bool have_scratch) {
 void glm_multicluster_scratch(int kp, int nch, size_t* part_doubles, size_t* counters) {
   const int tiles = (nch + kC - 1) / kC;
   *part_doubles = static_cast<size_t>(tiles) * 2 * 8 * (static_cast<size_t>(kp) * kC + kC);
-  *counters = static_cast<size_t>(tiles);
+  *counters = static_cast<size_t>(tiles) * 16;  // one per (tile, cluster rank)
 }
 
 // Padded design width for a model on the tensor-core path, or 0 if it does not qualify
