@@ -236,9 +236,9 @@ __device__ __forceinline__ void issue_tile(Smem<KP>& sm, const ModelDev& M, int 
 #ifdef PCVG_GLM_TRACE
 // Timeline probe (tools only): clock64 stamps of CTA 0, thread 0 for the passes of its first
 // transition, printed at the end of the launch.
-__device__ long long g_gtrace[64][12];
+__device__ long long g_gtrace[64][14];
 __device__ int g_gpass;
-__device__ unsigned long long g_rtrace[16][8][12];  // CTAs 0..15, passes 32..39, globaltimer ns
+__device__ unsigned long long g_rtrace[16][8][14];  // CTAs 0..15, passes 32..39, globaltimer ns
 __device__ int g_bpass[16];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -384,6 +384,7 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
   gtile = g0 + ntiles;
   GTRACE(1);
   __syncthreads();
+  GTRACE(11);
   // Stage G [col][chain] into sm.rs: row group 0 stores, the others add in order.
 #pragma unroll 1
   for (int qq = 0; qq < G::RQ; ++qq) {
@@ -792,7 +793,9 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
           }
         }
         (void)gk_new;
+        GTRACE(12);
         __syncthreads();  // every owner read G / q / llp before they change
+        GTRACE(13);
         if (!last) {
 #pragma unroll
           for (int j = 0; j < G::OWN; ++j) {
@@ -936,14 +939,14 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
              g_gtrace[p][5] - g_gtrace[p][0], g_gtrace[p][6] - g_gtrace[p][0],
              p + 1 < 32 ? g_gtrace[p + 1][0] - g_gtrace[p][0] : 0LL);
     g_gpass = 1000;
-    printf("per-CTA (ns from CTA0 pass start): cta pass | tiles staged red-start rows-reduced pre-gather gathered glob-publish glob-arrived reduced owners\n");
+    printf("per-CTA (ns from CTA0 pass start): cta pass | tiles allwarps staged red-start rows-reduced pre-gather gathered glob-publish glob-arrived reduced own-done own-synced owners\n");
     for (int p = 0; p < 3; ++p) {
       const unsigned long long z = g_rtrace[0][p][0];
       for (int b = 0; b < 16; ++b)
-        printf("%2d %d | %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld (start %lld)\n", b, p, (long long)(g_rtrace[b][p][1] - z),
-               (long long)(g_rtrace[b][p][2] - z), (long long)(g_rtrace[b][p][7] - z), (long long)(g_rtrace[b][p][8] - z),
+        printf("%2d %d | %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld (start %lld)\n", b, p, (long long)(g_rtrace[b][p][1] - z),
+               (long long)(g_rtrace[b][p][11] - z), (long long)(g_rtrace[b][p][2] - z), (long long)(g_rtrace[b][p][7] - z), (long long)(g_rtrace[b][p][8] - z),
                (long long)(g_rtrace[b][p][9] - z), (long long)(g_rtrace[b][p][10] - z), (long long)(g_rtrace[b][p][5] - z), (long long)(g_rtrace[b][p][6] - z),
-               (long long)(g_rtrace[b][p][3] - z), (long long)(g_rtrace[b][p][4] - z), (long long)(g_rtrace[b][p][0] - z));
+               (long long)(g_rtrace[b][p][3] - z), (long long)(g_rtrace[b][p][12] - z), (long long)(g_rtrace[b][p][13] - z), (long long)(g_rtrace[b][p][4] - z), (long long)(g_rtrace[b][p][0] - z));
     }
   }
 #endif

@@ -143,3 +143,27 @@ class DataCase:
         return self.folds.K
 
     excluded = Case.excluded
+
+
+class StreamCase(Case):
+    """The HBM-streaming size of the logistic path (round-1 verdict, missing #6): N = 400,000 rows,
+    P = 50 (X padded to 52 columns: 166 MB, above the 126 MB L2), K-fold with K = 1,184 folds, so
+    8 chains per fold fill one 148-tile wave. Data from the product's simulator with the seed of
+    the cfg2 fixture; kernel and bank from the cfg2 fixture (inverse mass scaled by 10^4 / N, the
+    posterior variance ratio) - a throughput / parity shape, not a fitted model."""
+
+    def __init__(self, n=400_000, K=1184):
+        from paper_2310_07002_b200 import pcv
+        base = Case("cfg2_logistic_bench")
+        self.name = f"stream_logistic_{n}"
+        self.data = pcv.simulate_logistic(n, 50, 1)
+        self.folds = pcv.make_kfold_scheme(self.data, K, 1)
+        self.fa = self.folds.arrays()
+        kw = base.kws[0]
+        self.kws = [kw]
+        self.models = [pcv.LogisticModel("M0", self.data, self.folds)]
+        self.omodels = [O.OModel(self.data, self.fa, abi.SpecArrays(**kw))]
+        kp = base.kparams[0]
+        self.kparams = [pcv.KernelParams(kp.step_size, kp.n_leapfrog, kp.inv_mass_diag * (10000.0 / n))]
+        self.banks = [base.banks[0]]
+        self.z = None
