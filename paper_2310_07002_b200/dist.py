@@ -2,7 +2,8 @@
 
 SURVEY.md 8(e): each rank owns a contiguous fold range with all L chains of a fold, so per-fold
 R-hat/ESS/LogS need no communication. The only exchange is at check intervals: the per-fold
-tables (a few doubles per fold) are all-gathered in rank order = reference fold order, and every
+tables (a few doubles per fold) are all-gathered in rank order = reference fold order (tensor
+all-gathers: device buffers over NCCL, host buffers over gloo), and every
 rank merges them with pcvg_merge (engine.cpp:117-253) in fold order, so the merge itself is
 independent of the GPU count (the reference's thread-count invariance, test_engine.cpp:135-147).
 The per-fold inputs are bit-identical for any GPU count wherever a chain's arithmetic does not
@@ -26,56 +27,83 @@ def shard_range(K: int, rank: int, world: int) -> tuple[int, int]:
     return rank * K // world, (rank + 1) * K // world
 
 
-def gather_fold_tables(cols: dict, n_models: int, group=None) -> dict:
-    """All-gathers per-shard fold tables (model-major rows within each shard) into full tables in
-    model-major, fold order. Uses all_gather_object so it runs on NCCL and gloo alike."""
+def _coll_device(group=None):
+    """Device of the collective buffers: the rank's current CUDA device under NCCL, else the CPU
+    (gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _all_gather_rows(arr: np.ndarray, group=None) -> list:
+    """All-gathers a float64 array of n_rank rows (n_rank may differ by rank) with tensor
+    collectives: the row counts first, then the rows padded to the largest count. Returns the
+    per-rank arrays in rank order (NCCL moves device buffers over NVLink; gloo host buffers)."""
+    import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    parts = [None] * world
-    dist.all_gather_object(parts, {k: np.asarray(v) for k, v in cols.items()}, group=group)
+    dev = _coll_device(group)
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    tail = a.shape[1:]
+    n = torch.tensor([a.shape[0]], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n, group=group)
+    counts = [int(c.item()) for c in counts]
+    rows = max(counts)
+    buf = torch.zeros((rows,) + tail, dtype=torch.float64, device=dev)
+    if a.shape[0]:
+        buf[:a.shape[0]] = torch.from_numpy(a).to(dev)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return [p[:c].cpu().numpy() for p, c in zip(parts, counts)]
+
+
+def gather_fold_tables(cols: dict, n_models: int, group=None) -> dict:
+    """All-gathers per-shard fold tables (model-major rows within each shard) into full tables in
+    model-major, fold order: one [rows x columns] float64 all-gather (every column is a double or
+    an integer far below 2^53, so the round trip is exact)."""
+    names = [name for name, _ in abi.FOLD_COLUMNS]
+    mine = np.stack([np.asarray(cols[name], dtype=np.float64) for name in names], axis=1)
+    parts = _all_gather_rows(mine, group)
     out = {}
-    for name, _ in abi.FOLD_COLUMNS:
+    for j, name in enumerate(names):
+        dtype = np.asarray(cols[name]).dtype
         per_model = []
         for m in range(n_models):
-            chunks = []
             for p in parts:
-                arr = p[name]
-                nf = arr.shape[0] // n_models
-                chunks.append(arr[m * nf:(m + 1) * nf])
-            per_model.append(np.concatenate(chunks))
-        out[name] = np.concatenate(per_model)
+                nf = p.shape[0] // n_models
+                per_model.append(p[m * nf:(m + 1) * nf, j])
+        out[name] = np.concatenate(per_model).astype(dtype)
     return out
 
 
 def gather_rows(arr: np.ndarray, n_models: int, group=None) -> np.ndarray:
     """Same gather for per-chain / per-block arrays laid out model-major per shard."""
-    import torch.distributed as dist
-
-    world = dist.get_world_size(group)
-    parts = [None] * world
-    dist.all_gather_object(parts, np.asarray(arr), group=group)
+    a = np.asarray(arr)
+    parts = _all_gather_rows(a, group)
     per_model = []
     for m in range(n_models):
         for p in parts:
             n = p.shape[0] // n_models
             per_model.append(p[m * n:(m + 1) * n])
-    return np.concatenate(per_model)
+    return np.concatenate(per_model).astype(a.dtype)
 
 
 def shard_benchmark_offsets(failed_local, group=None) -> tuple[int, int]:
     """(non-failed folds before this shard, non-failed folds in total) from an all-gather of the
     per-shard non-failed counts: the global stream position of this shard's benchmark items
     (pcvg_benchmark, diagnostics.cpp:82-98)."""
-    import torch
     import torch.distributed as dist
 
-    mine = int(np.sum(np.asarray(failed_local) == 0)) if failed_local is not None else None
-    world = dist.get_world_size(group)
-    parts = [None] * world
-    dist.all_gather_object(parts, mine, group=group)
+    mine = int(np.sum(np.asarray(failed_local) == 0)) if failed_local is not None else 0
+    parts = _all_gather_rows(np.array([mine], dtype=np.float64), group)
+    counts = [int(p[0]) for p in parts]
     rank = dist.get_rank(group)
-    return int(sum(parts[:rank])), int(sum(parts))
+    return int(sum(counts[:rank])), int(sum(counts))
 
 
 def reduce_benchmark(rep_max: np.ndarray, needs_host: np.ndarray, device=None, group=None):
@@ -184,9 +212,8 @@ def run_pcv_sharded(inputs, cfg, device=0, group=None):
                     if name != "failed":
                         rep[name] = full[name]
                 rep["divergences"] = gather_rows(div, nm, group)
-                parts = [None] * world
-                dist.all_gather_object(parts, int(dropped), group=group)
-                rep["dropped_batch_draws"] = int(sum(parts))
+                parts = _all_gather_rows(np.array([float(dropped)]), group)
+                rep["dropped_batch_draws"] = int(sum(int(p[0]) for p in parts))
                 rep["iters_run"] = iters
             snaps.append([iters, rep["delta_hat"], rep["mcse"], rep["epistemic_se"], rep["prob_a_better"],
                           rep["ess_overall"], rep["rhat_max"]])

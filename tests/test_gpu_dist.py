@@ -29,8 +29,13 @@ sys.path[:0] = ["tests", "tests/golden", "."]
 import torch.distributed as tdist
 from parity_util import Case
 from paper_2310_07002_b200 import abi, dist, pcv
-name, cfgkw, out = sys.argv[1], eval(sys.argv[2]), sys.argv[3]
-tdist.init_process_group("gloo")
+name, cfgkw, out, backend = sys.argv[1], eval(sys.argv[2]), sys.argv[3], sys.argv[4]
+if backend == "nccl":
+    import torch
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+else:
+    tdist.init_process_group("gloo")
 case = Case(name)
 inputs = [pcv.ModelInput(m, pcv.FullDataFit(kp, bank), i)
           for i, (m, kp, bank) in enumerate(zip(case.models, case.kparams, case.banks))]
@@ -43,14 +48,14 @@ tdist.destroy_process_group()
 '''
 
 
-def run_sharded(name, cfgkw, world=2):
+def run_sharded(name, cfgkw, world=2, backend="gloo"):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     with tempfile.TemporaryDirectory() as tmp:
         out = os.path.join(tmp, "rep.pkl")
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-               "--master-addr", "127.0.0.1", "--master-port", str(port), "--no-python", sys.executable, "-c", WORKER, name, repr(cfgkw), out]
+               "--master-addr", "127.0.0.1", "--master-port", str(port), "--no-python", sys.executable, "-c", WORKER, name, repr(cfgkw), out, backend]
         r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, r.stderr[-4000:]
         with open(out, "rb") as f:
@@ -87,6 +92,23 @@ def test_sharded_bit_identical_to_single(name, cfgkw):
     for k in HEADLINE:
         assert a[k] == b[k] or (np.isnan(a[k]) and np.isnan(b[k])), (k, a[k], b[k])
     np.testing.assert_array_equal(np.sort(a["benchmark"]), np.sort(b["benchmark"]))
+    np.testing.assert_array_equal(a["snapshots"], b["snapshots"])
+
+
+def test_sharded_driver_over_nccl_one_rank():
+    """The same driver with the NCCL backend (one rank: NCCL refuses two ranks on one GPU): the
+    tensor all-gathers of the fold tables / block sums and the MAX all-reduce run on device buffers,
+    and the report equals pcvg_run bit for bit, early stop included."""
+    name = "seasonal_hvblock"
+    cfgkw = dict(chains=4, iters=200, warmup=30, batch_size=20, bench_draws=50, checkpoint_every=20, early_stop=1,
+                 seed=3)
+    a = run_sharded(name, cfgkw, world=1, backend="nccl")
+    b = run_single(name, cfgkw)
+    for k in COLUMNS:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    np.testing.assert_array_equal(a["divergences"], b["divergences"])
+    for k in HEADLINE:
+        assert a[k] == b[k] or (np.isnan(a[k]) and np.isnan(b[k])), (k, a[k], b[k])
     np.testing.assert_array_equal(a["snapshots"], b["snapshots"])
 
 
