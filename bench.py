@@ -292,7 +292,7 @@ def main():
     per_launch_ms = local_ms / args.steps
     achieved = FLOP_PER_CHAIN_STEP * (fe - fb) * L / (per_launch_ms * 1e-3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r02_ncu_glm_base.json")  # ncu --set full of the current kernel
+    prof = os.path.join(ROOT, "profiles", "r02_ncu_glm.json")  # ncu --set full of the current kernel
     if os.path.exists(prof):
         with open(prof) as fh:
             pj = json.load(fh)
@@ -309,7 +309,7 @@ def main():
                              "frac": achieved / peak, "traffic": traffic,
                              "flop_per_chain_step": FLOP_PER_CHAIN_STEP, "peak_source": peak_src,
                              "kernel": "glm32_kernel (tcgen05 kind::tf32)" if args.fp32 else "glm_kernel<logistic,52> (FP64 DMMA)",
-                             "traffic_source": "profiles/r02_ncu_glm_base.json (ncu --set full of the full-wave "
+                             "traffic_source": "profiles/r02_ncu_glm.json (ncu --set full of the full-wave "
                                                "sampling launch, dram read+write)"},
                 "clocks": clk.summary(), "gpu_launches": int(launches1 - launches0), "result": result}
     # e2e: the public API call with host buffers (pcvg_run: H2D of data/bank, Step 2 + Step 3,
