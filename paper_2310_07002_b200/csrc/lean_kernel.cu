@@ -243,16 +243,21 @@ __global__ void __launch_bounds__(kLeanBlock, MINB) lean_kernel(ModelDev M, Chai
   for (int64_t it = 0; it < A.n_iters; ++it) {
     // momentum refresh in dimension order (the reference's draw order), global half kick
     double pG[NGM], pa = 0.0, k0G = 0.0, k0g = 0.0;
-#pragma unroll
+    // unrolled for the small grouped shapes; rolled for seasonal AR (DIM = 15: one inlined copy of
+    // the Philox + Box-Muller code instead of 15 cut its kernel from ~20k to ~11k instructions and
+    // cfg4 ran 4.6% faster; rolling the 9-dimensional grouped loop cost cfg5 7%)
+    constexpr int kMomUnroll = DIM > 12 ? 1 : DIM;
+#pragma unroll kMomUnroll
     for (int d = 0; d < DIM; ++d) {
       const double z = R.normal();
+      const double p = z / sqrt(__ldg(M.inv_mass + d));  // = mG(slot_of_dim(d)), or ma for d = 0
       const int sl = slot_of_dim<FAM, NCM, PAR>(d);
       if (sl < 0) {
-        pa = z / sqrt(ma);
+        pa = p;
       } else {
 #pragma unroll
         for (int i = 0; i < NGM; ++i)
-          if (i == sl) pG[i] = z / sqrt(mG(i));
+          if (i == sl) pG[i] = p;
       }
     }
 #pragma unroll
