@@ -65,6 +65,8 @@ def main():
             "delta_hat": rep["delta_hat"], "mcse": rep["mcse"], "epistemic_se": rep["epistemic_se"],
             "rhat_max": rep["rhat_max"], "verdict_quantile_value": rep["verdict_quantile_value"],
             "verdict_pass": int(rep["verdict_pass"]), "chain_steps": chains * steps}
+    if "snapshots" in rep:  # per check interval: iters, delta_hat, mcse, epistemic_se, prob, ess, rhat_max
+        line["snapshots"] = [[float(v) for v in row] for row in np.asarray(rep["snapshots"])]
     if args.fit:
         fits = []
         with pcv.Context(0) as ctx:
