@@ -104,6 +104,7 @@ struct Smem {
   double llp[4][kC];                      // per row group: log-lik (logistic) / sum r^2 (gaussian)
   double gt[G::SCR * kLdS];               // cluster reduction: partial rows received from the other ranks
   double red[kMaxOwners][kC];             // owner partial sums (kinetic)
+  double lpp[kC];                         // this rank's log_pred partial per chain (cluster ranks split rows)
   double pri[kMaxOwners][kC];             // owner partial sums (log joint)
   double exp_tab[16];                     // 2^(-j/16)
   int exp_hi32[32], exp_lo32[32];          // 2^(-j/32) as high / low words (gradient-only sigmoid)
@@ -240,6 +241,11 @@ __device__ long long g_gtrace[64][14];
 __device__ int g_gpass;
 __device__ unsigned long long g_rtrace[16][8][14];  // CTAs 0..15, passes 32..39, globaltimer ns
 __device__ int g_bpass[16];
+__device__ unsigned long long g_ttrace[4][6];  // CTA 0, transitions 1..4: phase stamps (globaltimer)
+#define TTRACE(i)                                                                                \
+  do {                                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && it >= 1 && it <= 4) g_ttrace[it - 1][(i)] = gtimer(); \
+  } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -253,6 +259,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #else
 #define GTRACE(i) \
+  do {            \
+  } while (0)
+#define TTRACE(i) \
   do {            \
   } while (0)
 #endif
@@ -714,6 +723,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
   const double eps = M.step, half = 0.5 * M.step;
   const int n_lf = M.n_lf;
   for (int64_t it = 0; it < A.n_iters; ++it) {
+    TTRACE(0);
     if (A.mode != kModePred) {
       // -- momentum refresh (chain thread, reference draw order) -> staging in sm.rs
       double k0 = 0.0;
@@ -752,6 +762,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         if (bad) sm.bad[oc] = 1;
       }
       __syncthreads();
+      TTRACE(1);
       // -- leapfrog: n_lf gradient passes
       for (int s = 0; s < n_lf; ++s) {
         const bool last = s == n_lf - 1;
@@ -818,6 +829,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         if (blockIdx.x < 16 && threadIdx.x == 0) ++g_bpass[blockIdx.x];
 #endif
       }
+      TTRACE(2);
       // -- energies, Metropolis (chain thread)
       if (is_chain) {
         double k1 = 0.0;
@@ -869,10 +881,14 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         continue;
       }
     }
-    // -- log_pred at the current position (rank 0): the 8 owner threads of a chain split its fold's
-    //    test rows (K-fold: 1,000 rows at cfg2) with the position staged [k][chain] in sm.rs; the
-    //    chain thread adds the owner partials in owner order and updates the accumulators
-    if (writer) {
+    TTRACE(3);
+    // -- log_pred at the current position: the cs ranks of the tile's first cluster and the 8 owner
+    //    threads of a chain split its fold's test rows (K-fold: 1,000 rows at cfg2; row tt goes to
+    //    rank (tt / 8) % cs, owner tt % 8) with the position staged [k][chain] in sm.rs; each rank
+    //    adds its owner partials in owner order, rank 0's chain thread adds the rank partials in
+    //    rank order (DSMEM) and updates the accumulators
+    const bool lp_rank = clus == 0;
+    if (lp_rank) {
       const int cu = sm.cur[oc];
 #pragma unroll
       for (int j = 0; j < G::OWN; ++j) {
@@ -884,7 +900,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
     {
       double part = 0.0;
       const int ofold = sm.fold[oc];
-      if (writer && ovalid && ofold < M.K) {
+      if (lp_rank && ovalid && ofold < M.K) {
         const double* th = sm.rs + oc;
         double v_pred = 1.0;
         if constexpr (FAM == kGrouped) {
@@ -895,25 +911,59 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         }
         const int s0 = M.fold_seg[ofold], s1 = M.fold_seg[ofold + 1];
         const int r0 = M.seg_row[s0], r1 = M.seg_row[s1];  // the fold's test rows, contiguous
-        for (int tt = r0 + ok; tt < r1; tt += kOwners) {
+        for (int tt = r0 + crank * kOwners + ok; tt < r1; tt += kOwners * cs) {
           const int i = M.seg_rows[tt];
           const double* xrow = M.xr + static_cast<size_t>(i) * KP;
           double eta = 0.0;
-          for (int k = 0; k < dim; ++k) {
-            const int col = col_of<FAM>(M, k);
-            if (col >= 0) eta = fma(xrow[col], w_of<FAM>(M, k, th[k * kLdS]), eta);
+          if constexpr (FAM == kLogistic) {
+            // the padded row as KP / 2 independent 16-byte loads and four partial sums (column k
+            // of X is parameter k; padding columns are zero and get weight 0): a row's loads are
+            // in flight together instead of one dependent load + FMA per column (K-fold cfg2:
+            // 1,000 test rows per fold made log_pred ~1/3 of a transition)
+            static_assert(KP % 4 == 0, "row pairs");
+            const double2* x2 = reinterpret_cast<const double2*>(xrow);
+            double e4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < KP / 2; ++kk) {
+              const double2 xv = __ldg(x2 + kk);
+              const int k = 2 * kk;
+              const double w0 = k < dim ? th[k * kLdS] : 0.0;
+              const double w1 = k + 1 < dim ? th[(k + 1) * kLdS] : 0.0;
+              e4[(2 * kk) & 3] = fma(xv.x, w0, e4[(2 * kk) & 3]);
+              e4[(2 * kk + 1) & 3] = fma(xv.y, w1, e4[(2 * kk + 1) & 3]);
+            }
+            eta = (e4[0] + e4[1]) + (e4[2] + e4[3]);
+            part += bernoulli_logit(M.y[i], eta);
+          } else {
+            for (int k = 0; k < dim; ++k) {
+              const int col = col_of<FAM>(M, k);
+              if (col >= 0) eta = fma(xrow[col], w_of<FAM>(M, k, th[k * kLdS]), eta);
+            }
+            part += normal_logpdf(M.y[i], eta, v_pred);
           }
-          if constexpr (FAM == kLogistic) part += bernoulli_logit(M.y[i], eta);
-          else part += normal_logpdf(M.y[i], eta, v_pred);
         }
       }
       sm.red[ok][oc] = part;
     }
     __syncthreads();
-    if (cvalid && writer) {
-      double sp = 0.0;
+    double sp = 0.0;
+    if (is_chain) {
 #pragma unroll
       for (int o = 0; o < kOwners; ++o) sp += sm.red[o][tid];
+    }
+    if (cs > 1) {
+      if (is_chain) sm.lpp[tid] = sp;
+      cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+      cl.sync();  // every rank's partials published
+      if (cvalid && writer) {
+        sp = 0.0;
+        for (int q = 0; q < cs; ++q) sp += cl.map_shared_rank(sm.lpp, q)[tid];
+      }
+      // no rank may exit while rank 0 still reads its partials (the next transition's syncs order
+      // the reuse of sm.lpp otherwise)
+      if (it + 1 == A.n_iters || A.mode == kModePred) cl.sync();
+    }
+    if (cvalid && writer) {
       if (A.mode == kModePred) {
         if (A.out_a) A.out_a[gc] = sp;
       } else if (A.mode == kModeWarmup) {
@@ -927,10 +977,11 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
         glm_score_extra<FAM, KP>(M, S, gc, fold, S.pos + sm.cur[tid] * plane + gc,
                                  A.mode == kModeWarmup, writer, R);
     }
+    TTRACE(4);
     if (A.mode == kModePred) break;
   }
 #ifdef PCVG_GLM_TRACE
-  if (blockIdx.x == 0 && threadIdx.x == 0 && g_gpass >= 32 && g_gpass < 96) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_gpass >= 32 && g_gpass < 1000) {
     printf("pass: start tiles_done staged reduced owners_done | cluster-level-done arrived (cycles), cs=%d nc=%d\n",
            cs, nc);
     for (int p = 0; p < 32 && p < 64; ++p)
@@ -939,6 +990,11 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
              g_gtrace[p][5] - g_gtrace[p][0], g_gtrace[p][6] - g_gtrace[p][0],
              p + 1 < 32 ? g_gtrace[p + 1][0] - g_gtrace[p][0] : 0LL);
     g_gpass = 1000;
+    for (int t = 0; t < 3; ++t)
+      printf("transition %d (ns from start): momentum+kick %lld | passes %lld | metropolis %lld | log_pred+accum %lld | next %lld\n", t + 1,
+             (long long)(g_ttrace[t][1] - g_ttrace[t][0]), (long long)(g_ttrace[t][2] - g_ttrace[t][1]),
+             (long long)(g_ttrace[t][3] - g_ttrace[t][2]), (long long)(g_ttrace[t][4] - g_ttrace[t][3]),
+             (long long)(g_ttrace[t + 1][0] - g_ttrace[t][4]));
     printf("per-CTA (ns from CTA0 pass start): cta pass | tiles allwarps staged red-start rows-reduced pre-gather gathered glob-publish glob-arrived reduced own-done own-synced owners\n");
     for (int p = 0; p < 3; ++p) {
       const unsigned long long z = g_rtrace[0][p][0];
