@@ -119,6 +119,32 @@ struct ChainRng {
   }
 };
 
+// The Box-Muller pair ChainRng::normal() draws from stream words [wpos, wpos + 4) (two uniforms of
+// two words each, rng.hpp:70-87): *a is the value returned first, *b the one cached. Lets several
+// threads draw a chain's momenta in parallel at known stream positions with the same bits.
+__device__ __forceinline__ void normal_pair_at(uint32_t k0, uint32_t k1, uint64_t stream, uint64_t wpos,
+                                               double* a, double* b) {
+  const uint64_t blk = wpos >> 2;
+  const int o = static_cast<int>(wpos & 3);
+  const uint4 x = philox_block(blk, stream, k0, k1);
+  uint4 y = x;
+  if (o != 0) y = philox_block(blk + 1, stream, k0, k1);
+  auto word = [&](int i) -> uint32_t {  // word i (0..7) of blocks blk, blk + 1
+    const uint4 v = i < 4 ? x : y;
+    const int j = i & 3;
+    return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
+  };
+  const uint64_t v1 = static_cast<uint64_t>(word(o)) | (static_cast<uint64_t>(word(o + 1)) << 32);
+  const uint64_t v2 = static_cast<uint64_t>(word(o + 2)) | (static_cast<uint64_t>(word(o + 3)) << 32);
+  const double u1 = (static_cast<double>(v1 >> 11) + 0.5) * 0x1p-53;
+  const double u2 = (static_cast<double>(v2 >> 11) + 0.5) * 0x1p-53;
+  const double r = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincos(kTwoPi * u2, &sn, &cs);
+  *a = r * cs;
+  *b = r * sn;
+}
+
 __device__ __forceinline__ double logaddexp(double a, double b) {  // math.hpp:17-22
   if (a == -CUDART_INF) return b;
   if (b == -CUDART_INF) return a;

@@ -105,6 +105,9 @@ struct Smem {
   double gt[G::SCR * kLdS];               // cluster reduction: partial rows received from the other ranks
   double red[kMaxOwners][kC];             // owner partial sums (kinetic)
   double lpp[kC];                         // this rank's log_pred partial per chain (cluster ranks split rows)
+  unsigned long long rng_pos[kC];         // momentum draws: each chain's stream position,
+  double rng_cached[kC], rng_tail[kC];    // cached normal in / out,
+  int rng_has[kC];                        // and cached flag at the transition start
   double pri[kMaxOwners][kC];             // owner partial sums (log joint)
   double exp_tab[16];                     // 2^(-j/16)
   int exp_hi32[32], exp_lo32[32];          // 2^(-j/32) as high / low words (gradient-only sigmoid)
@@ -725,19 +728,59 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
   for (int64_t it = 0; it < A.n_iters; ++it) {
     TTRACE(0);
     if (A.mode != kModePred) {
-      // -- momentum refresh (chain thread, reference draw order) -> staging in sm.rs
+      // -- momentum refresh (reference draw order) -> staging in sm.rs. The Box-Muller pairs of a
+      //    chain sit at known positions of its stream, so its 8 owner threads draw them in parallel
+      //    (normal_pair_at, the same bits as R.normal()); the chain thread then advances its stream
+      //    past them and sums the kinetic energy in dimension order.
       double k0 = 0.0;
-      if (is_chain) {
-        for (int k = 0; k < dim; ++k) {
-          const double mk = __ldg(M.inv_mass + k);
-          double p;
-          if (A.mode == kModeProbe) p = cvalid ? A.probe_momentum[static_cast<size_t>(gc) * dim + k] : 0.0;
-          else p = R.normal() / sqrt(mk);
-          k0 += mk * p * p;
-          sm.rs[k * kLdS + tid] = p;
+      if (A.mode == kModeProbe) {
+        if (is_chain) {
+          for (int k = 0; k < dim; ++k) {
+            const double mk = __ldg(M.inv_mass + k);
+            const double p = cvalid ? A.probe_momentum[static_cast<size_t>(gc) * dim + k] : 0.0;
+            k0 += mk * p * p;
+            sm.rs[k * kLdS + tid] = p;
+          }
         }
-        sm.bad[tid] = 0;
+      } else {
+        if (is_chain) {
+          sm.rng_pos[tid] = R.pos;
+          sm.rng_has[tid] = R.has_cached ? 1 : 0;
+          sm.rng_cached[tid] = R.cached;
+        }
+        __syncthreads();
+        if (ovalid) {
+          const int h = sm.rng_has[oc];
+          const uint64_t pos0 = sm.rng_pos[oc];
+          const int npairs = (dim - h + 1) / 2;
+          if (ok == 0 && h) sm.rs[oc] = sm.rng_cached[oc] / sqrt(__ldg(M.inv_mass));
+          const uint64_t stream = S.rng_stream[ogc];
+          for (int j = ok; j < npairs; j += kOwners) {
+            double a, b;
+            normal_pair_at(static_cast<uint32_t>(S.seed), static_cast<uint32_t>(S.seed >> 32), stream,
+                           pos0 + 4ull * j, &a, &b);
+            const int k = h + 2 * j;
+            sm.rs[k * kLdS + oc] = a / sqrt(__ldg(M.inv_mass + k));
+            if (k + 1 < dim) sm.rs[(k + 1) * kLdS + oc] = b / sqrt(__ldg(M.inv_mass + k + 1));
+            else sm.rng_tail[oc] = b;  // odd count: the pair's second value stays cached
+          }
+        }
+        __syncthreads();
+        if (cvalid) {
+          const int h = R.has_cached ? 1 : 0;
+          const int npairs = (dim - h + 1) / 2;
+          R.pos += 4ull * npairs;
+          R.buf_block = ~0ull;
+          R.has_cached = ((dim - h) & 1) != 0;
+          if (R.has_cached) R.cached = sm.rng_tail[tid];
+          for (int k = 0; k < dim; ++k) {
+            const double mk = __ldg(M.inv_mass + k);
+            const double p = sm.rs[k * kLdS + tid];
+            k0 += mk * p * p;
+          }
+        }
       }
+      if (is_chain) sm.bad[tid] = 0;
       __syncthreads();
       // -- half kick + first drift (owners)
       double pown[G::OWN];
