@@ -5,7 +5,7 @@
 mkdir -p gpurun_out
 NAME=$1; KRE=$2; SKIP=$3; shift 3
 timeout 600 "$@" > gpurun_out/plain_$NAME.log 2>&1 || { echo "plain run failed"; tail -5 gpurun_out/plain_$NAME.log; exit 1; }
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$KRE -s $SKIP -c 1 -o /tmp/$NAME "$@" > gpurun_out/ncu_$NAME.log 2>&1
+timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:$KRE -s $SKIP -c 1 -o /tmp/$NAME "$@" > gpurun_out/ncu_$NAME.log 2>&1
 echo "ncu rc=$?"; tail -3 gpurun_out/ncu_$NAME.log
 ncu -i /tmp/$NAME.ncu-rep --page raw --csv > gpurun_out/${NAME}_raw.csv 2>/dev/null
 ncu -i /tmp/$NAME.ncu-rep --page source --csv > gpurun_out/${NAME}_src.csv 2>/dev/null
