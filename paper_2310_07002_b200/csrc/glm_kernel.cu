@@ -100,6 +100,8 @@ struct Smem {
   int ks[kStages][G::TM];
   double rs[(KP > 64 ? KP : 64) * kLdS];  // per-warp R blocks; reused as G and momentum staging
   double qs[G::DIMP * kLdS];              // parameters, [k][chain]
+  double im[G::DIMP];                     // inverse mass (shared memory: the device-scope acquire of the
+                                          // multi-cluster reduction invalidates L1 every pass)
   double ws[KP * kLdS];                   // GEMM weights, [col][chain]
   double llp[4][kC];                      // per row group: log-lik (logistic) / sum r^2 (gaussian)
   double gt[G::SCR * kLdS];               // cluster reduction: partial rows received from the other ranks
@@ -643,6 +645,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
     sm.exp_lo32[tid] = __double2loint(v);
   }
   for (int i = tid; i < KP * kLdS; i += kThreads) sm.ws[i] = 0.0;
+  for (int i = tid; i < dim; i += kThreads) sm.im[i] = __ldg(M.inv_mass + i);
   fence_mbar_init();
   uint32_t gtile = 0;
 
@@ -736,7 +739,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
       if (A.mode == kModeProbe) {
         if (is_chain) {
           for (int k = 0; k < dim; ++k) {
-            const double mk = __ldg(M.inv_mass + k);
+            const double mk = sm.im[k];
             const double p = cvalid ? A.probe_momentum[static_cast<size_t>(gc) * dim + k] : 0.0;
             k0 += mk * p * p;
             sm.rs[k * kLdS + tid] = p;
@@ -753,15 +756,15 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
           const int h = sm.rng_has[oc];
           const uint64_t pos0 = sm.rng_pos[oc];
           const int npairs = (dim - h + 1) / 2;
-          if (ok == 0 && h) sm.rs[oc] = sm.rng_cached[oc] / sqrt(__ldg(M.inv_mass));
+          if (ok == 0 && h) sm.rs[oc] = sm.rng_cached[oc] / sqrt(sm.im[0]);
           const uint64_t stream = S.rng_stream[ogc];
           for (int j = ok; j < npairs; j += kOwners) {
             double a, b;
             normal_pair_at(static_cast<uint32_t>(S.seed), static_cast<uint32_t>(S.seed >> 32), stream,
                            pos0 + 4ull * j, &a, &b);
             const int k = h + 2 * j;
-            sm.rs[k * kLdS + oc] = a / sqrt(__ldg(M.inv_mass + k));
-            if (k + 1 < dim) sm.rs[(k + 1) * kLdS + oc] = b / sqrt(__ldg(M.inv_mass + k + 1));
+            sm.rs[k * kLdS + oc] = a / sqrt(sm.im[k]);
+            if (k + 1 < dim) sm.rs[(k + 1) * kLdS + oc] = b / sqrt(sm.im[k + 1]);
             else sm.rng_tail[oc] = b;  // odd count: the pair's second value stays cached
           }
         }
@@ -774,7 +777,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
           R.has_cached = ((dim - h) & 1) != 0;
           if (R.has_cached) R.cached = sm.rng_tail[tid];
           for (int k = 0; k < dim; ++k) {
-            const double mk = __ldg(M.inv_mass + k);
+            const double mk = sm.im[k];
             const double p = sm.rs[k * kLdS + tid];
             k0 += mk * p * p;
           }
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
             if (ovalid) {
               const size_t gi = cu * plane + static_cast<size_t>(k) * nch + ogc;
               p = sm.rs[k * kLdS + oc] + half * S.grad[gi];
-              q = S.pos[gi] + eps * __ldg(M.inv_mass + k) * p;
+              q = S.pos[gi] + eps * sm.im[k] * p;
               bad |= !isfinite(q);
             }
             put_q(k, q);
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
             pown[j] += scale * g;
             bad |= !isfinite(pown[j]);
             if (last) {
-              part += __ldg(M.inv_mass + k) * pown[j] * pown[j];
+              part += sm.im[k] * pown[j] * pown[j];
               part2 += logp_of<FAM, KP>(M, sm, k, oc, q);
               // the proposal plane: rank 0 of a cluster (its ranks sync on the cluster barrier); over
               // several clusters every CTA stores the same bits and reads back its own stores
@@ -855,7 +858,7 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
           for (int j = 0; j < G::OWN; ++j) {
             const int k = ok + kOwners * j;
             if (k < dim) {
-              const double q = sm.qs[k * kLdS + oc] + eps * __ldg(M.inv_mass + k) * pown[j];
+              const double q = sm.qs[k * kLdS + oc] + eps * sm.im[k] * pown[j];
               bad |= !isfinite(q);
               put_q(k, q);
             }
