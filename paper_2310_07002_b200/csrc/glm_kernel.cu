@@ -399,41 +399,45 @@ __device__ void grad_pass(Smem<KP>& sm, const ModelDev& M, uint32_t& gtile, int 
   GTRACE(1);
   __syncthreads();
   GTRACE(11);
-  // Stage G [col][chain] into sm.rs: row group 0 stores, the others add in order.
-#pragma unroll 1
-  for (int qq = 0; qq < G::RQ; ++qq) {
-    if (rq == qq) {
+  // Stage G [col][chain] into sm.rs: every row group stores its partial at once - row group 0 into
+  // sm.rs, groups 1..3 into the idle TMA ring slots ([col][64], 16-byte granules XOR-swizzled by
+  // col so a warp's 8 columns hit distinct banks) - then all threads add the four in a fixed tree,
+  // (g0 + g1) + (g2 + g3): two barriers instead of four sequential rounds.
+  static_assert(G::RQ == 4, "four row groups");
+  static_assert(G::TM * KP + G::XPAD >= KP * kC, "a ring slot holds one G partial");
+  auto part_idx = [](int p, int ch) { return p * kC + (((ch >> 1) ^ ((p & 7) << 1)) << 1) + (ch & 1); };
 #pragma unroll
-      for (int pt = 0; pt < G::PT; ++pt) {
-        const int p = 8 * pt + (l >> 2);
-        if (p < KP) {
+  for (int pt = 0; pt < G::PT; ++pt) {
+    const int p = 8 * pt + (l >> 2);
+    if (p < KP) {
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            double2* dst = reinterpret_cast<double2*>(&sm.rs[p * kLdS + 16 * cg + 8 * j + 2 * (l & 3)]);
-            if (qq == 0) {
-              *dst = make_double2(gacc[pt][j][0], gacc[pt][j][1]);
-            } else {
-              const double2 v = *dst;
-              *dst = make_double2(v.x + gacc[pt][j][0], v.y + gacc[pt][j][1]);
-            }
-          }
-        }
-      }
-      if (VALUE || kGauss) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            double v = acc[j][e];
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 16);
-            if (l < 4) sm.llp[qq][16 * cg + 8 * j + 2 * l + e] = v;
-          }
+      for (int j = 0; j < 2; ++j) {
+        const int ch = 16 * cg + 8 * j + 2 * (l & 3);
+        double2* dst = rq == 0 ? reinterpret_cast<double2*>(&sm.rs[p * kLdS + ch])
+                               : reinterpret_cast<double2*>(&sm.xs[rq - 1][part_idx(p, ch)]);
+        *dst = make_double2(gacc[pt][j][0], gacc[pt][j][1]);
       }
     }
-    __syncthreads();
   }
+  if (VALUE || kGauss) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = acc[j][e];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (l < 4) sm.llp[rq][16 * cg + 8 * j + 2 * l + e] = v;
+      }
+  }
+  __syncthreads();
+  for (int i = tid; i < KP * kC; i += G::THREADS) {
+    const int p = i / kC, ch = i % kC, x = part_idx(p, ch);
+    double* d = &sm.rs[p * kLdS + ch];
+    *d = (*d + sm.xs[0][x]) + (sm.xs[1][x] + sm.xs[2][x]);
+  }
+  __syncthreads();
 }
 
 // Sums the staged partials (G in sm.rs rows 0..KP-1, residual statistic in sm.llp) over the CS CTAs
