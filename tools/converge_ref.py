@@ -4,7 +4,7 @@ t at which its own report meets the rule (verdict pass on `blocks` blocks, MCSE 
 Runs the compiled reference (oracle/_ref) at t = every*blocks, every*(blocks+1), ... on all host
 threads, with the same kernel, bank and seeds as tools/converge.py.
 
-  python tools/converge_ref.py [--config cfg1] [--iters 1000] [--every 50]
+  python tools/converge_ref.py [--config cfg1] [--iters 1000] [--every 50] [--start T]
 """
 import argparse
 import json
@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--every", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--start", type=int, default=0, help="first check point (default every * blocks)")
     args = ap.parse_args()
     from bench_configs import CONFIGS
     from parity_util import Case
@@ -35,7 +36,7 @@ def main():
     threads = os.cpu_count() or 1
     tried = []
     line = None
-    t = args.every * 5
+    t = args.start or args.every * 5
     while t <= args.iters:
         cfg = abi.run_config(chains=L, iters=t, warmup=args.warmup, batch_size=args.every, blocks=5, bench_draws=500,
                              seed=1)
