@@ -39,7 +39,6 @@ def main():
                           "step_size": f.kparams.step_size}
     if not args.no_ref:
         import _oracle as O
-        import numpy as np
         from paper_2310_07002_b200 import abi
         if O.have_ref():
             rm = O.RModel(case.data, case.fa, abi.SpecArrays(**case.kws[0]))
@@ -49,7 +48,6 @@ def main():
                                      "host_threads": os.cpu_count(),
                                      "kind": "reference adapt_full_data (oracle/_ref)"}
             line["reference_over_device"] = line["reference_cpu"]["wall_s"] / line["device"]["wall_s"]
-            del np
     print(json.dumps(line), flush=True)
 
 
