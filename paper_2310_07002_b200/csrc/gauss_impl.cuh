@@ -62,15 +62,8 @@ struct NormalCursor {
       i -= 1;
     }
     const int64_t pr = i >> 1;
-    if (pr != pair) {
-      R.pos = pos0 + 4 * static_cast<uint64_t>(pr);
-      const double u1 = R.uniform();
-      const double u2 = R.uniform();
-      const double r = sqrt(-2.0 * log(u1));
-      double s, c;
-      sincos(kTwoPi * u2, &s, &c);
-      ncos = r * c;
-      nsin = r * s;
+    if (pr != pair) {  // the pair R.normal() would draw at this stream position (same bits)
+      normal_pair_at(R.k0, R.k1, R.stream, pos0 + 4 * static_cast<uint64_t>(pr), &ncos, &nsin);
       pair = pr;
     }
     return (i & 1) ? nsin : ncos;
