@@ -31,6 +31,26 @@ CONFIGS = {
 }
 
 
+def make_case(name):
+    """The test fixture of a config with its fold scheme: cfg2k is BASELINE configs[1]'s K-fold scheme
+    on the cfg2 data and fit, cfg4r SURVEY 8(d)'s Racine per-point hv folds on the cfg4 data and fits."""
+    from parity_util import Case
+    fixture, _, _ = CONFIGS[name]
+    case = Case(fixture)
+    if name == "cfg2k":
+        from paper_2310_07002_b200 import pcv
+        case.folds = pcv.make_kfold_scheme(case.data, 10, 1)
+        case.models = [pcv.LogisticModel("M0", case.data, case.folds)]
+        case.fa = case.folds.arrays()
+    if name == "cfg4r":
+        from paper_2310_07002_b200 import pcv
+        case.folds = pcv.make_hv_racine_scheme(case.data, 5, 12)
+        case.models = [pcv.SeasonalARModel(f"M{m}", case.data, case.folds, kw["ar_order"], kw["dummies"],
+                                           kw["rho_transform"]) for m, kw in enumerate(case.kws)]
+        case.fa = case.folds.arrays()
+    return case
+
+
 def flops_per_chain_step(case, m):
     kw = case.kws[m]
     n = case.data.n_obs
@@ -105,18 +125,7 @@ def main():
     names = [n for n in CONFIGS if not args.only or n in args.only.split(",")]
     for name in names:
         fixture, L, desc = CONFIGS[name]
-        case = Case(fixture)
-        if name == "cfg2k":  # the K-fold scheme of BASELINE configs[1] on the same data and fit
-            from paper_2310_07002_b200 import pcv
-            case.folds = pcv.make_kfold_scheme(case.data, 10, 1)
-            case.models = [pcv.LogisticModel("M0", case.data, case.folds)]
-            case.fa = case.folds.arrays()
-        if name == "cfg4r":  # the Racine per-point hv variant on the same data and fits
-            from paper_2310_07002_b200 import pcv
-            case.folds = pcv.make_hv_racine_scheme(case.data, 5, 12)
-            case.models = [pcv.SeasonalARModel(f"M{m}", case.data, case.folds, kw["ar_order"], kw["dummies"],
-                                               kw["rho_transform"]) for m, kw in enumerate(case.kws)]
-            case.fa = case.folds.arrays()
+        case = make_case(name)
         steps = args.steps if name != "cfg5" else max(2, args.steps // 3)
         ms, cols = gpu_run(case, L, steps, args.warmup, args.policy)
         chains = case.K * L * len(case.models)

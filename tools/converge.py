@@ -36,11 +36,11 @@ def main():
                          "4 chains, 1000 warm-up + 2000 draws) on the same GPU, for the north star's "
                          "'comparable to a single full-data fit'")
     args = ap.parse_args()
-    from bench_configs import CONFIGS, cpu_sample
+    from bench_configs import CONFIGS, cpu_sample, make_case
     from parity_util import Case
     from paper_2310_07002_b200 import abi, pcv
     fixture, L, desc = CONFIGS[args.config]
-    case = Case(fixture)
+    case = make_case(args.config)
     cfg = abi.run_config(chains=L, iters=args.iters, warmup=args.warmup, batch_size=args.every, blocks=5,
                          bench_draws=500, seed=1, checkpoint_every=args.every, early_stop=1)
     t0 = time.perf_counter()

@@ -25,12 +25,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--start", type=int, default=0, help="first check point (default every * blocks)")
     args = ap.parse_args()
-    from bench_configs import CONFIGS
+    from bench_configs import CONFIGS, make_case
     from parity_util import Case
     from paper_2310_07002_b200 import abi
     import _oracle as O
     fixture, L, desc = CONFIGS[args.config]
-    case = Case(fixture)
+    case = make_case(args.config)
     models = [O.RModel(case.data, case.fa, abi.SpecArrays(**kw)) for kw in case.kws]
     kernels = [abi.KernelArrays(k.step_size, k.n_leapfrog, k.inv_mass_diag) for k in case.kparams]
     threads = os.cpu_count() or 1

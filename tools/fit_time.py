@@ -24,11 +24,11 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-ref", action="store_true")
     args = ap.parse_args()
-    from bench_configs import CONFIGS
+    from bench_configs import CONFIGS, make_case
     from parity_util import Case
     from paper_2310_07002_b200 import pcv
     fixture, _, desc = CONFIGS[args.config]
-    case = Case(fixture)
+    case = make_case(args.config)
     line = {"config": args.config, "workload": desc, "fit": "4 chains, 1000 warm-up + 2000 draws, n_lf 32"}
     with pcv.Context(0) as ctx:
         m = case.models[0]
