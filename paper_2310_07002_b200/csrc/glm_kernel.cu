@@ -1168,7 +1168,9 @@ cudaError_t launch_t(const ModelDev& M, const ChainsDev& S, const RunArgs& A, cu
     // rounding only (test_wave_tail_split_matches_unsplit); full-wave chains are bit-identical.
     const int r = tiles % sms, ntiles_rows = (M.n + Geom<KP>::TM - 1) / Geom<KP>::TM;
     int ct = 1;
-    while (ct < 8 && r * ct * 2 <= sms && ntiles_rows >= 4 * ct * 2) ct *= 2;
+    // double the cluster while the tail still fits on the SMs in one round: all r clusters must be
+    // co-resident (a cluster fits within one GPC), else the last ones wait for a second round
+    while (ct < 8 && r * ct * 2 <= sms && ntiles_rows >= 4 * ct * 2 && fits(ct * 2) >= r) ct *= 2;
     cudaError_t e = launch(0, tiles - r, 1, 1);
     if (e != cudaSuccess) return e;
     return launch(tiles - r, r, ct, 1);
