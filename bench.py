@@ -145,20 +145,34 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-CONVERGE_WORKLOAD = ("cfg4: seasonal AR(2)+11 dummies T=5000, hv-block K=100 h=12 (BASELINE configs[3], the "
-                     "early-stopping configuration), M_A + M_B x 4 chains, check every 50 iterations, at most 2000")
+CONVERGE_WORKLOADS = {
+    "cfg2k": ("cfg2 K-fold: logistic N=10000 P=50, K=10 (seed 1) x 8 chains (BASELINE configs[1], the bench "
+              "data and fit), check every 50 iterations, at most 2000"),
+    "cfg4": ("cfg4: seasonal AR(2)+11 dummies T=5000, hv-block K=100 h=12 (BASELINE configs[3], the "
+             "early-stopping configuration), M_A + M_B x 4 chains, check every 50 iterations, at most 2000"),
+}
 
 
-def time_to_converged(world, local, dist):
+def time_to_converged(world, local, dist, which="cfg2k"):
     """Wall-clock to R-hat-converged elpd (the second half of BASELINE.json's metric) through the
-    public API with host inputs: run_pcv with the early-stop rule on cfg4, one call
-    (one GPU) or the fold-sharded driver (N ranks), max over ranks."""
+    public API with host inputs: run_pcv with the early-stop rule, one call (one GPU)
+    or the fold-sharded driver (N ranks), max over ranks. cfg2 K-fold is the bench's own data, fit
+    and chain count per fold (its LOO scheme needs ~6,000 iterations); cfg4 is the
+    hv-block configuration of BASELINE configs[3]."""
     from make_golden import load
     from paper_2310_07002_b200 import pcv
-    d, f, models, _ = load("cfg4_seasonal_bench")
-    inputs = [pcv.ModelInput(pcv.SeasonalARModel(f"M{i}", d, f, kw["ar_order"], kw["dummies"], kw["rho_transform"]),
-                             pcv.FullDataFit(kp, bank), i) for i, (kw, kp, bank) in enumerate(models)]
-    cfg = pcv.RunConfig(chains=4, iters=2000, warmup=100, batch_size=50, blocks=5, bench_draws=500, seed=1,
+    if which == "cfg2k":
+        d, _, models, _ = load("cfg2_logistic_bench")
+        folds = pcv.make_kfold_scheme(d, 10, 1)
+        kp, bank = models[0][1], models[0][2]
+        inputs = [pcv.ModelInput(pcv.LogisticModel("M_A", d, folds), pcv.FullDataFit(kp, bank), 0)]
+        L, chains = 8, 10 * 8
+    else:
+        d, f, models, _ = load("cfg4_seasonal_bench")
+        inputs = [pcv.ModelInput(pcv.SeasonalARModel(f"M{i}", d, f, kw["ar_order"], kw["dummies"], kw["rho_transform"]),
+                                 pcv.FullDataFit(kp, bank), i) for i, (kw, kp, bank) in enumerate(models)]
+        L, chains = 4, 800
+    cfg = pcv.RunConfig(chains=L, iters=2000, warmup=100, batch_size=50, blocks=5, bench_draws=500, seed=1,
                         checkpoint_every=50, early_stop=1)
     if dist:
         dist.barrier()
@@ -174,12 +188,12 @@ def time_to_converged(world, local, dist):
         t = torch.tensor([wall], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall = float(t.item())
-    return {"workload": CONVERGE_WORKLOAD, "iters_run": int(rep["iters_run"]),
+    return {"workload": CONVERGE_WORKLOADS[which], "iters_run": int(rep["iters_run"]),
             "stopped_early": bool(rep["iters_run"] < cfg.iters), "wall_s": wall,
             "device_s": (rep["warmup_ms"] + rep["sampling_ms"]) / 1e3 if not dist else None,
             "rhat_max": rep["rhat_max"], "verdict_quantile_value": rep["verdict_quantile_value"],
             "delta_hat": rep["delta_hat"], "mcse": rep["mcse"], "epistemic_se": rep["epistemic_se"],
-            "chain_steps": 800 * (int(rep["iters_run"]) + cfg.warmup),
+            "chain_steps": chains * (int(rep["iters_run"]) + cfg.warmup),
             "note": "one pcv.run_pcv call with host inputs (upload, warm start, warm-up, sampling with the rule "
                     "at every check interval, report); the wall-clock includes the context's creation"}
 
@@ -357,9 +371,11 @@ def main():
                                    "shuffle benchmark (R=100, on device), report download and context "
                                    "teardown"}
     if not args.no_converge:
-        conv = time_to_converged(world, local, dist)
+        conv = time_to_converged(world, local, dist, "cfg2k")
+        conv4 = time_to_converged(world, local, dist, "cfg4")
         if line is not None:
             line["time_to_converged"] = conv
+            line["time_to_converged_cfg4"] = conv4
     if line is not None and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         cv, kind, sample = cpu_sample(K, 12, 1, threads)
