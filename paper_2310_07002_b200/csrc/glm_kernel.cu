@@ -47,6 +47,7 @@ constexpr int kC = 64;          // chains per CTA
 constexpr int kLdS = 68;        // leading dim of [k][chain] / [row][chain] shared arrays
 constexpr int kMaxOwners = 8;   // owner threads per chain at 512 threads
 constexpr int kStages = 3;      // TMA ring depth
+constexpr int kMaxClusters = 16;  // clusters per chain tile in multi-cluster launches
 
 // Warp layout: 4 chain groups (16 chains each) x RQ row groups. WREG (tested for KP = 52 with 8 warps
 // of 250 registers holding each warp's GEMM-weight fragments for the whole pass) ran 3% slower than
@@ -486,17 +487,19 @@ __device__ void reduce_clusters(Smem<KP>& sm, const ModelDev& M, int tile, int n
   __syncthreads();
   GTRACE(6);
   // every partial of an element loaded before any is added, then summed in cluster order
-  constexpr int kMaxNc = 8;
+  constexpr int kBatch = 8;  // loads in flight per batch (nc <= kMaxClusters = 16: two batches)
   for (int i = tid; i < n; i += kThreads) {
     const int row = r0 + i / kC, c = i % kC;
-    double v[kMaxNc];
+    double x = 0.0;
+    for (int q0 = 0; q0 < nc; q0 += kBatch) {
+      double v[kBatch];
 #pragma unroll
-    for (int q = 0; q < kMaxNc; ++q)
-      v[q] = q < nc ? __ldcg(base + static_cast<size_t>(q) * kE + row * kC + c) : 0.0;
-    double x = v[0];
+      for (int q = 0; q < kBatch; ++q)
+        v[q] = q0 + q < nc ? __ldcg(base + static_cast<size_t>(q0 + q) * kE + row * kC + c) : 0.0;
 #pragma unroll
-    for (int q = 1; q < kMaxNc; ++q)
-      if (q < nc) x += v[q];
+      for (int q = 0; q < kBatch; ++q)
+        if (q0 + q < nc) x = q0 + q == 0 ? v[q] : x + v[q];
+    }
     sm.rs[row * kLdS + c] = x;
   }
 }
@@ -1207,15 +1210,17 @@ int glm_clusters_per_tile(int n, int kp, int nch, int cs, bool have_scratch) {
   const int tm = kp <= 8 ? 256 : (kp <= 16 ? 128 : 64);
   const int tiles = (nch + kC - 1) / kC;
   const int ntiles = (n + tm - 1) / tm;
-  int nc = std::min(8, device_sm_count() / (tiles * cs));
-  while (nc > 1 && ntiles < 2 * cs * nc) --nc;
+  // up to kMaxClusters per tile, at least one row tile per CTA (a single tile - Step 1 - splits its
+  // 157 row tiles over up to 120 CTAs: 2 per CTA instead of 3 at 8 clusters)
+  int nc = std::min(kMaxClusters, device_sm_count() / (tiles * cs));
+  while (nc > 1 && ntiles < cs * nc) --nc;
   return std::max(nc, 1);
 }
 
 // Scratch of the multi-cluster launches of a model with nch chains: partial doubles and counters.
 void glm_multicluster_scratch(int kp, int nch, size_t* part_doubles, size_t* counters) {
   const int tiles = (nch + kC - 1) / kC;
-  *part_doubles = static_cast<size_t>(tiles) * 2 * 8 * (static_cast<size_t>(kp) * kC + kC);
+  *part_doubles = static_cast<size_t>(tiles) * 2 * kMaxClusters * (static_cast<size_t>(kp) * kC + kC);
   *counters = static_cast<size_t>(tiles) * 16;  // one per (tile, cluster rank)
 }
 
