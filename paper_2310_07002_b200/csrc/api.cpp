@@ -94,6 +94,23 @@ void ck(cudaError_t e, const char* what) {
 // (profiles/r02_teardown.log), and the next context on the device reuses it.
 thread_local cudaStream_t g_alloc_stream = nullptr;  // the calling context's stream (set by guarded())
 
+// Host-to-device copies and clears, ordered with every later kernel. A plain cudaMemcpy from pageable
+// host memory may return before its DMA has landed and cudaMemset is asynchronous, both on the legacy
+// stream, which the contexts' non-blocking streams do not wait for: a kernel on the context's stream
+// could read a buffer before its upload or clear completed (an intermittent acceptance-test failure:
+// a score-stream run read part of its streams before they arrived). Here the copy / clear runs on the
+// context's stream and the host waits for it, so any stream sees the data afterwards.
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st = g_alloc_stream) {
+  if (!bytes) return;
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "upload");
+  ck(cudaStreamSynchronize(st), "upload");
+}
+void dzero(void* p, size_t bytes, cudaStream_t st = g_alloc_stream) {
+  if (!bytes) return;
+  ck(cudaMemsetAsync(p, 0, bytes, st), "memset");
+  ck(cudaStreamSynchronize(st), "memset");
+}
+
 void retain_pool_memory() {
   static std::mutex mu;
   static std::vector<int> done;
@@ -132,7 +149,7 @@ struct DevBuf {
   }
   void upload(const std::vector<T>& v) {
     alloc(v.size());
-    if (!v.empty()) ck(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
+    if (!v.empty()) h2d(p, v.data(), sizeof(T) * v.size(), st);
   }
   std::vector<T> download(cudaStream_t s) const {
     std::vector<T> v(n);
@@ -885,8 +902,8 @@ void alloc_extra(ChainSet& cs, const HostModel& m, int kind, int fb, int nfold, 
   cs.xwarm.alloc(std::max<int64_t>(wb, 1));
   cs.xdev.alloc(std::max<int64_t>(wb, 1));
   cs.xcenter.alloc(std::max<int64_t>(cb, 1));
-  ck(cudaMemset(cs.xacc.p, 0, sizeof(double) * cs.xacc.n), "memset");
-  ck(cudaMemset(cs.xwarm.p, 0, sizeof(double) * cs.xwarm.n), "memset");
+  dzero(cs.xacc.p, sizeof(double) * cs.xacc.n);
+  dzero(cs.xwarm.p, sizeof(double) * cs.xwarm.n);
 }
 
 // Per-fold HS / DSS estimates of a shard at `iters` sampling iterations (engine.cpp:148-171):
@@ -1143,15 +1160,15 @@ std::unique_ptr<ChainSet> probe_chains(pcvg_ctx* ctx, const HostModel& m, int64_
   std::vector<double> pos(2 * static_cast<size_t>(m.dim) * n, 0.0);
   for (int64_t c = 0; c < n; ++c)
     for (int d = 0; d < m.dim; ++d) pos[static_cast<size_t>(d) * n + c] = theta[c * m.dim + d];
-  ck(cudaMemcpy(cs->pos.p, pos.data(), sizeof(double) * pos.size(), cudaMemcpyHostToDevice), "upload");
-  ck(cudaMemset(cs->grad.p, 0, sizeof(double) * cs->grad.n), "memset");
-  ck(cudaMemset(cs->cur.p, 0, n), "memset");
-  ck(cudaMemset(cs->rpos.p, 0, sizeof(uint64_t) * n), "memset");
-  ck(cudaMemset(cs->has.p, 0, n), "memset");
-  ck(cudaMemset(cs->cached.p, 0, sizeof(double) * n), "memset");
-  ck(cudaMemset(cs->div.p, 0, sizeof(int64_t) * n), "memset");
-  ck(cudaMemset(cs->warm.p, 0, sizeof(double) * n), "memset");
-  ck(cudaMemset(cs->stream.p, 0, sizeof(uint64_t) * n), "memset");
+  h2d(cs->pos.p, pos.data(), sizeof(double) * pos.size());
+  dzero(cs->grad.p, sizeof(double) * cs->grad.n);
+  dzero(cs->cur.p, n);
+  dzero(cs->rpos.p, sizeof(uint64_t) * n);
+  dzero(cs->has.p, n);
+  dzero(cs->cached.p, sizeof(double) * n);
+  dzero(cs->div.p, sizeof(int64_t) * n);
+  dzero(cs->warm.p, sizeof(double) * n);
+  dzero(cs->stream.p, sizeof(uint64_t) * n);
   cs->fold_override.upload(std::vector<int>(fold, fold + n));
   (void)ctx;
   return cs;
@@ -1303,7 +1320,7 @@ pcvg_status pcvg_hmc_chain(pcvg_ctx* ctx, int32_t slot, int32_t fold, int32_t ch
     auto cs = probe_chains(ctx, m, 1, &fold, theta0);
     const uint64_t st = stream_key(PCVG_STREAM_CHAIN_SAMPLING, static_cast<uint64_t>(m.model_id),
                                    static_cast<uint64_t>(fold), static_cast<uint64_t>(chain));
-    ck(cudaMemcpy(cs->stream.p, &st, sizeof st, cudaMemcpyHostToDevice), "upload");
+    h2d(cs->stream.p, &st, sizeof st);
     ChainsDev S = cs->view(1, 0, seed, static_cast<uint64_t>(m.model_id));
     launch_family(ctx, m, S, make_args(kModeEval, 0));
     DevBuf<double> tr;
@@ -1335,7 +1352,7 @@ pcvg_status pcvg_score_streams(pcvg_ctx* ctx, int32_t L, int64_t n, const double
     centers.upload(std::vector<double>{center});
     streams.upload(std::vector<double>(s, s + static_cast<size_t>(L) * n));
     ChainsDev S = cs.view(L, 0, 0, 0);
-    ck(cudaMemset(cs.warm.p, 0, sizeof(double) * L), "memset");
+    dzero(cs.warm.p, sizeof(double) * L);
     ck(launch_centers(S, 0, 0, centers.p, D, ctx->stream), "reset");  // nfold 0: no centre recompute
     ck(launch_feed_streams(S, streams.p, n, 0, n, n, D, b, ctx->stream), "feed");
     DevBuf<double> o;
@@ -1779,8 +1796,8 @@ pcvg_status pcvg_run_streams(pcvg_ctx* ctx, int32_t K, const double* s, const do
     ctx->sample_ms = ctx->warm_ms = 0.0;
     auto cs = std::make_unique<ChainSet>();
     cs->alloc(K * L, 1, D);
-    ck(cudaMemset(cs->div.p, 0, sizeof(int64_t) * cs->div.n), "memset");
-    ck(cudaMemset(cs->pending.p, 0, sizeof(int32_t) * cs->pending.n), "memset");
+    dzero(cs->div.p, sizeof(int64_t) * cs->div.n);
+    dzero(cs->pending.p, sizeof(int32_t) * cs->pending.n);
     auto cb = std::make_unique<DevBuf<double>>();
     cb->upload(std::vector<double>(centers, centers + K));
     ck(launch_centers(cs->view(L, 0, cfg->seed, 0), 0, 0, cb->p, D, ctx->stream), "reset");  // given centres
@@ -1912,14 +1929,14 @@ std::unique_ptr<ChainSet> adapt_chains(const HostModel& m, const std::vector<std
     cached[c] = rngs[c].cached();
     has[c] = rngs[c].has_cached() ? 1 : 0;
   }
-  ck(cudaMemcpy(cs->pos.p, p.data(), sizeof(double) * p.size(), cudaMemcpyHostToDevice), "upload");
-  ck(cudaMemset(cs->grad.p, 0, sizeof(double) * cs->grad.n), "memset");
-  ck(cudaMemset(cs->cur.p, 0, L), "memset");
-  ck(cudaMemset(cs->div.p, 0, sizeof(int64_t) * L), "memset");
-  ck(cudaMemset(cs->warm.p, 0, sizeof(double) * L), "memset");
-  ck(cudaMemcpy(cs->rpos.p, rp.data(), sizeof(uint64_t) * L, cudaMemcpyHostToDevice), "upload");
-  ck(cudaMemcpy(cs->cached.p, cached.data(), sizeof(double) * L, cudaMemcpyHostToDevice), "upload");
-  ck(cudaMemcpy(cs->has.p, has.data(), L, cudaMemcpyHostToDevice), "upload");
+  h2d(cs->pos.p, p.data(), sizeof(double) * p.size());
+  dzero(cs->grad.p, sizeof(double) * cs->grad.n);
+  dzero(cs->cur.p, L);
+  dzero(cs->div.p, sizeof(int64_t) * L);
+  dzero(cs->warm.p, sizeof(double) * L);
+  h2d(cs->rpos.p, rp.data(), sizeof(uint64_t) * L);
+  h2d(cs->cached.p, cached.data(), sizeof(double) * L);
+  h2d(cs->has.p, has.data(), L);
   cs->fold_override.upload(std::vector<int>(L, m.K));  // full-data sentinel fold
   return cs;
 }
@@ -2061,7 +2078,7 @@ extern "C" pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* d
       std::vector<uint64_t> st(L);
       for (int c = 0; c < L; ++c)
         st[c] = stream_key(PCVG_STREAM_FULL_DATA, static_cast<uint64_t>(model_id), static_cast<uint64_t>(c), 0);
-      ck(cudaMemcpy(cs->stream.p, st.data(), sizeof(uint64_t) * L, cudaMemcpyHostToDevice), "upload");
+      h2d(cs->stream.p, st.data(), sizeof(uint64_t) * L);
     }
     const ChainsDev S = cs->view(1, 0, seed, 0);
     DevBuf<double> h0b, h1b;
@@ -2108,7 +2125,7 @@ extern "C" pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* d
       auto probe = [&](double e) {
         HostRng fresh(seed, sst);
         auto ps = adapt_chains(m, {pos[0]}, {fresh}, 0);
-        ck(cudaMemcpy(ps->stream.p, &sst, sizeof sst, cudaMemcpyHostToDevice), "upload");
+        h2d(ps->stream.p, &sst, sizeof sst);
         ModelDev saved = md;
         md.step = e;
         md.n_lf = 1;
@@ -2179,7 +2196,7 @@ extern "C" pcvg_status pcvg_adapt_full_data(pcvg_ctx* ctx, const pcvg_dataset* d
             const double v = var * (n / (n + 5.0)) + 1e-3 * (5.0 / (n + 5.0));
             inv_mass[i] = std::max(v, 1e-10);
           }
-          ck(cudaMemcpy(im.p, inv_mass.data(), sizeof(double) * d, cudaMemcpyHostToDevice), "upload");
+          h2d(im.p, inv_mass.data(), sizeof(double) * d);
         }
         std::fill(wx.begin(), wx.end(), 0.0);
         std::fill(wx2.begin(), wx2.end(), 0.0);
