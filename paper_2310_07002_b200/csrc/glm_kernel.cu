@@ -593,10 +593,6 @@ __device__ void reduce_pass(Smem<KP>& sm, int cs, const ModelDev& M, int tile, i
   GTRACE(10);
 }
 
-__device__ __forceinline__ double bernoulli_logit(double y, double x) {
-  return y * x - (fmax(x, 0.0) + log1p(exp(-fabs(x))));
-}
-
 // HS / DSS state of one chain after hmc_step + log_pred (engine.cpp:360-373; warm-up
 // hmc.cpp:133-145), run by the chain thread over the fold's test rows in order: pred_derivs /
 // pred_sample of grouped_regression.cpp:190-213 (J = 1) and seasonal_ar.cpp:133-150. Every rank
@@ -1012,7 +1008,8 @@ __global__ void __launch_bounds__(Geom<KP>::THREADS, 1) glm_kernel(ModelDev M, C
               e4[(2 * kk + 1) & 3] = fma(xv.y, w1, e4[(2 * kk + 1) & 3]);
             }
             eta = (e4[0] + e4[1]) + (e4[2] + e4[3]);
-            part += bernoulli_logit(M.y[i], eta);
+            // log p(y | eta) = y eta - (max(eta, 0) + log1p(e^-|eta|)) with the value pass's exp / log1p
+            part += M.y[i] * eta - (fmax(eta, 0.0) + log1p_01(exp_neg(fabs(eta), sm.exp_tab), sm.l1p_rc, sm.l1p_lc));
           } else {
             for (int k = 0; k < dim; ++k) {
               const int col = col_of<FAM>(M, k);
