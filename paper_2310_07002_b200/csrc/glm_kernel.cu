@@ -15,10 +15,13 @@
 // sum of squares and the priors). One chain thread per chain runs the reference RNG stream,
 // energies, Metropolis test, log_pred and accumulators. Semantics follow hmc.cpp:22-99 and
 // engine.cpp:342-381.
-// Few-chain configurations (cfg4: 800 chains; K-fold cfg2: 80 chains) split the rows over a
-// thread-block cluster of CS CTAs that replicate one 64-chain tile: each CTA streams 1/CS of the
-// row tiles and the partial X^T R / residual sums are reduced through distributed shared memory in
-// fixed rank order, so every CTA of the cluster holds bit-identical state; rank 0 writes it back.
+// Few-chain configurations (K-fold cfg2: 80 chains; Step 1: one tile) split the rows over
+// thread-block clusters of CS CTAs that replicate one 64-chain tile, and over NC such clusters
+// (cooperative launch): each CTA streams its share of the row tiles; the partial X^T R / residual
+// sums are reduced by a push over DSMEM (bulk copies to row owners, rank-order sums, bulk copies
+// back; reduce_pass) and, across clusters, through global memory (reduce_clusters), so every CTA
+// of the tile holds bit-identical state; rank 0 writes it back. The wave tail of many-chain launches
+// runs the same way (clusters only). log_pred's test rows are split over the first cluster's ranks.
 #include <algorithm>
 #include <mutex>
 #include <cooperative_groups.h>
